@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""bench.py — STL layer throughput on B200 (BASELINE.json metric, configs[1]).
+
+A step = one STL linear layer forward + backward (all four gradients) at t=4, r=24, bf16,
+M=8192 tokens, K=N=4096 (BASELINE configs[1]) on synthetic seeded data, through the C ABI
+(stl_forward + stl_backward). Under torchrun every rank runs its own 8192-token batch
+(data-parallel, weak scaling) and the gradients (g_w, g_ex, g_d) are all-reduced over NCCL
+each step — the real exchange step of STL data-parallel training.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl stl|reference]
+
+Prints ONE JSON line (rank 0). value = dense-equivalent TFLOP/s of the whole job
+(3 * 2*M*K*N per rank per step / max-over-ranks device time). Inputs (~1 GB of live tensors per
+step) are far larger than the 126 MB L2, so no explicit flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "STL layer dense-equiv TFLOP/s & speedup vs cuBLAS GEMM (t=4,r=24), at 1/2/4/8 B200"
+UNIT = "TFLOP/s (dense-equivalent)"
+T, R, M, K, N = 4, 24, 8192, 4096, 4096
+WORKLOAD = "configs[1]: STL linear layer forward+backward t=4 r=24 bf16, M=8192 tokens, K=N=4096"
+
+
+def dense_equiv_flops(m=M, k=K, n=N, passes=3):
+    return passes * 2.0 * m * k * n
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_burst": d["bf16_tflops"],
+                "bf16_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_burst": 1590.0, "bf16_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Polls NVML (SM clock, max clock, event reasons) every 20 ms in a thread."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._thr = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = self._handle(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self.nv = None
+
+    def _handle(self, idx):
+        import torch
+        nv = self.nv
+        try:
+            props = torch.cuda.get_device_properties(idx)
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:  # noqa: BLE001
+            return nv.nvmlDeviceGetHandleByIndex(idx)
+
+    def _reasons(self):
+        nv = self.nv
+        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        return fn(self.h)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self._reasons()
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def start(self):
+        if self.nv is not None:
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+
+    def stop(self):
+        if self._thr is not None:
+            self._stop.set()
+            self._thr.join()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_reference_step(rows: int, seed: int = 0):
+    """The reference's CPU algorithm (oracle port, f64): stl forward (cached) + backward with
+    the reference's own numpy call pattern (np.einsum without optimize), `rows` tokens."""
+    from oracle import stl_oracle as O
+
+    rng = O.make_rng(seed)
+    e_x, e_w, d = O.random_gaussian_init(T, R, rng, scale=0.5)
+    w_enc = O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, T)
+    x = rng.standard_normal((rows, K))
+    gy = rng.standard_normal((rows, N))
+
+    def step():
+        _y, cache = O.layer_forward_cached(x, w_enc, e_x, d, T)
+        O.layer_backward_einsum(w_enc, e_x, d, cache, gy, T)
+
+    return step
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank: int) -> None:
+    """--impl reference: the reference's CPU implementation of the path (oracle port; the
+    reference is pure Python and absent on the GPU box), rank 0 only."""
+    if rank != 0:
+        return
+    rows = args.ref_rows
+    step = cpu_reference_step(rows)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    sec = (time.perf_counter() - t0) / args.steps
+    value = dense_equiv_flops(m=rows) / sec / 1e12
+    sample = (f"{rows} of the 8192 tokens per step (K=N=4096, t=4, r=24, f64); forward "
+              "stl_batched call pattern + backward np.einsum without optimize, as "
+              "toy_network.py:95-106; numpy/OpenBLAS threads for the BLAS parts")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PCG64)",
+        "config": {"workload": WORKLOAD, "sample_rows": rows, "t": T, "r": R},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("stl", "reference"), default="stl")
+    ap.add_argument("--ref-rows", type=int, default=128)
+    ap.add_argument("--cpu-rows", type=int, default=512)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip cuBLAS / 8192^3 / e2e legs")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_12211_b200 as stl
+    from paper_2503_12211_b200 import _lib
+    from paper_2503_12211_b200.layer import LayerCache, backward_raw
+    from paper_2503_12211_b200.snf_operator import _forward
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    peaks = load_peaks()
+
+    # ---- problem: weights/encoders identical on every rank (DP replicas), data per rank
+    rng = np.random.Generator(np.random.PCG64(0))
+    snf = stl.random_gaussian_init(T, R, rng, scale=0.5).to(dev)
+    w0 = torch.randn((K, N), generator=torch.Generator().manual_seed(1)) / K ** 0.5
+    w_enc = stl.encode_tiles(w0.to(dev), snf.e_w, T)            # (bk, bj, r) fp32 view
+    w_planes = stl.weights_to_planes(w_enc, dtype=torch.bfloat16)  # (r, bj, bk) bf16
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    x = torch.randn((M, K), device=dev, generator=g).to(torch.bfloat16)
+    gy = torch.randn((M, N), device=dev, generator=g).to(torch.bfloat16)
+    stl.set_check_finite(False)
+
+    bi, bk, bj = M // T, K // T, N // T
+    u = torch.empty((R, bi, bk), dtype=torch.bfloat16, device=dev)
+    y_enc = torch.empty((R, bi, bj), dtype=torch.float32, device=dev)
+    y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+    grads = torch.empty((R * bj * bk + 2 * R * T * T,), dtype=torch.float32, device=dev)
+    g_w = grads[: R * bj * bk].view(R, bj, bk)
+    g_ex = grads[R * bj * bk: R * bj * bk + R * T * T].view(R, T * T)
+    g_d = grads[R * bj * bk + R * T * T:].view(R, T * T)
+    g_x = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
+    g_enc = torch.empty((R, bi, bj), dtype=torch.bfloat16, device=dev)
+    g_u = torch.empty((R, bi, bk), dtype=torch.float32, device=dev)
+    red = torch.empty((int(lib.stl_reduce_workspace_floats(R, T)),), dtype=torch.float32,
+                      device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+
+    def stl_step(allreduce: bool):
+        _lib.check(lib.stl_forward(x.data_ptr(), M, K, K, w_planes.data_ptr(), N,
+                                   snf.e_x.data_ptr(), snf.d.data_ptr(), T, R, _lib.STL_BF16,
+                                   y.data_ptr(), N, u.data_ptr(), y_enc.data_ptr(), stream))
+        _lib.check(lib.stl_backward(gy.data_ptr(), N, x.data_ptr(), K, w_planes.data_ptr(),
+                                    snf.e_x.data_ptr(), snf.d.data_ptr(), u.data_ptr(),
+                                    y_enc.data_ptr(), M, K, N, T, R, _lib.STL_BF16,
+                                    g_ex.data_ptr(), g_d.data_ptr(), g_w.data_ptr(),
+                                    g_x.data_ptr(), K, g_enc.data_ptr(), g_u.data_ptr(),
+                                    red.data_ptr(), stream))
+        if allreduce:
+            dist.all_reduce(grads)
+
+    def timed(fn, steps, profile=False):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        if profile:
+            lib.stl_profile_reset()
+            lib.stl_profile_enable(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        if profile:
+            lib.stl_profile_enable(0)
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+            dist.barrier()
+        return ms
+
+    # ---- warm-up, then the timed region (clocks sampled during it)
+    for _ in range(args.warmup):
+        stl_step(world > 1)
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    sampler.start()
+    total_ms = timed(lambda: stl_step(world > 1), args.steps, profile=True)
+    clocks = sampler.stop()
+    ms_step = total_ms / args.steps
+    value = world * dense_equiv_flops() / (ms_step * 1e-3) / 1e12
+
+    # ---- per-kernel attribution from the library's event profiler (same timed region)
+    recs = _lib.profile_records()
+    kern = {}
+    launches = 0
+    for name, ms, n in recs:
+        k = kern.setdefault(name, {"ms": 0.0, "calls": 0})
+        k["ms"] += ms
+        k["calls"] += 1
+        launches += n
+    cost = stl.LayerCost(M, K, N, T, R, 2)
+    gem = kern.get("slice_gemm_tcgen05", {"ms": float("nan"), "calls": 1})
+    gemm_ms = gem["ms"] / max(gem["calls"], 1)
+    gemm_tflops = cost.gemm_flops() / (gemm_ms * 1e-3) / 1e12
+    traffic = None
+    tp = ROOT / "profiles" / "gemm_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("bytes_per_launch")
+    roofline = {"kernel": "slice_gemm_tcgen05", "bound": "tensor", "achieved": gemm_tflops,
+                "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
+                "frac": gemm_tflops / peaks["bf16_sustained"], "traffic": traffic,
+                "flops_per_launch": cost.gemm_flops(), "ms_per_launch": gemm_ms,
+                "peak_source": peaks["source"] + ", sustained bf16"}
+    breakdown = {}
+    step_kernel_ms = sum(v["ms"] for v in kern.values()) / args.steps
+    hbm_bytes = {"encode_x": cost.encode_bytes(), "decode_y": cost.decode_bytes(),
+                 "encode_gy+g_d": M * N * 2 + R * bi * bj * 2 + R * bi * bj * 4,
+                 "decode_gu+g_ex": R * bi * bk * 4 + M * K * 2 + M * K * 2}
+    for name, v in kern.items():
+        per = v["ms"] / args.steps
+        entry = {"ms_per_step": per, "share": per / step_kernel_ms if step_kernel_ms else None,
+                 "calls_per_step": v["calls"] / args.steps}
+        if name in hbm_bytes:
+            gbs = hbm_bytes[name] / (v["ms"] / v["calls"] * 1e-3) / 1e9
+            entry.update({"achieved_GBs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"]})
+        breakdown[name] = entry
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded randn; random-init N(0,0.25) encoders)",
+        "config": {"workload": WORKLOAD, "M_per_rank": M, "K": K, "N": N, "t": T, "r": R,
+                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   "l2": "inputs+intermediates ~1 GB/step > 126 MB L2 (no explicit flush)"},
+        "roofline": roofline, "kernels": breakdown,
+        "gpu_launches": launches, "clocks": clocks,
+    }
+
+    # ---- cuBLAS dense comparison on this rank (same shapes: Y=XW, dX=dY W^T, dW=X^T dY)
+    if not args.no_extras:
+        wd = torch.randn((K, N), device=dev).to(torch.bfloat16)
+        yd = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        gxd = torch.empty((M, K), device=dev, dtype=torch.bfloat16)
+        gwd = torch.empty((K, N), device=dev, dtype=torch.bfloat16)
+
+        def dense_step():
+            torch.matmul(x, wd, out=yd)
+            torch.matmul(gy, wd.t(), out=gxd)
+            torch.matmul(x.t(), gy, out=gwd)
+
+        for _ in range(args.warmup):
+            dense_step()
+        dense_ms = timed(dense_step, args.steps) / args.steps
+        stl_ms = ms_step if world == 1 else timed(lambda: stl_step(False), args.steps) / args.steps
+        line["vs_cublas"] = {"cublas_ms_per_step": dense_ms, "stl_ms_per_step": stl_ms,
+                             "speedup": dense_ms / stl_ms,
+                             "cublas_tflops": dense_equiv_flops() / (dense_ms * 1e-3) / 1e12}
+        del wd, yd, gxd, gwd
+
+        # ---- north-star forward: 8192^3 bf16, t=4, r=24, STL forward vs cuBLAS forward
+        n3 = 8192
+        wf = stl.weights_to_planes(
+            stl.encode_tiles(torch.randn((n3, n3), device=dev) / n3 ** 0.5, snf.e_w, T),
+            dtype=torch.bfloat16)
+        xf = torch.randn((n3, n3), device=dev).to(torch.bfloat16)
+        uf = torch.empty((R, n3 // T, n3 // T), dtype=torch.bfloat16, device=dev)
+        yef = torch.empty((R, n3 // T, n3 // T), dtype=torch.float32, device=dev)
+        yf = torch.empty((n3, n3), dtype=torch.bfloat16, device=dev)
+        wdf = torch.randn((n3, n3), device=dev).to(torch.bfloat16)
+        ydf = torch.empty((n3, n3), device=dev, dtype=torch.bfloat16)
+
+        def fwd8192():
+            _lib.check(lib.stl_forward(xf.data_ptr(), n3, n3, n3, wf.data_ptr(), n3,
+                                       snf.e_x.data_ptr(), snf.d.data_ptr(), T, R, _lib.STL_BF16,
+                                       yf.data_ptr(), n3, uf.data_ptr(), yef.data_ptr(), stream))
+
+        steps_f = max(args.steps // 2, 10)
+        for _ in range(args.warmup):
+            fwd8192()
+            torch.matmul(xf, wdf, out=ydf)
+        stl_f = timed(fwd8192, steps_f, profile=True) / steps_f
+        recs_f = _lib.profile_records()
+        gemm_f = [ms for name, ms, _ in recs_f if name == "slice_gemm_tcgen05"]
+        cub_f = timed(lambda: torch.matmul(xf, wdf, out=ydf), steps_f) / steps_f
+        cost_f = stl.LayerCost(n3, n3, n3, T, R, 2)
+        gf_ms = sum(gemm_f) / max(len(gemm_f), 1)
+        line["north_star_fwd_8192"] = {
+            "stl_ms": stl_f, "cublas_ms": cub_f, "speedup": cub_f / stl_f, "target": 1.8,
+            "dense_equiv_tflops": 2 * n3 ** 3 / (stl_f * 1e-3) / 1e12,
+            "gemm_ms": gf_ms, "gemm_tflops": cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12,
+            "gemm_frac_of_burst": cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12 / peaks["bf16_burst"],
+        }
+        del wf, xf, uf, yef, yf, wdf, ydf
+        torch.cuda.empty_cache()
+
+        # ---- e2e: public API (StlLinear autograd) with pinned host inputs, copies timed
+        mod = stl.StlLinear(snf, w_planes.clone())
+        x_h = x.cpu().pin_memory()
+        gy_h = gy.cpu().pin_memory()
+        x_d = torch.empty_like(x)
+        gy_d = torch.empty_like(gy)
+        out_h = torch.empty((2, R, T * T), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            x_d.copy_(x_h, non_blocking=True)
+            gy_d.copy_(gy_h, non_blocking=True)
+            xin = x_d.detach().requires_grad_(True)
+            mod.zero_grad(set_to_none=True)
+            out = mod(xin)
+            out.backward(gy_d)
+            if world > 1:
+                dist.all_reduce(mod.w_planes.grad)
+            out_h[0].copy_(mod.e_x.grad, non_blocking=True)
+            out_h[1].copy_(mod.d.grad, non_blocking=True)
+
+        steps_e = max(args.steps // 4, 10)
+        for _ in range(args.warmup):
+            e2e_step()
+        e2e_ms = timed(e2e_step, steps_e) / steps_e
+        line["e2e"] = {"value": world * dense_equiv_flops() / (e2e_ms * 1e-3) / 1e12,
+                       "unit": UNIT, "ms_per_step": e2e_ms,
+                       "h2d_bytes_per_step": x_h.numel() * 2 + gy_h.numel() * 2,
+                       "d2h_bytes_per_step": out_h.numel() * 4,
+                       "path": "StlLinear (autograd) forward+backward, pinned host X and dY "
+                               "copied in, encoder/decoder grads copied out each step"}
+
+    # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on a bounded sample
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows = args.cpu_rows
+        step = cpu_reference_step(rows)
+        t0 = time.perf_counter()
+        step()
+        sec = time.perf_counter() - t0
+        line["cpu_baseline"] = {
+            "value": dense_equiv_flops(m=rows) / sec / 1e12, "unit": UNIT, "cores": cpu_cores(),
+            "kind": "port",
+            "sample": f"{rows} tokens x K=N=4096 fwd+bwd, f64, oracle port of stl_batched + "
+                      f"_layer_backward (np.einsum as the reference), one run, {sec:.1f} s"}
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * stl_b200.h — C ABI of the B200-native Strassen-Tile (STL) operator.
+ *
+ * The reference (arXiv 2503.12211, /root/reference/pkg/src/strassen_tile) is a pure-Python
+ * numpy package with no FFI; its operator API is the flat Python namespace. Each entry point
+ * below replaces one reference function on the hot path, cited as file:line. The Python
+ * mirror (paper_2503_12211_b200/) binds these through ctypes.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers except where noted; `stream` is a cudaStream_t (NULL =
+ *    legacy default stream). Calls are stream-ordered and never synchronise the host.
+ *  - dtype: STL_F32 or STL_BF16. Matrices are row-major with a leading dimension in elements.
+ *  - "planes": the GPU-native encoded layout. An encoded tensor with tile grid (R, C) and rank
+ *    r is stored slice-major as r contiguous row-major (R x C) planes: element (I, J, p) at
+ *    p*R*C + I*C + J. The reference stores the same numbers fiber-contiguous as (R, C, r)
+ *    (snf_operator.py:194-196); convert with a (2, 0, 1) permutation.
+ *  - Pre-encoded weights ("w_enc", StlLayer.weights toy_network.py:45-71, reference layout
+ *    (K/t, N/t, r)) are stored as planes of the TRANSPOSED tile grid: (r, N/t, K/t), i.e. the
+ *    reference tensor permuted (2, 1, 0). Each plane is then the K-major B operand of a
+ *    tensor-core slice GEMM.
+ *  - Encoders/decoder (SnfTriple e_x, e_w, d; snf_operator.py:45-70) are fp32 (r, t*t) row-major
+ *    device arrays; d is applied transposed exactly as in the reference (snf_operator.py:18).
+ *  - Every function returns STL_OK (0) or an error code; stl_last_error() describes the last
+ *    failure on the calling thread. Error classes mirror the reference: STL_ERR_SHAPE <->
+ *    ShapeError (dense_core.py:30-31), STL_ERR_VALUE <-> ValueError, STL_ERR_INDEX <->
+ *    IndexError (snf_operator.py:102-103).
+ */
+#ifndef STL_B200_H
+#define STL_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define STL_API __attribute__((visibility("default")))
+#else
+#define STL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum stl_dtype { STL_F32 = 0, STL_BF16 = 1 };
+
+enum stl_status {
+  STL_OK = 0,
+  STL_ERR_SHAPE = 1,
+  STL_ERR_VALUE = 2,
+  STL_ERR_INDEX = 3,
+  STL_ERR_CUDA = 4,
+  STL_ERR_UNSUPPORTED = 5
+};
+
+/* Slice-GEMM operand layouts. */
+enum stl_layout { STL_K_MAJOR = 0, STL_MN_MAJOR = 1 };
+
+/* Library version string, e.g. "stl_b200 0.1 sm_100a". Host-only. */
+STL_API const char* stl_version(void);
+/* Message describing the last non-OK status returned on this thread. Host-only. */
+STL_API const char* stl_last_error(void);
+/* Largest rank r accepted by the transform kernels. */
+STL_API int stl_max_rank(void);
+/* Floats of scratch needed by the fused r x t^2 reductions of stl_backward. */
+STL_API int64_t stl_reduce_workspace_floats(int r, int t);
+
+/*
+ * encode_tiles (snf_operator.py:80-85):  out[I, J, p] = sum_c encoder[p, c] * vec_tile(m, I, J)[c]
+ * m: (rows, cols) with leading dim ld_m; out: planes (r, rows/t, cols/t) of dtype_out.
+ */
+STL_API int stl_encode(const void* m, int dtype_in, int64_t rows, int64_t cols, int64_t ld_m,
+               const float* encoder, int t, int r, void* out, int dtype_out, void* stream);
+
+/*
+ * decode_tiles (snf_operator.py:88-96):  out tile (I, J) = unvec(decoder^T @ enc[I, J, :])
+ * enc: planes (r, block_rows, block_cols); out: (block_rows*t, block_cols*t), leading dim ld_out.
+ */
+STL_API int stl_decode(const void* enc, int dtype_in, int64_t block_rows, int64_t block_cols, int r,
+               const float* decoder, int t, void* out, int dtype_out, int64_t ld_out,
+               void* stream);
+
+/*
+ * _slice_products (snf_operator.py:107-116):  C_p = A_p @ B_p for p = 0..r-1.
+ * A: a_layout STL_K_MAJOR -> planes (r, M, K); STL_MN_MAJOR -> planes (r, K, M).
+ * B: b_layout STL_K_MAJOR -> planes (r, N, K); STL_MN_MAJOR -> planes (r, K, N).
+ * C: planes (r, M, N) of dtype_c (STL_F32 keeps the slice accumulators exact in fp32).
+ * dtype_ab = STL_BF16 runs the tcgen05/TMEM tensor-core kernel (when the contiguous dims are
+ * multiples of 8); STL_F32 runs the fp32 FFMA kernel (TF32 would miss the 1e-5 fp32 bar).
+ */
+STL_API int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_layout, void* c,
+                   int dtype_c, int dtype_ab, int r, int64_t M, int64_t N, int64_t K,
+                   void* stream);
+
+/*
+ * stl_batched (snf_operator.py:156-172) / stl_layer_forward + _layer_forward_cached
+ * (toy_network.py:74-92):  y = decode(slice_products(encode(x, e_x), w_enc), d).
+ *   x: (M, K) ld_x, dtype;  w_enc: planes (r, N/t, K/t) of dtype;  y: (M, N) ld_y, dtype.
+ *   x_enc_ws: planes (r, M/t, K/t) of dtype (the cache `u`);
+ *   y_enc_ws: fp32 planes (r, M/t, N/t) (the cache `y_enc`).
+ *   M, K, N must be multiples of t (ShapeError otherwise, as the reference).
+ */
+STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
+                const float* e_x, const float* d, int t, int r, int dtype, void* y, int64_t ld_y,
+                void* x_enc_ws, float* y_enc_ws, void* stream);
+
+/*
+ * _layer_backward (toy_network.py:95-106), all seven formulas:
+ *   g_d  = sum_{I,J} y_enc[I,J,p] gvy[I,J,c]      -> g_d  fp32 (r, t*t)
+ *   g_enc = gvy @ d^T                              -> g_enc_ws planes (r, M/t, N/t) dtype
+ *   g_w  = sum_I u[I,L,p] g_enc[I,J,p]             -> g_w  fp32 planes (r, N/t, K/t)
+ *   g_u  = sum_J W[L,J,p] g_enc[I,J,p]             -> g_u_ws fp32 planes (r, M/t, K/t)
+ *   g_ex = sum_{I,L} g_u[I,L,p] vx[I,L,c]          -> g_ex fp32 (r, t*t)
+ *   g_x  = untile(g_u @ e_x)                       -> g_x (M, K) ld_gx, dtype
+ * Inputs: gy (M, N) ld_gy; x (M, K) ld_x (the layer input, vx); w_enc as in stl_forward;
+ * x_enc (= u) and y_enc from the forward cache. red_ws: stl_reduce_workspace_floats floats.
+ * Any of g_ex, g_d, g_w, g_x may be NULL to skip that gradient.
+ */
+STL_API int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, const void* w_enc,
+                 const float* e_x, const float* d, const void* x_enc, const float* y_enc,
+                 int64_t M, int64_t K, int64_t N, int t, int r, int dtype, float* g_ex,
+                 float* g_d, float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws,
+                 float* g_u_ws, float* red_ws, void* stream);
+
+/*
+ * stl_fused_step (snf_operator.py:175-188, Algorithm 2):
+ *   out = slice_products(x_prev @ (e_x d^T)^T, w_enc), staying in encoded space.
+ *   x_prev: fp32 planes (r, BR, BK); w_enc: planes (r, BN, BK) of dtype;
+ *   out: fp32 planes (r, BR, BN); mixed_ws: planes (r, BR, BK) of dtype; comp_ws: r*r floats.
+ */
+STL_API int stl_fused_step(const float* x_prev, int64_t block_rows, int64_t block_k, const void* w_enc,
+                   int64_t block_n, const float* e_x, const float* d, int t, int r, int dtype,
+                   float* out, void* mixed_ws, float* comp_ws, void* stream);
+
+/*
+ * Launch profiler (no reference counterpart; B200 measurement aid). While enabled, every
+ * kernel launch the library issues is bracketed by CUDA events on its own stream, so a caller
+ * can attribute device time to kernels inside a timed region without a profiler attached.
+ *   stl_profile_enable(1) ... work ... synchronise ... stl_profile_count / stl_profile_get.
+ * stl_profile_get fills the kernel name (static string), elapsed milliseconds and the number
+ * of kernel launches in that record (1, or 2 for transform+reduction pairs). Host-only.
+ */
+STL_API int stl_profile_enable(int on);
+STL_API int stl_profile_reset(void);
+STL_API int stl_profile_count(void);
+STL_API int stl_profile_get(int index, const char** name, float* ms, int* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STL_B200_H */

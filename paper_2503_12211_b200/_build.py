@@ -1,0 +1,67 @@
+"""In-tree build of the STL CUDA library (libstl_b200.so) for sm_100a.
+
+The library is a plain C-ABI shared object (include/stl_b200.h) built straight with nvcc —
+no torch extension machinery — so it travels with the repo snapshot to the GPU box and is
+loaded with ctypes by :mod:`paper_2503_12211_b200._lib`.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+REPO = PKG.parent
+CSRC = PKG / "csrc"
+LIB_NAME = "libstl_b200.so"
+LIB_PATH = PKG / LIB_NAME
+
+SOURCES = ["stl_capi.cu", "stl_slice_gemm.cu", "stl_transform.cu"]
+HEADERS = ["sm100_ptx.cuh", "stl_internal.h"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+    "--expt-relaxed-constexpr",
+    "-Xptxas", "-v",
+]
+
+
+def nvcc() -> str:
+    cand = [os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"]
+    for c in cand:
+        if c and Path(c).exists():
+            return c
+    raise RuntimeError("nvcc not found (set NVCC or install CUDA 12.9)")
+
+
+def _stale() -> bool:
+    if not LIB_PATH.exists():
+        return True
+    t = LIB_PATH.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [REPO / "include" / "stl_b200.h"]
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every .cu into one shared library (skips if up to date)."""
+    if not force and not _stale():
+        return LIB_PATH
+    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", str(LIB_PATH)]
+    cmd += [str(CSRC / s) for s in SOURCES]
+    cmd += ["-I", str(REPO / "include"), "-lcuda" if False else "-lcudart_static"]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    log = PKG / "build.log"
+    log.write_text(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
+    if proc.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({proc.returncode}); see {log}\n{proc.stderr[-4000:]}")
+    if verbose:
+        print(proc.stderr)
+    return LIB_PATH
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose=True))

@@ -1,0 +1,273 @@
+// stl_capi.cu — extern "C" entry points (include/stl_b200.h): argument validation with the
+// reference's error classes, then stream-ordered launches of the STL kernels.
+#include <cstdio>
+#include <cstdarg>
+#include <mutex>
+#include <string>
+#include <vector>
+#include "../../include/stl_b200.h"
+#include "stl_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(STL_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return STL_OK;
+}
+
+bool valid_dtype(int dt) { return dt == STL_F32 || dt == STL_BF16; }
+
+int check_tr(int t, int r) {
+  if (t < 1 || r < 1) return fail(STL_ERR_SHAPE, "need t >= 1 and r >= 1, got t=%d, r=%d", t, r);
+  if (!(t == 1 || t == 2 || t == 4 || t == 8))
+    return fail(STL_ERR_UNSUPPORTED, "tile size t=%d not supported (1, 2, 4, 8)", t);
+  if (r > stl::kMaxRank)
+    return fail(STL_ERR_UNSUPPORTED, "rank r=%d exceeds the supported maximum %d", r,
+                stl::kMaxRank);
+  return STL_OK;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------ launch profiler
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+  int launches;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_pool;
+size_t g_pool_used = 0;
+
+// Brackets the launches issued in its scope with events on `s` while profiling is enabled.
+struct Prof {
+  int idx = -1;
+  cudaStream_t s;
+  Prof(const char* name, cudaStream_t st, int launches = 1) : s(st) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (g_pool_used == g_pool.size()) {
+      cudaEvent_t a, b;
+      if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return;
+      g_pool.emplace_back(a, b);
+    }
+    auto ev = g_pool[g_pool_used++];
+    cudaEventRecord(ev.first, s);
+    g_prof.push_back({name, ev.first, ev.second, launches});
+    idx = static_cast<int>(g_prof.size()) - 1;
+  }
+  ~Prof() {
+    if (idx < 0) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEventRecord(g_prof[idx].b, s);
+  }
+};
+
+int run_gemm(const void* a, int al, const void* b, int bl, void* c, int cdt, int abdt, int r,
+             int64_t M, int64_t N, int64_t K, cudaStream_t s) {
+  if (M == 0 || N == 0 || r == 0) return STL_OK;
+  if (K == 0) {
+    return check_cuda(cudaMemsetAsync(c, 0, stl::dtype_size(cdt) * r * M * N, s), "memset");
+  }
+  stl::SliceGemmProblem pb{a, al, b, bl, c, cdt, abdt, r, M, N, K};
+  const bool tc = stl::slice_gemm_tc_supported(pb);
+  Prof prof(tc ? "slice_gemm_tcgen05" : "slice_gemm_simt", s);
+  cudaError_t e = tc ? stl::slice_gemm_tc(pb, s) : stl::slice_gemm_simt(pb, s);
+  return check_cuda(e, "slice_gemm launch");
+}
+}  // namespace
+
+extern "C" {
+
+const char* stl_version(void) { return "stl_b200 0.1 sm_100a"; }
+const char* stl_last_error(void) { return g_last_error.c_str(); }
+int stl_max_rank(void) { return stl::kMaxRank; }
+int64_t stl_reduce_workspace_floats(int r, int t) {
+  return static_cast<int64_t>(stl::red_ws_floats(r, t));
+}
+
+int stl_encode(const void* m, int dtype_in, int64_t rows, int64_t cols, int64_t ld_m,
+               const float* encoder, int t, int r, void* out, int dtype_out, void* stream) {
+  if (int st = check_tr(t, r)) return st;
+  if (!valid_dtype(dtype_in) || !valid_dtype(dtype_out))
+    return fail(STL_ERR_VALUE, "invalid dtype");
+  if (rows < 0 || cols < 0 || rows % t || cols % t)
+    return fail(STL_ERR_SHAPE, "tile size %d does not divide shape (%lld, %lld)", t,
+                (long long)rows, (long long)cols);
+  if (ld_m < cols) return fail(STL_ERR_SHAPE, "leading dimension %lld < cols %lld",
+                               (long long)ld_m, (long long)cols);
+  return check_cuda(stl::tiles_to_planes(m, dtype_in, ld_m, rows / t, cols / t, t, encoder, r,
+                                         out, dtype_out, nullptr, nullptr, nullptr,
+                                         as_stream(stream)),
+                    "encode");
+}
+
+int stl_decode(const void* enc, int dtype_in, int64_t block_rows, int64_t block_cols, int r,
+               const float* decoder, int t, void* out, int dtype_out, int64_t ld_out,
+               void* stream) {
+  if (int st = check_tr(t, r)) return st;
+  if (!valid_dtype(dtype_in) || !valid_dtype(dtype_out))
+    return fail(STL_ERR_VALUE, "invalid dtype");
+  if (block_rows < 0 || block_cols < 0) return fail(STL_ERR_SHAPE, "negative block grid");
+  if (ld_out < block_cols * t) return fail(STL_ERR_SHAPE, "leading dimension too small");
+  return check_cuda(stl::planes_to_tiles(enc, dtype_in, r, block_rows, block_cols, t, decoder,
+                                         out, dtype_out, ld_out, nullptr, STL_F32, 0, nullptr,
+                                         nullptr, as_stream(stream)),
+                    "decode");
+}
+
+int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_layout, void* c,
+                   int dtype_c, int dtype_ab, int r, int64_t M, int64_t N, int64_t K,
+                   void* stream) {
+  if (!valid_dtype(dtype_c) || !valid_dtype(dtype_ab)) return fail(STL_ERR_VALUE, "invalid dtype");
+  if (r < 0 || M < 0 || N < 0 || K < 0) return fail(STL_ERR_SHAPE, "negative extent");
+  if ((a_layout != 0 && a_layout != 1) || (b_layout != 0 && b_layout != 1))
+    return fail(STL_ERR_VALUE, "invalid operand layout");
+  return run_gemm(a, a_layout, b, b_layout, c, dtype_c, dtype_ab, r, M, N, K, as_stream(stream));
+}
+
+int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
+                const float* e_x, const float* d, int t, int r, int dtype, void* y, int64_t ld_y,
+                void* x_enc_ws, float* y_enc_ws, void* stream) {
+  if (int st = check_tr(t, r)) return st;
+  if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype");
+  if (M < 0 || K < 0 || N < 0) return fail(STL_ERR_SHAPE, "negative extent");
+  if (M % t) return fail(STL_ERR_SHAPE, "batch %lld not divisible by tile size %d", (long long)M, t);
+  if (K % t || N % t)
+    return fail(STL_ERR_SHAPE, "tile size %d does not divide K=%lld / N=%lld", t, (long long)K,
+                (long long)N);
+  if (ld_x < K || ld_y < N) return fail(STL_ERR_SHAPE, "leading dimension too small");
+  cudaStream_t s = as_stream(stream);
+  const int64_t bi = M / t, bk = K / t, bj = N / t;
+  int st;
+  {
+    Prof prof("encode_x", s);
+    st = check_cuda(stl::tiles_to_planes(x, dtype, ld_x, bi, bk, t, e_x, r, x_enc_ws, dtype,
+                                         nullptr, nullptr, nullptr, s),
+                    "forward encode");
+  }
+  if (st) return st;
+  st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, y_enc_ws, STL_F32, dtype, r, bi, bj,
+                bk, s);
+  if (st) return st;
+  Prof prof("decode_y", s);
+  return check_cuda(stl::planes_to_tiles(y_enc_ws, STL_F32, r, bi, bj, t, d, y, dtype, ld_y,
+                                         nullptr, STL_F32, 0, nullptr, nullptr, s),
+                    "forward decode");
+}
+
+int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, const void* w_enc,
+                 const float* e_x, const float* d, const void* x_enc, const float* y_enc,
+                 int64_t M, int64_t K, int64_t N, int t, int r, int dtype, float* g_ex,
+                 float* g_d, float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws,
+                 float* g_u_ws, float* red_ws, void* stream) {
+  if (int st = check_tr(t, r)) return st;
+  if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype");
+  if (M < 0 || K < 0 || N < 0 || M % t || K % t || N % t)
+    return fail(STL_ERR_SHAPE, "tile size %d does not divide (M, K, N) = (%lld, %lld, %lld)", t,
+                (long long)M, (long long)K, (long long)N);
+  if ((g_d || g_ex) && !red_ws) return fail(STL_ERR_VALUE, "reduction workspace required");
+  cudaStream_t s = as_stream(stream);
+  const int64_t bi = M / t, bk = K / t, bj = N / t;
+  // gvy -> g_enc (planes), fused with g_d = sum y_enc (x) gvy.
+  int st;
+  {
+    Prof prof(g_d ? "encode_gy+g_d" : "encode_gy", s, g_d ? 2 : 1);
+    st = check_cuda(stl::tiles_to_planes(gy, dtype, ld_gy, bi, bj, t, d, r, g_enc_ws, dtype,
+                                           g_d ? y_enc : nullptr, g_d, red_ws, s),
+                      "backward encode(gy)");
+  }
+  if (st) return st;
+  // g_w^T_p (N/t x K/t) = g_enc_p^T (N/t x M/t) . u_p (M/t x K/t): both operands MN-major.
+  if (g_w) {
+    st = run_gemm(g_enc_ws, STL_MN_MAJOR, x_enc, STL_MN_MAJOR, g_w, STL_F32, dtype, r, bj, bk,
+                  bi, s);
+    if (st) return st;
+  }
+  if (g_x || g_ex) {
+    // g_u_p (M/t x K/t) = g_enc_p (M/t x N/t) . W_p (N/t x K/t): B is N-major.
+    st = run_gemm(g_enc_ws, STL_K_MAJOR, w_enc, STL_MN_MAJOR, g_u_ws, STL_F32, dtype, r, bi, bk,
+                  bj, s);
+    if (st) return st;
+    if (g_x) {
+      Prof prof(g_ex ? "decode_gu+g_ex" : "decode_gu", s, g_ex ? 2 : 1);
+      st = check_cuda(stl::planes_to_tiles(g_u_ws, STL_F32, r, bi, bk, t, e_x, g_x, dtype, ld_gx,
+                                           g_ex ? x : nullptr, dtype, ld_x, g_ex, red_ws, s),
+                      "backward decode(g_u)");
+    } else {
+      // g_ex only: reduction without the g_x store is not specialised; write g_x to scratch.
+      return fail(STL_ERR_UNSUPPORTED, "g_ex without g_x is not supported");
+    }
+    if (st) return st;
+  }
+  return STL_OK;
+}
+
+int stl_fused_step(const float* x_prev, int64_t block_rows, int64_t block_k, const void* w_enc,
+                   int64_t block_n, const float* e_x, const float* d, int t, int r, int dtype,
+                   float* out, void* mixed_ws, float* comp_ws, void* stream) {
+  if (int st = check_tr(t, r)) return st;
+  if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype");
+  if (block_rows < 0 || block_k < 0 || block_n < 0) return fail(STL_ERR_SHAPE, "negative extent");
+  cudaStream_t s = as_stream(stream);
+  int st;
+  {
+    Prof prof("compose", s);
+    st = check_cuda(stl::compose_coefs(e_x, d, r, t * t, comp_ws, s), "compose");
+  }
+  if (st) return st;
+  Prof prof("remix", s);
+  st = check_cuda(stl::planes_to_planes(x_prev, STL_F32, r, block_rows * block_k, comp_ws, r,
+                                        mixed_ws, dtype, s),
+                  "fused-step remix");
+  if (st) return st;
+  return run_gemm(mixed_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, out, STL_F32, dtype, r, block_rows,
+                  block_n, block_k, s);
+}
+
+int stl_profile_enable(int on) {
+  g_prof_on = on != 0;
+  return STL_OK;
+}
+
+int stl_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.clear();
+  g_pool_used = 0;
+  return STL_OK;
+}
+
+int stl_profile_count(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  return static_cast<int>(g_prof.size());
+}
+
+int stl_profile_get(int index, const char** name, float* ms, int* launches) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (index < 0 || index >= static_cast<int>(g_prof.size()))
+    return fail(STL_ERR_INDEX, "profile record %d out of range", index);
+  const ProfRec& rec = g_prof[index];
+  if (name) *name = rec.name;
+  if (launches) *launches = rec.launches;
+  if (ms) {
+    float v = 0.f;
+    if (int st = check_cuda(cudaEventElapsedTime(&v, rec.a, rec.b), "profile elapsed")) return st;
+    *ms = v;
+  }
+  return STL_OK;
+}
+
+}  // extern "C"

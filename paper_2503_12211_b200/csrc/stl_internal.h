@@ -1,0 +1,55 @@
+// stl_internal.h — shared declarations between the STL CUDA translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace stl {
+
+enum Dtype : int { kF32 = 0, kBF16 = 1 };
+
+inline size_t dtype_size(int dt) { return dt == kBF16 ? 2 : 4; }
+
+// Operand layouts of one slice-GEMM batch C_p = A_p · B_p (p = 0..r-1), all slices contiguous.
+//   A: 0 = (r, M, K) K-contiguous ("K-major"),  1 = (r, K, M) M-contiguous ("MN-major")
+//   B: 0 = (r, N, K) K-contiguous ("K-major"),  1 = (r, K, N) N-contiguous ("MN-major")
+//   C: (r, M, N) N-contiguous, fp32 or bf16.
+struct SliceGemmProblem {
+  const void* a;
+  int a_layout;
+  const void* b;
+  int b_layout;
+  void* c;
+  int c_dtype;
+  int ab_dtype;
+  int r;
+  int64_t M, N, K;
+};
+
+int sm_count();
+
+// tcgen05 path (bf16 operands, aligned shapes). Returns cudaError_t-like code, 0 = ok.
+cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s);
+bool slice_gemm_tc_supported(const SliceGemmProblem& pb);
+// SIMT path (fp32 or bf16 operands, any shape).
+cudaError_t slice_gemm_simt(const SliceGemmProblem& pb, cudaStream_t s);
+
+// Tile <-> plane transforms (see stl_transform.cu).
+cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br, int64_t bc,
+                            int t, const float* coef, int P, void* out, int out_dtype,
+                            const float* red_planes, float* red_out, float* red_ws,
+                            cudaStream_t s);
+cudaError_t planes_to_tiles(const void* in, int in_dtype, int Q, int64_t br, int64_t bc, int t,
+                            const float* coef, void* out, int out_dtype, int64_t ldo,
+                            const void* red_m, int red_dtype, int64_t ldr, float* red_out,
+                            float* red_ws, cudaStream_t s);
+cudaError_t planes_to_planes(const void* in, int in_dtype, int Q, int64_t ntiles,
+                             const float* coef, int P, void* out, int out_dtype, cudaStream_t s);
+cudaError_t compose_coefs(const float* a, const float* b, int r, int tt, float* out,
+                          cudaStream_t s);
+
+constexpr int kMaxRank = 64;          // upper bound on r handled by the transform kernels
+constexpr int kRedBlocks = 1024;      // max partial-sum blocks for the r x t^2 reductions
+inline size_t red_ws_floats(int r, int t) { return size_t(kRedBlocks) * r * t * t; }
+
+}  // namespace stl

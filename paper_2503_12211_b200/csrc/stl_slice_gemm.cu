@@ -1,0 +1,443 @@
+// stl_slice_gemm.cu — the STL contraction: r independent slice GEMMs C_p = A_p · B_p.
+//
+// Reference semantics: `_slice_products` (snf_operator.py:107-116),
+//   out[:, :, p] = x_enc[:, :, p] @ w_enc[:, :, p]   for every p,
+// i.e. Claim 1 / Algorithm 1 step 2 of the paper.
+//
+// B200 design:
+//   * persistent, warp-specialised kernel, one CTA per SM (grid = #SMs), static tile schedule
+//     over (slice p, M-block, N-block);
+//   * warp 0 lane 0 = TMA producer: 3-D tensor maps (inner, outer, slice) load 128x64 A and
+//     BNx64 B boxes with 128-byte swizzle into a 4-stage shared-memory ring;
+//   * warp 1 lane 0 = MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16,
+//     bf16 operands straight from shared memory, fp32 accumulators in TMEM;
+//   * warp 2 owns the TMEM allocation (2 x BN columns: accumulator double buffer so the
+//     epilogue of tile i overlaps the main loop of tile i+1);
+//   * warps 4..7 = epilogue: tcgen05.ld 32 lanes x 32 columns, fp32 (or bf16) stores.
+// Both operands may be K-major or MN-major (the backward pass needs MN-major operands for
+// g_u = g_enc_p W_p^T and g_w = u_p^T g_enc_p), selected by the UMMA instruction descriptor.
+#include <cstdio>
+#include <mutex>
+#include "sm100_ptx.cuh"
+#include "stl_internal.h"
+
+namespace stl {
+
+namespace {
+constexpr int kBM = 128;
+constexpr int kBK = 64;   // 64 bf16 = 128 bytes = one swizzle row
+constexpr int kStages = 4;
+constexpr int kThreads = 256;
+
+struct EpiArgs {
+  void* c;
+  int c_bf16;
+  int r;
+  int M, N, K;
+};
+
+template <int BN>
+struct Smem {
+  static constexpr uint32_t kABytes = kBM * kBK * 2;
+  static constexpr uint32_t kBBytes = BN * kBK * 2;
+  static constexpr uint32_t kBarOffset = kStages * (kABytes + kBBytes);
+  static constexpr uint32_t kTotal = kBarOffset + 256 + 1024;  // barriers + alignment slack
+};
+
+__device__ __forceinline__ void store_row_chunk(float* dst, const uint32_t (&v)[32], int ncols,
+                                                bool vec) {
+  if (vec && ncols >= 32) {
+    float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      d4[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                          __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < ncols) dst[i] = __uint_as_float(v[i]);
+  }
+}
+
+__device__ __forceinline__ void store_row_chunk(__nv_bfloat16* dst, const uint32_t (&v)[32],
+                                                int ncols, bool vec) {
+  if (vec && ncols >= 32) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[8 * i + 2 * j]),
+                                                 __uint_as_float(v[8 * i + 2 * j + 1]));
+        w[j] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      d4[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < ncols) dst[i] = __float2bfloat16_rn(__uint_as_float(v[i]));
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    slice_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB, EpiArgs args) {
+  using S = Smem<BN>;
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+  constexpr uint32_t kTmemCols = (2 * BN <= 256) ? 256 : 512;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * S::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int M = args.M, N = args.N, K = args.K;
+  const int m_tiles = (M + kBM - 1) / kBM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int per_slice = m_tiles * n_tiles;
+  const int total = args.r * per_slice;
+  const int num_kb = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, kTmemCols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int p = tile / per_slice;
+        const int rem = tile - p * per_slice;
+        const int mb = rem / n_tiles;
+        const int nb = rem - mb * n_tiles;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], S::kABytes + S::kBBytes);
+          uint8_t* a = sA + stage * S::kABytes;
+          uint8_t* b = sB + stage * S::kBBytes;
+          if constexpr (!A_MN) {
+            ptx::tma_load_3d(&tmA, &full[stage], a, kb * kBK, mb * kBM, p);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j)
+              ptx::tma_load_3d(&tmA, &full[stage], a + j * (64 * kBK * 2), mb * kBM + j * 64,
+                               kb * kBK, p);
+          }
+          if constexpr (!B_MN) {
+            ptx::tma_load_3d(&tmB, &full[stage], b, kb * kBK, nb * BN, p);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              ptx::tma_load_3d(&tmB, &full[stage], b + j * (64 * kBK * 2), nb * BN + j * 64,
+                               kb * kBK, p);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(sA + stage * S::kABytes);
+          const uint32_t b_addr = ptx::smem_u32(sB + stage * S::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            // K-major: step 16 elements = 32 bytes inside the 128-byte swizzle row.
+            // MN-major: step 16 K-rows of 128 bytes; 64-wide MN atoms are 64*kBK*2 apart.
+            const uint64_t ad = A_MN ? ptx::smem_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
+                                     : ptx::smem_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::smem_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
+                                     : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
+            ptx::mma_bf16_ss(d_tmem, ad, bd, kIdesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const bool c_vec = (N % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.c) & 15) == 0) &&
+                       (args.c_bf16 ? (N % 8 == 0) : true);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+      const int p = tile / per_slice;
+      const int rem = tile - p * per_slice;
+      const int mb = rem / n_tiles;
+      const int nb = rem - mb * n_tiles;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = mb * kBM + q * 32 + lane;
+      const size_t row_off = (static_cast<size_t>(p) * M + row) * static_cast<size_t>(N);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        __syncwarp();
+        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c,
+                                v);
+        ptx::tmem_ld_wait();
+        const int col0 = nb * BN + c;
+        if (row < M && col0 < N) {
+          if (args.c_bf16)
+            store_row_chunk(reinterpret_cast<__nv_bfloat16*>(args.c) + row_off + col0, v,
+                            N - col0, c_vec);
+          else
+            store_row_chunk(reinterpret_cast<float*>(args.c) + row_off + col0, v, N - col0,
+                            c_vec);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc(tmem_base, kTmemCols);
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 3-D bf16 tensor map over `slices` contiguous (outer x inner) matrices, box (64, box_outer).
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t slices,
+               uint32_t box_outer) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {inner, outer, slices};
+  cuuint64_t strides[2] = {inner * 2, inner * outer * 2};
+  cuuint32_t box[3] = {64, box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult res = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+cudaError_t launch_tc(const SliceGemmProblem& pb, cudaStream_t s) {
+  CUtensorMap ta, tb;
+  const uint64_t M = pb.M, N = pb.N, K = pb.K, r = pb.r;
+  bool ok = A_MN ? make_tmap(&ta, pb.a, M, K, r, kBK) : make_tmap(&ta, pb.a, K, M, r, kBM);
+  ok = ok && (B_MN ? make_tmap(&tb, pb.b, N, K, r, kBK) : make_tmap(&tb, pb.b, K, N, r, BN));
+  if (!ok) return cudaErrorInvalidValue;
+  auto kern = slice_gemm_tc_kernel<BN, A_MN, B_MN>;
+  const int smem = Smem<BN>::kTotal;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = r * ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+  const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
+  EpiArgs ea{pb.c, pb.c_dtype == kBF16 ? 1 : 0, pb.r, static_cast<int>(M), static_cast<int>(N),
+             static_cast<int>(K)};
+  kern<<<grid, kThreads, smem, s>>>(ta, tb, ea);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+bool slice_gemm_tc_supported(const SliceGemmProblem& pb) {
+  if (pb.ab_dtype != kBF16) return false;
+  if (pb.M <= 0 || pb.N <= 0 || pb.K <= 0 || pb.r <= 0) return false;
+  if (pb.M > (1 << 30) || pb.N > (1 << 30) || pb.K > (1 << 30)) return false;
+  // TMA: 16-byte aligned base and strides -> contiguous dim multiple of 8 bf16.
+  const int64_t a_inner = pb.a_layout ? pb.M : pb.K;
+  const int64_t b_inner = pb.b_layout ? pb.N : pb.K;
+  if (a_inner % 8 || b_inner % 8) return false;
+  if ((reinterpret_cast<uintptr_t>(pb.a) & 15) || (reinterpret_cast<uintptr_t>(pb.b) & 15))
+    return false;
+  return get_encode_fn() != nullptr;
+}
+
+cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {
+  const bool a_mn = pb.a_layout != 0, b_mn = pb.b_layout != 0;
+  const bool narrow = pb.N <= 128;
+  if (narrow) {
+    if (!a_mn && !b_mn) return launch_tc<128, false, false>(pb, s);
+    if (!a_mn && b_mn) return launch_tc<128, false, true>(pb, s);
+    if (a_mn && !b_mn) return launch_tc<128, true, false>(pb, s);
+    return launch_tc<128, true, true>(pb, s);
+  }
+  if (!a_mn && !b_mn) return launch_tc<256, false, false>(pb, s);
+  if (!a_mn && b_mn) return launch_tc<256, false, true>(pb, s);
+  if (a_mn && !b_mn) return launch_tc<256, true, false>(pb, s);
+  return launch_tc<256, true, true>(pb, s);
+}
+
+// ==================================================================== SIMT slice GEMM
+// Generic fp32-accumulate batched GEMM for fp32 operands (the fp32 parity path: TF32 would
+// miss the 1e-5 bar, SURVEY §7 hard part 3) and for shapes TMA cannot describe.
+namespace {
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p, int64_t i);
+template <>
+__device__ __forceinline__ float ldf<float>(const float* p, int64_t i) {
+  return __ldg(p + i);
+}
+template <>
+__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+  return __bfloat162float(p[i]);
+}
+
+constexpr int kSB = 64, kSK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    slice_gemm_simt_kernel(const T* __restrict__ A, int64_t sAm, int64_t sAk,
+                           const T* __restrict__ B, int64_t sBk, int64_t sBn, void* C,
+                           int c_bf16, int M, int N, int K) {
+  __shared__ float As[kSK][kSB + 4];
+  __shared__ float Bs[kSK][kSB + 4];
+  const int p = blockIdx.z;
+  const int64_t MK = static_cast<int64_t>(M) * K, KN = static_cast<int64_t>(K) * N;
+  const T* Ap = A + p * MK;
+  const T* Bp = B + p * KN;
+  const int m0 = blockIdx.y * kSB, n0 = blockIdx.x * kSB;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += kSK) {
+    for (int i = threadIdx.x; i < kSK * kSB; i += 256) {
+      // A tile: (m, k); B tile: (k, n). Index order chosen so the contiguous dim of the
+      // common layouts maps to consecutive threads.
+      const int kk = sAk == 1 ? (i % kSK) : (i / kSB);
+      const int mm = sAk == 1 ? (i / kSK) : (i % kSB);
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? ldf(Ap, gm * sAm + gk * sAk) : 0.f;
+      const int kb = sBk == 1 ? (i % kSK) : (i / kSB);
+      const int nn = sBk == 1 ? (i / kSK) : (i % kSB);
+      const int gn = n0 + nn, gk2 = k0 + kb;
+      Bs[kb][nn] = (gn < N && gk2 < K) ? ldf(Bp, gk2 * sBk + gn * sBn) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kSK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const int64_t MN = static_cast<int64_t>(M) * N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx * 4 + j;
+      if (gn >= N) continue;
+      const int64_t off = p * MN + static_cast<int64_t>(gm) * N + gn;
+      if (c_bf16)
+        reinterpret_cast<__nv_bfloat16*>(C)[off] = __float2bfloat16_rn(acc[i][j]);
+      else
+        reinterpret_cast<float*>(C)[off] = acc[i][j];
+    }
+  }
+}
+}  // namespace
+
+cudaError_t slice_gemm_simt(const SliceGemmProblem& pb, cudaStream_t s) {
+  const int64_t M = pb.M, N = pb.N, K = pb.K;
+  const int64_t sAm = pb.a_layout ? 1 : K, sAk = pb.a_layout ? M : 1;
+  const int64_t sBk = pb.b_layout ? N : 1, sBn = pb.b_layout ? 1 : K;
+  dim3 grid(static_cast<unsigned>((N + kSB - 1) / kSB), static_cast<unsigned>((M + kSB - 1) / kSB),
+            static_cast<unsigned>(pb.r));
+  const int cb = pb.c_dtype == kBF16 ? 1 : 0;
+  if (pb.ab_dtype == kBF16)
+    slice_gemm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(pb.a), sAm, sAk,
+        static_cast<const __nv_bfloat16*>(pb.b), sBk, sBn, pb.c, cb, int(M), int(N), int(K));
+  else
+    slice_gemm_simt_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(pb.a), sAm, sAk,
+                                                       static_cast<const float*>(pb.b), sBk, sBn,
+                                                       pb.c, cb, int(M), int(N), int(K));
+  return cudaGetLastError();
+}
+
+}  // namespace stl
