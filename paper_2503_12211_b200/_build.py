@@ -18,7 +18,7 @@ CSRC = PKG / "csrc"
 LIB_NAME = "libstl_b200.so"
 LIB_PATH = PKG / LIB_NAME
 
-SOURCES = ["stl_capi.cu", "stl_slice_gemm.cu", "stl_transform.cu"]
+SOURCES = ["stl_capi.cu", "stl_slice_gemm.cu", "stl_transform.cu", "stl_transform4.cu"]
 HEADERS = ["sm100_ptx.cuh", "stl_internal.h"]
 
 NVCC_FLAGS = [

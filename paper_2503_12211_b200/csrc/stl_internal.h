@@ -45,6 +45,15 @@ cudaError_t planes_to_tiles(const void* in, int in_dtype, int Q, int64_t br, int
                             float* red_ws, cudaStream_t s);
 cudaError_t planes_to_planes(const void* in, int in_dtype, int Q, int64_t ntiles,
                              const float* coef, int P, void* out, int out_dtype, cudaStream_t s);
+// t = 4 vectorised fast paths (stl_transform4.cu); cudaErrorNotSupported -> use generic.
+cudaError_t tiles_to_planes4(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
+                             const float* coef, int P, void* out, int odt, const float* rp,
+                             float* ro, float* rw, cudaStream_t s);
+cudaError_t planes_to_tiles4(const void* in, int idt, int Q, int64_t br, int64_t bc,
+                             const float* coef, void* out, int odt, int64_t ldo, const void* rm,
+                             int rdt, int64_t ldr, float* ro, float* rw, cudaStream_t s);
+// out[o] = sum_b partial[b * n + o], deterministic fixed-order tree.
+cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t s);
 cudaError_t compose_coefs(const float* a, const float* b, int r, int tt, float* out,
                           cudaStream_t s);
 

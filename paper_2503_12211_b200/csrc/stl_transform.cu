@@ -261,16 +261,6 @@ __global__ void __launch_bounds__(kTB)
   }
 }
 
-// out[o] = sum_b partial[b][o] in fixed block order (deterministic).
-__global__ void k_sum_partials(const float* __restrict__ partial, int nblocks, int n,
-                               float* __restrict__ out) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= n) return;
-  float s = 0.f;
-  for (int b = 0; b < nblocks; ++b) s += partial[static_cast<int64_t>(b) * n + o];
-  out[o] = s;
-}
-
 // out (r x r) = a (r x tt) . b^T (b is r x tt):  the fused-step composite e_x @ d.T.
 __global__ void k_compose(const float* __restrict__ a, const float* __restrict__ b, int r, int tt,
                           float* __restrict__ out) {
@@ -304,7 +294,7 @@ cudaError_t t2p_launch(const void* m, int64_t ldm, int64_t br, int64_t bc, const
     if (e != cudaSuccess) return e;
     k<<<grid, kTB, smem, s>>>(static_cast<const Tin*>(m), ldm, br, bc, coef, P,
                               static_cast<Tout*>(out), red_planes, red_ws, vec);
-    k_sum_partials<<<(P * TT + 127) / 128, 128, 0, s>>>(red_ws, grid, P * TT, red_out);
+    if (cudaError_t e2 = sum_partials(red_ws, grid, P * TT, red_out, s)) return e2;
   } else {
     const int grid = grid_for(ntiles, sm_count() * 16);
     const size_t smem = sizeof(float) * P * TT;
@@ -332,7 +322,7 @@ cudaError_t p2t_launch(const void* in, int Q, int64_t br, int64_t bc, const floa
     k<<<grid, kTB, smem, s>>>(static_cast<const Tin*>(in), Q, br, bc, coef,
                               static_cast<Tout*>(out), ldo, static_cast<const Tr*>(red_m), ldr,
                               red_ws, vo, vr);
-    k_sum_partials<<<(Q * TT + 127) / 128, 128, 0, s>>>(red_ws, grid, Q * TT, red_out);
+    if (cudaError_t e2 = sum_partials(red_ws, grid, Q * TT, red_out, s)) return e2;
   } else {
     const int grid = grid_for(ntiles, sm_count() * 16);
     const size_t smem = sizeof(float) * Q * TT;
@@ -385,6 +375,11 @@ cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br,
                             const float* red_planes, float* red_out, float* red_ws,
                             cudaStream_t s) {
   if (br * bc == 0) return cudaSuccess;
+  if (t == 4) {
+    cudaError_t e = tiles_to_planes4(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes,
+                                     red_out, red_ws, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (t) {
     case 1: return t2p_dispatch<1>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_out, red_ws, s);
     case 2: return t2p_dispatch<2>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_out, red_ws, s);
@@ -399,6 +394,11 @@ cudaError_t planes_to_tiles(const void* in, int in_dtype, int Q, int64_t br, int
                             const void* red_m, int red_dtype, int64_t ldr, float* red_out,
                             float* red_ws, cudaStream_t s) {
   if (br * bc == 0) return cudaSuccess;
+  if (t == 4) {
+    cudaError_t e = planes_to_tiles4(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m,
+                                     red_dtype, ldr, red_out, red_ws, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (t) {
     case 1: return p2t_dispatch<1>(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m, red_dtype, ldr, red_out, red_ws, s);
     case 2: return p2t_dispatch<2>(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m, red_dtype, ldr, red_out, red_ws, s);
