@@ -17,6 +17,7 @@
 // Both operands may be K-major or MN-major (the backward pass needs MN-major operands for
 // g_u = g_enc_p W_p^T and g_w = u_p^T g_enc_p), selected by the UMMA instruction descriptor.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include "sm100_ptx.cuh"
 #include "stl_internal.h"
@@ -249,6 +250,195 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) ptx::tmem_dealloc(tmem_base, kTmemCols);
 }
 
+
+// ==================================================================== CTA-pair variant
+// cta_group::2: a cluster of 2 CTAs (one TPC) computes a 256 x BN tile. Each CTA stages its
+// 128 rows of A and its BN/2 columns of B (half the B bytes per SM of the 1-CTA kernel, and
+// 32 KB stages -> a 6-deep ring); the even CTA issues tcgen05.mma.cta_group::2 for both, and
+// each CTA's epilogue drains its own 128 TMEM lanes.
+template <int BN>
+struct Smem2 {
+  static constexpr int kStages = BN == 256 ? 6 : 8;
+  static constexpr uint32_t kABytes = 128 * kBK * 2;
+  static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
+  static constexpr uint32_t kBarOffset = kStages * (kABytes + kBBytes);
+  static constexpr uint32_t kTotal = kBarOffset + 512 + 1024;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    slice_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA,
+                          const __grid_constant__ CUtensorMap tmB, EpiArgs args) {
+  using S = Smem2<BN>;
+  constexpr int kSt = S::kStages;
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(256, BN, A_MN, B_MN);
+  constexpr uint32_t kTmemCols = (2 * BN <= 256) ? 256 : 512;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kSt * S::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty = full + kSt;
+  uint64_t* tfull = empty + kSt;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int M = args.M, N = args.N, K = args.K;
+  const int m_tiles = (M + 255) / 256;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int per_slice = m_tiles * n_tiles;
+  const int total = args.r * per_slice;
+  const int num_kb = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kSt; ++s) {
+      ptx::mbar_init(&full[s], 2);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 8);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, kTmemCols);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < total; tile += nclusters) {
+        const int p = tile / per_slice;
+        const int rem = tile - p * per_slice;
+        const int mb = rem / n_tiles;
+        const int nb = rem - mb * n_tiles;
+        const int m0 = mb * 256 + static_cast<int>(rank) * 128;
+        const int n0 = nb * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (S::kABytes + S::kBBytes));
+          uint8_t* a = sA + stage * S::kABytes;
+          uint8_t* b = sB + stage * S::kBBytes;
+          if constexpr (!A_MN) {
+            ptx::tma_load_3d_2sm(&tmA, &full[stage], a, kb * kBK, m0, p);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              ptx::tma_load_3d_2sm(&tmA, &full[stage], a + j * (64 * kBK * 2), m0 + j * 64,
+                                   kb * kBK, p);
+          }
+          if constexpr (!B_MN) {
+            ptx::tma_load_3d_2sm(&tmB, &full[stage], b, kb * kBK, n0, p);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 128; ++j)
+              ptx::tma_load_3d_2sm(&tmB, &full[stage], b + j * (64 * kBK * 2), n0 + j * 64,
+                                   kb * kBK, p);
+          }
+          if (!leader) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0));
+          if (++stage == kSt) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ------------------------------------------------------------ MMA issuer (even CTA)
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = cluster; tile < total; tile += nclusters, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(sA + stage * S::kABytes);
+          const uint32_t b_addr = ptx::smem_u32(sB + stage * S::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = A_MN ? ptx::smem_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
+                                     : ptx::smem_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::smem_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
+                                     : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
+            ptx::mma_bf16_ss_2sm(d_tmem, ad, bd, kIdesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          ptx::mma_commit_2sm(&empty[stage]);
+          if (++stage == kSt) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit_2sm(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue (both CTAs)
+    const int q = warp & 3;
+    const bool c_vec = (N % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.c) & 15) == 0) &&
+                       (args.c_bf16 ? (N % 8 == 0) : true);
+    int it = 0;
+    for (int tile = cluster; tile < total; tile += nclusters, ++it) {
+      const int p = tile / per_slice;
+      const int rem = tile - p * per_slice;
+      const int mb = rem / n_tiles;
+      const int nb = rem - mb * n_tiles;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = mb * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
+      const size_t row_off = (static_cast<size_t>(p) * M + row) * static_cast<size_t>(N);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        __syncwarp();
+        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c,
+                                v);
+        ptx::tmem_ld_wait();
+        const int col0 = nb * BN + c;
+        if (row < M && col0 < N) {
+          if (args.c_bf16)
+            store_row_chunk(reinterpret_cast<__nv_bfloat16*>(args.c) + row_off + col0, v,
+                            N - col0, c_vec);
+          else
+            store_row_chunk(reinterpret_cast<float*>(args.c) + row_off + col0, v, N - col0,
+                            c_vec);
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, kTmemCols);
+}
+
 // ------------------------------------------------------------------ host side
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -303,6 +493,27 @@ cudaError_t launch_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+
+template <int BN, bool A_MN, bool B_MN>
+cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
+  CUtensorMap ta, tb;
+  const uint64_t M = pb.M, N = pb.N, K = pb.K, r = pb.r;
+  bool ok = A_MN ? make_tmap(&ta, pb.a, M, K, r, kBK) : make_tmap(&ta, pb.a, K, M, r, 128);
+  ok = ok && (B_MN ? make_tmap(&tb, pb.b, N, K, r, kBK) : make_tmap(&tb, pb.b, K, N, r, BN / 2));
+  if (!ok) return cudaErrorInvalidValue;
+  auto kern = slice_gemm_tc2_kernel<BN, A_MN, B_MN>;
+  const int smem = Smem2<BN>::kTotal;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = r * ((M + 255) / 256) * ((N + BN - 1) / BN);
+  const int pairs = sm_count() / 2;
+  const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
+  EpiArgs ea{pb.c, pb.c_dtype == kBF16 ? 1 : 0, pb.r, static_cast<int>(M), static_cast<int>(N),
+             static_cast<int>(K)};
+  kern<<<grid, kThreads, smem, s>>>(ta, tb, ea);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 int sm_count() {
@@ -331,6 +542,22 @@ bool slice_gemm_tc_supported(const SliceGemmProblem& pb) {
 
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   const bool a_mn = pb.a_layout != 0, b_mn = pb.b_layout != 0;
+  static const int force1 = [] {
+    const char* e = getenv("STL_GEMM_1CTA");
+    return e ? atoi(e) : 0;
+  }();
+  if (pb.M > 128 && !force1) {
+    if (pb.N <= 128) {
+      if (!a_mn && !b_mn) return launch_tc2<128, false, false>(pb, s);
+      if (!a_mn && b_mn) return launch_tc2<128, false, true>(pb, s);
+      if (a_mn && !b_mn) return launch_tc2<128, true, false>(pb, s);
+      return launch_tc2<128, true, true>(pb, s);
+    }
+    if (!a_mn && !b_mn) return launch_tc2<256, false, false>(pb, s);
+    if (!a_mn && b_mn) return launch_tc2<256, false, true>(pb, s);
+    if (a_mn && !b_mn) return launch_tc2<256, true, false>(pb, s);
+    return launch_tc2<256, true, true>(pb, s);
+  }
   const bool narrow = pb.N <= 128;
   if (narrow) {
     if (!a_mn && !b_mn) return launch_tc<128, false, false>(pb, s);

@@ -17,6 +17,7 @@ namespace stl {
 namespace {
 
 constexpr int kThreads4 = 128;
+constexpr int kChunk = 8;                      // planes loaded per batch
 constexpr int kStageTiles = 128;               // tiles per warp per reduction round
 constexpr int kStageStride = kStageTiles + 8;  // bf16 elements per staged row (conflict-free)
 
@@ -280,10 +281,19 @@ __global__ void __launch_bounds__(kThreads4)
         for (int c = 0; c < 16; ++c) x[t][c] = 0.f;
     }
     if constexpr (RED) {
-      for (int p = 0; p < P; ++p) {
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (valid) Vec4<float>::load(red_planes + p * ntiles + off, v);
-        R.stage_plane(p, v);
+      for (int p0 = 0; p0 < P; p0 += kChunk) {
+        float v[kChunk][4];
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          if (valid && p0 + j < P) {
+            Vec4<float>::load(red_planes + (p0 + j) * ntiles + off, v[j]);
+          } else {
+            v[j][0] = v[j][1] = v[j][2] = v[j][3] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j)
+          if (p0 + j < P) R.stage_plane(p0 + j, v[j]);
       }
       R.stage_tiles(x);
       R.accumulate();
@@ -323,20 +333,33 @@ __global__ void __launch_bounds__(kThreads4)
       for (int t = 0; t < 4; ++t)
 #pragma unroll
         for (int c = 0; c < 16; ++c) acc[t][c] = 0.f;
-#pragma unroll 4
-      for (int q = 0; q < Q; ++q) {
-        float v[4];
-        Vec4<Tin>::load(in + q * ntiles + off, v);
-        if constexpr (RED) R.stage_plane(q, v);
-        const float4* cp = reinterpret_cast<const float4*>(sc + q * 16);
+      // Planes are consumed in chunks of kChunk: all loads of a chunk are issued before any
+      // use, so each thread keeps kChunk x 16 bytes in flight.
+      for (int q0 = 0; q0 < Q; q0 += kChunk) {
+        float v[kChunk][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 c4 = cp[i];
-          const float cf[4] = {c4.x, c4.y, c4.z, c4.w};
+        for (int j = 0; j < kChunk; ++j) {
+          if (q0 + j < Q) {
+            Vec4<Tin>::load(in + (q0 + j) * ntiles + off, v[j]);
+          } else {
+            v[j][0] = v[j][1] = v[j][2] = v[j][3] = 0.f;
+          }
+        }
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < kChunk; ++j) {
+          if (q0 + j >= Q) break;
+          if constexpr (RED) R.stage_plane(q0 + j, v[j]);
+          const float4* cp = reinterpret_cast<const float4*>(sc + (q0 + j) * 16);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) acc[t][4 * i + j] = fmaf(cf[j], v[t], acc[t][4 * i + j]);
+          for (int i = 0; i < 4; ++i) {
+            const float4 c4 = cp[i];
+            const float cf[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                acc[t][4 * i + jj] = fmaf(cf[jj], v[j][t], acc[t][4 * i + jj]);
+          }
         }
       }
       Tout* dst = out + I * 4 * ldo + J0 * 4;
