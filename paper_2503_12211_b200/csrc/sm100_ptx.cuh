@@ -170,9 +170,10 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(saddr), "r"(rank));
   return out;
 }
+// Remote arrive (default .release.cta semantics: no GPU-scope fence is emitted; TMA data is
+// tracked by transaction bytes and TMEM reads by tcgen05.wait::ld, so no release is needed).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA load: both CTAs of the pair issue it; transaction bytes land on the even CTA's
 // mbarrier (peer bit of the barrier address cleared), data lands in the issuing CTA's smem.
