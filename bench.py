@@ -221,7 +221,9 @@ def main() -> None:
 
     bi, bk, bj = M // T, K // T, N // T
     u = torch.empty((R, bi, bk), dtype=torch.bfloat16, device=dev)
-    y_enc = torch.empty((R, bi, bj), dtype=torch.float32, device=dev)
+    y_enc = torch.empty((R, bi, bj), dtype=torch.bfloat16, device=dev)
+    fwd_scratch = torch.empty((int(lib.stl_forward_scratch_bytes(M, K, N, T, R, _lib.STL_BF16)),),
+                              dtype=torch.uint8, device=dev)
     y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
     grads = torch.empty((R * bj * bk + 2 * R * T * T,), dtype=torch.float32, device=dev)
     g_w = grads[: R * bj * bk].view(R, bj, bk)
@@ -237,7 +239,8 @@ def main() -> None:
     def stl_step(allreduce: bool):
         _lib.check(lib.stl_forward(x.data_ptr(), M, K, K, w_planes.data_ptr(), N,
                                    snf.e_x.data_ptr(), snf.d.data_ptr(), T, R, _lib.STL_BF16,
-                                   y.data_ptr(), N, u.data_ptr(), y_enc.data_ptr(), stream))
+                                   y.data_ptr(), N, u.data_ptr(), y_enc.data_ptr(),
+                                   fwd_scratch.data_ptr(), fwd_scratch.numel(), stream))
         _lib.check(lib.stl_backward(gy.data_ptr(), N, x.data_ptr(), K, w_planes.data_ptr(),
                                     snf.e_x.data_ptr(), snf.d.data_ptr(), u.data_ptr(),
                                     y_enc.data_ptr(), M, K, N, T, R, _lib.STL_BF16,
@@ -357,7 +360,8 @@ def main() -> None:
             dtype=torch.bfloat16)
         xf = torch.randn((n3, n3), device=dev).to(torch.bfloat16)
         uf = torch.empty((R, n3 // T, n3 // T), dtype=torch.bfloat16, device=dev)
-        yef = torch.empty((R, n3 // T, n3 // T), dtype=torch.float32, device=dev)
+        sf = torch.empty((int(lib.stl_forward_scratch_bytes(n3, n3, n3, T, R, _lib.STL_BF16)),),
+                         dtype=torch.uint8, device=dev)
         yf = torch.empty((n3, n3), dtype=torch.bfloat16, device=dev)
         wdf = torch.randn((n3, n3), device=dev).to(torch.bfloat16)
         ydf = torch.empty((n3, n3), device=dev, dtype=torch.bfloat16)
@@ -365,7 +369,8 @@ def main() -> None:
         def fwd8192():
             _lib.check(lib.stl_forward(xf.data_ptr(), n3, n3, n3, wf.data_ptr(), n3,
                                        snf.e_x.data_ptr(), snf.d.data_ptr(), T, R, _lib.STL_BF16,
-                                       yf.data_ptr(), n3, uf.data_ptr(), yef.data_ptr(), stream))
+                                       yf.data_ptr(), n3, uf.data_ptr(), None, sf.data_ptr(),
+                                       sf.numel(), stream))
 
         steps_f = max(args.steps // 2, 10)
         for _ in range(args.warmup):
@@ -373,7 +378,8 @@ def main() -> None:
             torch.matmul(xf, wdf, out=ydf)
         stl_f = timed(fwd8192, steps_f, profile=True) / steps_f
         recs_f = _lib.profile_records()
-        gemm_f = [ms for name, ms, _ in recs_f if name == "slice_gemm_tcgen05"]
+        gemm_f = [ms for name, ms, _ in recs_f
+                  if name in ("slice_gemm_tcgen05", "slice_gemm_decode_fused")]
         cub_f = timed(lambda: torch.matmul(xf, wdf, out=ydf), steps_f) / steps_f
         cost_f = stl.LayerCost(n3, n3, n3, T, R, 2)
         gf_ms = sum(gemm_f) / max(len(gemm_f), 1)
@@ -383,7 +389,7 @@ def main() -> None:
             "gemm_ms": gf_ms, "gemm_tflops": cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12,
             "gemm_frac_of_burst": cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12 / peaks["bf16_burst"],
         }
-        del wf, xf, uf, yef, yf, wdf, ydf
+        del wf, xf, uf, sf, yf, wdf, ydf
         torch.cuda.empty_cache()
 
         # ---- e2e: public API (StlLinear autograd) with pinned host inputs, copies timed

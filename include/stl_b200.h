@@ -94,13 +94,23 @@ STL_API int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_lay
  * stl_batched (snf_operator.py:156-172) / stl_layer_forward + _layer_forward_cached
  * (toy_network.py:74-92):  y = decode(slice_products(encode(x, e_x), w_enc), d).
  *   x: (M, K) ld_x, dtype;  w_enc: planes (r, N/t, K/t) of dtype;  y: (M, N) ld_y, dtype.
- *   x_enc_ws: planes (r, M/t, K/t) of dtype (the cache `u`);
- *   y_enc_ws: fp32 planes (r, M/t, N/t) (the cache `y_enc`).
+ *   x_enc_ws: planes (r, M/t, K/t) of dtype (also the cache `u`);
+ *   y_enc_cache: NULL, or planes (r, M/t, N/t) of dtype receiving the slice products (the
+ *                cache `y_enc` for stl_backward; fp32 in fp32 mode, bf16 in bf16 mode);
+ *   scratch: device workspace of at least stl_forward_scratch_bytes(...) bytes.
  *   M, K, N must be multiples of t (ShapeError otherwise, as the reference).
+ * bf16 with t = 4 runs the decode-fused tcgen05 kernel (slice products stay in L2); other
+ * cases run encode -> slice GEMM -> decode with fp32 slice products in `scratch`.
  */
+STL_API int64_t stl_forward_scratch_bytes(int64_t M, int64_t K, int64_t N, int t, int r,
+                                          int dtype);
 STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
                 const float* e_x, const float* d, int t, int r, int dtype, void* y, int64_t ld_y,
-                void* x_enc_ws, float* y_enc_ws, void* stream);
+                void* x_enc_ws, void* y_enc_cache, void* scratch, int64_t scratch_bytes,
+                void* stream);
+
+/* Enable (1, default) or disable (0) the decode-fused kernels (A/B testing). Host-only. */
+STL_API int stl_set_fusion(int enabled);
 
 /*
  * _layer_backward (toy_network.py:95-106), all seven formulas:
@@ -111,11 +121,12 @@ STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const
  *   g_ex = sum_{I,L} g_u[I,L,p] vx[I,L,c]          -> g_ex fp32 (r, t*t)
  *   g_x  = untile(g_u @ e_x)                       -> g_x (M, K) ld_gx, dtype
  * Inputs: gy (M, N) ld_gy; x (M, K) ld_x (the layer input, vx); w_enc as in stl_forward;
- * x_enc (= u) and y_enc from the forward cache. red_ws: stl_reduce_workspace_floats floats.
+ * x_enc (= u) and y_enc (planes of dtype) from the forward cache. red_ws:
+ * stl_reduce_workspace_floats floats.
  * Any of g_ex, g_d, g_w, g_x may be NULL to skip that gradient.
  */
 STL_API int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, const void* w_enc,
-                 const float* e_x, const float* d, const void* x_enc, const float* y_enc,
+                 const float* e_x, const float* d, const void* x_enc, const void* y_enc,
                  int64_t M, int64_t K, int64_t N, int t, int r, int dtype, float* g_ex,
                  float* g_d, float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws,
                  float* g_u_ws, float* red_ws, void* stream);

@@ -32,8 +32,11 @@ SIGNATURES = {
                     c_int64, c_void_p], c_int),
     "stl_slice_gemm": ([c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_int, c_int,
                         c_int64, c_int64, c_int64, c_void_p], c_int),
+    "stl_forward_scratch_bytes": ([c_int64, c_int64, c_int64, c_int, c_int, c_int], c_int64),
     "stl_forward": ([c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
-                     c_int, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p], c_int),
+                     c_int, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                     c_int64, c_void_p], c_int),
+    "stl_set_fusion": ([c_int], c_int),
     "stl_backward": ([c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                       c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_int,
                       c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,

@@ -110,7 +110,7 @@ int stl_encode(const void* m, int dtype_in, int64_t rows, int64_t cols, int64_t 
   if (ld_m < cols) return fail(STL_ERR_SHAPE, "leading dimension %lld < cols %lld",
                                (long long)ld_m, (long long)cols);
   return check_cuda(stl::tiles_to_planes(m, dtype_in, ld_m, rows / t, cols / t, t, encoder, r,
-                                         out, dtype_out, nullptr, nullptr, nullptr,
+                                         out, dtype_out, nullptr, STL_F32, nullptr, nullptr,
                                          as_stream(stream)),
                     "encode");
 }
@@ -139,9 +139,31 @@ int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_layout, voi
   return run_gemm(a, a_layout, b, b_layout, c, dtype_c, dtype_ab, r, M, N, K, as_stream(stream));
 }
 
+namespace {
+bool g_fusion = true;
+
+bool fused_forward_shape(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
+  if (!g_fusion || t != 4 || dtype != STL_BF16) return false;
+  return stl::fused_decode_supported(t, r, M / t, N / t, K / t, dtype, nullptr, nullptr, 0);
+}
+}  // namespace
+
+int stl_set_fusion(int enabled) {
+  g_fusion = enabled != 0;
+  return STL_OK;
+}
+
+int64_t stl_forward_scratch_bytes(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
+  if (t < 1 || r < 1 || M < 0 || K < 0 || N < 0) return 0;
+  if (fused_forward_shape(M, K, N, t, r, dtype))
+    return static_cast<int64_t>(stl::fused_decode_scratch_bytes(r, M / t, N / t));
+  return static_cast<int64_t>(r) * (M / t) * (N / t) * 4;
+}
+
 int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
                 const float* e_x, const float* d, int t, int r, int dtype, void* y, int64_t ld_y,
-                void* x_enc_ws, float* y_enc_ws, void* stream) {
+                void* x_enc_ws, void* y_enc_cache, void* scratch, int64_t scratch_bytes,
+                void* stream) {
   if (int st = check_tr(t, r)) return st;
   if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype");
   if (M < 0 || K < 0 || N < 0) return fail(STL_ERR_SHAPE, "negative extent");
@@ -152,25 +174,57 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
   if (ld_x < K || ld_y < N) return fail(STL_ERR_SHAPE, "leading dimension too small");
   cudaStream_t s = as_stream(stream);
   const int64_t bi = M / t, bk = K / t, bj = N / t;
+  if (M == 0 || N == 0) return STL_OK;
   int st;
   {
     Prof prof("encode_x", s);
     st = check_cuda(stl::tiles_to_planes(x, dtype, ld_x, bi, bk, t, e_x, r, x_enc_ws, dtype,
-                                         nullptr, nullptr, nullptr, s),
+                                         nullptr, STL_F32, nullptr, nullptr, s),
                     "forward encode");
   }
   if (st) return st;
-  st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, y_enc_ws, STL_F32, dtype, r, bi, bj,
-                bk, s);
+  const bool fused = fused_forward_shape(M, K, N, t, r, dtype) && bk > 0 && ld_y % 8 == 0 &&
+                     (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
+                     stl::fused_decode_supported(t, r, bi, bj, bk, dtype, x_enc_ws, w_enc, 0);
+  if (fused) {
+    const size_t need = stl::fused_decode_scratch_bytes(r, bi, bj);
+    if (scratch_bytes < static_cast<int64_t>(need))
+      return fail(STL_ERR_VALUE, "scratch too small: %lld < %lld bytes", (long long)scratch_bytes,
+                  (long long)need);
+    Prof prof("slice_gemm_decode_fused", s);
+    return check_cuda(stl::fused_gemm_decode(x_enc_ws, w_enc, STL_K_MAJOR, r, bi, bj, bk, d, y,
+                                             ld_y, dtype, y_enc_cache, dtype, scratch, s),
+                      "fused forward");
+  }
+  float* yenc = nullptr;
+  if (dtype == STL_F32 && y_enc_cache) {
+    yenc = static_cast<float*>(y_enc_cache);
+  } else {
+    const int64_t need = static_cast<int64_t>(r) * bi * bj * 4;
+    if (scratch_bytes < need)
+      return fail(STL_ERR_VALUE, "scratch too small: %lld < %lld bytes", (long long)scratch_bytes,
+                  (long long)need);
+    yenc = static_cast<float*>(scratch);
+  }
+  st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, yenc, STL_F32, dtype, r, bi, bj, bk, s);
   if (st) return st;
-  Prof prof("decode_y", s);
-  return check_cuda(stl::planes_to_tiles(y_enc_ws, STL_F32, r, bi, bj, t, d, y, dtype, ld_y,
-                                         nullptr, STL_F32, 0, nullptr, nullptr, s),
+  {
+    Prof prof("decode_y", s);
+    st = check_cuda(stl::planes_to_tiles(yenc, STL_F32, r, bi, bj, t, d, y, dtype, ld_y, nullptr,
+                                         STL_F32, 0, nullptr, nullptr, s),
                     "forward decode");
+  }
+  if (st) return st;
+  if (y_enc_cache && dtype == STL_BF16) {
+    Prof prof("cache_cast", s);
+    st = check_cuda(stl::cast_f32_to_bf16(yenc, y_enc_cache, static_cast<int64_t>(r) * bi * bj, s),
+                    "cache cast");
+  }
+  return st;
 }
 
 int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, const void* w_enc,
-                 const float* e_x, const float* d, const void* x_enc, const float* y_enc,
+                 const float* e_x, const float* d, const void* x_enc, const void* y_enc,
                  int64_t M, int64_t K, int64_t N, int t, int r, int dtype, float* g_ex,
                  float* g_d, float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws,
                  float* g_u_ws, float* red_ws, void* stream) {
@@ -187,7 +241,7 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
   {
     Prof prof(g_d ? "encode_gy+g_d" : "encode_gy", s, g_d ? 2 : 1);
     st = check_cuda(stl::tiles_to_planes(gy, dtype, ld_gy, bi, bj, t, d, r, g_enc_ws, dtype,
-                                           g_d ? y_enc : nullptr, g_d, red_ws, s),
+                                           g_d ? y_enc : nullptr, dtype, g_d, red_ws, s),
                       "backward encode(gy)");
   }
   if (st) return st;

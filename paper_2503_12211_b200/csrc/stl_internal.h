@@ -1,6 +1,7 @@
 // stl_internal.h — shared declarations between the STL CUDA translation units.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -28,6 +29,20 @@ struct SliceGemmProblem {
 
 int sm_count();
 
+// 3-D bf16 tensor map over `slices` contiguous (outer x inner) matrices, 128B swizzle.
+bool make_bf16_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t slices, uint32_t box_inner, uint32_t box_outer);
+
+// Decode-fused slice GEMM (stl_fused_gemm.cu): y = decode(A_p . B_p, dec), t = 4, bf16.
+bool fused_decode_supported(int t, int r, int64_t M, int64_t N, int64_t K, int ab_dtype,
+                            const void* a, const void* b, int b_layout);
+size_t fused_decode_scratch_bytes(int r, int64_t M, int64_t N);
+cudaError_t fused_gemm_decode(const void* a, const void* b, int b_layout, int r, int64_t M,
+                              int64_t N, int64_t K, const float* dec, void* y, int64_t ldy,
+                              int y_dtype, void* cache, int cache_dtype, void* scratch,
+                              cudaStream_t s);
+cudaError_t cast_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s);
+
 // tcgen05 path (bf16 operands, aligned shapes). Returns cudaError_t-like code, 0 = ok.
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s);
 bool slice_gemm_tc_supported(const SliceGemmProblem& pb);
@@ -35,10 +50,11 @@ bool slice_gemm_tc_supported(const SliceGemmProblem& pb);
 cudaError_t slice_gemm_simt(const SliceGemmProblem& pb, cudaStream_t s);
 
 // Tile <-> plane transforms (see stl_transform.cu).
+// red_planes (optional) are P planes (br, bc) of red_dtype.
 cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br, int64_t bc,
                             int t, const float* coef, int P, void* out, int out_dtype,
-                            const float* red_planes, float* red_out, float* red_ws,
-                            cudaStream_t s);
+                            const void* red_planes, int red_dtype, float* red_out,
+                            float* red_ws, cudaStream_t s);
 cudaError_t planes_to_tiles(const void* in, int in_dtype, int Q, int64_t br, int64_t bc, int t,
                             const float* coef, void* out, int out_dtype, int64_t ldo,
                             const void* red_m, int red_dtype, int64_t ldr, float* red_out,
@@ -47,8 +63,8 @@ cudaError_t planes_to_planes(const void* in, int in_dtype, int Q, int64_t ntiles
                              const float* coef, int P, void* out, int out_dtype, cudaStream_t s);
 // t = 4 vectorised fast paths (stl_transform4.cu); cudaErrorNotSupported -> use generic.
 cudaError_t tiles_to_planes4(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
-                             const float* coef, int P, void* out, int odt, const float* rp,
-                             float* ro, float* rw, cudaStream_t s);
+                             const float* coef, int P, void* out, int odt, const void* rp,
+                             int rdt, float* ro, float* rw, cudaStream_t s);
 cudaError_t planes_to_tiles4(const void* in, int idt, int Q, int64_t br, int64_t bc,
                              const float* coef, void* out, int odt, int64_t ldo, const void* rm,
                              int rdt, int64_t ldr, float* ro, float* rw, cudaStream_t s);

@@ -459,19 +459,9 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 3-D bf16 tensor map over `slices` contiguous (outer x inner) matrices, box (64, box_outer).
 bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t slices,
                uint32_t box_outer) {
-  EncodeTiledFn fn = get_encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[3] = {inner, outer, slices};
-  cuuint64_t strides[2] = {inner * 2, inner * outer * 2};
-  cuuint32_t box[3] = {64, box_outer, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult res = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
-                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return res == CUDA_SUCCESS;
+  return make_bf16_tmap(m, base, inner, outer, slices, 64, box_outer);
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -515,6 +505,20 @@ cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
 }
 
 }  // namespace
+
+bool make_bf16_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t slices, uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {inner, outer, slices};
+  cuuint64_t strides[2] = {inner * 2, inner * outer * 2};
+  cuuint32_t box[3] = {box_inner, box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult res = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS;
+}
 
 int sm_count() {
   static int n = 0;

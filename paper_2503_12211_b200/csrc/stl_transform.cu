@@ -103,11 +103,11 @@ __device__ __forceinline__ void reduce_stage(const float* sp, int SP, const floa
   }
 }
 
-template <int T, typename Tin, typename Tout, bool RED>
+template <int T, typename Tin, typename Tout, bool RED, typename Tr>
 __global__ void __launch_bounds__(kTB)
     k_tiles_to_planes(const Tin* __restrict__ m, int64_t ldm, int64_t br, int64_t bc,
                       const float* __restrict__ coef, int P, Tout* __restrict__ out,
-                      const float* __restrict__ red_planes, float* __restrict__ red_partial,
+                      const Tr* __restrict__ red_planes, float* __restrict__ red_partial,
                       int vec) {
   constexpr int TT = T * T;
   constexpr int MAXO = RED ? (kMaxRank * TT + kTB - 1) / kTB : 1;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kTB)
 #pragma unroll
       for (int c = 0; c < TT; ++c) sx[threadIdx.x * SX + c] = x[c];
       for (int p = 0; p < P; ++p)
-        sp[threadIdx.x * SP + p] = valid ? red_planes[p * ntiles + idx] : 0.f;
+        sp[threadIdx.x * SP + p] = valid ? to_f(red_planes[p * ntiles + idx]) : 0.f;
       __syncthreads();
       reduce_stage<TT, MAXO>(sp, SP, sx, SX, P, racc);
     }
@@ -279,9 +279,9 @@ int grid_for(int64_t ntiles, int cap) {
   return static_cast<int>(g);
 }
 
-template <int T, typename Tin, typename Tout>
+template <int T, typename Tin, typename Tout, typename Tr>
 cudaError_t t2p_launch(const void* m, int64_t ldm, int64_t br, int64_t bc, const float* coef,
-                       int P, void* out, const float* red_planes, float* red_out, float* red_ws,
+                       int P, void* out, const void* red_planes, float* red_out, float* red_ws,
                        cudaStream_t s) {
   constexpr int TT = T * T;
   const int64_t ntiles = br * bc;
@@ -289,16 +289,17 @@ cudaError_t t2p_launch(const void* m, int64_t ldm, int64_t br, int64_t bc, const
   if (red_planes) {
     const int grid = grid_for(ntiles, kRedBlocks);
     const size_t smem = sizeof(float) * (P * TT + kTB * (TT + 1) + kTB * (P | 1));
-    auto k = k_tiles_to_planes<T, Tin, Tout, true>;
+    auto k = k_tiles_to_planes<T, Tin, Tout, true, Tr>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     k<<<grid, kTB, smem, s>>>(static_cast<const Tin*>(m), ldm, br, bc, coef, P,
-                              static_cast<Tout*>(out), red_planes, red_ws, vec);
+                              static_cast<Tout*>(out), static_cast<const Tr*>(red_planes), red_ws,
+                              vec);
     if (cudaError_t e2 = sum_partials(red_ws, grid, P * TT, red_out, s)) return e2;
   } else {
     const int grid = grid_for(ntiles, sm_count() * 16);
     const size_t smem = sizeof(float) * P * TT;
-    k_tiles_to_planes<T, Tin, Tout, false><<<grid, kTB, smem, s>>>(
+    k_tiles_to_planes<T, Tin, Tout, false, float><<<grid, kTB, smem, s>>>(
         static_cast<const Tin*>(m), ldm, br, bc, coef, P, static_cast<Tout*>(out), nullptr,
         nullptr, vec);
   }
@@ -333,17 +334,26 @@ cudaError_t p2t_launch(const void* in, int Q, int64_t br, int64_t bc, const floa
   return cudaGetLastError();
 }
 
+template <int T, typename Tr>
+cudaError_t t2p_dispatch_r(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
+                           const float* coef, int P, void* out, int odt, const void* rp,
+                           float* ro, float* rw, cudaStream_t s) {
+  if (mdt == kBF16 && odt == kBF16)
+    return t2p_launch<T, __nv_bfloat16, __nv_bfloat16, Tr>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
+  if (mdt == kBF16 && odt == kF32)
+    return t2p_launch<T, __nv_bfloat16, float, Tr>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
+  if (mdt == kF32 && odt == kBF16)
+    return t2p_launch<T, float, __nv_bfloat16, Tr>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
+  return t2p_launch<T, float, float, Tr>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
+}
+
 template <int T>
 cudaError_t t2p_dispatch(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
-                         const float* coef, int P, void* out, int odt, const float* rp,
+                         const float* coef, int P, void* out, int odt, const void* rp, int rdt,
                          float* ro, float* rw, cudaStream_t s) {
-  if (mdt == kBF16 && odt == kBF16)
-    return t2p_launch<T, __nv_bfloat16, __nv_bfloat16>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
-  if (mdt == kBF16 && odt == kF32)
-    return t2p_launch<T, __nv_bfloat16, float>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
-  if (mdt == kF32 && odt == kBF16)
-    return t2p_launch<T, float, __nv_bfloat16>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
-  return t2p_launch<T, float, float>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
+  if (rp && rdt == kBF16)
+    return t2p_dispatch_r<T, __nv_bfloat16>(m, mdt, ldm, br, bc, coef, P, out, odt, rp, ro, rw, s);
+  return t2p_dispatch_r<T, float>(m, mdt, ldm, br, bc, coef, P, out, odt, rp, ro, rw, s);
 }
 
 template <int T, typename Tin, typename Tout>
@@ -372,19 +382,19 @@ cudaError_t p2t_dispatch(const void* in, int idt, int Q, int64_t br, int64_t bc,
 
 cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br, int64_t bc,
                             int t, const float* coef, int P, void* out, int out_dtype,
-                            const float* red_planes, float* red_out, float* red_ws,
-                            cudaStream_t s) {
+                            const void* red_planes, int red_dtype, float* red_out,
+                            float* red_ws, cudaStream_t s) {
   if (br * bc == 0) return cudaSuccess;
   if (t == 4) {
     cudaError_t e = tiles_to_planes4(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes,
-                                     red_out, red_ws, s);
+                                     red_dtype, red_out, red_ws, s);
     if (e != cudaErrorNotSupported) return e;
   }
   switch (t) {
-    case 1: return t2p_dispatch<1>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_out, red_ws, s);
-    case 2: return t2p_dispatch<2>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_out, red_ws, s);
-    case 4: return t2p_dispatch<4>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_out, red_ws, s);
-    case 8: return t2p_dispatch<8>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_out, red_ws, s);
+    case 1: return t2p_dispatch<1>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_dtype, red_out, red_ws, s);
+    case 2: return t2p_dispatch<2>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_dtype, red_out, red_ws, s);
+    case 4: return t2p_dispatch<4>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_dtype, red_out, red_ws, s);
+    case 8: return t2p_dispatch<8>(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes, red_dtype, red_out, red_ws, s);
     default: return cudaErrorInvalidValue;
   }
 }

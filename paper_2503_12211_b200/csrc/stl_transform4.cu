@@ -222,11 +222,11 @@ __device__ __forceinline__ void finish_partial(MmaReducer& R, unsigned char* sme
 }
 
 // encode: out[p][I][J] = sum_c coef[p][c] * tile(I, J)[c];  RED: red[p][c] += planes[p] * tile.
-template <typename Tin, typename Tout, bool RED>
+template <typename Tin, typename Tout, bool RED, typename Tr>
 __global__ void __launch_bounds__(kThreads4)
     k_encode4(const Tin* __restrict__ m, int64_t ldm, int64_t br, int64_t bc,
               const float* __restrict__ coef, int P, Tout* __restrict__ out,
-              const float* __restrict__ red_planes, float* __restrict__ red_partial) {
+              const Tr* __restrict__ red_planes, float* __restrict__ red_partial) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* sc = reinterpret_cast<float*>(smem);
   for (int i = threadIdx.x; i < P * 16; i += kThreads4) sc[i] = coef[i];
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kThreads4)
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
           if (valid && p0 + j < P) {
-            Vec4<float>::load(red_planes + (p0 + j) * ntiles + off, v[j]);
+            Vec4<Tr>::load(red_planes + (p0 + j) * ntiles + off, v[j]);
           } else {
             v[j][0] = v[j][1] = v[j][2] = v[j][3] = 0.f;
           }
@@ -427,21 +427,31 @@ cudaError_t prep(K k, size_t smem) {
                               static_cast<int>(smem));
 }
 
+template <typename Tin, typename Tout, typename Tr>
+cudaError_t enc4_red(const void* m, int64_t ldm, int64_t br, int64_t bc, const float* coef, int P,
+                     void* out, const void* rp, float* ro, float* rw, cudaStream_t s) {
+  const int64_t nq = br * (bc / 4);
+  const size_t smem = coef_bytes(P) + stage_bytes(P) + red_bytes(P);
+  auto k = k_encode4<Tin, Tout, true, Tr>;
+  if (cudaError_t e = prep(k, smem)) return e;
+  const int grid = grid4(nq, sm_count() * 3);
+  k<<<grid, kThreads4, smem, s>>>(static_cast<const Tin*>(m), ldm, br, bc, coef, P,
+                                  static_cast<Tout*>(out), static_cast<const Tr*>(rp), rw);
+  k_sum_partials_tree<<<P * 16, 256, 0, s>>>(rw, grid, P * 16, ro);
+  return cudaGetLastError();
+}
+
 template <typename Tin, typename Tout>
 cudaError_t enc4(const void* m, int64_t ldm, int64_t br, int64_t bc, const float* coef, int P,
-                 void* out, const float* rp, float* ro, float* rw, cudaStream_t s) {
+                 void* out, const void* rp, int rdt, float* ro, float* rw, cudaStream_t s) {
   const int64_t nq = br * (bc / 4);
   if (rp) {
-    const size_t smem = coef_bytes(P) + stage_bytes(P) + red_bytes(P);
-    auto k = k_encode4<Tin, Tout, true>;
-    if (cudaError_t e = prep(k, smem)) return e;
-    const int grid = grid4(nq, sm_count() * 3);
-    k<<<grid, kThreads4, smem, s>>>(static_cast<const Tin*>(m), ldm, br, bc, coef, P,
-                                    static_cast<Tout*>(out), rp, rw);
-    k_sum_partials_tree<<<P * 16, 256, 0, s>>>(rw, grid, P * 16, ro);
+    if (rdt == kBF16)
+      return enc4_red<Tin, Tout, __nv_bfloat16>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
+    return enc4_red<Tin, Tout, float>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
   } else {
     const size_t smem = coef_bytes(P);
-    auto k = k_encode4<Tin, Tout, false>;
+    auto k = k_encode4<Tin, Tout, false, float>;
     if (cudaError_t e = prep(k, smem)) return e;
     k<<<grid4(nq, sm_count() * 16), kThreads4, smem, s>>>(
         static_cast<const Tin*>(m), ldm, br, bc, coef, P, static_cast<Tout*>(out), nullptr,
@@ -485,17 +495,33 @@ cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, c
 
 // Fast-path dispatch; returns cudaErrorNotSupported when the generic kernels must be used.
 cudaError_t tiles_to_planes4(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
-                             const float* coef, int P, void* out, int odt, const float* rp,
-                             float* ro, float* rw, cudaStream_t s) {
+                             const float* coef, int P, void* out, int odt, const void* rp,
+                             int rdt, float* ro, float* rw, cudaStream_t s) {
   if (bc % 4 || ldm % 8 || !aligned16(m) || !aligned16(out)) return cudaErrorNotSupported;
   if (rp && (mdt != kBF16 || P > 32 || !aligned16(rp))) return cudaErrorNotSupported;
   if (mdt == kBF16 && odt == kBF16)
-    return enc4<__nv_bfloat16, __nv_bfloat16>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
+    return enc4<__nv_bfloat16, __nv_bfloat16>(m, ldm, br, bc, coef, P, out, rp, rdt, ro, rw, s);
   if (mdt == kBF16)
-    return enc4<__nv_bfloat16, float>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
+    return enc4<__nv_bfloat16, float>(m, ldm, br, bc, coef, P, out, rp, rdt, ro, rw, s);
   if (rp) return cudaErrorNotSupported;
-  if (odt == kBF16) return enc4<float, __nv_bfloat16>(m, ldm, br, bc, coef, P, out, nullptr, ro, rw, s);
-  return enc4<float, float>(m, ldm, br, bc, coef, P, out, nullptr, ro, rw, s);
+  if (odt == kBF16)
+    return enc4<float, __nv_bfloat16>(m, ldm, br, bc, coef, P, out, nullptr, 0, ro, rw, s);
+  return enc4<float, float>(m, ldm, br, bc, coef, P, out, nullptr, 0, ro, rw, s);
+}
+
+__global__ void k_cast_f32_bf16(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+cudaError_t cast_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  int64_t g = (n + 255) / 256;
+  if (g > sm_count() * 32) g = sm_count() * 32;
+  k_cast_f32_bf16<<<static_cast<int>(g), 256, 0, s>>>(in, static_cast<__nv_bfloat16*>(out), n);
+  return cudaGetLastError();
 }
 
 cudaError_t planes_to_tiles4(const void* in, int idt, int Q, int64_t br, int64_t bc,

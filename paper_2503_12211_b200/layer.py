@@ -60,7 +60,7 @@ class LayerCache(NamedTuple):
 
     vx: the layer input itself (the reference keeps tile_fibers(x), the same numbers);
     u: encoded input planes (r, M/t, K/t) in the compute dtype;
-    y_enc: slice products, fp32 planes (r, M/t, N/t).
+    y_enc: slice products, planes (r, M/t, N/t) in the compute dtype (fp32 or bf16).
     """
 
     vx: torch.Tensor

@@ -211,8 +211,17 @@ def _slice_products(x_enc, w_enc) -> torch.Tensor:
     return out.permute(1, 2, 0)
 
 
+def forward_scratch(M: int, K: int, N: int, t: int, r: int, dtype: torch.dtype,
+                    device: torch.device) -> torch.Tensor:
+    """Device workspace for stl_forward (from the torch caching allocator, stream-safe)."""
+    nbytes = int(_lib.load().stl_forward_scratch_bytes(M, K, N, t, r, _dt(dtype)))
+    return torch.empty((max(nbytes, 1),), dtype=torch.uint8, device=device)
+
+
 def _forward(x: torch.Tensor, w_planes: torch.Tensor, snf: SnfTriple, keep_cache: bool = False):
-    """Shared forward launch: returns y (and the (u, y_enc) planes when keep_cache)."""
+    """Shared forward launch: returns y (and the (u, y_enc) planes when keep_cache).
+
+    The cached y_enc planes are in the compute dtype (fp32 or bf16)."""
     t, r = snf.t, snf.r
     M, K = x.shape
     bk, bj = w_planes.shape[2], w_planes.shape[1]
@@ -222,13 +231,20 @@ def _forward(x: torch.Tensor, w_planes: torch.Tensor, snf: SnfTriple, keep_cache
     dev = x.device
     snf.on(dev)
     u = torch.empty((r, M // t, bk), dtype=x.dtype, device=dev)
-    y_enc = torch.empty((r, M // t, bj), dtype=torch.float32, device=dev)
+    y_enc = torch.empty((r, M // t, bj), dtype=x.dtype, device=dev) if keep_cache else None
     y = torch.empty((M, N), dtype=x.dtype, device=dev)
+    scratch = forward_scratch(M, K, N, t, r, x.dtype, dev)
     _lib.check(_lib.load().stl_forward(
         x.data_ptr(), M, K, x.stride(0), w_planes.data_ptr(), N, snf.e_x.data_ptr(),
         snf.d.data_ptr(), t, r, _dt(x.dtype), y.data_ptr(), y.stride(0), u.data_ptr(),
-        y_enc.data_ptr(), _stream(dev)))
+        y_enc.data_ptr() if y_enc is not None else None, scratch.data_ptr(), scratch.numel(),
+        _stream(dev)))
     return (y, u, y_enc) if keep_cache else y
+
+
+def set_fusion(enabled: bool) -> None:
+    """Enable/disable the decode-fused kernels (A/B testing; default on)."""
+    _lib.load().stl_set_fusion(1 if enabled else 0)
 
 
 def stl_batched(x, w_encoded, snf) -> torch.Tensor:

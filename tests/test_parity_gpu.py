@@ -362,3 +362,33 @@ def test_edge_cases():
     m = torch.randn((8, 8), device=DEV)
     enc = stl.encode_tiles(m, np.eye(16), 4)
     assert torch.equal(stl.decode_tiles(enc, np.eye(16), 4), m)
+
+
+# ----------------------------------------------------------------- decode-fused forward
+@pytest.mark.parametrize("M,K,N,r", [(1024, 1024, 1024, 24), (1200, 512, 1040, 24),
+                                     (2048, 256, 512, 1), (1024, 512, 2048, 16),
+                                     (1032, 264, 1056, 49), (8192, 1024, 1024, 32)])
+def test_fused_decode_matches_unfused_and_oracle(M, K, N, r):
+    t = 4
+    rng = O.make_rng(M + N + r)
+    e_x, e_w, d = O.random_gaussian_init(t, r, rng, scale=0.5)
+    x_dev, x64 = bf16_round(rng.standard_normal((M, K)))
+    w_dev, w64 = bf16_round(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
+    layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
+    try:
+        stl.set_fusion(False)
+        y_u, c_u = stl._layer_forward_cached(layer, x_dev)
+        stl.set_fusion(True)
+        y_f, c_f = stl._layer_forward_cached(layer, x_dev)
+    finally:
+        stl.set_fusion(True)
+    torch.cuda.synchronize()
+    assert rel(y_f, y_u) <= 1e-6
+    assert torch.equal(c_f.u, c_u.u)
+    assert rel(c_f.y_enc, c_u.y_enc) <= 1e-6
+    slab = slice(0, min(M, 256))
+    ref = O.stl_batched(x64[slab], w64, e_x, d, t)
+    assert rel(y_f[slab], ref) <= BF16_TOL
+    # the last rows (ragged final 256-row block) against the oracle too
+    tail = slice(max(0, M - 64), M)
+    assert rel(y_f[tail], O.stl_batched(x64[tail], w64, e_x, d, t)) <= BF16_TOL
