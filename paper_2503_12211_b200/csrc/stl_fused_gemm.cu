@@ -17,6 +17,7 @@
 // Scratch slots are recycled only after every chunk of the block that used them is decoded.
 // All waits are bounded (trap after 10 s), and the grid never exceeds one CTA per SM.
 #include "sm100_pair_pipeline.cuh"
+#include <cstdlib>
 #include "stl_internal.h"
 
 namespace stl {
@@ -358,7 +359,12 @@ cudaError_t fused_gemm_decode(const void* a, const void* b, int b_layout, int r,
   fa.nslot = fused_nslot(r, nblocks);
   const int smem = FL::kRingBytes + FL::kBarBytes + kMaxRank * 16 * 4 + 1024;
   const int64_t tiles = static_cast<int64_t>(nblocks) * r;
-  const int pairs = sm_count() / 2;
+  int pairs = sm_count() / 2;
+  static const int env_pairs = [] {
+    const char* e = getenv("STL_FUSED_PAIRS");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_pairs > 0 && env_pairs < pairs) pairs = env_pairs;
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
   if (b_layout) {
     auto k = fused_gemm_decode_kernel<true>;

@@ -47,11 +47,13 @@ def test_status_mapping_without_gpu():
     with pytest.raises(ShapeError, match="does not divide"):
         _lib.check(st)
     # r = 0 -> ShapeError like SnfTriple.__post_init__ (snf_operator.py:60-61)
-    st = lib.stl_forward(None, 8, 8, 8, None, 8, None, None, 4, 0, 0, None, 8, None, None, None)
+    st = lib.stl_forward(None, 8, 8, 8, None, 8, None, None, 4, 0, 0, None, 8, None, None, None, 0,
+                         None)
     with pytest.raises(ShapeError):
         _lib.check(st)
     # batch not divisible by t -> ShapeError (toy_network.py:78-79)
-    st = lib.stl_forward(None, 6, 8, 8, None, 8, None, None, 4, 4, 0, None, 8, None, None, None)
+    st = lib.stl_forward(None, 6, 8, 8, None, 8, None, None, 4, 4, 0, None, 8, None, None, None, 0,
+                         None)
     with pytest.raises(ShapeError, match="batch"):
         _lib.check(st)
     # bad dtype -> ValueError
