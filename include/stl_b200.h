@@ -109,7 +109,8 @@ STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const
                 void* x_enc_ws, void* y_enc_cache, void* scratch, int64_t scratch_bytes,
                 void* stream);
 
-/* Enable (1, default) or disable (0) the decode-fused kernels (A/B testing). Host-only. */
+/* A/B switches (host-only): bit 0 = enable the decode-fused forward (default on);
+ * bit 1 = force the FFMA tile transforms instead of the tensor-core (mma.sync) ones. */
 STL_API int stl_set_fusion(int enabled);
 
 /*

@@ -149,7 +149,8 @@ bool fused_forward_shape(int64_t M, int64_t K, int64_t N, int t, int r, int dtyp
 }  // namespace
 
 int stl_set_fusion(int enabled) {
-  g_fusion = enabled != 0;
+  g_fusion = (enabled & 1) != 0;
+  stl::set_transform_mma((enabled & 2) == 0);  // bit 1 = force the FFMA transforms
   return STL_OK;
 }
 

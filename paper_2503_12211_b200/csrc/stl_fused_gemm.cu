@@ -17,6 +17,7 @@
 // Scratch slots are recycled only after every chunk of the block that used them is decoded.
 // All waits are bounded (trap after 10 s), and the grid never exceeds one CTA per SM.
 #include "sm100_pair_pipeline.cuh"
+#include <cstdio>
 #include <cstdlib>
 #include "stl_internal.h"
 
@@ -28,8 +29,6 @@ constexpr int kFStages = 6;
 constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kFThreads = 128 + kEpiThreads;
-constexpr int kBlockQuads = 256 * (kFBN / 4);  // 4-tile quads per output block
-constexpr int kDecChunk = 8;
 
 struct FusedArgs {
   int r, M, N, K;          // slice GEMM dims: M = I tiles, N = J tiles, K = contraction tiles
@@ -43,6 +42,7 @@ struct FusedArgs {
   unsigned* written;       // per-block: CTA drains completed (target 2r)
   unsigned* decoded;       // per-block: decode chunks completed (target 2r)
   int nslot;
+  unsigned long long* dbg;  // optional [grid][4] phase timers (ns): tfull wait, drain, block wait, decode
 };
 
 using FL = pair::Layout<kFBN, kFStages>;
@@ -60,31 +60,12 @@ __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
     if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
   }
 }
-__device__ __forceinline__ float4 ld_cg4(const float* p) {
-  float4 v;
-  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
-  return v;
-}
-__device__ __forceinline__ void st_cg4(float* p, float a, float b, float c, float d) {
-  asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
-               "f"(d)
-               : "memory");
-}
 __device__ __forceinline__ void epi_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
 template <typename T>
 __device__ __forceinline__ void store16(T* dst, const float (&v)[16]);
-template <>
-__device__ __forceinline__ void store16<float>(float* dst, const float (&v)[16]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    *reinterpret_cast<float4*>(dst + 4 * i) =
-        make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-}
 template <>
 __device__ __forceinline__ void store16<__nv_bfloat16>(__nv_bfloat16* dst, const float (&v)[16]) {
   uint32_t w[8];
@@ -97,45 +78,105 @@ __device__ __forceinline__ void store16<__nv_bfloat16>(__nv_bfloat16* dst, const
   *reinterpret_cast<uint4*>(dst + 8) = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
-// Decode one 4-tile quad (row I, tiles J0..J0+3) of a block whose r slices sit in `slot`.
-template <typename Ty>
-__device__ __forceinline__ void decode_quad(const float* __restrict__ slot, int r, int rl,
-                                            int jq, const float* __restrict__ sdec, Ty* dst,
-                                            int64_t ldy) {
-  float acc[4][16];
+__device__ __forceinline__ float ld_cg(const float* p) {
+  float v;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Decoder as mma B fragments (K = p, N = c), split hi + lo bf16: thread (g, q) holds
+// B[2q, 2q+1][g] and B[2q+8, 2q+9][g] of every 16-wide K step and 8-wide N tile.
+constexpr int kMaxKs = kMaxRank / 16;
+struct DecFrags {
+  uint32_t hi[kMaxKs][2][2], lo[kMaxKs][2][2];
+};
+__device__ __forceinline__ void load_dec_frags(const float* sdec, int r, DecFrags& f) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int ks = 0; ks < kMaxKs; ++ks)
 #pragma unroll
-    for (int c = 0; c < 16; ++c) acc[t][c] = 0.f;
-  const float* base = slot + static_cast<size_t>(rl) * kFBN + jq * 4;
-  for (int p0 = 0; p0 < r; p0 += kDecChunk) {
-    float4 v[kDecChunk];
+    for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-    for (int j = 0; j < kDecChunk; ++j)
-      v[j] = (p0 + j < r) ? ld_cg4(base + static_cast<size_t>(p0 + j) * 256 * kFBN)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int j = 0; j < kDecChunk; ++j) {
-      if (p0 + j >= r) break;
-      const float vt[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-      const float4* cp = reinterpret_cast<const float4*>(sdec + (p0 + j) * 16);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4 c4 = cp[i];
-        const float cf[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-          for (int t = 0; t < 4; ++t) acc[t][4 * i + jj] = fmaf(cf[jj], vt[t], acc[t][4 * i + jj]);
+      for (int h = 0; h < 2; ++h) {
+        const int p0 = ks * 16 + 2 * q + 8 * h;
+        const int c = nt * 8 + g;
+        const float d0 = p0 < r ? sdec[p0 * 16 + c] : 0.f;
+        const float d1 = p0 + 1 < r ? sdec[(p0 + 1) * 16 + c] : 0.f;
+        const float h0 = __bfloat162float(__float2bfloat16_rn(d0));
+        const float h1 = __bfloat162float(__float2bfloat16_rn(d1));
+        f.hi[ks][nt][h] = pack2(h0, h1);
+        f.lo[ks][nt][h] = pack2(d0 - h0, d1 - h1);
       }
+}
+
+// Decode 16 consecutive tiles (block row rl, tiles j0..j0+15) of a block whose r slices sit in
+// `slot` (fp32 planes 256 x 256): out tile[c] = sum_p Z[p][tile] * dec[p][c] on the tensor
+// cores (m16n8k16: M = tiles, K = p, N = c), Z split hi + lo bf16.
+template <typename Ty>
+__device__ __forceinline__ void decode_mtile(const float* __restrict__ slot, int r, int rl,
+                                             int j0, const DecFrags& f, Ty* __restrict__ y,
+                                             int64_t ldy, int I, int J0, int Nvalid) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  const float* base = slot + static_cast<size_t>(rl) * kFBN + j0 + g;
+  const int nks = (r + 15) >> 4;
+#pragma unroll
+  for (int ks = 0; ks < kMaxKs; ++ks) {
+    if (ks >= nks) break;
+    float v[2][4];  // [tile g / g+8][p = 2q, 2q+1, 2q+8, 2q+9]
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int p = ks * 16 + 2 * q + (h & 1) + 8 * (h >> 1);
+      const bool ok = p < r;
+      const float* src = base + static_cast<size_t>(p) * 256 * kFBN;
+      v[0][h] = ok ? ld_cg(src) : 0.f;
+      v[1][h] = ok ? ld_cg(src + 8) : 0.f;
+    }
+    uint32_t ah[4], al[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      // a0 = (tile g, p 2q..), a1 = (tile g+8, p 2q..), a2 = (g, 2q+8..), a3 = (g+8, 2q+8..)
+      const int t = i & 1, hh = (i >> 1) * 2;
+      const float x0 = v[t][hh], x1 = v[t][hh + 1];
+      const float h0 = __bfloat162float(__float2bfloat16_rn(x0));
+      const float h1 = __bfloat162float(__float2bfloat16_rn(x1));
+      ah[i] = pack2(h0, h1);
+      al[i] = pack2(x0 - h0, x1 - h1);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      mma16816(acc[nt], ah, f.hi[ks][nt][0], f.hi[ks][nt][1]);
+      mma16816(acc[nt], al, f.hi[ks][nt][0], f.hi[ks][nt][1]);
+      mma16816(acc[nt], ah, f.lo[ks][nt][0], f.lo[ks][nt][1]);
     }
   }
+  // C[tile][c]: (acc[nt][0], [1]) -> tile g, c = 8nt + 2q (+1); ([2], [3]) -> tile g + 8.
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    float row[16];
+  for (int nt = 0; nt < 2; ++nt) {
+    const int a = 2 * nt + (q >> 1), b = 2 * (q & 1);
 #pragma unroll
-    for (int e = 0; e < 16; ++e) row[e] = acc[e >> 2][a * 4 + (e & 3)];
-    store16(dst + a * ldy, row);
+    for (int t = 0; t < 2; ++t) {
+      const int J = J0 + g + 8 * t;
+      if (J >= Nvalid) continue;
+      Ty* dst = y + (static_cast<int64_t>(I) * 4 + a) * ldy + static_cast<int64_t>(J) * 4 + b;
+      if constexpr (sizeof(Ty) == 2) {
+        *reinterpret_cast<uint32_t*>(dst) = pack2(acc[nt][2 * t], acc[nt][2 * t + 1]);
+      } else {
+        *reinterpret_cast<float2*>(dst) = make_float2(acc[nt][2 * t], acc[nt][2 * t + 1]);
+      }
+    }
   }
 }
 
@@ -207,6 +248,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1)
     const int etid = threadIdx.x - 128;  // 0..255
     const unsigned target = 2u * static_cast<unsigned>(r);
     const size_t slot_elems = static_cast<size_t>(r) * 256 * kFBN;
+    DecFrags dfr;
+    load_dec_frags(sdec, r, dfr);
     int it = 0;
     for (int tile = cluster; tile < total; tile += nclusters, ++it) {
       const pair::TileCoord tc = map(tile);
@@ -219,8 +262,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1)
         if (etid == 0) wait_count(&args.decoded[b - args.nslot], target);
         epi_bar();
       }
+      const uint64_t t_a = ptx::globaltimer_ns();
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
+      const uint64_t t_b = ptx::globaltimer_ns();
       // 1. drain TMEM -> scratch (fp32) [+ cache planes]
       const int rl = static_cast<int>(rank) * 128 + q * 32 + lane;  // row within block
       float* srow = slot + (static_cast<size_t>(tc.p) * 256 + rl) * kFBN + half * 128;
@@ -235,8 +280,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1)
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          st_cg4(srow + c + 4 * i, __uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          *reinterpret_cast<float4*>(srow + c + 4 * i) =
+              make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                          __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
         if (args.cache != nullptr && grow < M) {
           const size_t off = (static_cast<size_t>(tc.p) * M + grow) * N + gcol0 + c;
           const int ncol = N - (gcol0 + c);
@@ -269,32 +315,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
       // 2. publish this CTA's half of slice p, then wait for the whole block
-      __threadfence();
+      //    (cooperative-groups grid-sync pattern: CTA barrier, one gpu-scope fence + atomic).
       epi_bar();
+      const uint64_t t_c = ptx::globaltimer_ns();
       if (etid == 0) {
+        __threadfence();
         atomicAdd(&args.written[b], 1u);
         wait_count(&args.written[b], target);
       }
       epi_bar();
-      // 3. decode chunk (2p + rank) of 2r
+      const uint64_t t_d = ptx::globaltimer_ns();
+      // 3. decode m-tiles [mt_lo, mt_hi) of the block's 256 x (256/16) m-tiles (16 tiles each)
       const int chunk = 2 * tc.p + static_cast<int>(rank);
-      const int q_lo = static_cast<int>((static_cast<int64_t>(chunk) * kBlockQuads) / (2 * r));
-      const int q_hi = static_cast<int>((static_cast<int64_t>(chunk + 1) * kBlockQuads) / (2 * r));
-      for (int qi = q_lo + etid; qi < q_hi; qi += kEpiThreads) {
-        const int brl = qi / (kFBN / 4), jq = qi - brl * (kFBN / 4);
-        const int I = tc.mb * 256 + brl, J0 = tc.nb * kFBN + jq * 4;
+      constexpr int kBlockMt = 256 * (kFBN / 16);
+      const int mt_lo = static_cast<int>((static_cast<int64_t>(chunk) * kBlockMt) / (2 * r));
+      const int mt_hi = static_cast<int>((static_cast<int64_t>(chunk + 1) * kBlockMt) / (2 * r));
+      for (int mt = mt_lo + ew; mt < mt_hi; mt += kEpiWarps) {
+        const int brl = mt / (kFBN / 16), j0 = (mt - brl * (kFBN / 16)) * 16;
+        const int I = tc.mb * 256 + brl, J0 = tc.nb * kFBN + j0;
         if (I >= M || J0 >= N) continue;
-        const int64_t yoff = static_cast<int64_t>(I) * 4 * args.ldy + static_cast<int64_t>(J0) * 4;
         if (args.y_bf16)
-          decode_quad(slot, r, brl, jq, sdec, reinterpret_cast<__nv_bfloat16*>(args.y) + yoff,
-                      args.ldy);
+          decode_mtile(slot, r, brl, j0, dfr, reinterpret_cast<__nv_bfloat16*>(args.y), args.ldy,
+                       I, J0, N);
         else
-          decode_quad(slot, r, brl, jq, sdec, reinterpret_cast<float*>(args.y) + yoff, args.ldy);
+          decode_mtile(slot, r, brl, j0, dfr, reinterpret_cast<float*>(args.y), args.ldy, I, J0,
+                       N);
       }
       epi_bar();
       if (etid == 0) {
         __threadfence();
         atomicAdd(&args.decoded[b], 1u);
+        if (args.dbg) {
+          unsigned long long* d = args.dbg + 4 * blockIdx.x;
+          d[0] += t_b - t_a;
+          d[1] += t_c - t_b;
+          d[2] += t_d - t_c;
+          d[3] += ptx::globaltimer_ns() - t_d;
+        }
       }
     }
   }
@@ -357,6 +414,11 @@ cudaError_t fused_gemm_decode(const void* a, const void* b, int b_layout, int r,
   fa.decoded = counters + nblocks;
   fa.scratch = reinterpret_cast<float*>(static_cast<uint8_t*>(scratch) + kCounterBytes(nblocks));
   fa.nslot = fused_nslot(r, nblocks);
+  static const bool dbg_on = getenv("STL_FUSED_DEBUG") != nullptr;
+  static unsigned long long* dbg = nullptr;
+  if (dbg_on && !dbg) cudaMalloc(&dbg, 4 * 4096 * sizeof(unsigned long long));
+  if (dbg_on) cudaMemsetAsync(dbg, 0, 4 * 4096 * sizeof(unsigned long long), s);
+  fa.dbg = dbg_on ? dbg : nullptr;
   const int smem = FL::kRingBytes + FL::kBarBytes + kMaxRank * 16 * 4 + 1024;
   const int64_t tiles = static_cast<int64_t>(nblocks) * r;
   int pairs = sm_count() / 2;
@@ -374,6 +436,22 @@ cudaError_t fused_gemm_decode(const void* a, const void* b, int b_layout, int r,
     auto k = fused_gemm_decode_kernel<false>;
     if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
     k<<<grid, kFThreads, smem, s>>>(ta, tb, fa);
+  }
+  if (dbg_on) {
+    unsigned long long h[4 * 296] = {};
+    cudaMemcpyAsync(h, dbg, sizeof(unsigned long long) * 4 * grid, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double sum[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+    for (int i = 0; i < grid; ++i)
+      for (int j = 0; j < 4; ++j) {
+        sum[j] += h[4 * i + j];
+        mx[j] = mx[j] > h[4 * i + j] ? mx[j] : h[4 * i + j];
+      }
+    fprintf(stderr, "[fused dbg] grid=%d tiles/pair=%.1f  avg us: tfull_wait=%.1f drain=%.1f "
+            "block_wait=%.1f decode=%.1f | max: %.1f %.1f %.1f %.1f\n", grid,
+            double(tiles) / (grid / 2), sum[0] / grid / 1e3, sum[1] / grid / 1e3,
+            sum[2] / grid / 1e3, sum[3] / grid / 1e3, mx[0] / 1e3, mx[1] / 1e3, mx[2] / 1e3,
+            mx[3] / 1e3);
   }
   return cudaGetLastError();
 }

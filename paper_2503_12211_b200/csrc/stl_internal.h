@@ -68,6 +68,15 @@ cudaError_t tiles_to_planes4(const void* m, int mdt, int64_t ldm, int64_t br, in
 cudaError_t planes_to_tiles4(const void* in, int idt, int Q, int64_t br, int64_t bc,
                              const float* coef, void* out, int odt, int64_t ldo, const void* rm,
                              int rdt, int64_t ldr, float* ro, float* rw, cudaStream_t s);
+// Tensor-core (mma.sync) t = 4 transforms (stl_transform_mma.cu); set_transform_mma(false)
+// routes t = 4 to the FFMA kernels (A/B testing).
+void set_transform_mma(bool on);
+cudaError_t tiles_to_planes_mma(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
+                                const float* coef, int P, void* out, int odt, const void* rp,
+                                int rdt, float* ro, float* rw, cudaStream_t s);
+cudaError_t planes_to_tiles_mma(const void* in, int idt, int Q, int64_t br, int64_t bc,
+                                const float* coef, void* out, int odt, int64_t ldo, const void* rm,
+                                int rdt, int64_t ldr, float* ro, float* rw, cudaStream_t s);
 // out[o] = sum_b partial[b * n + o], deterministic fixed-order tree.
 cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t s);
 cudaError_t compose_coefs(const float* a, const float* b, int r, int tt, float* out,

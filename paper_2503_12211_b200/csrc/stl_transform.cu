@@ -380,11 +380,19 @@ cudaError_t p2t_dispatch(const void* in, int idt, int Q, int64_t br, int64_t bc,
 
 }  // namespace
 
+bool g_use_mma = true;
+void set_transform_mma(bool on) { g_use_mma = on; }
+
 cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br, int64_t bc,
                             int t, const float* coef, int P, void* out, int out_dtype,
                             const void* red_planes, int red_dtype, float* red_out,
                             float* red_ws, cudaStream_t s) {
   if (br * bc == 0) return cudaSuccess;
+  if (t == 4 && g_use_mma) {
+    cudaError_t e = tiles_to_planes_mma(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype,
+                                        red_planes, red_dtype, red_out, red_ws, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (t == 4) {
     cudaError_t e = tiles_to_planes4(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes,
                                      red_dtype, red_out, red_ws, s);
@@ -404,6 +412,11 @@ cudaError_t planes_to_tiles(const void* in, int in_dtype, int Q, int64_t br, int
                             const void* red_m, int red_dtype, int64_t ldr, float* red_out,
                             float* red_ws, cudaStream_t s) {
   if (br * bc == 0) return cudaSuccess;
+  if (t == 4 && g_use_mma) {
+    cudaError_t e = planes_to_tiles_mma(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m,
+                                        red_dtype, ldr, red_out, red_ws, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (t == 4) {
     cudaError_t e = planes_to_tiles4(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m,
                                      red_dtype, ldr, red_out, red_ws, s);
