@@ -77,13 +77,18 @@ struct Prof {
 };
 
 int run_gemm(const void* a, int al, const void* b, int bl, void* c, int cdt, int abdt, int r,
-             int64_t M, int64_t N, int64_t K, cudaStream_t s) {
+             int64_t M, int64_t N, int64_t K, cudaStream_t s, void* c2 = nullptr,
+             bool* c2_done = nullptr) {
   if (M == 0 || N == 0 || r == 0) return STL_OK;
   if (K == 0) {
     return check_cuda(cudaMemsetAsync(c, 0, stl::dtype_size(cdt) * r * M * N, s), "memset");
   }
   stl::SliceGemmProblem pb{a, al, b, bl, c, cdt, abdt, r, M, N, K};
   const bool tc = stl::slice_gemm_tc_supported(pb);
+  if (tc && c2) {
+    pb.c2 = c2;
+    if (c2_done) *c2_done = true;
+  }
   Prof prof(tc ? "slice_gemm_tcgen05" : "slice_gemm_simt", s);
   cudaError_t e = tc ? stl::slice_gemm_tc(pb, s) : stl::slice_gemm_simt(pb, s);
   return check_cuda(e, "slice_gemm launch");
@@ -207,7 +212,9 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
                   (long long)need);
     yenc = static_cast<float*>(scratch);
   }
-  st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, yenc, STL_F32, dtype, r, bi, bj, bk, s);
+  bool cache_done = false;
+  st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, yenc, STL_F32, dtype, r, bi, bj, bk, s,
+                (y_enc_cache && dtype == STL_BF16) ? y_enc_cache : nullptr, &cache_done);
   if (st) return st;
   {
     Prof prof("decode_y", s);
@@ -216,7 +223,7 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
                     "forward decode");
   }
   if (st) return st;
-  if (y_enc_cache && dtype == STL_BF16) {
+  if (y_enc_cache && dtype == STL_BF16 && !cache_done) {
     Prof prof("cache_cast", s);
     st = check_cuda(stl::cast_f32_to_bf16(yenc, y_enc_cache, static_cast<int64_t>(r) * bi * bj, s),
                     "cache cast");

@@ -25,6 +25,7 @@ struct SliceGemmProblem {
   int ab_dtype;
   int r;
   int64_t M, N, K;
+  void* c2 = nullptr;  // optional bf16 copy of C (tcgen05 path only)
 };
 
 int sm_count();

@@ -35,6 +35,7 @@ struct EpiArgs {
   int c_bf16;
   int r;
   int M, N, K;
+  __nv_bfloat16* c2;  // optional bf16 copy of C (the forward's training cache)
 };
 
 template <int BN>
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else
             store_row_chunk(reinterpret_cast<float*>(args.c) + row_off + col0, v, N - col0,
                             c_vec);
+          if (args.c2) store_row_chunk(args.c2 + row_off + col0, v, N - col0, N % 8 == 0);
         }
       }
       ptx::tc_fence_before();
@@ -425,6 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           else
             store_row_chunk(reinterpret_cast<float*>(args.c) + row_off + col0, v, N - col0,
                             c_vec);
+          if (args.c2) store_row_chunk(args.c2 + row_off + col0, v, N - col0, N % 8 == 0);
         }
       }
       ptx::tc_fence_before();
@@ -478,7 +481,7 @@ cudaError_t launch_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   const int64_t tiles = r * ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
   EpiArgs ea{pb.c, pb.c_dtype == kBF16 ? 1 : 0, pb.r, static_cast<int>(M), static_cast<int>(N),
-             static_cast<int>(K)};
+             static_cast<int>(K), static_cast<__nv_bfloat16*>(pb.c2)};
   kern<<<grid, kThreads, smem, s>>>(ta, tb, ea);
   return cudaGetLastError();
 }
@@ -499,7 +502,7 @@ cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
   const int pairs = sm_count() / 2;
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
   EpiArgs ea{pb.c, pb.c_dtype == kBF16 ? 1 : 0, pb.r, static_cast<int>(M), static_cast<int>(N),
-             static_cast<int>(K)};
+             static_cast<int>(K), static_cast<__nv_bfloat16*>(pb.c2)};
   kern<<<grid, kThreads, smem, s>>>(ta, tb, ea);
   return cudaGetLastError();
 }

@@ -71,45 +71,40 @@ struct RedAcc {
   // One k-step over 16 tiles [jm, jm+16) of tile row I.
   //   A (M = p, K = tiles): planes Zp[p][tile] (bf16 exact, or fp32 split hi/lo)
   //   B (K = tiles, N = c): X tile values (bf16 matrix, exact)
+  // K rows are permuted (k = 2q, 2q+1, 2q+8, 2q+9 <-> tiles 4q .. 4q+3; a consistent K
+  // permutation of A and B leaves the product unchanged) so each thread's A elements are four
+  // consecutive tiles of one plane: one 16-byte (fp32) or 8-byte (bf16) load.
   template <typename Tz>
   __device__ void step(const Tz* __restrict__ zrow, int64_t plane_stride, int P,
                        const __nv_bfloat16* __restrict__ xrow0, int64_t ldx) {
     const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-    // B fragments: b0 = X[tile 2q, 2q+1][c], b1 = X[tile 2q+8, 2q+9][c], c = 8nt + g
     uint32_t b[2][2];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       const int c = 8 * nt + g;
-      const __nv_bfloat16* xr = xrow0 + (c >> 2) * ldx + (c & 3);
-      b[nt][0] = ld_bf16_pair(xr + 4 * (2 * q), xr + 4 * (2 * q + 1));
-      b[nt][1] = ld_bf16_pair(xr + 4 * (2 * q + 8), xr + 4 * (2 * q + 9));
+      const __nv_bfloat16* xr = xrow0 + (c >> 2) * ldx + (c & 3) + 16 * q;
+      b[nt][0] = ld_bf16_pair(xr, xr + 4);
+      b[nt][1] = ld_bf16_pair(xr + 8, xr + 12);
     }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       if (16 * mt >= P) break;
       const int p0 = 16 * mt + g, p1 = p0 + 8;
       if constexpr (sizeof(Tz) == 2) {
-        const uint32_t a0 = p0 < P ? ld_u32(zrow + p0 * plane_stride + 2 * q) : 0u;
-        const uint32_t a1 = p1 < P ? ld_u32(zrow + p1 * plane_stride + 2 * q) : 0u;
-        const uint32_t a2 = p0 < P ? ld_u32(zrow + p0 * plane_stride + 2 * q + 8) : 0u;
-        const uint32_t a3 = p1 < P ? ld_u32(zrow + p1 * plane_stride + 2 * q + 8) : 0u;
+        uint2 u0 = make_uint2(0u, 0u), u1 = u0;
+        if (p0 < P) u0 = *reinterpret_cast<const uint2*>(zrow + p0 * plane_stride + 4 * q);
+        if (p1 < P) u1 = *reinterpret_cast<const uint2*>(zrow + p1 * plane_stride + 4 * q);
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) mma(acc[mt][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
+        for (int nt = 0; nt < 2; ++nt) mma(acc[mt][nt], u0.x, u1.x, u0.y, u1.y, b[nt][0], b[nt][1]);
       } else {
-        float2 v0 = make_float2(0.f, 0.f), v1 = v0, v2 = v0, v3 = v0;
-        if (p0 < P) {
-          v0 = *reinterpret_cast<const float2*>(zrow + p0 * plane_stride + 2 * q);
-          v2 = *reinterpret_cast<const float2*>(zrow + p0 * plane_stride + 2 * q + 8);
-        }
-        if (p1 < P) {
-          v1 = *reinterpret_cast<const float2*>(zrow + p1 * plane_stride + 2 * q);
-          v3 = *reinterpret_cast<const float2*>(zrow + p1 * plane_stride + 2 * q + 8);
-        }
+        float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+        if (p0 < P) v0 = *reinterpret_cast<const float4*>(zrow + p0 * plane_stride + 4 * q);
+        if (p1 < P) v1 = *reinterpret_cast<const float4*>(zrow + p1 * plane_stride + 4 * q);
         uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
-        split2(v0.x, v0.y, h0, l0);
-        split2(v1.x, v1.y, h1, l1);
-        split2(v2.x, v2.y, h2, l2);
-        split2(v3.x, v3.y, h3, l3);
+        split2(v0.x, v0.y, h0, l0);  // a0: (p0, tiles 4q, 4q+1)
+        split2(v1.x, v1.y, h1, l1);  // a1: (p1, tiles 4q, 4q+1)
+        split2(v0.z, v0.w, h2, l2);  // a2: (p0, tiles 4q+2, 4q+3)
+        split2(v1.z, v1.w, h3, l3);  // a3
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           mma(acc[mt][nt], h0, h1, h2, h3, b[nt][0], b[nt][1]);
@@ -275,60 +270,81 @@ __global__ void __launch_bounds__(kThreadsM)
     const int64_t rem_mt = (bc - J0) >> 4;
     const int nmt = rem_mt < kMtPerTask ? static_cast<int>(rem_mt) : kMtPerTask;
     const Tz* zrow = z + I * bc + J0;
-    for (int mi = 0; mi < nmt; ++mi) {
-      float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-      const Tz* zt = zrow + 16 * mi + g;  // tile g of this m-tile
+    // 32-tile groups; M rows permuted so thread (g, q) owns tiles 4g .. 4g+3 of the group:
+    // m-tile A rows g, g+8 <-> tiles 4g, 4g+1; m-tile B rows g, g+8 <-> tiles 4g+2, 4g+3.
+    for (int gi = 0; gi < (nmt >> 1); ++gi) {
+      const Tz* zt = zrow + 32 * gi + 4 * g;
+      float acc[2][2][4] = {};  // [m-tile A/B][n-tile][frag]
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
         if (ks >= KS) break;
-        // a0 = Z[p 2q, 2q+1][tile g], a1 = tile g+8, a2 = Z[p 2q+8, +9][tile g], a3 = tile g+8
-        float v[4][2];
+        float v[4][4];  // [plane 2q, 2q+1, 2q+8, 2q+9][tile 4g + i]
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-          const int p = 16 * ks + 2 * q + (h >> 1) * 8;
-          const int t = (h & 1) * 8;
-          const float x0 = p < Q ? static_cast<float>(zt[p * ntiles + t]) : 0.f;
-          const float x1 = p + 1 < Q ? static_cast<float>(zt[(p + 1) * ntiles + t]) : 0.f;
-          v[h][0] = x0;
-          v[h][1] = x1;
-        }
-        if constexpr (sizeof(Tz) == 2) {
-          const uint32_t a0 = pack2(v[0][0], v[0][1]), a1 = pack2(v[1][0], v[1][1]);
-          const uint32_t a2 = pack2(v[2][0], v[2][1]), a3 = pack2(v[3][0], v[3][1]);
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            mma(acc[nt], a0, a1, a2, a3, bh[ks][nt][0], bh[ks][nt][1]);
-            mma(acc[nt], a0, a1, a2, a3, bl[ks][nt][0], bl[ks][nt][1]);
+          const int p = 16 * ks + 2 * q + (h & 1) + 8 * (h >> 1);
+          if (p < Q) {
+            if constexpr (sizeof(Tz) == 2) {
+              const uint2 u = *reinterpret_cast<const uint2*>(zt + p * ntiles);
+              const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+              const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+              v[h][0] = f0.x; v[h][1] = f0.y; v[h][2] = f1.x; v[h][3] = f1.y;
+            } else {
+              const float4 f = *reinterpret_cast<const float4*>(zt + p * ntiles);
+              v[h][0] = f.x; v[h][1] = f.y; v[h][2] = f.z; v[h][3] = f.w;
+            }
+          } else {
+            v[h][0] = v[h][1] = v[h][2] = v[h][3] = 0.f;
           }
-        } else {
-          uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
-          split2(v[0][0], v[0][1], h0, l0);
-          split2(v[1][0], v[1][1], h1, l1);
-          split2(v[2][0], v[2][1], h2, l2);
-          split2(v[3][0], v[3][1], h3, l3);
+        }
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            mma(acc[nt], h0, h1, h2, h3, bh[ks][nt][0], bh[ks][nt][1]);
-            mma(acc[nt], l0, l1, l2, l3, bh[ks][nt][0], bh[ks][nt][1]);
-            mma(acc[nt], h0, h1, h2, h3, bl[ks][nt][0], bl[ks][nt][1]);
+        for (int m = 0; m < 2; ++m) {
+          // a0 = (tile 4g+2m, planes 2q, 2q+1), a1 = (tile 4g+2m+1, ...), a2/a3: planes 2q+8, +9
+          const int t0 = 2 * m, t1 = 2 * m + 1;
+          if constexpr (sizeof(Tz) == 2) {
+            const uint32_t a0 = pack2(v[0][t0], v[1][t0]), a1 = pack2(v[0][t1], v[1][t1]);
+            const uint32_t a2 = pack2(v[2][t0], v[3][t0]), a3 = pack2(v[2][t1], v[3][t1]);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              mma(acc[m][nt], a0, a1, a2, a3, bh[ks][nt][0], bh[ks][nt][1]);
+              mma(acc[m][nt], a0, a1, a2, a3, bl[ks][nt][0], bl[ks][nt][1]);
+            }
+          } else {
+            uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
+            split2(v[0][t0], v[1][t0], h0, l0);
+            split2(v[0][t1], v[1][t1], h1, l1);
+            split2(v[2][t0], v[3][t0], h2, l2);
+            split2(v[2][t1], v[3][t1], h3, l3);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              mma(acc[m][nt], h0, h1, h2, h3, bh[ks][nt][0], bh[ks][nt][1]);
+              mma(acc[m][nt], l0, l1, l2, l3, bh[ks][nt][0], bh[ks][nt][1]);
+              mma(acc[m][nt], h0, h1, h2, h3, bl[ks][nt][0], bl[ks][nt][1]);
+            }
           }
         }
       }
-      // C[tile][c]: c0,c1 -> tile g, c = 8nt + 2q (+1) = row 2nt + (q>>1), cols 2(q&1)..
+      // C: m-tile m, frag (0,1) -> tile 4g+2m, (2,3) -> tile 4g+2m+1; c = 8nt + 2q (+1) =
+      // tile row 2nt + (q>>1), cols 2(q&1), 2(q&1)+1.
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int a = 2 * nt + (q >> 1), b = 2 * (q & 1);
+      for (int m = 0; m < 2; ++m)
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int64_t J = J0 + 16 * mi + g + 8 * t;
-          Tout* dst = out + (I * 4 + a) * ldo + J * 4 + b;
-          if constexpr (sizeof(Tout) == 2)
-            *reinterpret_cast<uint32_t*>(dst) = pack2(acc[nt][2 * t], acc[nt][2 * t + 1]);
-          else
-            *reinterpret_cast<float2*>(dst) = make_float2(acc[nt][2 * t], acc[nt][2 * t + 1]);
+        for (int nt = 0; nt < 2; ++nt) {
+          const int a = 2 * nt + (q >> 1), b = 2 * (q & 1);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int64_t J = J0 + 32 * gi + 4 * g + 2 * m + t;
+            Tout* dst = out + (I * 4 + a) * ldo + J * 4 + b;
+            if constexpr (sizeof(Tout) == 2)
+              *reinterpret_cast<uint32_t*>(dst) = pack2(acc[m][nt][2 * t], acc[m][nt][2 * t + 1]);
+            else
+              *reinterpret_cast<float2*>(dst) = make_float2(acc[m][nt][2 * t], acc[m][nt][2 * t + 1]);
+          }
         }
+      if constexpr (RED) {
+        const __nv_bfloat16* xg = xr + I * 4 * ldr + (J0 + 32 * gi) * 4;
+        R.step(zrow + 32 * gi, ntiles, Q, xg, ldr);
+        R.step(zrow + 32 * gi + 16, ntiles, Q, xg + 64, ldr);
       }
-      if constexpr (RED) R.step(zrow + 16 * mi, ntiles, Q, xr + I * 4 * ldr + (J0 + 16 * mi) * 4, ldr);
     }
   }
   if constexpr (RED) R.finish(sred, Q, red_partial);
@@ -407,7 +423,7 @@ cudaError_t tiles_to_planes_mma(const void* m, int mdt, int64_t ldm, int64_t br,
 cudaError_t planes_to_tiles_mma(const void* in, int idt, int Q, int64_t br, int64_t bc,
                                 const float* coef, void* out, int odt, int64_t ldo, const void* rm,
                                 int rdt, int64_t ldr, float* ro, float* rw, cudaStream_t s) {
-  if (odt != kBF16 || bc % 16 || ldo % 8 || Q > 64 || !al16(in) || !al16(out))
+  if (odt != kBF16 || bc % 32 || ldo % 8 || Q > 64 || !al16(in) || !al16(out))
     return cudaErrorNotSupported;
   if (rm && (rdt != kBF16 || Q > 32 || ldr % 8 || !al16(rm))) return cudaErrorNotSupported;
   if (idt == kF32) {
