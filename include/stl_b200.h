@@ -110,7 +110,8 @@ STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const
                 void* stream);
 
 /* A/B switches (host-only): bit 0 = enable the decode-fused forward (default on);
- * bit 1 = force the FFMA tile transforms instead of the tensor-core (mma.sync) ones. */
+ * bit 1 = force the FFMA tile transforms instead of the tensor-core (mma.sync) ones;
+ * bit 2 = also use the tensor-core decode (experimental). */
 STL_API int stl_set_fusion(int enabled);
 
 /*

@@ -155,7 +155,8 @@ bool fused_forward_shape(int64_t M, int64_t K, int64_t N, int t, int r, int dtyp
 
 int stl_set_fusion(int enabled) {
   g_fusion = (enabled & 1) != 0;
-  stl::set_transform_mma((enabled & 2) == 0);  // bit 1 = force the FFMA transforms
+  stl::set_transform_mma((enabled & 2) == 0);         // bit 1 = force the FFMA transforms
+  stl::set_transform_mma_decode((enabled & 4) != 0);  // bit 2 = mma decode (experimental)
   return STL_OK;
 }
 

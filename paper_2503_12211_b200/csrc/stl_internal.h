@@ -72,6 +72,7 @@ cudaError_t planes_to_tiles4(const void* in, int idt, int Q, int64_t br, int64_t
 // Tensor-core (mma.sync) t = 4 transforms (stl_transform_mma.cu); set_transform_mma(false)
 // routes t = 4 to the FFMA kernels (A/B testing).
 void set_transform_mma(bool on);
+void set_transform_mma_decode(bool on);
 cudaError_t tiles_to_planes_mma(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
                                 const float* coef, int P, void* out, int odt, const void* rp,
                                 int rdt, float* ro, float* rw, cudaStream_t s);

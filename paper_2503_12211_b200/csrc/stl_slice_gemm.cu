@@ -258,20 +258,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 128 rows of A and its BN/2 columns of B (half the B bytes per SM of the 1-CTA kernel, and
 // 32 KB stages -> a 6-deep ring); the even CTA issues tcgen05.mma.cta_group::2 for both, and
 // each CTA's epilogue drains its own 128 TMEM lanes.
-template <int BN>
+template <int BN, bool DUAL>
 struct Smem2 {
-  static constexpr int kStages = BN == 256 ? 6 : 8;
+  // ring depth chosen so ring + epilogue staging fits the 227 KB opt-in limit
+  static constexpr int kStages = BN == 256 ? (DUAL ? 5 : 6) : (DUAL ? 7 : 8);
   static constexpr uint32_t kABytes = 128 * kBK * 2;
   static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
-  static constexpr uint32_t kBarOffset = kStages * (kABytes + kBBytes);
+  static constexpr uint32_t kRing = kStages * (kABytes + kBBytes);
+  // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B fp32 [+ 32 x 64 B bf16 copy])
+  static constexpr uint32_t kStageF = 32 * 128, kStageH = 32 * 64;
+  static constexpr uint32_t kWarpStage = 2 * (kStageF + (DUAL ? kStageH : 0));
+  static constexpr uint32_t kBarOffset = kRing + 4 * kWarpStage;
   static constexpr uint32_t kTotal = kBarOffset + 512 + 1024;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool DUAL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     slice_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA,
-                          const __grid_constant__ CUtensorMap tmB, EpiArgs args) {
-  using S = Smem2<BN>;
+                          const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmC,
+                          const __grid_constant__ CUtensorMap tmC2, EpiArgs args) {
+  using S = Smem2<BN, DUAL>;
   constexpr int kSt = S::kStages;
   constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(256, BN, A_MN, B_MN);
   constexpr uint32_t kTmemCols = (2 * BN <= 256) ? 256 : 512;
@@ -397,9 +404,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
+    // TMEM -> registers -> 128B-swizzled smem (32 rows x 32 fp32 per warp and chunk) -> TMA
+    // bulk store; TMA clips rows >= M / cols >= N. Two staging buffers per warp.
     const int q = warp & 3;
-    const bool c_vec = (N % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.c) & 15) == 0) &&
-                       (args.c_bf16 ? (N % 8 == 0) : true);
+    uint8_t* stage_base = smem + S::kRing + q * S::kWarpStage;
+    int chunk_no = 0;
     int it = 0;
     for (int tile = cluster; tile < total; tile += nclusters, ++it) {
       const int p = tile / per_slice;
@@ -410,30 +419,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row = mb * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
-      const size_t row_off = (static_cast<size_t>(p) * M + row) * static_cast<size_t>(N);
+      const int row0 = mb * 256 + static_cast<int>(rank) * 128 + q * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < BN; c += 32, ++chunk_no) {
         uint32_t v[32];
         __syncwarp();
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c,
                                 v);
+        const int buf = chunk_no & 1;
+        uint8_t* sf = stage_base + buf * (S::kStageF + (DUAL ? S::kStageH : 0));
+        // the TMA store that last read this buffer (two chunks ago) must be done reading
+        if (lane == 0) ptx::bulk_wait_read<1>();
+        __syncwarp();
         ptx::tmem_ld_wait();
-        const int col0 = nb * BN + c;
-        if (row < M && col0 < N) {
-          if (args.c_bf16)
-            store_row_chunk(reinterpret_cast<__nv_bfloat16*>(args.c) + row_off + col0, v,
-                            N - col0, c_vec);
-          else
-            store_row_chunk(reinterpret_cast<float*>(args.c) + row_off + col0, v, N - col0,
-                            c_vec);
-          if (args.c2) store_row_chunk(args.c2 + row_off + col0, v, N - col0, N % 8 == 0);
+        if (nb * BN + c < N && row0 < M) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(sf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          if constexpr (DUAL) {
+            uint8_t* sh = sf + S::kStageF;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * e]),
+                                                         __uint_as_float(v[8 * j + 2 * e + 1]));
+                w[e] = *reinterpret_cast<uint32_t*>(&h);
+              }
+              *reinterpret_cast<uint4*>(sh + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_3d(&tmC, sf, nb * BN + c, row0, p);
+            if constexpr (DUAL) ptx::tma_store_3d(&tmC2, sf + S::kStageF, nb * BN + c, row0, p);
+            ptx::bulk_commit();
+          }
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
     }
+    if (lane == 0) ptx::bulk_wait_all();
   }
 
   ptx::tc_fence_before();
@@ -487,24 +520,49 @@ cudaError_t launch_tc(const SliceGemmProblem& pb, cudaStream_t s) {
 }
 
 
-template <int BN, bool A_MN, bool B_MN>
+bool make_out_tmap(CUtensorMap* m, const void* base, bool bf16, uint64_t N, uint64_t M,
+                   uint64_t r) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  const uint64_t es = bf16 ? 2 : 4;
+  cuuint64_t dims[3] = {N, M, r};
+  cuuint64_t strides[2] = {N * es, N * M * es};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult res = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                    const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN, bool DUAL>
 cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc, tc2;
   const uint64_t M = pb.M, N = pb.N, K = pb.K, r = pb.r;
   bool ok = A_MN ? make_tmap(&ta, pb.a, M, K, r, kBK) : make_tmap(&ta, pb.a, K, M, r, 128);
   ok = ok && (B_MN ? make_tmap(&tb, pb.b, N, K, r, kBK) : make_tmap(&tb, pb.b, K, N, r, BN / 2));
+  ok = ok && make_out_tmap(&tc, pb.c, false, N, M, r);
+  if (DUAL) ok = ok && make_out_tmap(&tc2, pb.c2, true, N, M, r);
+  else tc2 = tc;
   if (!ok) return cudaErrorInvalidValue;
-  auto kern = slice_gemm_tc2_kernel<BN, A_MN, B_MN>;
-  const int smem = Smem2<BN>::kTotal;
+  auto kern = slice_gemm_tc2_kernel<BN, A_MN, B_MN, DUAL>;
+  const int smem = Smem2<BN, DUAL>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t tiles = r * ((M + 255) / 256) * ((N + BN - 1) / BN);
   const int pairs = sm_count() / 2;
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
-  EpiArgs ea{pb.c, pb.c_dtype == kBF16 ? 1 : 0, pb.r, static_cast<int>(M), static_cast<int>(N),
-             static_cast<int>(K), static_cast<__nv_bfloat16*>(pb.c2)};
-  kern<<<grid, kThreads, smem, s>>>(ta, tb, ea);
+  EpiArgs ea{pb.c, 0, pb.r, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
+             static_cast<__nv_bfloat16*>(pb.c2)};
+  kern<<<grid, kThreads, smem, s>>>(ta, tb, tc, tc2, ea);
   return cudaGetLastError();
+}
+
+template <int BN, bool A_MN, bool B_MN>
+cudaError_t launch_tc2_any(const SliceGemmProblem& pb, cudaStream_t s) {
+  return pb.c2 ? launch_tc2<BN, A_MN, B_MN, true>(pb, s) : launch_tc2<BN, A_MN, B_MN, false>(pb, s);
 }
 
 }  // namespace
@@ -553,17 +611,22 @@ cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {
     const char* e = getenv("STL_GEMM_1CTA");
     return e ? atoi(e) : 0;
   }();
-  if (pb.M > 128 && !force1) {
+  // The pair kernel stores C with TMA (fp32 output, 16-byte aligned rows); other cases use the
+  // 1-CTA kernel's direct-store epilogue.
+  const bool pair_ok = pb.M > 128 && !force1 && pb.c_dtype == kF32 && pb.N % 4 == 0 &&
+                       (reinterpret_cast<uintptr_t>(pb.c) & 15) == 0 &&
+                       (!pb.c2 || (pb.N % 8 == 0 && (reinterpret_cast<uintptr_t>(pb.c2) & 15) == 0));
+  if (pair_ok) {
     if (pb.N <= 128) {
-      if (!a_mn && !b_mn) return launch_tc2<128, false, false>(pb, s);
-      if (!a_mn && b_mn) return launch_tc2<128, false, true>(pb, s);
-      if (a_mn && !b_mn) return launch_tc2<128, true, false>(pb, s);
-      return launch_tc2<128, true, true>(pb, s);
+      if (!a_mn && !b_mn) return launch_tc2_any<128, false, false>(pb, s);
+      if (!a_mn && b_mn) return launch_tc2_any<128, false, true>(pb, s);
+      if (a_mn && !b_mn) return launch_tc2_any<128, true, false>(pb, s);
+      return launch_tc2_any<128, true, true>(pb, s);
     }
-    if (!a_mn && !b_mn) return launch_tc2<256, false, false>(pb, s);
-    if (!a_mn && b_mn) return launch_tc2<256, false, true>(pb, s);
-    if (a_mn && !b_mn) return launch_tc2<256, true, false>(pb, s);
-    return launch_tc2<256, true, true>(pb, s);
+    if (!a_mn && !b_mn) return launch_tc2_any<256, false, false>(pb, s);
+    if (!a_mn && b_mn) return launch_tc2_any<256, false, true>(pb, s);
+    if (a_mn && !b_mn) return launch_tc2_any<256, true, false>(pb, s);
+    return launch_tc2_any<256, true, true>(pb, s);
   }
   const bool narrow = pb.N <= 128;
   if (narrow) {

@@ -381,7 +381,9 @@ cudaError_t p2t_dispatch(const void* in, int idt, int Q, int64_t br, int64_t bc,
 }  // namespace
 
 bool g_use_mma = true;
+bool g_use_mma_decode = false;  // mma decode is slower than FFMA today (scattered stores)
 void set_transform_mma(bool on) { g_use_mma = on; }
+void set_transform_mma_decode(bool on) { g_use_mma_decode = on; }
 
 cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br, int64_t bc,
                             int t, const float* coef, int P, void* out, int out_dtype,
@@ -412,7 +414,7 @@ cudaError_t planes_to_tiles(const void* in, int in_dtype, int Q, int64_t br, int
                             const void* red_m, int red_dtype, int64_t ldr, float* red_out,
                             float* red_ws, cudaStream_t s) {
   if (br * bc == 0) return cudaSuccess;
-  if (t == 4 && g_use_mma) {
+  if (t == 4 && g_use_mma && g_use_mma_decode) {
     cudaError_t e = planes_to_tiles_mma(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m,
                                         red_dtype, ldr, red_out, red_ws, s);
     if (e != cudaErrorNotSupported) return e;

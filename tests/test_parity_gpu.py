@@ -409,7 +409,7 @@ def test_mma_transforms_match_ffma(M, K, N, r):
     layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
     outs = {}
     try:
-        for mode in (2, 0):  # bit 1: FFMA transforms; bit 0 off: unfused forward
+        for mode in (2, 4):  # bit 1: FFMA transforms; bit 2: mma decode; bit 0 off: unfused
             _lib.load().stl_set_fusion(mode)
             y, cache = stl._layer_forward_cached(layer, x_dev)
             outs[mode] = (y, cache.u, cache.y_enc) + tuple(stl._layer_backward(layer, cache, gy_dev))
@@ -421,6 +421,6 @@ def test_mma_transforms_match_ffma(M, K, N, r):
         tuple(O.layer_backward(w64, e_x, d, cache_ref, gy64, t))
     names = ("y", "u", "y_enc", "g_ex", "g_d", "g_w", "g_x")
     for i, name in enumerate(names):
-        a, b = outs[0][i], outs[2][i]
+        a, b = outs[4][i], outs[2][i]
         assert rel(a, b) <= 2e-3, (name, rel(a, b))
         assert rel(a, refs[i]) <= BF16_TOL, (name, rel(a, refs[i]))
