@@ -99,8 +99,8 @@ STL_API int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_lay
  *                cache `y_enc` for stl_backward; fp32 in fp32 mode, bf16 in bf16 mode);
  *   scratch: device workspace of at least stl_forward_scratch_bytes(...) bytes.
  *   M, K, N must be multiples of t (ShapeError otherwise, as the reference).
- * bf16 with t = 4 runs the decode-fused tcgen05 kernel (slice products stay in L2); other
- * cases run encode -> slice GEMM -> decode with fp32 slice products in `scratch`.
+ * Default path: encode -> slice GEMM -> decode with fp32 slice products in `scratch`; with
+ * stl_set_fusion bit 0, bf16 t = 4 runs the decode-fused tcgen05 kernel instead.
  */
 STL_API int64_t stl_forward_scratch_bytes(int64_t M, int64_t K, int64_t N, int t, int r,
                                           int dtype);
@@ -109,7 +109,8 @@ STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const
                 void* x_enc_ws, void* y_enc_cache, void* scratch, int64_t scratch_bytes,
                 void* stream);
 
-/* A/B switches (host-only): bit 0 = enable the decode-fused forward (default on);
+/* A/B switches (host-only): bit 0 = enable the decode-fused forward (default off:
+ * it is slower than encode + GEMM + decode today);
  * bit 1 = force the FFMA tile transforms instead of the tensor-core (mma.sync) ones;
  * bit 2 = also use the tensor-core decode (experimental). */
 STL_API int stl_set_fusion(int enabled);

@@ -145,7 +145,7 @@ int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_layout, voi
 }
 
 namespace {
-bool g_fusion = true;
+bool g_fusion = false;  // decode-fused forward is opt-in until it beats the unfused path
 
 bool fused_forward_shape(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
   if (!g_fusion || t != 4 || dtype != STL_BF16) return false;

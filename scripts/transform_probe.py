@@ -33,4 +33,4 @@ for mode in (0, 2, 1, 3):
         agg[name] = agg.get(name, 0) + ms / n
     print(json.dumps({"mode": mode, "fused": mode & 1, "ffma": (mode >> 1) & 1,
                       "ms_step": e0.elapsed_time(e1) / n, "kernels_ms": {k: round(v, 4) for k, v in agg.items()}}))
-lib.stl_set_fusion(1)
+lib.stl_set_fusion(0)

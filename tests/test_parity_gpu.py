@@ -381,7 +381,7 @@ def test_fused_decode_matches_unfused_and_oracle(M, K, N, r):
         stl.set_fusion(True)
         y_f, c_f = stl._layer_forward_cached(layer, x_dev)
     finally:
-        stl.set_fusion(True)
+        stl.set_fusion(False)
     torch.cuda.synchronize()
     assert rel(y_f, y_u) <= 1e-3  # same math, different summation order / bf16 rounding
     assert torch.equal(c_f.u, c_u.u)
@@ -414,7 +414,7 @@ def test_mma_transforms_match_ffma(M, K, N, r):
             y, cache = stl._layer_forward_cached(layer, x_dev)
             outs[mode] = (y, cache.u, cache.y_enc) + tuple(stl._layer_backward(layer, cache, gy_dev))
     finally:
-        _lib.load().stl_set_fusion(1)
+        _lib.load().stl_set_fusion(0)
     torch.cuda.synchronize()
     y_ref, cache_ref = O.layer_forward_cached(x64, w64, e_x, d, t)
     refs = (y_ref, cache_ref[1].transpose(2, 0, 1), cache_ref[2].transpose(2, 0, 1)) + \
