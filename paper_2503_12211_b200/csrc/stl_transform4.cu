@@ -18,8 +18,8 @@ namespace {
 
 constexpr int kThreads4 = 128;
 constexpr int kChunk = 8;                      // planes loaded per batch
-constexpr int kStageTiles = 128;               // tiles per warp per reduction round
-constexpr int kStageStride = kStageTiles + 8;  // bf16 elements per staged row (conflict-free)
+// Reducer staging: a warp stages 32 * TPT tiles per round (TPT tiles per lane), rows padded by
+// 8 bf16 so ldmatrix row addresses spread over all banks.
 
 template <typename T> struct Vec4;  // four consecutive elements
 template <> struct Vec4<float> {
@@ -91,7 +91,10 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
 
 // Per-warp tensor-core reducer for red[p][c] (p < P <= 32, c < 16) over staged tiles.
 // Staging (bf16, row stride kStageStride): hi[P] rows, lo[P] rows, x[16] rows, one zero row.
+template <int TPT>
 struct MmaReducer {
+  static constexpr int kStageTiles = 32 * TPT;
+  static constexpr int kStageStride = kStageTiles + 8;
   __nv_bfloat16* base;  // this warp's staging area
   int P;
   float acc[2][2][4];   // [m-tile (p 0-15, 16-31)][n-tile (c 0-7, 8-15)][fragment]
@@ -115,32 +118,36 @@ struct MmaReducer {
   __device__ __nv_bfloat16* lo(int p) const { return base + (P + p) * kStageStride; }
   __device__ __nv_bfloat16* xr(int c) const { return base + (2 * P + c) * kStageStride; }
 
-  // Lane `lane` owns staged tiles 4*lane .. 4*lane+3.
-  __device__ void stage_plane(int p, const float (&v)[4]) {
-    const int col = 4 * (threadIdx.x & 31);
-    float h[4], l[4];
+  // Lane `lane` owns staged tiles TPT*lane .. TPT*lane+TPT-1.
+  __device__ void stage_plane(int p, const float (&v)[TPT]) {
+    const int col = TPT * (threadIdx.x & 31);
+    uint32_t uh[TPT / 2], ul[TPT / 2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      h[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
-      l[i] = v[i] - h[i];
+    for (int i = 0; i < TPT / 2; ++i) {
+      const float h0 = __bfloat162float(__float2bfloat16_rn(v[2 * i]));
+      const float h1 = __bfloat162float(__float2bfloat16_rn(v[2 * i + 1]));
+      uh[i] = pack_bf16(h0, h1);
+      ul[i] = pack_bf16(v[2 * i] - h0, v[2 * i + 1] - h1);
     }
-    uint2 uh, ul;
-    uh.x = pack_bf16(h[0], h[1]);
-    uh.y = pack_bf16(h[2], h[3]);
-    ul.x = pack_bf16(l[0], l[1]);
-    ul.y = pack_bf16(l[2], l[3]);
-    *reinterpret_cast<uint2*>(hi(p) + col) = uh;
-    *reinterpret_cast<uint2*>(lo(p) + col) = ul;
+    if constexpr (TPT == 4) {
+      *reinterpret_cast<uint2*>(hi(p) + col) = make_uint2(uh[0], uh[1]);
+      *reinterpret_cast<uint2*>(lo(p) + col) = make_uint2(ul[0], ul[1]);
+    } else {
+      *reinterpret_cast<uint32_t*>(hi(p) + col) = uh[0];
+      *reinterpret_cast<uint32_t*>(lo(p) + col) = ul[0];
+    }
   }
-  // x[tile][c] for the lane's 4 tiles.
-  __device__ void stage_tiles(const float (&x)[4][16]) {
-    const int col = 4 * (threadIdx.x & 31);
+  // x[tile][c] for the lane's TPT tiles.
+  __device__ void stage_tiles(const float (&x)[TPT][16]) {
+    const int col = TPT * (threadIdx.x & 31);
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-      uint2 u;
-      u.x = pack_bf16(x[0][c], x[1][c]);
-      u.y = pack_bf16(x[2][c], x[3][c]);
-      *reinterpret_cast<uint2*>(xr(c) + col) = u;
+      if constexpr (TPT == 4) {
+        *reinterpret_cast<uint2*>(xr(c) + col) =
+            make_uint2(pack_bf16(x[0][c], x[1][c]), pack_bf16(x[2][c], x[3][c]));
+      } else {
+        *reinterpret_cast<uint32_t*>(xr(c) + col) = pack_bf16(x[0][c], x[1][c]);
+      }
     }
   }
   __device__ void accumulate() {
@@ -201,16 +208,17 @@ struct MmaReducer {
 
 // Shared-memory carve-up: coefficients (P*16 floats), per-warp reducer staging, final sums.
 __host__ __device__ inline size_t coef_bytes(int P) { return ((P * 16 * 4) + 15) / 16 * 16; }
+template <int TPT>
 __host__ __device__ inline size_t stage_bytes(int P) {
-  return size_t(4) * (2 * P + 17) * kStageStride * 2;
+  return size_t(4) * (2 * P + 17) * (32 * TPT + 8) * 2;
 }
 __host__ __device__ inline size_t red_bytes(int P) { return size_t(4) * P * 16 * 4; }
 
-template <bool RED>
-__device__ __forceinline__ void finish_partial(MmaReducer& R, unsigned char* smem, int P,
+template <bool RED, int TPT>
+__device__ __forceinline__ void finish_partial(MmaReducer<TPT>& R, unsigned char* smem, int P,
                                                float* __restrict__ red_partial) {
   if constexpr (RED) {
-    float* red = reinterpret_cast<float*>(smem + coef_bytes(P) + stage_bytes(P));
+    float* red = reinterpret_cast<float*>(smem + coef_bytes(P) + stage_bytes<TPT>(P));
     const int warp = threadIdx.x >> 5;
     R.dump(red + warp * P * 16);
     __syncthreads();
@@ -230,10 +238,10 @@ __global__ void __launch_bounds__(kThreads4)
   extern __shared__ __align__(16) unsigned char smem[];
   float* sc = reinterpret_cast<float*>(smem);
   for (int i = threadIdx.x; i < P * 16; i += kThreads4) sc[i] = coef[i];
-  MmaReducer R;
+  MmaReducer<4> R;
   if constexpr (RED) {
     __nv_bfloat16* st = reinterpret_cast<__nv_bfloat16*>(smem + coef_bytes(P)) +
-                        (threadIdx.x >> 5) * MmaReducer::stage_elems(P);
+                        (threadIdx.x >> 5) * MmaReducer<4>::stage_elems(P);
     R.init(st, P);
   }
   __syncthreads();
@@ -299,26 +307,65 @@ __global__ void __launch_bounds__(kThreads4)
       R.accumulate();
     }
   }
-  finish_partial<RED>(R, smem, P, red_partial);
+  finish_partial<RED, 4>(R, smem, P, red_partial);
 }
 
 // decode: out tile(I, J)[c] = sum_q coef[q][c] * in[q][I][J];  RED: red[q][c] += in[q] * tile'.
-template <typename Tin, typename Tout, bool RED, typename Tr>
-__global__ void __launch_bounds__(kThreads4)
+// One thread owns TPT horizontally adjacent tiles (TPT = 2 keeps registers low enough for
+// ~24 resident warps per SM, which this HBM-bound kernel needs to hide latency).
+template <int TPT, typename T> struct VecN;
+template <> struct VecN<2, float> {
+  __device__ static void load(const float* p, float (&v)[2]) {
+    const float2 u = *reinterpret_cast<const float2*>(p);
+    v[0] = u.x; v[1] = u.y;
+  }
+};
+template <> struct VecN<2, __nv_bfloat16> {
+  __device__ static void load(const __nv_bfloat16* p, float (&v)[2]) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+    v[0] = f.x; v[1] = f.y;
+  }
+};
+template <typename T> struct VecN<4, T> {
+  __device__ static void load(const T* p, float (&v)[4]) { Vec4<T>::load(p, v); }
+};
+// a tile-row segment of TPT tiles (4*TPT elements)
+template <int TPT, typename T>
+__device__ __forceinline__ void store_seg4(T* p, const float (&v)[4 * TPT]) {
+#pragma unroll
+  for (int i = 0; i < TPT; ++i) {
+    const float w[4] = {v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]};
+    Vec4<T>::store(p + 4 * i, w);
+  }
+}
+template <int TPT, typename T>
+__device__ __forceinline__ void load_seg4(const T* p, float (&v)[4 * TPT]) {
+#pragma unroll
+  for (int i = 0; i < TPT; ++i) {
+    float w[4];
+    Vec4<T>::load(p + 4 * i, w);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[4 * i + j] = w[j];
+  }
+}
+
+template <int TPT, typename Tin, typename Tout, bool RED, typename Tr>
+__global__ void __launch_bounds__(kThreads4, RED ? 4 : 6)
     k_decode4(const Tin* __restrict__ in, int Q, int64_t br, int64_t bc,
               const float* __restrict__ coef, Tout* __restrict__ out, int64_t ldo,
               const Tr* __restrict__ red_m, int64_t ldr, float* __restrict__ red_partial) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int kCh = kChunk;
   float* sc = reinterpret_cast<float*>(smem);
   for (int i = threadIdx.x; i < Q * 16; i += kThreads4) sc[i] = coef[i];
-  MmaReducer R;
+  MmaReducer<TPT> R;
   if constexpr (RED) {
     __nv_bfloat16* st = reinterpret_cast<__nv_bfloat16*>(smem + coef_bytes(Q)) +
-                        (threadIdx.x >> 5) * MmaReducer::stage_elems(Q);
+                        (threadIdx.x >> 5) * MmaReducer<TPT>::stage_elems(Q);
     R.init(st, Q);
   }
   __syncthreads();
-  const int64_t bq = bc >> 2, nq = br * bq, ntiles = br * bc;
+  const int64_t bq = bc / TPT, nq = br * bq, ntiles = br * bc;
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads4; base < nq;
        base += static_cast<int64_t>(gridDim.x) * kThreads4) {
     const int64_t qd = base + threadIdx.x;
@@ -326,27 +373,26 @@ __global__ void __launch_bounds__(kThreads4)
     int64_t I = 0, J0 = 0, off = 0;
     if (valid) {
       I = qd / bq;
-      J0 = (qd - I * bq) * 4;
+      J0 = (qd - I * bq) * TPT;
       off = I * bc + J0;
-      float acc[4][16];
+      float acc[TPT][16];
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < TPT; ++t)
 #pragma unroll
         for (int c = 0; c < 16; ++c) acc[t][c] = 0.f;
-      // Planes are consumed in chunks of kChunk: all loads of a chunk are issued before any
-      // use, so each thread keeps kChunk x 16 bytes in flight.
-      for (int q0 = 0; q0 < Q; q0 += kChunk) {
-        float v[kChunk][4];
+      for (int q0 = 0; q0 < Q; q0 += kCh) {
+        float v[kCh][TPT];
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
+        for (int j = 0; j < kCh; ++j) {
           if (q0 + j < Q) {
-            Vec4<Tin>::load(in + (q0 + j) * ntiles + off, v[j]);
+            VecN<TPT, Tin>::load(in + (q0 + j) * ntiles + off, v[j]);
           } else {
-            v[j][0] = v[j][1] = v[j][2] = v[j][3] = 0.f;
+#pragma unroll
+            for (int t = 0; t < TPT; ++t) v[j][t] = 0.f;
           }
         }
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
+        for (int j = 0; j < kCh; ++j) {
           if (q0 + j >= Q) break;
           if constexpr (RED) R.stage_plane(q0 + j, v[j]);
           const float4* cp = reinterpret_cast<const float4*>(sc + (q0 + j) * 16);
@@ -357,7 +403,7 @@ __global__ void __launch_bounds__(kThreads4)
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
-              for (int t = 0; t < 4; ++t)
+              for (int t = 0; t < TPT; ++t)
                 acc[t][4 * i + jj] = fmaf(cf[jj], v[j][t], acc[t][4 * i + jj]);
           }
         }
@@ -365,29 +411,31 @@ __global__ void __launch_bounds__(kThreads4)
       Tout* dst = out + I * 4 * ldo + J0 * 4;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        float row[16];
+        float row[4 * TPT];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) row[e] = acc[e >> 2][a * 4 + (e & 3)];
-        store_row16(dst + a * ldo, row);
+        for (int e = 0; e < 4 * TPT; ++e) row[e] = acc[e >> 2][a * 4 + (e & 3)];
+        store_seg4<TPT>(dst + a * ldo, row);
       }
     } else if constexpr (RED) {
-      const float z[4] = {0.f, 0.f, 0.f, 0.f};
+      float z[TPT];
+#pragma unroll
+      for (int t = 0; t < TPT; ++t) z[t] = 0.f;
       for (int q = 0; q < Q; ++q) R.stage_plane(q, z);
     }
     if constexpr (RED) {
-      float x[4][16];
+      float x[TPT][16];
       if (valid) {
         const Tr* src = red_m + I * 4 * ldr + J0 * 4;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          float row[16];
-          load_row16(src + a * ldr, row);
+          float row[4 * TPT];
+          load_seg4<TPT>(src + a * ldr, row);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) x[e >> 2][a * 4 + (e & 3)] = row[e];
+          for (int e = 0; e < 4 * TPT; ++e) x[e >> 2][a * 4 + (e & 3)] = row[e];
         }
       } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < TPT; ++t)
 #pragma unroll
           for (int c = 0; c < 16; ++c) x[t][c] = 0.f;
       }
@@ -395,7 +443,7 @@ __global__ void __launch_bounds__(kThreads4)
       R.accumulate();
     }
   }
-  finish_partial<RED>(R, smem, Q, red_partial);
+  finish_partial<RED, TPT>(R, smem, Q, red_partial);
 }
 
 // out[o] = sum_b partial[b][o]: one block per output, fixed-order tree (deterministic).
@@ -431,7 +479,7 @@ template <typename Tin, typename Tout, typename Tr>
 cudaError_t enc4_red(const void* m, int64_t ldm, int64_t br, int64_t bc, const float* coef, int P,
                      void* out, const void* rp, float* ro, float* rw, cudaStream_t s) {
   const int64_t nq = br * (bc / 4);
-  const size_t smem = coef_bytes(P) + stage_bytes(P) + red_bytes(P);
+  const size_t smem = coef_bytes(P) + stage_bytes<4>(P) + red_bytes(P);
   auto k = k_encode4<Tin, Tout, true, Tr>;
   if (cudaError_t e = prep(k, smem)) return e;
   const int grid = grid4(nq, sm_count() * 3);
@@ -463,19 +511,20 @@ cudaError_t enc4(const void* m, int64_t ldm, int64_t br, int64_t bc, const float
 template <typename Tin, typename Tout>
 cudaError_t dec4(const void* in, int Q, int64_t br, int64_t bc, const float* coef, void* out,
                  int64_t ldo, const void* rm, int64_t ldr, float* ro, float* rw, cudaStream_t s) {
-  const int64_t nq = br * (bc / 4);
+  constexpr int TPT = 2;
+  const int64_t nq = br * (bc / TPT);
   if (rm) {
-    const size_t smem = coef_bytes(Q) + stage_bytes(Q) + red_bytes(Q);
-    auto k = k_decode4<Tin, Tout, true, __nv_bfloat16>;
+    const size_t smem = coef_bytes(Q) + stage_bytes<TPT>(Q) + red_bytes(Q);
+    auto k = k_decode4<TPT, Tin, Tout, true, __nv_bfloat16>;
     if (cudaError_t e = prep(k, smem)) return e;
-    const int grid = grid4(nq, sm_count() * 3);
+    const int grid = grid4(nq, sm_count() * 5);
     k<<<grid, kThreads4, smem, s>>>(static_cast<const Tin*>(in), Q, br, bc, coef,
                                     static_cast<Tout*>(out), ldo,
                                     static_cast<const __nv_bfloat16*>(rm), ldr, rw);
     k_sum_partials_tree<<<Q * 16, 256, 0, s>>>(rw, grid, Q * 16, ro);
   } else {
     const size_t smem = coef_bytes(Q);
-    auto k = k_decode4<Tin, Tout, false, __nv_bfloat16>;
+    auto k = k_decode4<TPT, Tin, Tout, false, __nv_bfloat16>;
     if (cudaError_t e = prep(k, smem)) return e;
     k<<<grid4(nq, sm_count() * 16), kThreads4, smem, s>>>(
         static_cast<const Tin*>(in), Q, br, bc, coef, static_cast<Tout*>(out), ldo, nullptr, 0,
