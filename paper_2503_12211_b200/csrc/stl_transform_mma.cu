@@ -242,8 +242,10 @@ __global__ void __launch_bounds__(kThreadsM)
                  const float* __restrict__ coef, Tout* __restrict__ out, int64_t ldo,
                  const __nv_bfloat16* __restrict__ xr, int64_t ldr, float* __restrict__ red_partial) {
   extern __shared__ __align__(16) unsigned char smem[];
-  float* sred = reinterpret_cast<float*>(smem);
+  constexpr int kOutStride = 128 + (sizeof(Tout) == 2 ? 8 : 4);  // padded staged output row
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  Tout* ostage = reinterpret_cast<Tout*>(smem) + warp * 4 * kOutStride;
+  float* sred = reinterpret_cast<float*>(smem + kWarpsM * 4 * kOutStride * sizeof(Tout));
   const int KS = (Q + 15) >> 4;
   // D as B fragments (K = p, N = c): b0 = D[16ks+2q, +1][c], b1 = D[16ks+2q+8, +9][c], c = 8nt+g
   uint32_t bh[4][2][2], bl[4][2][2];
@@ -324,7 +326,9 @@ __global__ void __launch_bounds__(kThreadsM)
         }
       }
       // C: m-tile m, frag (0,1) -> tile 4g+2m, (2,3) -> tile 4g+2m+1; c = 8nt + 2q (+1) =
-      // tile row 2nt + (q>>1), cols 2(q&1), 2(q&1)+1.
+      // tile row 2nt + (q>>1), cols 2(q&1), 2(q&1)+1. Staged per warp as the 4 output rows of
+      // the 32-tile group (4 x 128 elements), then written as coalesced 256/512-byte rows.
+      __syncwarp();
 #pragma unroll
       for (int m = 0; m < 2; ++m)
 #pragma unroll
@@ -332,14 +336,23 @@ __global__ void __launch_bounds__(kThreadsM)
           const int a = 2 * nt + (q >> 1), b = 2 * (q & 1);
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            const int64_t J = J0 + 32 * gi + 4 * g + 2 * m + t;
-            Tout* dst = out + (I * 4 + a) * ldo + J * 4 + b;
+            Tout* d = ostage + a * kOutStride + (4 * g + 2 * m + t) * 4 + b;
             if constexpr (sizeof(Tout) == 2)
-              *reinterpret_cast<uint32_t*>(dst) = pack2(acc[m][nt][2 * t], acc[m][nt][2 * t + 1]);
+              *reinterpret_cast<uint32_t*>(d) = pack2(acc[m][nt][2 * t], acc[m][nt][2 * t + 1]);
             else
-              *reinterpret_cast<float2*>(dst) = make_float2(acc[m][nt][2 * t], acc[m][nt][2 * t + 1]);
+              *reinterpret_cast<float2*>(d) = make_float2(acc[m][nt][2 * t], acc[m][nt][2 * t + 1]);
           }
         }
+      __syncwarp();
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        Tout* dst = out + (I * 4 + a) * ldo + (J0 + 32 * gi) * 4 + 4 * lane;
+        const Tout* src = ostage + a * kOutStride + 4 * lane;
+        if constexpr (sizeof(Tout) == 2)
+          *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(src);
+        else
+          *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
+      }
       if constexpr (RED) {
         const __nv_bfloat16* xg = xr + I * 4 * ldr + (J0 + 32 * gi) * 4;
         R.step(zrow + 32 * gi, ntiles, Q, xg, ldr);
@@ -385,7 +398,8 @@ template <typename Tz, typename Tout, bool RED>
 cudaError_t launch_dec(const void* in, int Q, int64_t br, int64_t bc, const float* coef, void* out,
                        int64_t ldo, const void* rm, int64_t ldr, float* ro, float* rw,
                        cudaStream_t s) {
-  const size_t smem = RED ? kWarpsM * Q * 16 * 4 : 0;
+  constexpr int kOutStride = 128 + (sizeof(Tout) == 2 ? 8 : 4);
+  const size_t smem = kWarpsM * 4 * kOutStride * sizeof(Tout) + (RED ? kWarpsM * Q * 16 * 4 : 0);
   auto k = k_decode_mma<Tz, Tout, RED>;
   if (cudaError_t e = set_smem(k, smem)) return e;
   const int64_t ntasks = br * ((bc + kTaskTiles - 1) / kTaskTiles);
