@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kThreadsM)
 
 // ---------------------------------------------------------------------------------------------
 // decode: Q planes (fp32 or bf16) -> tiles. RED: g_ex += Z (x) X' (X' = bf16 matrix).
-template <typename Tz, typename Tout, bool RED>
+template <typename Tz, typename Tout, bool RED, int KST>
 __global__ void __launch_bounds__(kThreadsM)
     k_decode_mma(const Tz* __restrict__ z, int Q, int64_t br, int64_t bc,
                  const float* __restrict__ coef, Tout* __restrict__ out, int64_t ldo,
@@ -246,11 +246,10 @@ __global__ void __launch_bounds__(kThreadsM)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   Tout* ostage = reinterpret_cast<Tout*>(smem) + warp * 4 * kOutStride;
   float* sred = reinterpret_cast<float*>(smem + kWarpsM * 4 * kOutStride * sizeof(Tout));
-  const int KS = (Q + 15) >> 4;
   // D as B fragments (K = p, N = c): b0 = D[16ks+2q, +1][c], b1 = D[16ks+2q+8, +9][c], c = 8nt+g
-  uint32_t bh[4][2][2], bl[4][2][2];
+  uint32_t bh[KST][2][2], bl[KST][2][2];
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks)
+  for (int ks = 0; ks < KST; ++ks)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
@@ -274,30 +273,43 @@ __global__ void __launch_bounds__(kThreadsM)
     const Tz* zrow = z + I * bc + J0;
     // 32-tile groups; M rows permuted so thread (g, q) owns tiles 4g .. 4g+3 of the group:
     // m-tile A rows g, g+8 <-> tiles 4g, 4g+1; m-tile B rows g, g+8 <-> tiles 4g+2, 4g+3.
-    for (int gi = 0; gi < (nmt >> 1); ++gi) {
-      const Tz* zt = zrow + 32 * gi + 4 * g;
+    const int ngroups = nmt >> 1;
+    for (int gp = 0; gp < ngroups; gp += 2) {
+      // issue the loads of two 32-tile groups before any math (memory-level parallelism)
+      float vv[2][KST][4][4];  // [group][k-step][plane 2q, 2q+1, 2q+8, 2q+9][tile 4g + i]
+#pragma unroll
+      for (int gg = 0; gg < 2; ++gg) {
+        const bool gok = gp + gg < ngroups;
+        const Tz* zt = zrow + 32 * (gp + gg) + 4 * g;
+#pragma unroll
+        for (int ks = 0; ks < KST; ++ks)
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int p = 16 * ks + 2 * q + (h & 1) + 8 * (h >> 1);
+            float* v = vv[gg][ks][h];
+            if (gok && p < Q) {
+              if constexpr (sizeof(Tz) == 2) {
+                const uint2 u = *reinterpret_cast<const uint2*>(zt + p * ntiles);
+                const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+                const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+                v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
+              } else {
+                const float4 f = *reinterpret_cast<const float4*>(zt + p * ntiles);
+                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+              }
+            } else {
+              v[0] = v[1] = v[2] = v[3] = 0.f;
+            }
+          }
+      }
+#pragma unroll
+      for (int gg = 0; gg < 2; ++gg) {
+      const int gi = gp + gg;
+      if (gi >= ngroups) break;
       float acc[2][2][4] = {};  // [m-tile A/B][n-tile][frag]
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        if (ks >= KS) break;
-        float v[4][4];  // [plane 2q, 2q+1, 2q+8, 2q+9][tile 4g + i]
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int p = 16 * ks + 2 * q + (h & 1) + 8 * (h >> 1);
-          if (p < Q) {
-            if constexpr (sizeof(Tz) == 2) {
-              const uint2 u = *reinterpret_cast<const uint2*>(zt + p * ntiles);
-              const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-              const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-              v[h][0] = f0.x; v[h][1] = f0.y; v[h][2] = f1.x; v[h][3] = f1.y;
-            } else {
-              const float4 f = *reinterpret_cast<const float4*>(zt + p * ntiles);
-              v[h][0] = f.x; v[h][1] = f.y; v[h][2] = f.z; v[h][3] = f.w;
-            }
-          } else {
-            v[h][0] = v[h][1] = v[h][2] = v[h][3] = 0.f;
-          }
-        }
+      for (int ks = 0; ks < KST; ++ks) {
+        float (&v)[4][4] = vv[gg][ks];
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           // a0 = (tile 4g+2m, planes 2q, 2q+1), a1 = (tile 4g+2m+1, ...), a2/a3: planes 2q+8, +9
@@ -325,9 +337,6 @@ __global__ void __launch_bounds__(kThreadsM)
           }
         }
       }
-      // C: m-tile m, frag (0,1) -> tile 4g+2m, (2,3) -> tile 4g+2m+1; c = 8nt + 2q (+1) =
-      // tile row 2nt + (q>>1), cols 2(q&1), 2(q&1)+1. Staged per warp as the 4 output rows of
-      // the 32-tile group (4 x 128 elements), then written as coalesced 256/512-byte rows.
       __syncwarp();
 #pragma unroll
       for (int m = 0; m < 2; ++m)
@@ -357,6 +366,7 @@ __global__ void __launch_bounds__(kThreadsM)
         const __nv_bfloat16* xg = xr + I * 4 * ldr + (J0 + 32 * gi) * 4;
         R.step(zrow + 32 * gi, ntiles, Q, xg, ldr);
         R.step(zrow + 32 * gi + 16, ntiles, Q, xg + 64, ldr);
+      }
       }
     }
   }
@@ -394,13 +404,13 @@ cudaError_t launch_enc(const void* m, int64_t ldm, int64_t br, int64_t bc, const
   return cudaGetLastError();
 }
 
-template <typename Tz, typename Tout, bool RED>
-cudaError_t launch_dec(const void* in, int Q, int64_t br, int64_t bc, const float* coef, void* out,
-                       int64_t ldo, const void* rm, int64_t ldr, float* ro, float* rw,
-                       cudaStream_t s) {
+template <typename Tz, typename Tout, bool RED, int KST>
+cudaError_t launch_dec_k(const void* in, int Q, int64_t br, int64_t bc, const float* coef,
+                         void* out, int64_t ldo, const void* rm, int64_t ldr, float* ro, float* rw,
+                         cudaStream_t s) {
   constexpr int kOutStride = 128 + (sizeof(Tout) == 2 ? 8 : 4);
   const size_t smem = kWarpsM * 4 * kOutStride * sizeof(Tout) + (RED ? kWarpsM * Q * 16 * 4 : 0);
-  auto k = k_decode_mma<Tz, Tout, RED>;
+  auto k = k_decode_mma<Tz, Tout, RED, KST>;
   if (cudaError_t e = set_smem(k, smem)) return e;
   const int64_t ntasks = br * ((bc + kTaskTiles - 1) / kTaskTiles);
   const int grid = grid_m(ntasks, sm_count() * (RED ? 4 : 8));
@@ -409,6 +419,18 @@ cudaError_t launch_dec(const void* in, int Q, int64_t br, int64_t bc, const floa
                                   static_cast<const __nv_bfloat16*>(rm), ldr, rw);
   if (RED) return sum_partials(rw, grid, Q * 16, ro, s);
   return cudaGetLastError();
+}
+
+template <typename Tz, typename Tout, bool RED>
+cudaError_t launch_dec(const void* in, int Q, int64_t br, int64_t bc, const float* coef, void* out,
+                       int64_t ldo, const void* rm, int64_t ldr, float* ro, float* rw,
+                       cudaStream_t s) {
+  switch ((Q + 15) / 16) {
+    case 1: return launch_dec_k<Tz, Tout, RED, 1>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
+    case 2: return launch_dec_k<Tz, Tout, RED, 2>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
+    case 3: return launch_dec_k<Tz, Tout, RED, 3>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
+    default: return launch_dec_k<Tz, Tout, RED, 4>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
+  }
 }
 
 }  // namespace
