@@ -157,6 +157,7 @@ int stl_set_fusion(int enabled) {
   g_fusion = (enabled & 1) != 0;
   stl::set_transform_mma((enabled & 2) == 0);         // bit 1 = force the FFMA transforms
   stl::set_transform_mma_decode((enabled & 4) != 0);  // bit 2 = mma decode (experimental)
+  stl::set_transform_stream((enabled & 8) == 0);      // bit 3 = disable the streaming transforms
   return STL_OK;
 }
 

@@ -79,6 +79,16 @@ cudaError_t tiles_to_planes_mma(const void* m, int mdt, int64_t ldm, int64_t br,
 cudaError_t planes_to_tiles_mma(const void* in, int idt, int Q, int64_t br, int64_t bc,
                                 const float* coef, void* out, int odt, int64_t ldo, const void* rm,
                                 int rdt, int64_t ldr, float* ro, float* rw, cudaStream_t s);
+// HBM-streaming bulk-async t = 4 transforms (stl_stream.cu), tried first for t = 4;
+// cudaErrorNotSupported -> the kernels above. set_transform_stream(false) disables them.
+void set_transform_stream(bool on);
+cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
+                                   const float* coef, int P, void* out, int odt, const void* rp,
+                                   int rdt, float* ro, float* rw, cudaStream_t s);
+cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, int64_t bc,
+                                   const float* coef, void* out, int odt, int64_t ldo,
+                                   const void* rm, int rdt, int64_t ldr, float* ro, float* rw,
+                                   cudaStream_t s);
 // out[o] = sum_b partial[b * n + o], deterministic fixed-order tree.
 cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t s);
 cudaError_t compose_coefs(const float* a, const float* b, int r, int tt, float* out,

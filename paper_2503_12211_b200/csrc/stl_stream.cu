@@ -1,0 +1,654 @@
+// stl_stream.cu — HBM-streaming t = 4 tile transforms (the production bf16 path).
+//
+// The four per-layer tile transforms of the STL step, each one pass over HBM:
+//   kEnc    : planes[p][I][J] = sum_c E[p][c] tile(I, J)[c]          encode_tiles (snf_operator.py:80-85)
+//   kEncRed : kEnc, plus  R[p][c] += sum_tiles Z[p][tile] tile[c]     g_enc and g_d of _layer_backward
+//                                                                     (toy_network.py:100-101)
+//   kDec    : tile(I, J)[c] = sum_p Z[p][I][J] D[p][c]                decode_tiles (snf_operator.py:88-96)
+//   kDecRed : kDec, plus  R[p][c] += sum_tiles Z[p][tile] X[tile][c]  g_x and g_ex (toy_network.py:104-105)
+// Tiles follow the reference layout contract (dense_core.py:98-108): element c = 4a + b of
+// tile (I, J) is m[4I + a, 4J + b].
+//
+// B200 structure: one persistent CTA per SM = 1 producer warp + 8 consumer warps. A unit is a
+// row segment of up to 256 tiles (tile row I, tiles J0 .. J0+255): its 4 matrix rows are 4
+// contiguous 2 KB runs and each of its plane segments is one contiguous run, so the producer
+// moves a unit with cp.async.bulk (1-D bulk copies, completion on an mbarrier) into a
+// multi-stage shared-memory ring with padded rows (bank-conflict-free fragment loads). The
+// consumers run the per-tile change of basis on the tensor cores (mma.sync m16n8k16, bf16 in,
+// fp32 accumulate; fp32 operands split into bf16 hi + lo so products keep ~16 mantissa bits),
+// stage the output unit in shared memory and one thread writes it back with bulk stores.
+// Loads, math and stores of different units overlap; every byte is read and written once.
+// Reductions accumulate in MMA fragments per warp, are summed over warps in a fixed order and
+// over CTAs by a fixed-order tree (deterministic).
+#include <cstdio>
+#include "sm100_ptx.cuh"
+#include "stl_internal.h"
+
+namespace stl {
+namespace {
+
+enum Mode { kEnc = 0, kEncRed = 1, kDec = 2, kDecRed = 3 };
+
+constexpr int kT = 256;                     // tiles per unit
+constexpr int kCWarps = 8;                  // consumer warps
+constexpr int kCThreads = 32 * kCWarps;
+constexpr int kSThreads = kCThreads + 32;   // + producer warp
+constexpr int kMaxStages = 8;
+constexpr uint32_t kRowPad = 64;            // matrix rows: 16-word bank shift per row
+
+template <int MODE> constexpr bool has_rows() { return MODE != kDec; }
+template <int MODE> constexpr bool has_planes_in() { return MODE != kEnc; }
+template <int MODE> constexpr bool is_enc() { return MODE == kEnc || MODE == kEncRed; }
+template <int MODE> constexpr bool has_red() { return MODE == kEncRed || MODE == kDecRed; }
+
+struct Layout {
+  uint32_t pl_bytes;     // plane box of a stage (TMA, 128B-swizzled, 1024-aligned)
+  uint32_t row_stride, rows_bytes;  // padded matrix rows of a stage
+  uint32_t stage_bytes;
+  uint32_t out_stride, out_bytes;   // one output staging buffer
+  uint32_t red_bytes;
+  uint32_t nstages;
+  uint32_t total;                   // dynamic smem incl. barriers and alignment slack
+};
+
+__host__ __device__ inline uint32_t rup(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+template <int MODE, typename ZT>
+__host__ __device__ inline Layout make_layout(int P) {
+  Layout L{};
+  L.pl_bytes = has_planes_in<MODE>() ? rup(P * kT * sizeof(ZT), 1024) : 0;
+  L.row_stride = kT * 4 * 2 + kRowPad;
+  L.rows_bytes = has_rows<MODE>() ? 4 * L.row_stride : 0;
+  L.stage_bytes = rup(L.pl_bytes + L.rows_bytes, 1024);
+  if (is_enc<MODE>()) {
+    L.out_stride = 0;  // swizzled plane box
+    L.out_bytes = rup(P * kT * 2, 1024);
+  } else {
+    L.out_stride = kT * 4 * 2 + kRowPad;
+    L.out_bytes = rup(4 * L.out_stride, 1024);
+  }
+  L.red_bytes = has_red<MODE>() ? kCWarps * P * 16 * 4 : 0;
+  const uint32_t budget = 200 * 1024;
+  const uint32_t fixed = 2 * L.out_bytes + L.red_bytes;
+  uint32_t ns = (budget - fixed) / L.stage_bytes;
+  L.nstages = ns > kMaxStages ? kMaxStages : (ns < 2 ? 2 : ns);
+  L.total = L.nstages * L.stage_bytes + fixed + 2 * kMaxStages * 8 + 1024;
+  return L;
+}
+
+struct StreamArgs {
+  const __nv_bfloat16* mat;  // ENC*: input matrix; DEC_RED: reduction matrix X
+  int64_t ldm;
+  void* out;                 // DEC*: output matrix (ENC* planes go out through tm_out)
+  int64_t ldo;
+  const float* coef;         // P x 16 (encoder rows for ENC*, decoder rows for DEC*)
+  float* red_partial;        // [gridDim.x][P * 16]
+  int P;
+  int64_t br, bc;
+  int64_t upr;               // units per tile row
+  int64_t nunits;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                   reinterpret_cast<uint64_t>(dst)),
+               "r"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* m, uint64_t* bar, uint32_t dst,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, uint32_t src, int c0, int c1,
+                                             int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void cbar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kCThreads) : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.b16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds64f(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// fp32 pair -> bf16 hi pair + bf16 lo pair (x = hi + lo to ~2^-16 relative)
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  lo = pack2(x0 - hf.x, x1 - hf.y);
+}
+__device__ __forceinline__ void mma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                    uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// two bf16 from (lo16 of a, lo16 of b) -> packed pair
+__device__ __forceinline__ uint32_t pair16(uint32_t a, uint32_t b) { return a | (b << 16); }
+
+// A unit's planes in shared memory as the TMA box {W, P, T/W} lands them with 128-byte swizzle:
+// 128-byte rows indexed (chunk * P + p), chunk = t / W, W = 128 / sizeof(Z) tiles per row; the
+// 16-byte chunk index inside a row is XORed with (row & 7).
+template <int ZSZ>
+__device__ __forceinline__ uint32_t pl_addr(uint32_t base, int P, int p, int t) {
+  constexpr int W = 128 / ZSZ;
+  const uint32_t row = static_cast<uint32_t>((t / W) * P + p);
+  const uint32_t byte = static_cast<uint32_t>((t % W) * ZSZ);
+  return base + row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15));
+}
+
+// Swizzled plane-box offset of (plane p, tile t). Adding (16 ks + 8 h) planes to p adds
+// (16 ks + 8 h) * 128 bytes and leaves the XOR term unchanged, so per-thread offsets are computed
+// once for p < 8 and the plane-group steps become immediates.
+template <int ZSZ>
+__device__ __forceinline__ uint32_t pl_off(int P, int p, int t) {
+  return pl_addr<ZSZ>(0u, P, p, t);
+}
+
+// Work split of a 256-tile unit over the 8 consumer warps (offset tables below assume it):
+//   ENC n-tiles (8 tiles):  warp w -> n-tiles w + 8k, k < 4
+//   DEC m-tiles (16 tiles): warp w -> m-tiles w + 8k, k < 2
+//   RED k-steps (16 tiles): warp w -> k-steps w + 8k, k < 2
+static_assert(kT == 256 && kCWarps == 8, "offset tables assume 256-tile units and 8 warps");
+
+// ------------------------------------------------------------------ the kernel
+// MT = number of 16-plane groups (ceil(P / 16)), a template so every plane loop unrolls.
+template <int MODE, typename ZT, int MT>
+__global__ void __launch_bounds__(kSThreads, 1)
+    k_stream(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+             StreamArgs args, Layout L) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const uint32_t s_stages = ptx::smem_u32(smem);
+  const uint32_t s_out = s_stages + L.nstages * L.stage_bytes;
+  float* s_red = reinterpret_cast<float*>(smem + L.nstages * L.stage_bytes + 2 * L.out_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.nstages * L.stage_bytes +
+                                               2 * L.out_bytes + L.red_bytes);
+  uint64_t* empty = full + kMaxStages;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int P = args.P;
+  constexpr int ZSZ = sizeof(ZT);
+  const uint32_t nunits = static_cast<uint32_t>(args.nunits);
+  const uint32_t upr = static_cast<uint32_t>(args.upr);
+  const uint32_t bc = static_cast<uint32_t>(args.bc);
+
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < L.nstages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], kCWarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == kCWarps && lane == 0) {
+    if constexpr (has_planes_in<MODE>()) ptx::prefetch_tmap(&tm_in);
+    if constexpr (is_enc<MODE>()) ptx::prefetch_tmap(&tm_out);
+  }
+  __syncthreads();
+
+  if (warp == kCWarps) {
+    // ---------------------------------------------------------------- producer
+    // lane 0: the plane box (one 4-D TMA op); lanes 0..3: matrix row a (1-D bulk copy into a
+    // padded row).
+    uint32_t it = 0;
+    for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+      const uint32_t stage = it % L.nstages;
+      const uint32_t phase = (it / L.nstages) & 1;
+      const uint32_t I = u / upr;
+      const uint32_t J0 = (u - I * upr) * kT;
+      const uint32_t Tw = min(bc - J0, static_cast<uint32_t>(kT));
+      ptx::mbar_wait(&empty[stage], phase ^ 1);
+      const uint32_t rows_b = has_rows<MODE>() ? Tw * 8 : 0;
+      const uint32_t st = s_stages + stage * L.stage_bytes;
+      if (lane == 0) {
+        ptx::mbar_arrive_expect_tx(&full[stage],
+                                   4 * rows_b + (has_planes_in<MODE>() ? P * kT * ZSZ : 0));
+        if constexpr (has_planes_in<MODE>())
+          tma_load_4d(&tm_in, &full[stage], st, 0, 0, static_cast<int>(J0 / (128 / ZSZ)),
+                      static_cast<int>(I));
+      }
+      if constexpr (has_rows<MODE>()) {
+        if (lane < 4)
+          bulk_g2s(st + L.pl_bytes + lane * L.row_stride,
+                   args.mat + (4 * static_cast<int64_t>(I) + lane) * args.ldm + 4 * J0, rows_b,
+                   &full[stage]);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumers
+  const int ctid = threadIdx.x;
+  const uint32_t RS = L.row_stride;
+  // Coefficient fragments, split hi + lo.
+  //  ENC (A = E, M = p, K = c): a0 = E[16m+g][2q, 2q+1], a1 = E[16m+g+8][..], a2/a3: c + 8.
+  //  DEC (B = D, K = p, N = c): b0 = (D[16ks+2q][c], D[16ks+2q+1][c]), b1: planes + 8.
+  uint32_t fh[MT][4], fl[MT][4];
+  if constexpr (is_enc<MODE>()) {
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int p = 16 * m + g + 8 * (i & 1), c = 2 * q + 8 * (i >> 1);
+        const float e0 = p < P ? args.coef[p * 16 + c] : 0.f;
+        const float e1 = p < P ? args.coef[p * 16 + c + 1] : 0.f;
+        split2(e0, e1, fh[m][i], fl[m][i]);
+      }
+  } else {
+#pragma unroll
+    for (int ks = 0; ks < MT; ++ks)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // i = nt * 2 + h
+        const int nt = i >> 1, h = i & 1, c = 8 * nt + g;
+        const int pa = 16 * ks + 2 * q + 8 * h, pb = pa + 1;
+        const float d0 = pa < P ? args.coef[pa * 16 + c] : 0.f;
+        const float d1 = pb < P ? args.coef[pb * 16 + c] : 0.f;
+        split2(d0, d1, fh[ks][i], fl[ks][i]);
+      }
+  }
+  // Per-thread shared-memory offsets (see the work split above).
+  // ENC: B loads at rows + xoff + 512k (+2 RS); C stores at buf + soff[k] + (16m + 8h) * 128.
+  const uint32_t xoff = (q >> 1) * RS + 64 * warp + 8 * g + 4 * (q & 1);
+  uint32_t soff[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) soff[k] = is_enc<MODE>() ? pl_off<2>(P, g, 8 * (warp + 8 * k) + 2 * q) : 0u;
+  // Stores/loads of planes >= P exist only in the last 16-plane group.
+  const bool lastp0 = 16 * (MT - 1) + g < P, lastp1 = 16 * (MT - 1) + g + 8 < P;
+  // RED: B loads at rows + rb[nt] + 1024k; A loads at planes + ra0/ra2[k] + (16mt + 8h) * 128.
+  uint32_t rb[2], ra0[2], ra2[2];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    const int c = 8 * nt + g;
+    rb[nt] = (c >> 2) * RS + 128 * warp + 16 * q + 2 * (c & 3);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int t = 16 * (warp + 8 * k) + 2 * q;
+    ra0[k] = has_red<MODE>() ? pl_off<ZSZ>(P, g, t) : 0u;
+    ra2[k] = has_red<MODE>() ? pl_off<ZSZ>(P, g, t + 8) : 0u;
+  }
+  // DEC: A loads at planes + da[k][j] + (16ks + 8h) * 128 (planes 2q + j + 16ks + 8h at tiles
+  // t0, t0 + 1, t0 = 16 (warp + 8k) + 2g); C stores at buf + ooff + 1024k + 2nt RS (+8).
+  uint32_t da[2][2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      da[k][j] = is_enc<MODE>() ? 0u : pl_off<ZSZ>(P, 2 * q + j, 16 * (warp + 8 * k) + 2 * g);
+  const uint32_t ooff = (q >> 1) * RS + 128 * warp + 16 * g + 4 * (q & 1);
+  bool dok[4];  // last plane group: planes 16(MT-1) + 2q + {0, 1, 8, 9} < P
+#pragma unroll
+  for (int j = 0; j < 4; ++j) dok[j] = 16 * (MT - 1) + 2 * q + (j & 1) + 8 * (j >> 1) < P;
+
+  float R[2][2][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) R[a][b][k] = 0.f;
+
+  uint32_t it = 0;
+  for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+    const uint32_t stage = it % L.nstages;
+    const uint32_t phase = (it / L.nstages) & 1;
+    const uint32_t I = u / upr;
+    const uint32_t J0 = (u - I * upr) * kT;
+    const int Tw = static_cast<int>(min(bc - J0, static_cast<uint32_t>(kT)));
+    const uint32_t buf = s_out + (it & 1) * L.out_bytes;
+    const uint32_t planes = s_stages + stage * L.stage_bytes;
+    const uint32_t rows = planes + L.pl_bytes;
+    ptx::mbar_wait(&full[stage], phase);
+    if (warp == 0) ptx::bulk_wait_read<1>();  // the stores that last read `buf` are done
+    cbar();
+
+    if constexpr (is_enc<MODE>()) {
+      // C^T[p][tile] = E . X^T per 8-tile n-tile. B: b0 = X[tile][c 2q, 2q+1] (row q>>1),
+      // b1 = row 2 + (q>>1). Banks: 16 (q>>1) + 2g + (q&1) -> conflict-free. C: plane 16m+g
+      // (c0, c1) / 16m+g+8 (c2, c3), tiles 8nt+2q, +1, into the swizzled plane box: the 8 planes
+      // g land in 8 different 16-byte chunks -> conflict-free.
+      const int nnt = Tw >> 3;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (warp + 8 * k < nnt) {
+          const uint32_t xb = rows + xoff + 512 * k;
+          const uint32_t b0 = lds32(xb), b1 = lds32(xb + 2 * RS);
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            float c[4] = {0.f, 0.f, 0.f, 0.f};
+            mma(c, fh[m][0], fh[m][1], fh[m][2], fh[m][3], b0, b1);
+            mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0, b1);
+            const uint32_t o = buf + soff[k] + 16 * m * 128;
+            if (m < MT - 1 || lastp0) sts32(o, pack2(c[0], c[1]));
+            if (m < MT - 1 || lastp1) sts32(o + 8 * 128, pack2(c[2], c[3]));
+          }
+        }
+      }
+    } else {
+      // C[tile][c] = Z^T . D per 16-tile m-tile; rows g / g+8 <-> tiles 2g / 2g+1 so each
+      // plane load is one 8-byte (fp32) or 4-byte (bf16) access; with the swizzle XOR a
+      // half-warp's loads hit 32 distinct banks.
+      const int nmt = Tw >> 4;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (warp + 8 * k < nmt) {
+          float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+          for (int ks = 0; ks < MT; ++ks) {
+            float v[4][2];  // planes 16ks + 2q + {0, 1, 8, 9} at tiles t0, t0 + 1
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t ad = planes + da[k][j & 1] + (16 * ks + 8 * (j >> 1)) * 128;
+              if (ks < MT - 1 || dok[j]) {
+                if constexpr (ZSZ == 4) {
+                  const float2 f = lds64f(ad);
+                  v[j][0] = f.x;
+                  v[j][1] = f.y;
+                } else {
+                  const uint32_t w = lds32(ad);
+                  const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+                  v[j][0] = f.x;
+                  v[j][1] = f.y;
+                }
+              } else {
+                v[j][0] = v[j][1] = 0.f;
+              }
+            }
+            // a0 = (row g = tile t0: planes 2q, 2q+1), a1 = row g+8 = tile t0+1, a2/a3: +8
+            if constexpr (ZSZ == 4) {
+              uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
+              split2(v[0][0], v[1][0], h0, l0);
+              split2(v[0][1], v[1][1], h1, l1);
+              split2(v[2][0], v[3][0], h2, l2);
+              split2(v[2][1], v[3][1], h3, l3);
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) {
+                const uint32_t bh0 = fh[ks][2 * nt], bh1 = fh[ks][2 * nt + 1];
+                mma(acc[nt], h0, h1, h2, h3, bh0, bh1);
+                mma(acc[nt], l0, l1, l2, l3, bh0, bh1);
+                mma(acc[nt], h0, h1, h2, h3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
+              }
+            } else {
+              const uint32_t a0 = pack2(v[0][0], v[1][0]), a1 = pack2(v[0][1], v[1][1]);
+              const uint32_t a2 = pack2(v[2][0], v[3][0]), a3 = pack2(v[2][1], v[3][1]);
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) {
+                mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
+                mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
+              }
+            }
+          }
+          // acc[nt][0,1] -> tile t0, c = 8nt + 2q (+1): row a = 2nt + (q>>1), col b = 2(q&1).
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const uint32_t o = buf + ooff + 1024 * k + 2 * nt * RS;
+            sts32(o, pack2(acc[nt][0], acc[nt][1]));
+            sts32(o + 8, pack2(acc[nt][2], acc[nt][3]));
+          }
+        }
+      }
+    }
+    if constexpr (has_red<MODE>()) {
+      // R[p][c] += sum over 16-tile k-steps of Z[p][tile] X[tile][c] (A = Z: M = p; B = X: N = c).
+      // B: b0 = (X[t0+2q][c], X[t0+2q+1][c]), b1 = tiles + 8, c = 8nt + g, 16-bit loads
+      // (words 16 (c>>2) + 4q + ((c&3)>>1): distinct). A: Z[p][t0+2q, +1] / [t0+2q+8, +9].
+      const int nks = Tw >> 4;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (warp + 8 * k < nks) {
+          uint32_t b[2][2];
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const uint32_t base = rows + rb[nt] + 1024 * k;
+            b[nt][0] = pair16(lds16(base), lds16(base + 8));
+            b[nt][1] = pair16(lds16(base + 64), lds16(base + 72));
+          }
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const bool ok0 = mt < MT - 1 || lastp0, ok1 = mt < MT - 1 || lastp1;
+            const uint32_t z0 = planes + ra0[k] + 16 * mt * 128, z2 = planes + ra2[k] + 16 * mt * 128;
+            if constexpr (ZSZ == 2) {
+              const uint32_t a0 = ok0 ? lds32(z0) : 0u, a2 = ok0 ? lds32(z2) : 0u;
+              const uint32_t a1 = ok1 ? lds32(z0 + 1024) : 0u, a3 = ok1 ? lds32(z2 + 1024) : 0u;
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) mma(R[mt][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
+            } else {
+              const float2 zero = make_float2(0.f, 0.f);
+              const float2 v0 = ok0 ? lds64f(z0) : zero, v2 = ok0 ? lds64f(z2) : zero;
+              const float2 v1 = ok1 ? lds64f(z0 + 1024) : zero, v3 = ok1 ? lds64f(z2 + 1024) : zero;
+              uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
+              split2(v0.x, v0.y, h0, l0);
+              split2(v1.x, v1.y, h1, l1);
+              split2(v2.x, v2.y, h2, l2);
+              split2(v3.x, v3.y, h3, l3);
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) {
+                mma(R[mt][nt], h0, h1, h2, h3, b[nt][0], b[nt][1]);
+                mma(R[mt][nt], l0, l1, l2, l3, b[nt][0], b[nt][1]);
+              }
+            }
+          }
+        }
+      }
+    }
+
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+    ptx::fence_proxy_async_smem();
+    cbar();
+    // warp 0 issues the unit's stores: the plane box (one 4-D TMA op, clipped at the matrix
+    // edge) or the 4 output rows (1-D bulk copies).
+    if (warp == 0) {
+      if constexpr (is_enc<MODE>()) {
+        if (lane == 0) tma_store_4d(&tm_out, buf, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
+      } else {
+        __nv_bfloat16* o =
+            static_cast<__nv_bfloat16*>(args.out) + (4 * static_cast<int64_t>(I)) * args.ldo + 4 * J0;
+        if (lane < 4) bulk_s2g(o + lane * args.ldo, buf + lane * L.out_stride, Tw * 8);
+      }
+      ptx::bulk_commit();
+    }
+  }
+  if (warp == 0) ptx::bulk_wait_all();
+
+  if constexpr (has_red<MODE>()) {
+    // per-warp fragments -> smem -> fixed-order sum over warps -> this CTA's partial
+    float* mine = s_red + warp * P * 16;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int c = 8 * nt + 2 * q, p0 = 16 * mt + g, p1 = p0 + 8;
+        if (p0 < P) {
+          mine[p0 * 16 + c] = R[mt][nt][0];
+          mine[p0 * 16 + c + 1] = R[mt][nt][1];
+        }
+        if (p1 < P) {
+          mine[p1 * 16 + c] = R[mt][nt][2];
+          mine[p1 * 16 + c + 1] = R[mt][nt][3];
+        }
+      }
+    cbar();
+    const int n = P * 16;
+    for (int o = ctid; o < n; o += kCThreads) {
+      float s = s_red[o];
+#pragma unroll
+      for (int w = 1; w < kCWarps; ++w) s += s_red[w * n + o];
+      args.red_partial[static_cast<int64_t>(blockIdx.x) * n + o] = s;
+    }
+  }
+}
+
+// 4-D plane map (W tiles, P planes, bc/W chunks, br rows) with box {W, P, kT/W, 1}, 128B swizzle.
+bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int64_t br, int64_t bc) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeFn>(nullptr);
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  if (!fn) return false;
+  const uint64_t W = 128 / zsz;
+  cuuint64_t dims[4] = {W, static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(bc / W),
+                        static_cast<cuuint64_t>(br)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(br * bc * zsz), 128,
+                           static_cast<cuuint64_t>(bc * zsz)};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(W), static_cast<cuuint32_t>(P),
+                       static_cast<cuuint32_t>(kT / W), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, zsz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  4, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    static bool warned = false;
+    if (!warned) fprintf(stderr, "[stl_b200] plane tensor map rejected (CUresult %d); using the "
+                                 "register transforms\n", static_cast<int>(r));
+    warned = true;
+  }
+  return r == CUDA_SUCCESS;
+}
+
+template <int MODE, typename ZT, int MT>
+cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
+                      cudaStream_t s) {
+  const Layout L = make_layout<MODE, ZT>(a.P);
+  CUtensorMap tin{}, tout{};
+  if (has_planes_in<MODE>() && !plane_tmap(&tin, planes_in, sizeof(ZT), a.P, a.br, a.bc))
+    return cudaErrorNotSupported;
+  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.br, a.bc))
+    return cudaErrorNotSupported;
+  auto k = k_stream<MODE, ZT, MT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(L.total));
+  if (e != cudaSuccess) return e;
+  a.upr = (a.bc + kT - 1) / kT;
+  a.nunits = a.br * a.upr;
+  int64_t grid = sm_count();
+  if (grid > a.nunits) grid = a.nunits;
+  if (grid < 1) return cudaSuccess;
+  k<<<static_cast<int>(grid), kSThreads, L.total, s>>>(tin, tout, a, L);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if constexpr (has_red<MODE>()) return sum_partials(a.red_partial, static_cast<int>(grid), a.P * 16, red_out, s);
+  return cudaSuccess;
+}
+
+template <int MODE, typename ZT>
+cudaError_t launch(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
+                   cudaStream_t s) {
+  switch ((a.P + 15) / 16) {
+    case 1: return launch_mt<MODE, ZT, 1>(a, planes_in, planes_out, red_out, s);
+    case 2: return launch_mt<MODE, ZT, 2>(a, planes_in, planes_out, red_out, s);
+    case 3: if constexpr (!has_red<MODE>()) return launch_mt<MODE, ZT, 3>(a, planes_in, planes_out, red_out, s);
+            return cudaErrorNotSupported;
+    case 4: if constexpr (!has_red<MODE>()) return launch_mt<MODE, ZT, 4>(a, planes_in, planes_out, red_out, s);
+            return cudaErrorNotSupported;
+    default: return cudaErrorNotSupported;
+  }
+}
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+bool g_use_stream = true;
+void set_transform_stream(bool on) { g_use_stream = on; }
+
+// encode (+ g_d-style reduction): bf16 matrix -> bf16 planes; red planes bf16 or fp32.
+cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
+                                   const float* coef, int P, void* out, int odt, const void* rp,
+                                   int rdt, float* ro, float* rw, cudaStream_t s) {
+  if (!g_use_stream || mdt != kBF16 || odt != kBF16 || bc % 64 || ldm % 8 || P < 1 || P > 64 ||
+      !al16(m) || !al16(out))
+    return cudaErrorNotSupported;
+  if (rp && (P > 32 || !al16(rp) || !ro || !rw)) return cudaErrorNotSupported;
+  StreamArgs a{};
+  a.mat = static_cast<const __nv_bfloat16*>(m);
+  a.ldm = ldm;
+  a.out = nullptr;
+  a.coef = coef;
+  a.red_partial = rw;
+  a.P = P;
+  a.br = br;
+  a.bc = bc;
+  if (!rp) return launch<kEnc, __nv_bfloat16>(a, nullptr, out, nullptr, s);
+  if (rdt == kBF16) return launch<kEncRed, __nv_bfloat16>(a, rp, out, ro, s);
+  return launch<kEncRed, float>(a, rp, out, ro, s);
+}
+
+// decode (+ g_ex-style reduction): fp32 or bf16 planes -> bf16 matrix; red matrix bf16.
+cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, int64_t bc,
+                                   const float* coef, void* out, int odt, int64_t ldo,
+                                   const void* rm, int rdt, int64_t ldr, float* ro, float* rw,
+                                   cudaStream_t s) {
+  if (!g_use_stream || odt != kBF16 || bc % 64 || ldo % 8 || Q < 1 || Q > 64 || !al16(in) ||
+      !al16(out))
+    return cudaErrorNotSupported;
+  if (rm && (rdt != kBF16 || Q > 32 || ldr % 8 || !al16(rm) || !ro || !rw))
+    return cudaErrorNotSupported;
+  StreamArgs a{};
+  a.mat = static_cast<const __nv_bfloat16*>(rm);
+  a.ldm = ldr;
+  a.out = out;
+  a.ldo = ldo;
+  a.coef = coef;
+  a.red_partial = rw;
+  a.P = Q;
+  a.br = br;
+  a.bc = bc;
+  if (rm) {
+    if (idt == kF32) return launch<kDecRed, float>(a, in, nullptr, ro, s);
+    return launch<kDecRed, __nv_bfloat16>(a, in, nullptr, ro, s);
+  }
+  if (idt == kF32) return launch<kDec, float>(a, in, nullptr, nullptr, s);
+  return launch<kDec, __nv_bfloat16>(a, in, nullptr, nullptr, s);
+}
+
+}  // namespace stl

@@ -390,6 +390,11 @@ cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br,
                             const void* red_planes, int red_dtype, float* red_out,
                             float* red_ws, cudaStream_t s) {
   if (br * bc == 0) return cudaSuccess;
+  if (t == 4) {
+    cudaError_t e = tiles_to_planes_stream(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype,
+                                           red_planes, red_dtype, red_out, red_ws, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (t == 4 && g_use_mma) {
     cudaError_t e = tiles_to_planes_mma(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype,
                                         red_planes, red_dtype, red_out, red_ws, s);
@@ -414,6 +419,11 @@ cudaError_t planes_to_tiles(const void* in, int in_dtype, int Q, int64_t br, int
                             const void* red_m, int red_dtype, int64_t ldr, float* red_out,
                             float* red_ws, cudaStream_t s) {
   if (br * bc == 0) return cudaSuccess;
+  if (t == 4) {
+    cudaError_t e = planes_to_tiles_stream(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo,
+                                           red_m, red_dtype, ldr, red_out, red_ws, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (t == 4 && g_use_mma && g_use_mma_decode) {
     cudaError_t e = planes_to_tiles_mma(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m,
                                         red_dtype, ldr, red_out, red_ws, s);
