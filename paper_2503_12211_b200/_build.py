@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     """Compile every .cu into one shared library (skips if up to date)."""
     if not force and not _stale():
         return LIB_PATH
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", str(LIB_PATH)]
+    cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("STL_NVCC_EXTRA", "").split(), "-shared", "-o", str(LIB_PATH)]
     cmd += [str(CSRC / s) for s in SOURCES]
     cmd += ["-I", str(REPO / "include"), "-lcuda" if False else "-lcudart_static"]
     proc = subprocess.run(cmd, capture_output=True, text=True)

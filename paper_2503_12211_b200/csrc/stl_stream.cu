@@ -21,6 +21,7 @@
 // Reductions accumulate in MMA fragments per warp, are summed over warps in a fixed order and
 // over CTAs by a fixed-order tree (deterministic).
 #include <cstdio>
+#include <cstdlib>
 #include "sm100_ptx.cuh"
 #include "stl_internal.h"
 
@@ -29,11 +30,10 @@ namespace {
 
 enum Mode { kEnc = 0, kEncRed = 1, kDec = 2, kDecRed = 3 };
 
-constexpr int kT = 256;                     // tiles per unit
-constexpr int kCWarps = 8;                  // consumer warps
+constexpr int kCWarps = 16;                 // consumer warps
 constexpr int kCThreads = 32 * kCWarps;
 constexpr int kSThreads = kCThreads + 32;   // + producer warp
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 16;
 constexpr uint32_t kRowPad = 64;            // matrix rows: 16-word bank shift per row
 
 template <int MODE> constexpr bool has_rows() { return MODE != kDec; }
@@ -53,8 +53,13 @@ struct Layout {
 
 __host__ __device__ inline uint32_t rup(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-template <int MODE, typename ZT>
-__host__ __device__ inline Layout make_layout(int P) {
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <int MODE, typename ZT, int kT>
+inline Layout make_layout(int P) {
   Layout L{};
   L.pl_bytes = has_planes_in<MODE>() ? rup(P * kT * sizeof(ZT), 1024) : 0;
   L.row_stride = kT * 4 * 2 + kRowPad;
@@ -68,9 +73,11 @@ __host__ __device__ inline Layout make_layout(int P) {
     L.out_bytes = rup(4 * L.out_stride, 1024);
   }
   L.red_bytes = has_red<MODE>() ? kCWarps * P * 16 * 4 : 0;
-  const uint32_t budget = 200 * 1024;
+  static const uint32_t budget = env_int("STL_STREAM_SMEM_KB", 200) * 1024;
+  static const uint32_t max_st = env_int("STL_STREAM_STAGES", 8);
   const uint32_t fixed = 2 * L.out_bytes + L.red_bytes;
   uint32_t ns = (budget - fixed) / L.stage_bytes;
+  if (ns > max_st) ns = max_st;
   L.nstages = ns > kMaxStages ? kMaxStages : (ns < 2 ? 2 : ns);
   L.total = L.nstages * L.stage_bytes + fixed + 2 * kMaxStages * 8 + 1024;
   return L;
@@ -87,6 +94,8 @@ struct StreamArgs {
   int64_t br, bc;
   int64_t upr;               // units per tile row
   int64_t nunits;
+  int stg;                   // 1: consumers write outputs with st.global (else TMA/bulk stores)
+  int nocompute;             // probe: skip the math (pure data movement)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -124,24 +133,6 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, uint32_t src,
 __device__ __forceinline__ void cbar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kCThreads) : "memory");
 }
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint32_t lds16(uint32_t a) {
-  unsigned short v;
-  asm volatile("ld.shared.b16 %0, [%1];" : "=h"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ float2 lds64f(uint32_t a) {
-  float2 v;
-  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
-}
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -155,7 +146,7 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
 }
 __device__ __forceinline__ void mma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                     uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
@@ -183,22 +174,27 @@ __device__ __forceinline__ uint32_t pl_off(int P, int p, int t) {
   return pl_addr<ZSZ>(0u, P, p, t);
 }
 
-// Work split of a 256-tile unit over the 8 consumer warps (offset tables below assume it):
-//   ENC n-tiles (8 tiles):  warp w -> n-tiles w + 8k, k < 4
-//   DEC m-tiles (16 tiles): warp w -> m-tiles w + 8k, k < 2
-//   RED k-steps (16 tiles): warp w -> k-steps w + 8k, k < 2
-static_assert(kT == 256 && kCWarps == 8, "offset tables assume 256-tile units and 8 warps");
+// Work split of a kT-tile unit over the C = kCWarps consumer warps:
+//   ENC n-tiles (8 tiles):  warp w -> n-tiles w + C k, k < kT / (8 C)
+//   DEC m-tiles (16 tiles): warp w -> m-tiles w + C k, k < kT / (16 C)
+//   RED k-steps (16 tiles): warp w -> k-steps w + C k, k < kT / (16 C)
 
 // ------------------------------------------------------------------ the kernel
 // MT = number of 16-plane groups (ceil(P / 16)), a template so every plane loop unrolls.
-template <int MODE, typename ZT, int MT>
+template <int MODE, typename ZT, int MT, int kT>
 __global__ void __launch_bounds__(kSThreads, 1)
     k_stream(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
              StreamArgs args, Layout L) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  const uint32_t s_stages = ptx::smem_u32(smem);
+  // 1024-aligned base kept as shared-array arithmetic so plain C++ loads compile to LDS and the
+  // compiler may schedule them; offsets below are relative to `smem`, `sbase` is its address.
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = ptx::smem_u32(smem);
+  auto lds32 = [smem](uint32_t o) { return *reinterpret_cast<const uint32_t*>(smem + o); };
+  auto lds16 = [smem](uint32_t o) -> uint32_t { return *reinterpret_cast<const uint16_t*>(smem + o); };
+  auto lds64f = [smem](uint32_t o) { return *reinterpret_cast<const float2*>(smem + o); };
+  auto sts32 = [smem](uint32_t o, uint32_t v) { *reinterpret_cast<uint32_t*>(smem + o) = v; };
+  const uint32_t s_stages = 0;
   const uint32_t s_out = s_stages + L.nstages * L.stage_bytes;
   float* s_red = reinterpret_cast<float*>(smem + L.nstages * L.stage_bytes + 2 * L.out_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.nstages * L.stage_bytes +
@@ -244,12 +240,12 @@ __global__ void __launch_bounds__(kSThreads, 1)
         ptx::mbar_arrive_expect_tx(&full[stage],
                                    4 * rows_b + (has_planes_in<MODE>() ? P * kT * ZSZ : 0));
         if constexpr (has_planes_in<MODE>())
-          tma_load_4d(&tm_in, &full[stage], st, 0, 0, static_cast<int>(J0 / (128 / ZSZ)),
+          tma_load_4d(&tm_in, &full[stage], sbase + st, 0, 0, static_cast<int>(J0 / (128 / ZSZ)),
                       static_cast<int>(I));
       }
       if constexpr (has_rows<MODE>()) {
         if (lane < 4)
-          bulk_g2s(st + L.pl_bytes + lane * L.row_stride,
+          bulk_g2s(sbase + st + L.pl_bytes + lane * L.row_stride,
                    args.mat + (4 * static_cast<int64_t>(I) + lane) * args.ldm + 4 * J0, rows_b,
                    &full[stage]);
       }
@@ -260,6 +256,9 @@ __global__ void __launch_bounds__(kSThreads, 1)
   // ------------------------------------------------------------------ consumers
   const int ctid = threadIdx.x;
   const uint32_t RS = L.row_stride;
+  constexpr int kNK = kT / (8 * kCWarps);    // ENC n-tile rounds per warp
+  constexpr int kMK = kT / (16 * kCWarps);   // DEC m-tile / RED k-step rounds per warp
+  static_assert(kNK >= 1 && kMK >= 1, "unit too small for the warp count");
   // Coefficient fragments, split hi + lo.
   //  ENC (A = E, M = p, K = c): a0 = E[16m+g][2q, 2q+1], a1 = E[16m+g+8][..], a2/a3: c + 8.
   //  DEC (B = D, K = p, N = c): b0 = (D[16ks+2q][c], D[16ks+2q+1][c]), b1: planes + 8.
@@ -289,32 +288,32 @@ __global__ void __launch_bounds__(kSThreads, 1)
   // Per-thread shared-memory offsets (see the work split above).
   // ENC: B loads at rows + xoff + 512k (+2 RS); C stores at buf + soff[k] + (16m + 8h) * 128.
   const uint32_t xoff = (q >> 1) * RS + 64 * warp + 8 * g + 4 * (q & 1);
-  uint32_t soff[4];
+  uint32_t soff[kNK];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) soff[k] = is_enc<MODE>() ? pl_off<2>(P, g, 8 * (warp + 8 * k) + 2 * q) : 0u;
+  for (int k = 0; k < kNK; ++k) soff[k] = is_enc<MODE>() ? pl_off<2>(P, g, 8 * (warp + kCWarps * k) + 2 * q) : 0u;
   // Stores/loads of planes >= P exist only in the last 16-plane group.
   const bool lastp0 = 16 * (MT - 1) + g < P, lastp1 = 16 * (MT - 1) + g + 8 < P;
   // RED: B loads at rows + rb[nt] + 1024k; A loads at planes + ra0/ra2[k] + (16mt + 8h) * 128.
-  uint32_t rb[2], ra0[2], ra2[2];
+  uint32_t rb[2], ra0[kMK], ra2[kMK];
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const int c = 8 * nt + g;
     rb[nt] = (c >> 2) * RS + 128 * warp + 16 * q + 2 * (c & 3);
   }
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int t = 16 * (warp + 8 * k) + 2 * q;
+  for (int k = 0; k < kMK; ++k) {
+    const int t = 16 * (warp + kCWarps * k) + 2 * q;
     ra0[k] = has_red<MODE>() ? pl_off<ZSZ>(P, g, t) : 0u;
     ra2[k] = has_red<MODE>() ? pl_off<ZSZ>(P, g, t + 8) : 0u;
   }
   // DEC: A loads at planes + da[k][j] + (16ks + 8h) * 128 (planes 2q + j + 16ks + 8h at tiles
   // t0, t0 + 1, t0 = 16 (warp + 8k) + 2g); C stores at buf + ooff + 1024k + 2nt RS (+8).
-  uint32_t da[2][2];
+  uint32_t da[kMK][2];
 #pragma unroll
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < kMK; ++k)
 #pragma unroll
     for (int j = 0; j < 2; ++j)
-      da[k][j] = is_enc<MODE>() ? 0u : pl_off<ZSZ>(P, 2 * q + j, 16 * (warp + 8 * k) + 2 * g);
+      da[k][j] = is_enc<MODE>() ? 0u : pl_off<ZSZ>(P, 2 * q + j, 16 * (warp + kCWarps * k) + 2 * g);
   const uint32_t ooff = (q >> 1) * RS + 128 * warp + 16 * g + 4 * (q & 1);
   bool dok[4];  // last plane group: planes 16(MT-1) + 2q + {0, 1, 8, 9} < P
 #pragma unroll
@@ -339,19 +338,18 @@ __global__ void __launch_bounds__(kSThreads, 1)
     const uint32_t planes = s_stages + stage * L.stage_bytes;
     const uint32_t rows = planes + L.pl_bytes;
     ptx::mbar_wait(&full[stage], phase);
-    if (warp == 0) ptx::bulk_wait_read<1>();  // the stores that last read `buf` are done
-    cbar();
 
-    if constexpr (is_enc<MODE>()) {
+    if (args.nocompute) {
+    } else if constexpr (is_enc<MODE>()) {
       // C^T[p][tile] = E . X^T per 8-tile n-tile. B: b0 = X[tile][c 2q, 2q+1] (row q>>1),
       // b1 = row 2 + (q>>1). Banks: 16 (q>>1) + 2g + (q&1) -> conflict-free. C: plane 16m+g
       // (c0, c1) / 16m+g+8 (c2, c3), tiles 8nt+2q, +1, into the swizzled plane box: the 8 planes
       // g land in 8 different 16-byte chunks -> conflict-free.
       const int nnt = Tw >> 3;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (warp + 8 * k < nnt) {
-          const uint32_t xb = rows + xoff + 512 * k;
+      for (int k = 0; k < kNK; ++k) {
+        if (warp + kCWarps * k < nnt) {
+          const uint32_t xb = rows + xoff + 64 * kCWarps * k;
           const uint32_t b0 = lds32(xb), b1 = lds32(xb + 2 * RS);
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
@@ -370,8 +368,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
       // half-warp's loads hit 32 distinct banks.
       const int nmt = Tw >> 4;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        if (warp + 8 * k < nmt) {
+      for (int k = 0; k < kMK; ++k) {
+        if (warp + kCWarps * k < nmt) {
           float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
           for (int ks = 0; ks < MT; ++ks) {
@@ -421,25 +419,25 @@ __global__ void __launch_bounds__(kSThreads, 1)
           // acc[nt][0,1] -> tile t0, c = 8nt + 2q (+1): row a = 2nt + (q>>1), col b = 2(q&1).
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
-            const uint32_t o = buf + ooff + 1024 * k + 2 * nt * RS;
+            const uint32_t o = buf + ooff + 128 * kCWarps * k + 2 * nt * RS;
             sts32(o, pack2(acc[nt][0], acc[nt][1]));
             sts32(o + 8, pack2(acc[nt][2], acc[nt][3]));
           }
         }
       }
     }
-    if constexpr (has_red<MODE>()) {
+    if (has_red<MODE>() && !args.nocompute) {
       // R[p][c] += sum over 16-tile k-steps of Z[p][tile] X[tile][c] (A = Z: M = p; B = X: N = c).
       // B: b0 = (X[t0+2q][c], X[t0+2q+1][c]), b1 = tiles + 8, c = 8nt + g, 16-bit loads
       // (words 16 (c>>2) + 4q + ((c&3)>>1): distinct). A: Z[p][t0+2q, +1] / [t0+2q+8, +9].
       const int nks = Tw >> 4;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        if (warp + 8 * k < nks) {
+      for (int k = 0; k < kMK; ++k) {
+        if (warp + kCWarps * k < nks) {
           uint32_t b[2][2];
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
-            const uint32_t base = rows + rb[nt] + 1024 * k;
+            const uint32_t base = rows + rb[nt] + 128 * kCWarps * k;
             b[nt][0] = pair16(lds16(base), lds16(base + 8));
             b[nt][1] = pair16(lds16(base + 64), lds16(base + 72));
           }
@@ -474,17 +472,44 @@ __global__ void __launch_bounds__(kSThreads, 1)
 
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+    if (args.stg) {
+      // Consumers copy the staged unit to global memory with 16-byte stores (coalesced rows).
+      cbar();
+      if constexpr (is_enc<MODE>()) {
+        __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(I) * bc + J0;
+        const int64_t ntiles = args.br * args.bc;
+        const int pieces = P * (Tw >> 3);  // 16-byte pieces: (p, chunk k, c16)
+        for (int i = ctid; i < pieces; i += kCThreads) {
+          const int p = i / (Tw >> 3), rest = i - p * (Tw >> 3), k = rest >> 3, c16 = rest & 7;
+          const uint32_t row = static_cast<uint32_t>(k * P + p);
+          const uint4 v = *reinterpret_cast<const uint4*>(smem + buf + row * 128 + ((c16 ^ (row & 7)) << 4));
+          *reinterpret_cast<uint4*>(ob + p * ntiles + 64 * k + 8 * c16) = v;
+        }
+      } else {
+        __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(args.out) + (4 * static_cast<int64_t>(I)) * args.ldo + 4 * J0;
+        const int per_row = Tw >> 1;  // 16-byte pieces per output row
+        for (int i = ctid; i < 4 * per_row; i += kCThreads) {
+          const int a = i / per_row, c = i - a * per_row;
+          const uint4 v = *reinterpret_cast<const uint4*>(smem + buf + a * L.out_stride + 16 * c);
+          *reinterpret_cast<uint4*>(ob + a * args.ldo + 8 * c) = v;
+        }
+      }
+      continue;
+    }
     ptx::fence_proxy_async_smem();
+    // The stores of the previous unit (other buffer) must have finished reading it before the
+    // barrier: the next unit writes that buffer. One barrier per unit.
+    if (warp == 0) ptx::bulk_wait_read<0>();
     cbar();
     // warp 0 issues the unit's stores: the plane box (one 4-D TMA op, clipped at the matrix
     // edge) or the 4 output rows (1-D bulk copies).
     if (warp == 0) {
       if constexpr (is_enc<MODE>()) {
-        if (lane == 0) tma_store_4d(&tm_out, buf, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
+        if (lane == 0) tma_store_4d(&tm_out, sbase + buf, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
       } else {
         __nv_bfloat16* o =
             static_cast<__nv_bfloat16*>(args.out) + (4 * static_cast<int64_t>(I)) * args.ldo + 4 * J0;
-        if (lane < 4) bulk_s2g(o + lane * args.ldo, buf + lane * L.out_stride, Tw * 8);
+        if (lane < 4) bulk_s2g(o + lane * args.ldo, sbase + buf + lane * L.out_stride, Tw * 8);
       }
       ptx::bulk_commit();
     }
@@ -520,7 +545,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
 }
 
 // 4-D plane map (W tiles, P planes, bc/W chunks, br rows) with box {W, P, kT/W, 1}, 128B swizzle.
-bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int64_t br, int64_t bc) {
+bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int64_t br, int64_t bc, int kT) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -555,20 +580,24 @@ bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int64_t br, in
   return r == CUDA_SUCCESS;
 }
 
-template <int MODE, typename ZT, int MT>
+template <int MODE, typename ZT, int MT, int kT>
 cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                       cudaStream_t s) {
-  const Layout L = make_layout<MODE, ZT>(a.P);
+  const Layout L = make_layout<MODE, ZT, kT>(a.P);
   CUtensorMap tin{}, tout{};
-  if (has_planes_in<MODE>() && !plane_tmap(&tin, planes_in, sizeof(ZT), a.P, a.br, a.bc))
+  if (has_planes_in<MODE>() && !plane_tmap(&tin, planes_in, sizeof(ZT), a.P, a.br, a.bc, kT))
     return cudaErrorNotSupported;
-  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.br, a.bc))
+  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.br, a.bc, kT))
     return cudaErrorNotSupported;
-  auto k = k_stream<MODE, ZT, MT>;
+  auto k = k_stream<MODE, ZT, MT, kT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(L.total));
   if (e != cudaSuccess) return e;
-  a.upr = (a.bc + kT - 1) / kT;
+  static const int stg = env_int("STL_STREAM_STG", 0);
+  a.stg = stg;
+  static const int noc = env_int("STL_STREAM_NOCOMPUTE", 0);
+  a.nocompute = noc;
+  a.upr = (a.bc + kT - 1) / kT;  // kT: this launch's unit
   a.nunits = a.br * a.upr;
   int64_t grid = sm_count();
   if (grid > a.nunits) grid = a.nunits;
@@ -580,15 +609,28 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   return cudaSuccess;
 }
 
+// 512-tile units whenever two pipeline stages fit in 200 KB (measured: longer bulk segments beat
+// deeper pipelines), else 256.
+template <int MODE, typename ZT, int MT>
+cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
+                     cudaStream_t s) {
+  static const int force_t = env_int("STL_STREAM_T", 0);
+  const Layout L512 = make_layout<MODE, ZT, 512>(a.P);
+  const bool use512 = force_t ? force_t == 512
+                              : (L512.nstages >= 2 && L512.total <= 227 * 1024 && a.bc >= 512);
+  if (use512) return launch_mt<MODE, ZT, MT, 512>(a, planes_in, planes_out, red_out, s);
+  return launch_mt<MODE, ZT, MT, 256>(a, planes_in, planes_out, red_out, s);
+}
+
 template <int MODE, typename ZT>
 cudaError_t launch(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                    cudaStream_t s) {
   switch ((a.P + 15) / 16) {
-    case 1: return launch_mt<MODE, ZT, 1>(a, planes_in, planes_out, red_out, s);
-    case 2: return launch_mt<MODE, ZT, 2>(a, planes_in, planes_out, red_out, s);
-    case 3: if constexpr (!has_red<MODE>()) return launch_mt<MODE, ZT, 3>(a, planes_in, planes_out, red_out, s);
+    case 1: return launch_t<MODE, ZT, 1>(a, planes_in, planes_out, red_out, s);
+    case 2: return launch_t<MODE, ZT, 2>(a, planes_in, planes_out, red_out, s);
+    case 3: if constexpr (!has_red<MODE>()) return launch_t<MODE, ZT, 3>(a, planes_in, planes_out, red_out, s);
             return cudaErrorNotSupported;
-    case 4: if constexpr (!has_red<MODE>()) return launch_mt<MODE, ZT, 4>(a, planes_in, planes_out, red_out, s);
+    case 4: if constexpr (!has_red<MODE>()) return launch_t<MODE, ZT, 4>(a, planes_in, planes_out, red_out, s);
             return cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
   }
@@ -612,7 +654,7 @@ cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t 
   StreamArgs a{};
   a.mat = static_cast<const __nv_bfloat16*>(m);
   a.ldm = ldm;
-  a.out = nullptr;
+  a.out = out;
   a.coef = coef;
   a.red_partial = rw;
   a.P = P;
