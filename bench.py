@@ -221,7 +221,8 @@ def main() -> None:
 
     bi, bk, bj = M // T, K // T, N // T
     u = torch.empty((R, bi, bk), dtype=torch.bfloat16, device=dev)
-    y_enc = torch.empty((R, bi, bj), dtype=torch.bfloat16, device=dev)
+    y_enc = torch.empty((int(lib.stl_cache_bytes(M, K, N, T, R, _lib.STL_BF16)),),
+                        dtype=torch.uint8, device=dev)  # forward cache (F24 slice products)
     fwd_scratch = torch.empty((int(lib.stl_forward_scratch_bytes(M, K, N, T, R, _lib.STL_BF16)),),
                               dtype=torch.uint8, device=dev)
     y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)

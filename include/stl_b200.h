@@ -40,7 +40,10 @@
 extern "C" {
 #endif
 
-enum stl_dtype { STL_F32 = 0, STL_BF16 = 1 };
+/* STL_F24 is never a user-facing input/output dtype: it names the bf16 path's intermediate
+ * format for fp32 slice products (the y_enc cache), fp32 rounded to 24 bits and stored as a
+ * 16-bit high plane set followed by an 8-bit low plane set (3 bytes per element). */
+enum stl_dtype { STL_F32 = 0, STL_BF16 = 1, STL_F24 = 2 };
 
 enum stl_status {
   STL_OK = 0,
@@ -95,8 +98,9 @@ STL_API int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_lay
  * (toy_network.py:74-92):  y = decode(slice_products(encode(x, e_x), w_enc), d).
  *   x: (M, K) ld_x, dtype;  w_enc: planes (r, N/t, K/t) of dtype;  y: (M, N) ld_y, dtype.
  *   x_enc_ws: planes (r, M/t, K/t) of dtype (also the cache `u`);
- *   y_enc_cache: NULL, or planes (r, M/t, N/t) of dtype receiving the slice products (the
- *                cache `y_enc` for stl_backward; fp32 in fp32 mode, bf16 in bf16 mode);
+ *   y_enc_cache: NULL, or stl_cache_bytes(...) bytes receiving the slice products (the cache
+ *                `y_enc` for stl_backward; fp32 planes in fp32 mode, F24 or bf16 planes in bf16
+ *                mode, see stl_cache_bytes);
  *   scratch: device workspace of at least stl_forward_scratch_bytes(...) bytes.
  *   M, K, N must be multiples of t (ShapeError otherwise, as the reference).
  * Default path: encode -> slice GEMM -> decode with fp32 slice products in `scratch`; with
@@ -104,6 +108,10 @@ STL_API int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_lay
  */
 STL_API int64_t stl_forward_scratch_bytes(int64_t M, int64_t K, int64_t N, int t, int r,
                                           int dtype);
+/* Bytes of the forward cache y_enc (r, M/t, N/t): fp32 planes (dtype STL_F32); on the bf16
+ * path STL_F24 planes (3 bytes per element) when t = 4, r <= 32, M/t > 128, N/t % 128 == 0 and
+ * K/t % 8 == 0, else bf16 planes. stl_backward reads the cache in the same format. */
+STL_API int64_t stl_cache_bytes(int64_t M, int64_t K, int64_t N, int t, int r, int dtype);
 STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
                 const float* e_x, const float* d, int t, int r, int dtype, void* y, int64_t ld_y,
                 void* x_enc_ws, void* y_enc_cache, void* scratch, int64_t scratch_bytes,
@@ -112,7 +120,8 @@ STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const
 /* A/B switches (host-only): bit 0 = enable the decode-fused forward (default off:
  * it is slower than encode + GEMM + decode today);
  * bit 1 = force the FFMA tile transforms instead of the tensor-core (mma.sync) ones;
- * bit 2 = also use the tensor-core decode (experimental). */
+ * bit 2 = also use the tensor-core decode (experimental); bit 3 = disable the streaming
+ * (TMA-pipelined) transforms; bit 4 = keep fp32 slice products instead of F24. */
 STL_API int stl_set_fusion(int enabled);
 
 /*

@@ -17,6 +17,7 @@ LIB_PATH = Path(__file__).resolve().with_name("libstl_b200.so")
 
 STL_F32 = 0
 STL_BF16 = 1
+STL_F24 = 2  # intermediate format of the bf16 path's fp32 slice products (see stl_cache_bytes)
 STL_K_MAJOR = 0
 STL_MN_MAJOR = 1
 
@@ -33,6 +34,7 @@ SIGNATURES = {
     "stl_slice_gemm": ([c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_int, c_int,
                         c_int64, c_int64, c_int64, c_void_p], c_int),
     "stl_forward_scratch_bytes": ([c_int64, c_int64, c_int64, c_int, c_int, c_int], c_int64),
+    "stl_cache_bytes": ([c_int64, c_int64, c_int64, c_int, c_int, c_int], c_int64),
     "stl_forward": ([c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                      c_int, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                      c_int64, c_void_p], c_int),

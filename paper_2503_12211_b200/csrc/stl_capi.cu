@@ -82,8 +82,10 @@ int run_gemm(const void* a, int al, const void* b, int bl, void* c, int cdt, int
   if (M == 0 || N == 0 || r == 0) return STL_OK;
   if (K == 0) {
     return check_cuda(cudaMemsetAsync(c, 0, stl::dtype_size(cdt) * r * M * N, s), "memset");
-  }
+  }  // (F24 zero = all-zero bytes)
   stl::SliceGemmProblem pb{a, al, b, bl, c, cdt, abdt, r, M, N, K};
+  if (cdt == stl::kF24 && !stl::slice_gemm_f24_supported(pb))
+    return fail(STL_ERR_VALUE, "F24 slice products need 16-byte aligned operands");
   const bool tc = stl::slice_gemm_tc_supported(pb);
   if (tc && c2) {
     pb.c2 = c2;
@@ -146,18 +148,35 @@ int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_layout, voi
 
 namespace {
 bool g_fusion = false;  // decode-fused forward is opt-in until it beats the unfused path
+bool g_f24 = true;      // F24 slice products on the bf16 t = 4 path (stl_set_fusion bit 4 clears)
 
 bool fused_forward_shape(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
   if (!g_fusion || t != 4 || dtype != STL_BF16) return false;
   return stl::fused_decode_supported(t, r, M / t, N / t, K / t, dtype, nullptr, nullptr, 0);
 }
+
+// Slice products C (rows x cols tiles, contraction kt) in F24: the CTA-pair GEMM writes them and
+// the streaming transforms read them. A pure function of the shape, so the forward (writing the
+// y_enc cache) and the backward (reading it) agree on the cache format.
+bool f24_products(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype) {
+  return g_f24 && dtype == STL_BF16 && t == 4 && r <= 32 && rows > 128 && cols % 128 == 0 &&
+         kt % 8 == 0;
+}
 }  // namespace
+
+int64_t stl_cache_bytes(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
+  if (t < 1 || r < 1 || M < 0 || K < 0 || N < 0) return 0;
+  const int64_t n = static_cast<int64_t>(r) * (M / t) * (N / t);
+  if (f24_products(M / t, N / t, K / t, t, r, dtype)) return 3 * n;
+  return n * (dtype == STL_BF16 ? 2 : 4);
+}
 
 int stl_set_fusion(int enabled) {
   g_fusion = (enabled & 1) != 0;
   stl::set_transform_mma((enabled & 2) == 0);         // bit 1 = force the FFMA transforms
   stl::set_transform_mma_decode((enabled & 4) != 0);  // bit 2 = mma decode (experimental)
   stl::set_transform_stream((enabled & 8) == 0);      // bit 3 = disable the streaming transforms
+  g_f24 = (enabled & 16) == 0;                        // bit 4 = fp32 slice products (no F24)
   return STL_OK;
 }
 
@@ -191,8 +210,8 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
                     "forward encode");
   }
   if (st) return st;
-  const bool fused = fused_forward_shape(M, K, N, t, r, dtype) && bk > 0 && ld_y % 8 == 0 &&
-                     (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
+  const bool fused = !y_enc_cache && fused_forward_shape(M, K, N, t, r, dtype) && bk > 0 &&
+                     ld_y % 8 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
                      stl::fused_decode_supported(t, r, bi, bj, bk, dtype, x_enc_ws, w_enc, 0);
   if (fused) {
     const size_t need = stl::fused_decode_scratch_bytes(r, bi, bj);
@@ -201,8 +220,20 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
                   (long long)need);
     Prof prof("slice_gemm_decode_fused", s);
     return check_cuda(stl::fused_gemm_decode(x_enc_ws, w_enc, STL_K_MAJOR, r, bi, bj, bk, d, y,
-                                             ld_y, dtype, y_enc_cache, dtype, scratch, s),
+                                             ld_y, dtype, nullptr, dtype, scratch, s),
                       "fused forward");
+  }
+  if (f24_products(bi, bj, bk, t, r, dtype)) {
+    // slice products in F24 straight into the cache (or scratch), decoded from there
+    void* prod = y_enc_cache ? y_enc_cache : scratch;
+    if (!y_enc_cache && scratch_bytes < 3 * static_cast<int64_t>(r) * bi * bj)
+      return fail(STL_ERR_VALUE, "scratch too small: %lld bytes", (long long)scratch_bytes);
+    st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, prod, stl::kF24, dtype, r, bi, bj, bk, s);
+    if (st) return st;
+    Prof prof("decode_y", s);
+    return check_cuda(stl::planes_to_tiles(prod, stl::kF24, r, bi, bj, t, d, y, dtype, ld_y, nullptr,
+                                           STL_F32, 0, nullptr, nullptr, s),
+                      "forward decode");
   }
   float* yenc = nullptr;
   if (dtype == STL_F32 && y_enc_cache) {
@@ -250,8 +281,9 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
   int st;
   {
     Prof prof(g_d ? "encode_gy+g_d" : "encode_gy", s, g_d ? 2 : 1);
+    const int cache_dt = f24_products(bi, bj, bk, t, r, dtype) ? stl::kF24 : dtype;
     st = check_cuda(stl::tiles_to_planes(gy, dtype, ld_gy, bi, bj, t, d, r, g_enc_ws, dtype,
-                                           g_d ? y_enc : nullptr, dtype, g_d, red_ws, s),
+                                           g_d ? y_enc : nullptr, cache_dt, g_d, red_ws, s),
                       "backward encode(gy)");
   }
   if (st) return st;
@@ -262,13 +294,15 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
     if (st) return st;
   }
   if (g_x || g_ex) {
-    // g_u_p (M/t x K/t) = g_enc_p (M/t x N/t) . W_p (N/t x K/t): B is N-major.
-    st = run_gemm(g_enc_ws, STL_K_MAJOR, w_enc, STL_MN_MAJOR, g_u_ws, STL_F32, dtype, r, bi, bk,
+    // g_u_p (M/t x K/t) = g_enc_p (M/t x N/t) . W_p (N/t x K/t): B is N-major. F24 on the bf16
+    // path (3 of the 4 bytes of g_u_ws used).
+    const int gu_dt = f24_products(bi, bk, bj, t, r, dtype) ? stl::kF24 : STL_F32;
+    st = run_gemm(g_enc_ws, STL_K_MAJOR, w_enc, STL_MN_MAJOR, g_u_ws, gu_dt, dtype, r, bi, bk,
                   bj, s);
     if (st) return st;
     if (g_x) {
       Prof prof(g_ex ? "decode_gu+g_ex" : "decode_gu", s, g_ex ? 2 : 1);
-      st = check_cuda(stl::planes_to_tiles(g_u_ws, STL_F32, r, bi, bk, t, e_x, g_x, dtype, ld_gx,
+      st = check_cuda(stl::planes_to_tiles(g_u_ws, gu_dt, r, bi, bk, t, e_x, g_x, dtype, ld_gx,
                                            g_ex ? x : nullptr, dtype, ld_x, g_ex, red_ws, s),
                       "backward decode(g_u)");
     } else {

@@ -7,9 +7,13 @@
 
 namespace stl {
 
-enum Dtype : int { kF32 = 0, kBF16 = 1 };
+// kF24: an fp32 quantity rounded to 24 bits (RNE) and stored as two plane sets — the high
+// 16 bits of every element (2 bytes each) followed by the next 8 bits (1 byte each) — so a
+// tensor of n elements occupies 3n bytes; value = as_float(hi << 16 | lo << 8), ~2^-16 relative.
+// Used for the bf16 path's fp32 slice products (forward cache y_enc, backward g_u).
+enum Dtype : int { kF32 = 0, kBF16 = 1, kF24 = 2 };
 
-inline size_t dtype_size(int dt) { return dt == kBF16 ? 2 : 4; }
+inline size_t dtype_size(int dt) { return dt == kBF16 ? 2 : (dt == kF24 ? 3 : 4); }
 
 // Operand layouts of one slice-GEMM batch C_p = A_p · B_p (p = 0..r-1), all slices contiguous.
 //   A: 0 = (r, M, K) K-contiguous ("K-major"),  1 = (r, K, M) M-contiguous ("MN-major")
@@ -47,6 +51,8 @@ cudaError_t cast_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t
 // tcgen05 path (bf16 operands, aligned shapes). Returns cudaError_t-like code, 0 = ok.
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s);
 bool slice_gemm_tc_supported(const SliceGemmProblem& pb);
+// F24 output (c_dtype = kF24) is produced by the CTA-pair kernel only.
+bool slice_gemm_f24_supported(const SliceGemmProblem& pb);
 // SIMT path (fp32 or bf16 operands, any shape).
 cudaError_t slice_gemm_simt(const SliceGemmProblem& pb, cudaStream_t s);
 

@@ -33,6 +33,8 @@ constexpr int kThreads = 256;
 struct EpiArgs {
   void* c;
   int c_bf16;
+  int nostore;  // probe: skip the C stores (measures the mainloop alone)
+  int unused;
   int r;
   int M, N, K;
   __nv_bfloat16* c2;  // optional bf16 copy of C (the forward's training cache)
@@ -258,27 +260,41 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 128 rows of A and its BN/2 columns of B (half the B bytes per SM of the 1-CTA kernel, and
 // 32 KB stages -> a 6-deep ring); the even CTA issues tcgen05.mma.cta_group::2 for both, and
 // each CTA's epilogue drains its own 128 TMEM lanes.
-template <int BN, bool DUAL>
+// Output modes of the pair kernel: fp32 C; fp32 C plus a bf16 copy (c2); or F24 — fp32 rounded
+// to 24 bits and stored as a 16-bit high plane set (c) followed by an 8-bit low plane set
+// (c + 2 * r * M * N bytes), 3 bytes per element at ~2^-16 relative precision.
+enum OutMode { kOutF32 = 0, kOutF32Bf16 = 1, kOutF24 = 2 };
+
+template <int BN, int OUT>
 struct Smem2 {
   // ring depth chosen so ring + epilogue staging fits the 227 KB opt-in limit
-  static constexpr int kStages = BN == 256 ? (DUAL ? 5 : 6) : (DUAL ? 7 : 8);
+  static constexpr int kStages = BN == 256 ? (OUT == kOutF32Bf16 ? 5 : 6) : (OUT == kOutF32Bf16 ? 7 : 8);
   static constexpr uint32_t kABytes = 128 * kBK * 2;
   static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
   static constexpr uint32_t kRing = kStages * (kABytes + kBBytes);
-  // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B fp32 [+ 32 x 64 B bf16 copy])
-  static constexpr uint32_t kStageF = 32 * 128, kStageH = 32 * 64;
-  static constexpr uint32_t kWarpStage = 2 * (kStageF + (DUAL ? kStageH : 0));
+  // epilogue staging per warp and buffer, 32 rows x 32 columns:
+  //   primary (fp32 128 B rows, or F24 high 64 B rows) + secondary (bf16 64 B rows / F24 low 32 B)
+  static constexpr uint32_t kStageF = OUT == kOutF24 ? 32 * 64 : 32 * 128;
+  static constexpr uint32_t kStageH = OUT == kOutF32Bf16 ? 32 * 64 : (OUT == kOutF24 ? 32 * 32 : 0);
+  static constexpr uint32_t kBufBytes = kStageF + kStageH;
+  static constexpr uint32_t kWarpStage = 2 * kBufBytes;
   static constexpr uint32_t kBarOffset = kRing + 4 * kWarpStage;
   static constexpr uint32_t kTotal = kBarOffset + 512 + 1024;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool DUAL>
+// fp32 -> 24-bit round-to-nearest-even bit pattern (low 8 bits zero)
+__device__ __forceinline__ uint32_t rne24(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u + 0x7Fu + ((u >> 8) & 1u)) & 0xFFFFFF00u;
+}
+
+template <int BN, bool A_MN, bool B_MN, int OUT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     slice_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA,
                           const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmC,
                           const __grid_constant__ CUtensorMap tmC2, EpiArgs args) {
-  using S = Smem2<BN, DUAL>;
+  using S = Smem2<BN, OUT>;
   constexpr int kSt = S::kStages;
   constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(256, BN, A_MN, B_MN);
   constexpr uint32_t kTmemCols = (2 * BN <= 256) ? 256 : 512;
@@ -427,18 +443,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c,
                                 v);
         const int buf = chunk_no & 1;
-        uint8_t* sf = stage_base + buf * (S::kStageF + (DUAL ? S::kStageH : 0));
+        uint8_t* sf = stage_base + buf * S::kBufBytes;
         // the TMA store that last read this buffer (two chunks ago) must be done reading
         if (lane == 0) ptx::bulk_wait_read<1>();
         __syncwarp();
         ptx::tmem_ld_wait();
-        if (nb * BN + c < N && row0 < M) {
+        if (nb * BN + c < N && row0 < M && !args.nostore) {
+          if constexpr (OUT == kOutF24) {
+            // high 16 bits: 64 B rows, 64B-swizzled; low 8 bits: 32 B rows, 32B-swizzled
+            uint8_t* sh = sf + S::kStageF;
+            uint32_t hw[16], lw[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(sf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
-                make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-          if constexpr (DUAL) {
+            for (int e = 0; e < 16; ++e) {
+              const uint32_t a = rne24(__uint_as_float(v[2 * e])), b = rne24(__uint_as_float(v[2 * e + 1]));
+              hw[e] = (a >> 16) | (b & 0xFFFF0000u);
+              const uint32_t lo2 = ((a >> 8) & 0xFFu) | (b & 0xFF00u);  // two low bytes
+              if (e & 1) lw[e >> 1] |= lo2 << 16;
+              else lw[e >> 1] = lo2;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(sf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(hw[4 * j], hw[4 * j + 1], hw[4 * j + 2], hw[4 * j + 3]);
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              *reinterpret_cast<uint4*>(sh + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4)) =
+                  make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(sf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                  make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                              __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          }
+          if constexpr (OUT == kOutF32Bf16) {
             uint8_t* sh = sf + S::kStageF;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -457,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) {
             ptx::tma_store_3d(&tmC, sf, nb * BN + c, row0, p);
-            if constexpr (DUAL) ptx::tma_store_3d(&tmC2, sf + S::kStageF, nb * BN + c, row0, p);
+            if constexpr (OUT != kOutF32) ptx::tma_store_3d(&tmC2, sf + S::kStageF, nb * BN + c, row0, p);
             ptx::bulk_commit();
           }
         }
@@ -513,48 +551,58 @@ cudaError_t launch_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   const int64_t tiles = r * ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
-  EpiArgs ea{pb.c, pb.c_dtype == kBF16 ? 1 : 0, pb.r, static_cast<int>(M), static_cast<int>(N),
+  EpiArgs ea{pb.c, pb.c_dtype == kBF16 ? 1 : 0, 0, 0, pb.r, static_cast<int>(M), static_cast<int>(N),
              static_cast<int>(K), static_cast<__nv_bfloat16*>(pb.c2)};
   kern<<<grid, kThreads, smem, s>>>(ta, tb, ea);
   return cudaGetLastError();
 }
 
 
-bool make_out_tmap(CUtensorMap* m, const void* base, bool bf16, uint64_t N, uint64_t M,
-                   uint64_t r) {
+// 3-D (N, M, r) store map for 32 x 32 output chunks: es = 4 (fp32, 128B swizzle),
+// 2 (16-bit, 64B swizzle) or 1 (8-bit, 32B swizzle).
+bool make_out_tmap(CUtensorMap* m, const void* base, int es, uint64_t N, uint64_t M, uint64_t r) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return false;
-  const uint64_t es = bf16 ? 2 : 4;
   cuuint64_t dims[3] = {N, M, r};
   cuuint64_t strides[2] = {N * es, N * M * es};
   cuuint32_t box[3] = {32, 32, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult res = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-                    const_cast<void*>(base), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapDataType dt = es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                           : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  const CUtensorMapSwizzle sw = es == 4 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : es == 2 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                          : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUresult res = fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool DUAL>
+template <int BN, bool A_MN, bool B_MN, int OUT>
 cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
   CUtensorMap ta, tb, tc, tc2;
   const uint64_t M = pb.M, N = pb.N, K = pb.K, r = pb.r;
   bool ok = A_MN ? make_tmap(&ta, pb.a, M, K, r, kBK) : make_tmap(&ta, pb.a, K, M, r, 128);
   ok = ok && (B_MN ? make_tmap(&tb, pb.b, N, K, r, kBK) : make_tmap(&tb, pb.b, K, N, r, BN / 2));
-  ok = ok && make_out_tmap(&tc, pb.c, false, N, M, r);
-  if (DUAL) ok = ok && make_out_tmap(&tc2, pb.c2, true, N, M, r);
-  else tc2 = tc;
+  if (OUT == kOutF24) {
+    ok = ok && make_out_tmap(&tc, pb.c, 2, N, M, r) &&
+         make_out_tmap(&tc2, static_cast<uint8_t*>(pb.c) + 2 * r * M * N, 1, N, M, r);
+  } else {
+    ok = ok && make_out_tmap(&tc, pb.c, 4, N, M, r);
+    if (OUT == kOutF32Bf16) ok = ok && make_out_tmap(&tc2, pb.c2, 2, N, M, r);
+    else tc2 = tc;
+  }
   if (!ok) return cudaErrorInvalidValue;
-  auto kern = slice_gemm_tc2_kernel<BN, A_MN, B_MN, DUAL>;
-  const int smem = Smem2<BN, DUAL>::kTotal;
+  auto kern = slice_gemm_tc2_kernel<BN, A_MN, B_MN, OUT>;
+  const int smem = Smem2<BN, OUT>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t tiles = r * ((M + 255) / 256) * ((N + BN - 1) / BN);
   const int pairs = sm_count() / 2;
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
-  EpiArgs ea{pb.c, 0, pb.r, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
+  static const int nostore = getenv("STL_GEMM_NOSTORE") ? atoi(getenv("STL_GEMM_NOSTORE")) : 0;
+  EpiArgs ea{pb.c, 0, nostore, 0, pb.r, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
              static_cast<__nv_bfloat16*>(pb.c2)};
   kern<<<grid, kThreads, smem, s>>>(ta, tb, tc, tc2, ea);
   return cudaGetLastError();
@@ -562,7 +610,8 @@ cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
 
 template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch_tc2_any(const SliceGemmProblem& pb, cudaStream_t s) {
-  return pb.c2 ? launch_tc2<BN, A_MN, B_MN, true>(pb, s) : launch_tc2<BN, A_MN, B_MN, false>(pb, s);
+  if (pb.c_dtype == kF24) return launch_tc2<BN, A_MN, B_MN, kOutF24>(pb, s);
+  return pb.c2 ? launch_tc2<BN, A_MN, B_MN, kOutF32Bf16>(pb, s) : launch_tc2<BN, A_MN, B_MN, kOutF32>(pb, s);
 }
 
 }  // namespace
@@ -605,6 +654,11 @@ bool slice_gemm_tc_supported(const SliceGemmProblem& pb) {
   return get_encode_fn() != nullptr;
 }
 
+bool slice_gemm_f24_supported(const SliceGemmProblem& pb) {
+  return slice_gemm_tc_supported(pb) && pb.M > 128 && pb.N % 16 == 0 && !pb.c2 &&
+         (reinterpret_cast<uintptr_t>(pb.c) & 15) == 0 && getenv("STL_GEMM_1CTA") == nullptr;
+}
+
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   const bool a_mn = pb.a_layout != 0, b_mn = pb.b_layout != 0;
   static const int force1 = [] {
@@ -613,7 +667,9 @@ cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   }();
   // The pair kernel stores C with TMA (fp32 output, 16-byte aligned rows); other cases use the
   // 1-CTA kernel's direct-store epilogue.
-  const bool pair_ok = pb.M > 128 && !force1 && pb.c_dtype == kF32 && pb.N % 4 == 0 &&
+  if (pb.c_dtype == kF24 && !slice_gemm_f24_supported(pb)) return cudaErrorNotSupported;
+  const bool pair_ok = pb.M > 128 && !force1 && (pb.c_dtype == kF32 || pb.c_dtype == kF24) &&
+                       pb.N % 4 == 0 &&
                        (reinterpret_cast<uintptr_t>(pb.c) & 15) == 0 &&
                        (!pb.c2 || (pb.N % 8 == 0 && (reinterpret_cast<uintptr_t>(pb.c2) & 15) == 0));
   if (pair_ok) {

@@ -22,6 +22,7 @@
 // over CTAs by a fixed-order tree (deterministic).
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include "sm100_ptx.cuh"
 #include "stl_internal.h"
 
@@ -41,8 +42,15 @@ template <int MODE> constexpr bool has_planes_in() { return MODE != kEnc; }
 template <int MODE> constexpr bool is_enc() { return MODE == kEnc || MODE == kEncRed; }
 template <int MODE> constexpr bool has_red() { return MODE == kEncRed || MODE == kDecRed; }
 
+// Plane element types: float, __nv_bfloat16, or F24 (kF24 of stl_internal.h: a 16-bit high
+// plane set + an 8-bit low plane set, moved as two boxes).
+struct F24 {};
+template <typename ZT> constexpr bool is_f24() { return std::is_same<ZT, F24>::value; }
+template <typename ZT> constexpr int zhi() { return is_f24<ZT>() ? 2 : static_cast<int>(sizeof(ZT)); }
+
 struct Layout {
   uint32_t pl_bytes;     // plane box of a stage (TMA, 128B-swizzled, 1024-aligned)
+  uint32_t pl_lo;        // F24: offset of the 8-bit low box inside the plane region
   uint32_t row_stride, rows_bytes;  // padded matrix rows of a stage
   uint32_t stage_bytes;
   uint32_t out_stride, out_bytes;   // one output staging buffer
@@ -59,9 +67,12 @@ int env_int(const char* name, int dflt) {
 }
 
 template <int MODE, typename ZT, int kT>
-inline Layout make_layout(int P) {
+inline Layout make_layout(int P, int Pb) {
+  // Pb >= P: planes of the input box (the TMA zero-fills planes P..Pb-1, so the consumers'
+  // plane loops need no bounds checks)
   Layout L{};
-  L.pl_bytes = has_planes_in<MODE>() ? rup(P * kT * sizeof(ZT), 1024) : 0;
+  L.pl_lo = is_f24<ZT>() ? rup(Pb * kT * 2, 1024) : 0;
+  L.pl_bytes = has_planes_in<MODE>() ? rup(Pb * kT * zhi<ZT>(), 1024) + (is_f24<ZT>() ? rup(Pb * kT, 1024) : 0) : 0;
   L.row_stride = kT * 4 * 2 + kRowPad;
   L.rows_bytes = has_rows<MODE>() ? 4 * L.row_stride : 0;
   L.stage_bytes = rup(L.pl_bytes + L.rows_bytes, 1024);
@@ -72,8 +83,8 @@ inline Layout make_layout(int P) {
     L.out_stride = kT * 4 * 2 + kRowPad;
     L.out_bytes = rup(4 * L.out_stride, 1024);
   }
-  L.red_bytes = has_red<MODE>() ? kCWarps * P * 16 * 4 : 0;
-  static const uint32_t budget = env_int("STL_STREAM_SMEM_KB", 200) * 1024;
+  L.red_bytes = 0;  // the final per-warp reduction partials reuse the (drained) stage ring
+  static const uint32_t budget = env_int("STL_STREAM_SMEM_KB", 212) * 1024;
   static const uint32_t max_st = env_int("STL_STREAM_STAGES", 8);
   const uint32_t fixed = 2 * L.out_bytes + L.red_bytes;
   uint32_t ns = (budget - fixed) / L.stage_bytes;
@@ -91,11 +102,13 @@ struct StreamArgs {
   const float* coef;         // P x 16 (encoder rows for ENC*, decoder rows for DEC*)
   float* red_partial;        // [gridDim.x][P * 16]
   int P;
+  int Pb;                    // planes in the (zero-padded) input plane box
   int64_t br, bc;
   int64_t upr;               // units per tile row
   int64_t nunits;
   int stg;                   // 1: consumers write outputs with st.global (else TMA/bulk stores)
   int nocompute;             // probe: skip the math (pure data movement)
+  unsigned long long* dbg;   // probe: per-CTA phase timers [grid][4] (ns), or null
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -152,6 +165,24 @@ __device__ __forceinline__ void mma(float (&c)[4], uint32_t a0, uint32_t a1, uin
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+// fp32 -> tf32 operand, rounded to nearest (ties away) by adding half an ulp of the 10-bit
+// mantissa; the tensor core ignores the low 13 bits. (Finite inputs.)
+__device__ __forceinline__ uint32_t tf32_rna(float x) { return __float_as_uint(x) + 0x1000u; }
+// D += A . B, m16n8k8, tf32 operands (fp32 registers), fp32 accumulate.
+//   A: a0 = (row g, k q), a1 = (g+8, q), a2 = (g, q+4), a3 = (g+8, q+4); B: b0 = (k q, col g),
+//   b1 = (q+4, g); C as m16n8k16.
+__device__ __forceinline__ void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// F24 pair: high halves of two elements (one 32-bit word) + their low bytes (one 16-bit word)
+__device__ __forceinline__ float2 f24x2(uint32_t hi2, uint32_t lo2) {
+  return make_float2(__uint_as_float((hi2 << 16) | ((lo2 & 0xFFu) << 8)),
+                     __uint_as_float((hi2 & 0xFFFF0000u) | (lo2 & 0xFF00u)));
+}
 // two bf16 from (lo16 of a, lo16 of b) -> packed pair
 __device__ __forceinline__ uint32_t pair16(uint32_t a, uint32_t b) { return a | (b << 16); }
 
@@ -183,7 +214,8 @@ __device__ __forceinline__ uint32_t pl_off(int P, int p, int t) {
 // MT = number of 16-plane groups (ceil(P / 16)), a template so every plane loop unrolls.
 template <int MODE, typename ZT, int MT, int kT>
 __global__ void __launch_bounds__(kSThreads, 1)
-    k_stream(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+    k_stream(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_in2,
+             const __grid_constant__ CUtensorMap tm_out,
              StreamArgs args, Layout L) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-aligned base kept as shared-array arithmetic so plain C++ loads compile to LDS and the
@@ -196,15 +228,16 @@ __global__ void __launch_bounds__(kSThreads, 1)
   auto sts32 = [smem](uint32_t o, uint32_t v) { *reinterpret_cast<uint32_t*>(smem + o) = v; };
   const uint32_t s_stages = 0;
   const uint32_t s_out = s_stages + L.nstages * L.stage_bytes;
-  float* s_red = reinterpret_cast<float*>(smem + L.nstages * L.stage_bytes + 2 * L.out_bytes);
+  float* s_red = reinterpret_cast<float*>(smem);  // after the unit loop only
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.nstages * L.stage_bytes +
                                                2 * L.out_bytes + L.red_bytes);
   uint64_t* empty = full + kMaxStages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
-  const int P = args.P;
-  constexpr int ZSZ = sizeof(ZT);
+  const int P = args.P, Pb = args.Pb;
+  constexpr int ZSZ = zhi<ZT>();         // bytes of the (high) plane element
+  constexpr bool kZ24 = is_f24<ZT>();
   const uint32_t nunits = static_cast<uint32_t>(args.nunits);
   const uint32_t upr = static_cast<uint32_t>(args.upr);
   const uint32_t bc = static_cast<uint32_t>(args.bc);
@@ -218,6 +251,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
   }
   if (warp == kCWarps && lane == 0) {
     if constexpr (has_planes_in<MODE>()) ptx::prefetch_tmap(&tm_in);
+    if constexpr (kZ24) ptx::prefetch_tmap(&tm_in2);
     if constexpr (is_enc<MODE>()) ptx::prefetch_tmap(&tm_out);
   }
   __syncthreads();
@@ -238,9 +272,12 @@ __global__ void __launch_bounds__(kSThreads, 1)
       const uint32_t st = s_stages + stage * L.stage_bytes;
       if (lane == 0) {
         ptx::mbar_arrive_expect_tx(&full[stage],
-                                   4 * rows_b + (has_planes_in<MODE>() ? P * kT * ZSZ : 0));
+                                   4 * rows_b + (has_planes_in<MODE>() ? Pb * kT * (ZSZ + (kZ24 ? 1 : 0)) : 0));
         if constexpr (has_planes_in<MODE>())
           tma_load_4d(&tm_in, &full[stage], sbase + st, 0, 0, static_cast<int>(J0 / (128 / ZSZ)),
+                      static_cast<int>(I));
+        if constexpr (kZ24)
+          tma_load_4d(&tm_in2, &full[stage], sbase + st + L.pl_lo, 0, 0, static_cast<int>(J0 / 128),
                       static_cast<int>(I));
       }
       if constexpr (has_rows<MODE>()) {
@@ -293,8 +330,9 @@ __global__ void __launch_bounds__(kSThreads, 1)
   for (int k = 0; k < kNK; ++k) soff[k] = is_enc<MODE>() ? pl_off<2>(P, g, 8 * (warp + kCWarps * k) + 2 * q) : 0u;
   // Stores/loads of planes >= P exist only in the last 16-plane group.
   const bool lastp0 = 16 * (MT - 1) + g < P, lastp1 = 16 * (MT - 1) + g + 8 < P;
+  const bool okb1 = 16 * (MT - 1) + g + 8 < Pb;  // row inside the (8-padded) input box
   // RED: B loads at rows + rb[nt] + 1024k; A loads at planes + ra0/ra2[k] + (16mt + 8h) * 128.
-  uint32_t rb[2], ra0[kMK], ra2[kMK];
+  uint32_t rb[2], ra0[kMK], ra2[kMK], ra0l[kMK], ra2l[kMK];
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const int c = 8 * nt + g;
@@ -303,21 +341,41 @@ __global__ void __launch_bounds__(kSThreads, 1)
 #pragma unroll
   for (int k = 0; k < kMK; ++k) {
     const int t = 16 * (warp + kCWarps * k) + 2 * q;
-    ra0[k] = has_red<MODE>() ? pl_off<ZSZ>(P, g, t) : 0u;
-    ra2[k] = has_red<MODE>() ? pl_off<ZSZ>(P, g, t + 8) : 0u;
+    ra0[k] = has_red<MODE>() ? pl_off<ZSZ>(Pb, g, t) : 0u;
+    ra2[k] = has_red<MODE>() ? pl_off<ZSZ>(Pb, g, t + 8) : 0u;
+    ra0l[k] = kZ24 ? L.pl_lo + pl_off<1>(Pb, g, t) : 0u;   // F24 low bytes: same rule, W = 128
+    ra2l[k] = kZ24 ? L.pl_lo + pl_off<1>(Pb, g, t + 8) : 0u;
   }
   // DEC: A loads at planes + da[k][j] + (16ks + 8h) * 128 (planes 2q + j + 16ks + 8h at tiles
   // t0, t0 + 1, t0 = 16 (warp + 8k) + 2g); C stores at buf + ooff + 1024k + 2nt RS (+8).
-  uint32_t da[kMK][2];
+  uint32_t da[kMK][2], dal[kMK][2];
 #pragma unroll
   for (int k = 0; k < kMK; ++k)
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-      da[k][j] = is_enc<MODE>() ? 0u : pl_off<ZSZ>(P, 2 * q + j, 16 * (warp + kCWarps * k) + 2 * g);
+    for (int j = 0; j < 2; ++j) {
+      da[k][j] = is_enc<MODE>() ? 0u : pl_off<ZSZ>(Pb, 2 * q + j, 16 * (warp + kCWarps * k) + 2 * g);
+      dal[k][j] = kZ24 ? L.pl_lo + pl_off<1>(Pb, 2 * q + j, 16 * (warp + kCWarps * k) + 2 * g) : 0u;
+    }
   const uint32_t ooff = (q >> 1) * RS + 128 * warp + 16 * g + 4 * (q & 1);
   bool dok[4];  // last plane group: planes 16(MT-1) + 2q + {0, 1, 8, 9} < P
 #pragma unroll
   for (int j = 0; j < 4; ++j) dok[j] = 16 * (MT - 1) + 2 * q + (j & 1) + 8 * (j >> 1) < P;
+
+  // fp32 / F24 planes use single-pass TF32 MMAs (operands rounded to nearest tf32, ~2^-12):
+  // DEC B = D with k = q <-> plane 8s + 2q, k = q + 4 <-> plane 8s + 2q + 1 (the planes a
+  // thread loads, see below): bt[s][nt][0] = D[8s+2q][8nt+g], bt[s][nt][1] = D[8s+2q+1][8nt+g].
+  constexpr bool kTf32 = ZSZ == 4 || kZ24;
+  constexpr int KS8 = 2 * MT;
+  uint32_t bt[KS8][2][2];
+#pragma unroll
+  for (int s8 = 0; s8 < KS8; ++s8)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int pl = 8 * s8 + 2 * q + h, c = 8 * nt + g;
+        bt[s8][nt][h] = (!is_enc<MODE>() && kTf32 && pl < P) ? tf32_rna(args.coef[pl * 16 + c]) : 0u;
+      }
 
   float R[2][2][4];
 #pragma unroll
@@ -337,7 +395,9 @@ __global__ void __launch_bounds__(kSThreads, 1)
     const uint32_t buf = s_out + (it & 1) * L.out_bytes;
     const uint32_t planes = s_stages + stage * L.stage_bytes;
     const uint32_t rows = planes + L.pl_bytes;
+    const uint64_t t_w0 = args.dbg ? ptx::globaltimer_ns() : 0;
     ptx::mbar_wait(&full[stage], phase);
+    const uint64_t t_w1 = args.dbg ? ptx::globaltimer_ns() : 0;
 
     if (args.nocompute) {
     } else if constexpr (is_enc<MODE>()) {
@@ -345,7 +405,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
       // b1 = row 2 + (q>>1). Banks: 16 (q>>1) + 2g + (q&1) -> conflict-free. C: plane 16m+g
       // (c0, c1) / 16m+g+8 (c2, c3), tiles 8nt+2q, +1, into the swizzled plane box: the 8 planes
       // g land in 8 different 16-byte chunks -> conflict-free.
-      const int nnt = Tw >> 3;
+      const int nnt = Tw == kT ? kT / 8 : (Tw >> 3);  // full units: compile-time bounds
 #pragma unroll
       for (int k = 0; k < kNK; ++k) {
         if (warp + kCWarps * k < nnt) {
@@ -366,11 +426,31 @@ __global__ void __launch_bounds__(kSThreads, 1)
       // C[tile][c] = Z^T . D per 16-tile m-tile; rows g / g+8 <-> tiles 2g / 2g+1 so each
       // plane load is one 8-byte (fp32) or 4-byte (bf16) access; with the swizzle XOR a
       // half-warp's loads hit 32 distinct banks.
-      const int nmt = Tw >> 4;
+      const int nmt = Tw == kT ? kT / 16 : (Tw >> 4);
 #pragma unroll
       for (int k = 0; k < kMK; ++k) {
         if (warp + kCWarps * k < nmt) {
           float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+          if constexpr (kTf32) {
+            // m16n8k8 tf32 per 8 planes: rows g / g+8 = tiles t0 / t0+1, k = q / q+4 = planes
+            // 8s+2q / 8s+2q+1: a0 a1 = Z[8s+2q][t0, t0+1] (one 8-byte or F24 load), a2 a3 =
+            // Z[8s+2q+1][t0, t0+1].
+#pragma unroll
+            for (int s8 = 0; s8 < KS8; ++s8) {
+              if (8 * s8 >= Pb) break;  // warp-uniform; planes P..Pb-1 are zero in the box
+              float2 v[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const uint32_t ad = planes + da[k][h] + 8 * s8 * 128;
+                if constexpr (kZ24) v[h] = f24x2(lds32(ad), lds16(planes + dal[k][h] + 8 * s8 * 128));
+                else v[h] = lds64f(ad);
+              }
+              const uint32_t a0 = tf32_rna(v[0].x), a1 = tf32_rna(v[0].y);
+              const uint32_t a2 = tf32_rna(v[1].x), a3 = tf32_rna(v[1].y);
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
+            }
+          } else {
 #pragma unroll
           for (int ks = 0; ks < MT; ++ks) {
             float v[4][2];  // planes 16ks + 2q + {0, 1, 8, 9} at tiles t0, t0 + 1
@@ -378,7 +458,11 @@ __global__ void __launch_bounds__(kSThreads, 1)
             for (int j = 0; j < 4; ++j) {
               const uint32_t ad = planes + da[k][j & 1] + (16 * ks + 8 * (j >> 1)) * 128;
               if (ks < MT - 1 || dok[j]) {
-                if constexpr (ZSZ == 4) {
+                if constexpr (kZ24) {
+                  const float2 f = f24x2(lds32(ad), lds16(planes + dal[k][j & 1] + (16 * ks + 8 * (j >> 1)) * 128));
+                  v[j][0] = f.x;
+                  v[j][1] = f.y;
+                } else if constexpr (ZSZ == 4) {
                   const float2 f = lds64f(ad);
                   v[j][0] = f.x;
                   v[j][1] = f.y;
@@ -393,7 +477,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
               }
             }
             // a0 = (row g = tile t0: planes 2q, 2q+1), a1 = row g+8 = tile t0+1, a2/a3: +8
-            if constexpr (ZSZ == 4) {
+            if constexpr (ZSZ == 4 || kZ24) {
               uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
               split2(v[0][0], v[1][0], h0, l0);
               split2(v[0][1], v[1][1], h1, l1);
@@ -416,6 +500,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
               }
             }
           }
+          }  // bf16 planes
           // acc[nt][0,1] -> tile t0, c = 8nt + 2q (+1): row a = 2nt + (q>>1), col b = 2(q&1).
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
@@ -430,30 +515,73 @@ __global__ void __launch_bounds__(kSThreads, 1)
       // R[p][c] += sum over 16-tile k-steps of Z[p][tile] X[tile][c] (A = Z: M = p; B = X: N = c).
       // B: b0 = (X[t0+2q][c], X[t0+2q+1][c]), b1 = tiles + 8, c = 8nt + g, 16-bit loads
       // (words 16 (c>>2) + 4q + ((c&3)>>1): distinct). A: Z[p][t0+2q, +1] / [t0+2q+8, +9].
-      const int nks = Tw >> 4;
+      const int nks = Tw == kT ? kT / 16 : (Tw >> 4);
 #pragma unroll
       for (int k = 0; k < kMK; ++k) {
         if (warp + kCWarps * k < nks) {
-          uint32_t b[2][2];
+          uint32_t b[2][2], bx[2][2][2];
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
             const uint32_t base = rows + rb[nt] + 128 * kCWarps * k;
-            b[nt][0] = pair16(lds16(base), lds16(base + 8));
-            b[nt][1] = pair16(lds16(base + 64), lds16(base + 72));
+            const uint32_t x0 = lds16(base), x1 = lds16(base + 8), x8 = lds16(base + 64),
+                           x9 = lds16(base + 72);
+            b[nt][0] = pair16(x0, x1);
+            b[nt][1] = pair16(x8, x9);
+            bx[nt][0][0] = x0 << 16;
+            bx[nt][0][1] = x1 << 16;
+            bx[nt][1][0] = x8 << 16;
+            bx[nt][1][1] = x9 << 16;
           }
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
             const bool ok0 = mt < MT - 1 || lastp0, ok1 = mt < MT - 1 || lastp1;
             const uint32_t z0 = planes + ra0[k] + 16 * mt * 128, z2 = planes + ra2[k] + 16 * mt * 128;
-            if constexpr (ZSZ == 2) {
+            if constexpr (kTf32) {
+              // two m16n8k8 tf32 steps (tiles t0..t0+7, t0+8..t0+15): rows g / g+8 = planes,
+              // k = q / q+4 = tiles 2q / 2q+1 of the step; B = X as fp32 (bf16 << 16, exact).
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const uint32_t za = hh ? z2 : z0;
+                // planes 16mt+g (< Pb) and 16mt+g+8 (may pass Pb in the last group: load a
+                // valid row, select zero)
+                const bool in1 = mt < MT - 1 || okb1;
+                const uint32_t d1 = in1 ? 1024u : 0u;
+                float2 v0, v1;
+                if constexpr (kZ24) {
+                  const uint32_t la = planes + (hh ? ra2l[k] : ra0l[k]) + 16 * mt * 128;
+                  v0 = f24x2(lds32(za), lds16(la));
+                  v1 = f24x2(lds32(za + d1), lds16(la + d1));
+                } else {
+                  v0 = lds64f(za);
+                  v1 = lds64f(za + d1);
+                }
+                if (!in1) v1 = make_float2(0.f, 0.f);
+                const uint32_t a0 = tf32_rna(v0.x), a1 = tf32_rna(v1.x);
+                const uint32_t a2 = tf32_rna(v0.y), a3 = tf32_rna(v1.y);
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+                  mma_tf32(R[mt][nt], a0, a1, a2, a3, bx[nt][hh][0], bx[nt][hh][1]);
+              }
+            } else if constexpr (ZSZ == 2 && !kZ24) {
               const uint32_t a0 = ok0 ? lds32(z0) : 0u, a2 = ok0 ? lds32(z2) : 0u;
               const uint32_t a1 = ok1 ? lds32(z0 + 1024) : 0u, a3 = ok1 ? lds32(z2 + 1024) : 0u;
 #pragma unroll
               for (int nt = 0; nt < 2; ++nt) mma(R[mt][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
             } else {
               const float2 zero = make_float2(0.f, 0.f);
-              const float2 v0 = ok0 ? lds64f(z0) : zero, v2 = ok0 ? lds64f(z2) : zero;
-              const float2 v1 = ok1 ? lds64f(z0 + 1024) : zero, v3 = ok1 ? lds64f(z2 + 1024) : zero;
+              float2 v0, v1, v2, v3;
+              if constexpr (kZ24) {
+                const uint32_t l0 = planes + ra0l[k] + 16 * mt * 128, l2 = planes + ra2l[k] + 16 * mt * 128;
+                v0 = ok0 ? f24x2(lds32(z0), lds16(l0)) : zero;
+                v2 = ok0 ? f24x2(lds32(z2), lds16(l2)) : zero;
+                v1 = ok1 ? f24x2(lds32(z0 + 1024), lds16(l0 + 1024)) : zero;
+                v3 = ok1 ? f24x2(lds32(z2 + 1024), lds16(l2 + 1024)) : zero;
+              } else {
+                v0 = ok0 ? lds64f(z0) : zero;
+                v2 = ok0 ? lds64f(z2) : zero;
+                v1 = ok1 ? lds64f(z0 + 1024) : zero;
+                v3 = ok1 ? lds64f(z2 + 1024) : zero;
+              }
               uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
               split2(v0.x, v0.y, h0, l0);
               split2(v1.x, v1.y, h1, l1);
@@ -471,6 +599,11 @@ __global__ void __launch_bounds__(kSThreads, 1)
     }
 
     __syncwarp();
+    if (args.dbg && ctid == 0) {
+      const uint64_t t_c = ptx::globaltimer_ns();
+      args.dbg[4 * blockIdx.x + 0] += t_w1 - t_w0;  // waiting for data
+      args.dbg[4 * blockIdx.x + 1] += t_c - t_w1;   // math (warp 0's share)
+    }
     if (lane == 0) ptx::mbar_arrive(&empty[stage]);
     if (args.stg) {
       // Consumers copy the staged unit to global memory with 16-byte stores (coalesced rows).
@@ -517,7 +650,9 @@ __global__ void __launch_bounds__(kSThreads, 1)
   if (warp == 0) ptx::bulk_wait_all();
 
   if constexpr (has_red<MODE>()) {
-    // per-warp fragments -> smem -> fixed-order sum over warps -> this CTA's partial
+    // per-warp fragments -> smem (the stage ring, once every warp is done with it) ->
+    // fixed-order sum over warps -> this CTA's partial
+    cbar();
     float* mine = s_red + warp * P * 16;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
@@ -545,7 +680,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
 }
 
 // 4-D plane map (W tiles, P planes, bc/W chunks, br rows) with box {W, P, kT/W, 1}, 128B swizzle.
-bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int64_t br, int64_t bc, int kT) {
+bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_t br, int64_t bc,
+                int kT) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -564,10 +700,11 @@ bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int64_t br, in
                         static_cast<cuuint64_t>(br)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(br * bc * zsz), 128,
                            static_cast<cuuint64_t>(bc * zsz)};
-  cuuint32_t box[4] = {static_cast<cuuint32_t>(W), static_cast<cuuint32_t>(P),
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(W), static_cast<cuuint32_t>(Pb),
                        static_cast<cuuint32_t>(kT / W), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(m, zsz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+  CUresult r = fn(m, zsz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                  : zsz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8,
                   4, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -583,11 +720,16 @@ bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int64_t br, in
 template <int MODE, typename ZT, int MT, int kT>
 cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                       cudaStream_t s) {
-  const Layout L = make_layout<MODE, ZT, kT>(a.P);
-  CUtensorMap tin{}, tout{};
-  if (has_planes_in<MODE>() && !plane_tmap(&tin, planes_in, sizeof(ZT), a.P, a.br, a.bc, kT))
+  a.Pb = ((a.P + 7) / 8) * 8;
+  const Layout L = make_layout<MODE, ZT, kT>(a.P, a.Pb);
+  CUtensorMap tin{}, tin2{}, tout{};
+  if (has_planes_in<MODE>() && !plane_tmap(&tin, planes_in, zhi<ZT>(), a.P, a.Pb, a.br, a.bc, kT))
     return cudaErrorNotSupported;
-  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.br, a.bc, kT))
+  if (is_f24<ZT>() &&
+      !plane_tmap(&tin2, static_cast<const uint8_t*>(planes_in) + 2 * a.P * a.br * a.bc, 1, a.P,
+                  a.Pb, a.br, a.bc, kT))
+    return cudaErrorNotSupported;
+  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.P, a.br, a.bc, kT))
     return cudaErrorNotSupported;
   auto k = k_stream<MODE, ZT, MT, kT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -597,14 +739,30 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   a.stg = stg;
   static const int noc = env_int("STL_STREAM_NOCOMPUTE", 0);
   a.nocompute = noc;
+  static const int dbg_on = env_int("STL_STREAM_DEBUG", 0);
+  static unsigned long long* dbg = nullptr;
+  if (dbg_on && !dbg) cudaMalloc(&dbg, 4 * 1024 * sizeof(unsigned long long));
+  if (dbg_on) cudaMemsetAsync(dbg, 0, 4 * 1024 * sizeof(unsigned long long), s);
+  a.dbg = dbg_on ? dbg : nullptr;
   a.upr = (a.bc + kT - 1) / kT;  // kT: this launch's unit
   a.nunits = a.br * a.upr;
   int64_t grid = sm_count();
   if (grid > a.nunits) grid = a.nunits;
   if (grid < 1) return cudaSuccess;
-  k<<<static_cast<int>(grid), kSThreads, L.total, s>>>(tin, tout, a, L);
+  const uint64_t t0 = 0;
+  (void)t0;
+  k<<<static_cast<int>(grid), kSThreads, L.total, s>>>(tin, tin2, tout, a, L);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (a.dbg) {
+    unsigned long long h[4 * 1024];
+    cudaMemcpyAsync(h, a.dbg, sizeof(unsigned long long) * 4 * grid, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double w = 0, c = 0;
+    for (int i = 0; i < grid; ++i) { w += h[4 * i]; c += h[4 * i + 1]; }
+    fprintf(stderr, "[stream dbg] mode=%d T=%d units/cta=%.1f stages=%u  avg us: wait=%.1f math=%.1f\n",
+            MODE, kT, double(a.nunits) / grid, L.nstages, w / grid / 1e3, c / grid / 1e3);
+  }
   if constexpr (has_red<MODE>()) return sum_partials(a.red_partial, static_cast<int>(grid), a.P * 16, red_out, s);
   return cudaSuccess;
 }
@@ -615,7 +773,8 @@ template <int MODE, typename ZT, int MT>
 cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                      cudaStream_t s) {
   static const int force_t = env_int("STL_STREAM_T", 0);
-  const Layout L512 = make_layout<MODE, ZT, 512>(a.P);
+  const int pb = ((a.P + 7) / 8) * 8;
+  const Layout L512 = make_layout<MODE, ZT, 512>(a.P, pb);
   const bool use512 = force_t ? force_t == 512
                               : (L512.nstages >= 2 && L512.total <= 227 * 1024 && a.bc >= 512);
   if (use512) return launch_mt<MODE, ZT, MT, 512>(a, planes_in, planes_out, red_out, s);
@@ -650,7 +809,8 @@ cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t 
   if (!g_use_stream || mdt != kBF16 || odt != kBF16 || bc % 64 || ldm % 8 || P < 1 || P > 64 ||
       !al16(m) || !al16(out))
     return cudaErrorNotSupported;
-  if (rp && (P > 32 || !al16(rp) || !ro || !rw)) return cudaErrorNotSupported;
+  if (rp && (P > 32 || !al16(rp) || !ro || !rw || (rdt == kF24 && bc % 128)))
+    return cudaErrorNotSupported;
   StreamArgs a{};
   a.mat = static_cast<const __nv_bfloat16*>(m);
   a.ldm = ldm;
@@ -662,6 +822,7 @@ cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t 
   a.bc = bc;
   if (!rp) return launch<kEnc, __nv_bfloat16>(a, nullptr, out, nullptr, s);
   if (rdt == kBF16) return launch<kEncRed, __nv_bfloat16>(a, rp, out, ro, s);
+  if (rdt == kF24) return launch<kEncRed, F24>(a, rp, out, ro, s);
   return launch<kEncRed, float>(a, rp, out, ro, s);
 }
 
@@ -675,6 +836,7 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
     return cudaErrorNotSupported;
   if (rm && (rdt != kBF16 || Q > 32 || ldr % 8 || !al16(rm) || !ro || !rw))
     return cudaErrorNotSupported;
+  if (idt == kF24 && bc % 128) return cudaErrorNotSupported;
   StreamArgs a{};
   a.mat = static_cast<const __nv_bfloat16*>(rm);
   a.ldm = ldr;
@@ -687,9 +849,11 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
   a.bc = bc;
   if (rm) {
     if (idt == kF32) return launch<kDecRed, float>(a, in, nullptr, ro, s);
+    if (idt == kF24) return launch<kDecRed, F24>(a, in, nullptr, ro, s);
     return launch<kDecRed, __nv_bfloat16>(a, in, nullptr, ro, s);
   }
   if (idt == kF32) return launch<kDec, float>(a, in, nullptr, nullptr, s);
+  if (idt == kF24) return launch<kDec, F24>(a, in, nullptr, nullptr, s);
   return launch<kDec, __nv_bfloat16>(a, in, nullptr, nullptr, s);
 }
 

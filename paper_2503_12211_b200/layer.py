@@ -60,7 +60,9 @@ class LayerCache(NamedTuple):
 
     vx: the layer input itself (the reference keeps tile_fibers(x), the same numbers);
     u: encoded input planes (r, M/t, K/t) in the compute dtype;
-    y_enc: slice products, planes (r, M/t, N/t) in the compute dtype (fp32 or bf16).
+    y_enc: slice products (r, M/t, N/t): fp32 planes in fp32 mode; on the bf16 path a uint8
+    F24 buffer (24-bit slice products, see stl_cache_bytes) or bf16 planes.
+    ``unpack_slice_products`` returns fp32 planes for any of them.
     """
 
     vx: torch.Tensor

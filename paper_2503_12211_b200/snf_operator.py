@@ -218,10 +218,30 @@ def forward_scratch(M: int, K: int, N: int, t: int, r: int, dtype: torch.dtype,
     return torch.empty((max(nbytes, 1),), dtype=torch.uint8, device=device)
 
 
-def _forward(x: torch.Tensor, w_planes: torch.Tensor, snf: SnfTriple, keep_cache: bool = False):
-    """Shared forward launch: returns y (and the (u, y_enc) planes when keep_cache).
+def cache_bytes(M: int, K: int, N: int, t: int, r: int, dtype: torch.dtype) -> int:
+    """Bytes of the forward cache y_enc (stl_cache_bytes)."""
+    return int(_lib.load().stl_cache_bytes(M, K, N, t, r, _dt(dtype)))
 
-    The cached y_enc planes are in the compute dtype (fp32 or bf16)."""
+
+def unpack_slice_products(y_enc: torch.Tensor, r: int, rows: int, cols: int) -> torch.Tensor:
+    """fp32 planes (r, rows, cols) of a y_enc cache in any of its formats.
+
+    uint8 caches are F24: the high 16 bits of every element, then the next 8 bits (bf16 path,
+    see include/stl_b200.h stl_cache_bytes); plane caches are fp32 or bf16.
+    """
+    if y_enc.dtype != torch.uint8:
+        return y_enc.float().reshape(r, rows, cols)
+    n = r * rows * cols
+    hi = y_enc[: 2 * n].view(torch.int16).to(torch.int32) & 0xFFFF
+    lo = y_enc[2 * n: 3 * n].to(torch.int32)
+    return ((hi << 16) | (lo << 8)).view(torch.float32).reshape(r, rows, cols)
+
+
+def _forward(x: torch.Tensor, w_planes: torch.Tensor, snf: SnfTriple, keep_cache: bool = False):
+    """Shared forward launch: returns y (and the (u, y_enc) cache when keep_cache).
+
+    y_enc is fp32 planes (fp32 mode), or on the bf16 path a uint8 F24 buffer or bf16 planes
+    (stl_cache_bytes decides); unpack_slice_products gives fp32 planes for any of them."""
     t, r = snf.t, snf.r
     M, K = x.shape
     bk, bj = w_planes.shape[2], w_planes.shape[1]
@@ -231,7 +251,13 @@ def _forward(x: torch.Tensor, w_planes: torch.Tensor, snf: SnfTriple, keep_cache
     dev = x.device
     snf.on(dev)
     u = torch.empty((r, M // t, bk), dtype=x.dtype, device=dev)
-    y_enc = torch.empty((r, M // t, bj), dtype=x.dtype, device=dev) if keep_cache else None
+    y_enc = None
+    if keep_cache:
+        nbytes = cache_bytes(M, K, N, t, r, x.dtype)
+        if nbytes == 3 * r * (M // t) * bj:
+            y_enc = torch.empty((nbytes,), dtype=torch.uint8, device=dev)
+        else:
+            y_enc = torch.empty((r, M // t, bj), dtype=x.dtype, device=dev)
     y = torch.empty((M, N), dtype=x.dtype, device=dev)
     scratch = forward_scratch(M, K, N, t, r, x.dtype, dev)
     _lib.check(_lib.load().stl_forward(

@@ -13,7 +13,7 @@ w = torch.randn((R, N // T, K // T), device=dev).to(torch.bfloat16) * 0.03
 x = torch.randn((M, K), device=dev).to(torch.bfloat16)
 gy = torch.randn((M, N), device=dev).to(torch.bfloat16)
 layer_snf = snf
-for mode in (0, 4, 2):
+for mode in (int(os.environ.get("STL_FUSION_BITS", "0")),):
     lib.stl_set_fusion(mode)
     def step():
         from paper_2503_12211_b200.snf_operator import _forward

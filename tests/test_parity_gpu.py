@@ -377,15 +377,15 @@ def test_fused_decode_matches_unfused_and_oracle(M, K, N, r):
     layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
     try:
         stl.set_fusion(False)
-        y_u, c_u = stl._layer_forward_cached(layer, x_dev)
-        stl.set_fusion(True)
-        y_f, c_f = stl._layer_forward_cached(layer, x_dev)
+        y_u = stl.stl_layer_forward(layer, x_dev)
+        stl.set_fusion(True)  # the decode-fused kernel serves cache-free forwards
+        y_f = stl.stl_layer_forward(layer, x_dev)
     finally:
         stl.set_fusion(False)
     torch.cuda.synchronize()
-    assert rel(y_f, y_u) <= 1e-3  # same math, different summation order / bf16 rounding
-    assert torch.equal(c_f.u, c_u.u)
-    assert rel(c_f.y_enc, c_u.y_enc) <= 1e-6
+    # same math in different precisions (FFMA fp32 vs TF32 tensor-core decode) and summation
+    # order, both rounded to bf16: differ by about one bf16 ulp in a few elements
+    assert rel(y_f, y_u) <= 2e-3
     slab = slice(0, min(M, 256))
     ref = O.stl_batched(x64[slab], w64, e_x, d, t)
     assert rel(y_f[slab], ref) <= BF16_TOL
@@ -409,10 +409,13 @@ def test_mma_transforms_match_ffma(M, K, N, r):
     layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
     outs = {}
     try:
-        for mode in (2, 4):  # bit 1: FFMA transforms; bit 2: mma decode; bit 0 off: unfused
+        # 2|8|16: FFMA transforms, no streaming kernels, fp32 slice products;
+        # 4|8|16: register-mma transforms; 0: streaming transforms + F24 slice products
+        for mode in (2 | 8 | 16, 4 | 8 | 16, 0):
             _lib.load().stl_set_fusion(mode)
             y, cache = stl._layer_forward_cached(layer, x_dev)
-            outs[mode] = (y, cache.u, cache.y_enc) + tuple(stl._layer_backward(layer, cache, gy_dev))
+            y_enc = stl.unpack_slice_products(cache.y_enc, r, M // t, N // t)
+            outs[mode] = (y, cache.u, y_enc) + tuple(stl._layer_backward(layer, cache, gy_dev))
     finally:
         _lib.load().stl_set_fusion(0)
     torch.cuda.synchronize()
@@ -421,6 +424,7 @@ def test_mma_transforms_match_ffma(M, K, N, r):
         tuple(O.layer_backward(w64, e_x, d, cache_ref, gy64, t))
     names = ("y", "u", "y_enc", "g_ex", "g_d", "g_w", "g_x")
     for i, name in enumerate(names):
-        a, b = outs[4][i], outs[2][i]
-        assert rel(a, b) <= 2e-3, (name, rel(a, b))
-        assert rel(a, refs[i]) <= BF16_TOL, (name, rel(a, refs[i]))
+        for mode in (4 | 8 | 16, 0):
+            a, b = outs[mode][i], outs[2 | 8 | 16][i]
+            assert rel(a, b) <= 2e-3, (name, mode, rel(a, b))
+            assert rel(a, refs[i]) <= BF16_TOL, (name, mode, rel(a, refs[i]))
