@@ -33,6 +33,9 @@ enum Mode { kEnc = 0, kEncRed = 1, kDec = 2, kDecRed = 3 };
 
 constexpr int kCWarps = 16;                 // consumer warps
 constexpr int kCThreads = 32 * kCWarps;
+// Consumer groups taking alternate units: two 8-warp groups for the plain transforms (their
+// per-unit math is short, so two units in flight hide its latency), one 16-warp group for the
+// fused reductions (more math per unit: splitting it 16 ways wins).
 constexpr int kSThreads = kCThreads + 32;   // + producer warp
 constexpr int kMaxStages = 16;
 constexpr uint32_t kRowPad = 64;            // matrix rows: 16-word bank shift per row
@@ -41,6 +44,7 @@ template <int MODE> constexpr bool has_rows() { return MODE != kDec; }
 template <int MODE> constexpr bool has_planes_in() { return MODE != kEnc; }
 template <int MODE> constexpr bool is_enc() { return MODE == kEnc || MODE == kEncRed; }
 template <int MODE> constexpr bool has_red() { return MODE == kEncRed || MODE == kDecRed; }
+template <int MODE> constexpr int groups_of() { return has_red<MODE>() ? 1 : 2; }
 
 // Plane element types: float, __nv_bfloat16, or F24 (kF24 of stl_internal.h: a 16-bit high
 // plane set + an 8-bit low plane set, moved as two boxes).
@@ -86,11 +90,11 @@ inline Layout make_layout(int P, int Pb) {
   L.red_bytes = 0;  // the final per-warp reduction partials reuse the (drained) stage ring
   static const uint32_t budget = env_int("STL_STREAM_SMEM_KB", 212) * 1024;
   static const uint32_t max_st = env_int("STL_STREAM_STAGES", 8);
-  const uint32_t fixed = 2 * L.out_bytes + L.red_bytes;
+  const uint32_t fixed = 2 * groups_of<MODE>() * L.out_bytes + L.red_bytes;
   uint32_t ns = (budget - fixed) / L.stage_bytes;
   if (ns > max_st) ns = max_st;
   L.nstages = ns > kMaxStages ? kMaxStages : (ns < 2 ? 2 : ns);
-  L.total = L.nstages * L.stage_bytes + fixed + 2 * kMaxStages * 8 + 1024;
+  L.total = L.nstages * L.stage_bytes + fixed + 2 * kMaxStages * 8 + 1024;  // + barriers, align
   return L;
 }
 
@@ -145,6 +149,11 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, uint32_t src,
 }
 __device__ __forceinline__ void cbar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kCThreads) : "memory");
+}
+// barrier of one consumer group of NT threads (ids 2, 3)
+template <int NT>
+__device__ __forceinline__ void gbar(int grp) {
+  asm volatile("bar.sync %0, %1;" ::"r"(2 + grp), "n"(NT) : "memory");
 }
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -205,7 +214,7 @@ __device__ __forceinline__ uint32_t pl_off(int P, int p, int t) {
   return pl_addr<ZSZ>(0u, P, p, t);
 }
 
-// Work split of a kT-tile unit over the C = kCWarps consumer warps:
+// Work split of a kT-tile unit over the C = kGWarps warps of the consumer group that owns it:
 //   ENC n-tiles (8 tiles):  warp w -> n-tiles w + C k, k < kT / (8 C)
 //   DEC m-tiles (16 tiles): warp w -> m-tiles w + C k, k < kT / (16 C)
 //   RED k-steps (16 tiles): warp w -> k-steps w + C k, k < kT / (16 C)
@@ -230,7 +239,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
   const uint32_t s_out = s_stages + L.nstages * L.stage_bytes;
   float* s_red = reinterpret_cast<float*>(smem);  // after the unit loop only
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.nstages * L.stage_bytes +
-                                               2 * L.out_bytes + L.red_bytes);
+                                               2 * groups_of<MODE>() * L.out_bytes + L.red_bytes);
+  constexpr int kGroups = groups_of<MODE>();
+  constexpr int kGWarps = kCWarps / kGroups;  // warps per group
+  constexpr int kGThreads = 32 * kGWarps;
   uint64_t* empty = full + kMaxStages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -245,7 +257,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < L.nstages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], kCWarps);
+      ptx::mbar_init(&empty[s], kGWarps);
     }
     ptx::fence_mbar_init();
   }
@@ -293,8 +305,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
   // ------------------------------------------------------------------ consumers
   const int ctid = threadIdx.x;
   const uint32_t RS = L.row_stride;
-  constexpr int kNK = kT / (8 * kCWarps);    // ENC n-tile rounds per warp
-  constexpr int kMK = kT / (16 * kCWarps);   // DEC m-tile / RED k-step rounds per warp
+  constexpr int kNK = kT / (8 * kGWarps);    // ENC n-tile rounds per warp
+  constexpr int kMK = kT / (16 * kGWarps);   // DEC m-tile / RED k-step rounds per warp
+  const int grp = warp / kGWarps, wl = warp % kGWarps;  // group, warp within the group
+  const int gtid = wl * 32 + lane;
   static_assert(kNK >= 1 && kMK >= 1, "unit too small for the warp count");
   // Coefficient fragments, split hi + lo.
   //  ENC (A = E, M = p, K = c): a0 = E[16m+g][2q, 2q+1], a1 = E[16m+g+8][..], a2/a3: c + 8.
@@ -324,10 +338,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
   }
   // Per-thread shared-memory offsets (see the work split above).
   // ENC: B loads at rows + xoff + 512k (+2 RS); C stores at buf + soff[k] + (16m + 8h) * 128.
-  const uint32_t xoff = (q >> 1) * RS + 64 * warp + 8 * g + 4 * (q & 1);
+  const uint32_t xoff = (q >> 1) * RS + 64 * wl + 8 * g + 4 * (q & 1);
   uint32_t soff[kNK];
 #pragma unroll
-  for (int k = 0; k < kNK; ++k) soff[k] = is_enc<MODE>() ? pl_off<2>(P, g, 8 * (warp + kCWarps * k) + 2 * q) : 0u;
+  for (int k = 0; k < kNK; ++k) soff[k] = is_enc<MODE>() ? pl_off<2>(P, g, 8 * (wl + kGWarps * k) + 2 * q) : 0u;
   // Stores/loads of planes >= P exist only in the last 16-plane group.
   const bool lastp0 = 16 * (MT - 1) + g < P, lastp1 = 16 * (MT - 1) + g + 8 < P;
   const bool okb1 = 16 * (MT - 1) + g + 8 < Pb;  // row inside the (8-padded) input box
@@ -336,11 +350,11 @@ __global__ void __launch_bounds__(kSThreads, 1)
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const int c = 8 * nt + g;
-    rb[nt] = (c >> 2) * RS + 128 * warp + 16 * q + 2 * (c & 3);
+    rb[nt] = (c >> 2) * RS + 128 * wl + 16 * q + 2 * (c & 3);
   }
 #pragma unroll
   for (int k = 0; k < kMK; ++k) {
-    const int t = 16 * (warp + kCWarps * k) + 2 * q;
+    const int t = 16 * (wl + kGWarps * k) + 2 * q;
     ra0[k] = has_red<MODE>() ? pl_off<ZSZ>(Pb, g, t) : 0u;
     ra2[k] = has_red<MODE>() ? pl_off<ZSZ>(Pb, g, t + 8) : 0u;
     ra0l[k] = kZ24 ? L.pl_lo + pl_off<1>(Pb, g, t) : 0u;   // F24 low bytes: same rule, W = 128
@@ -353,10 +367,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
   for (int k = 0; k < kMK; ++k)
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      da[k][j] = is_enc<MODE>() ? 0u : pl_off<ZSZ>(Pb, 2 * q + j, 16 * (warp + kCWarps * k) + 2 * g);
-      dal[k][j] = kZ24 ? L.pl_lo + pl_off<1>(Pb, 2 * q + j, 16 * (warp + kCWarps * k) + 2 * g) : 0u;
+      da[k][j] = is_enc<MODE>() ? 0u : pl_off<ZSZ>(Pb, 2 * q + j, 16 * (wl + kGWarps * k) + 2 * g);
+      dal[k][j] = kZ24 ? L.pl_lo + pl_off<1>(Pb, 2 * q + j, 16 * (wl + kGWarps * k) + 2 * g) : 0u;
     }
-  const uint32_t ooff = (q >> 1) * RS + 128 * warp + 16 * g + 4 * (q & 1);
+  const uint32_t ooff = (q >> 1) * RS + 128 * wl + 16 * g + 4 * (q & 1);
   bool dok[4];  // last plane group: planes 16(MT-1) + 2q + {0, 1, 8, 9} < P
 #pragma unroll
   for (int j = 0; j < 4; ++j) dok[j] = 16 * (MT - 1) + 2 * q + (j & 1) + 8 * (j >> 1) < P;
@@ -385,14 +399,15 @@ __global__ void __launch_bounds__(kSThreads, 1)
 #pragma unroll
       for (int k = 0; k < 4; ++k) R[a][b][k] = 0.f;
 
-  uint32_t it = 0;
-  for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+  // group grp takes this CTA's units it = grp, grp + 2, ... (stage it % nstages)
+  for (uint32_t u = blockIdx.x + grp * gridDim.x, it = grp; u < nunits;
+       u += kGroups * gridDim.x, it += kGroups) {
     const uint32_t stage = it % L.nstages;
     const uint32_t phase = (it / L.nstages) & 1;
     const uint32_t I = u / upr;
     const uint32_t J0 = (u - I * upr) * kT;
     const int Tw = static_cast<int>(min(bc - J0, static_cast<uint32_t>(kT)));
-    const uint32_t buf = s_out + (it & 1) * L.out_bytes;
+    const uint32_t buf = s_out + (grp * 2 + ((it / kGroups) & 1)) * L.out_bytes;
     const uint32_t planes = s_stages + stage * L.stage_bytes;
     const uint32_t rows = planes + L.pl_bytes;
     const uint64_t t_w0 = args.dbg ? ptx::globaltimer_ns() : 0;
@@ -408,8 +423,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
       const int nnt = Tw == kT ? kT / 8 : (Tw >> 3);  // full units: compile-time bounds
 #pragma unroll
       for (int k = 0; k < kNK; ++k) {
-        if (warp + kCWarps * k < nnt) {
-          const uint32_t xb = rows + xoff + 64 * kCWarps * k;
+        if (wl + kGWarps * k < nnt) {
+          const uint32_t xb = rows + xoff + 64 * kGWarps * k;
           const uint32_t b0 = lds32(xb), b1 = lds32(xb + 2 * RS);
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
@@ -429,7 +444,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
       const int nmt = Tw == kT ? kT / 16 : (Tw >> 4);
 #pragma unroll
       for (int k = 0; k < kMK; ++k) {
-        if (warp + kCWarps * k < nmt) {
+        if (wl + kGWarps * k < nmt) {
           float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
           if constexpr (kTf32) {
             // m16n8k8 tf32 per 8 planes: rows g / g+8 = tiles t0 / t0+1, k = q / q+4 = planes
@@ -504,7 +519,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
           // acc[nt][0,1] -> tile t0, c = 8nt + 2q (+1): row a = 2nt + (q>>1), col b = 2(q&1).
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
-            const uint32_t o = buf + ooff + 128 * kCWarps * k + 2 * nt * RS;
+            const uint32_t o = buf + ooff + 128 * kGWarps * k + 2 * nt * RS;
             sts32(o, pack2(acc[nt][0], acc[nt][1]));
             sts32(o + 8, pack2(acc[nt][2], acc[nt][3]));
           }
@@ -518,11 +533,11 @@ __global__ void __launch_bounds__(kSThreads, 1)
       const int nks = Tw == kT ? kT / 16 : (Tw >> 4);
 #pragma unroll
       for (int k = 0; k < kMK; ++k) {
-        if (warp + kCWarps * k < nks) {
+        if (wl + kGWarps * k < nks) {
           uint32_t b[2][2], bx[2][2][2];
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
-            const uint32_t base = rows + rb[nt] + 128 * kCWarps * k;
+            const uint32_t base = rows + rb[nt] + 128 * kGWarps * k;
             const uint32_t x0 = lds16(base), x1 = lds16(base + 8), x8 = lds16(base + 64),
                            x9 = lds16(base + 72);
             b[nt][0] = pair16(x0, x1);
@@ -607,12 +622,12 @@ __global__ void __launch_bounds__(kSThreads, 1)
     if (lane == 0) ptx::mbar_arrive(&empty[stage]);
     if (args.stg) {
       // Consumers copy the staged unit to global memory with 16-byte stores (coalesced rows).
-      cbar();
+      gbar<kGThreads>(grp);
       if constexpr (is_enc<MODE>()) {
         __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(I) * bc + J0;
         const int64_t ntiles = args.br * args.bc;
         const int pieces = P * (Tw >> 3);  // 16-byte pieces: (p, chunk k, c16)
-        for (int i = ctid; i < pieces; i += kCThreads) {
+        for (int i = gtid; i < pieces; i += kGThreads) {
           const int p = i / (Tw >> 3), rest = i - p * (Tw >> 3), k = rest >> 3, c16 = rest & 7;
           const uint32_t row = static_cast<uint32_t>(k * P + p);
           const uint4 v = *reinterpret_cast<const uint4*>(smem + buf + row * 128 + ((c16 ^ (row & 7)) << 4));
@@ -621,7 +636,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
       } else {
         __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(args.out) + (4 * static_cast<int64_t>(I)) * args.ldo + 4 * J0;
         const int per_row = Tw >> 1;  // 16-byte pieces per output row
-        for (int i = ctid; i < 4 * per_row; i += kCThreads) {
+        for (int i = gtid; i < 4 * per_row; i += kGThreads) {
           const int a = i / per_row, c = i - a * per_row;
           const uint4 v = *reinterpret_cast<const uint4*>(smem + buf + a * L.out_stride + 16 * c);
           *reinterpret_cast<uint4*>(ob + a * args.ldo + 8 * c) = v;
@@ -632,11 +647,11 @@ __global__ void __launch_bounds__(kSThreads, 1)
     ptx::fence_proxy_async_smem();
     // The stores of the previous unit (other buffer) must have finished reading it before the
     // barrier: the next unit writes that buffer. One barrier per unit.
-    if (warp == 0) ptx::bulk_wait_read<0>();
-    cbar();
-    // warp 0 issues the unit's stores: the plane box (one 4-D TMA op, clipped at the matrix
-    // edge) or the 4 output rows (1-D bulk copies).
-    if (warp == 0) {
+    if (wl == 0) ptx::bulk_wait_read<0>();
+    gbar<kGThreads>(grp);
+    // the group's warp 0 issues the unit's stores: the plane box (one 4-D TMA op, clipped at
+    // the matrix edge) or the 4 output rows (1-D bulk copies).
+    if (wl == 0) {
       if constexpr (is_enc<MODE>()) {
         if (lane == 0) tma_store_4d(&tm_out, sbase + buf, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
       } else {
@@ -647,7 +662,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
       ptx::bulk_commit();
     }
   }
-  if (warp == 0) ptx::bulk_wait_all();
+  if (wl == 0) ptx::bulk_wait_all();
 
   if constexpr (has_red<MODE>()) {
     // per-warp fragments -> smem (the stage ring, once every warp is done with it) ->
@@ -776,7 +791,8 @@ cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, floa
   const int pb = ((a.P + 7) / 8) * 8;
   const Layout L512 = make_layout<MODE, ZT, 512>(a.P, pb);
   const bool use512 = force_t ? force_t == 512
-                              : (L512.nstages >= 2 && L512.total <= 227 * 1024 && a.bc >= 512);
+                              : (L512.nstages >= 2 * groups_of<MODE>() && L512.total <= 227 * 1024 &&
+                                 a.bc >= 512);
   if (use512) return launch_mt<MODE, ZT, MT, 512>(a, planes_in, planes_out, red_out, s);
   return launch_mt<MODE, ZT, MT, 256>(a, planes_in, planes_out, red_out, s);
 }
