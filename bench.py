@@ -294,7 +294,8 @@ def main() -> None:
         k["ms"] += ms
         k["calls"] += 1
         launches += n
-    cost = stl.LayerCost(M, K, N, T, R, 2)
+    p_bytes = 3 if int(lib.stl_cache_bytes(M, K, N, T, R, _lib.STL_BF16)) == 3 * R * bi * bj else 4
+    cost = stl.LayerCost(M, K, N, T, R, 2, p_bytes)
     gem = kern.get("slice_gemm_tcgen05", {"ms": float("nan"), "calls": 1})
     gemm_ms = gem["ms"] / max(gem["calls"], 1)
     gemm_tflops = cost.gemm_flops() / (gemm_ms * 1e-3) / 1e12
@@ -310,8 +311,8 @@ def main() -> None:
     breakdown = {}
     step_kernel_ms = sum(v["ms"] for v in kern.values()) / args.steps
     hbm_bytes = {"encode_x": cost.encode_bytes(), "decode_y": cost.decode_bytes(),
-                 "encode_gy+g_d": M * N * 2 + R * bi * bj * 2 + R * bi * bj * 4,
-                 "decode_gu+g_ex": R * bi * bk * 4 + M * K * 2 + M * K * 2}
+                 "encode_gy+g_d": cost.encode_gy_gd_bytes(),
+                 "decode_gu+g_ex": cost.decode_gu_gex_bytes()}
     for name, v in kern.items():
         per = v["ms"] / args.steps
         entry = {"ms_per_step": per, "share": per / step_kernel_ms if step_kernel_ms else None,

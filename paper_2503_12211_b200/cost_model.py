@@ -50,6 +50,7 @@ class LayerCost:
     t: int
     r: int
     s: int = 2  # bytes per scalar of the compute dtype
+    p: int = 4  # bytes per stored slice product (4 = fp32, 3 = F24 on the bf16 path)
 
     @property
     def bi(self):
@@ -87,10 +88,18 @@ class LayerCost:
 
     def gemm_fwd_bytes(self) -> int:
         return (self.r * self.bi * self.bk * self.s + self.r * self.bj * self.bk * self.s
-                + self.r * self.bi * self.bj * 4)
+                + self.r * self.bi * self.bj * self.p)
 
     def decode_bytes(self) -> int:
-        return self.r * self.bi * self.bj * 4 + self.M * self.N * self.s
+        return self.r * self.bi * self.bj * self.p + self.M * self.N * self.s
+
+    def encode_gy_gd_bytes(self) -> int:
+        """gY in, y_enc cache in, g_enc planes out (the g_d reduction rides along)."""
+        return self.M * self.N * self.s + self.r * self.bi * self.bj * (self.p + self.s)
+
+    def decode_gu_gex_bytes(self) -> int:
+        """g_u products in, X in (for g_ex), g_x out."""
+        return self.r * self.bi * self.bk * self.p + 2 * self.M * self.K * self.s
 
     def forward_min_bytes(self) -> int:
         """|X| + |W_enc| + |Y|: the fused lower bound."""
