@@ -31,12 +31,13 @@ namespace {
 
 enum Mode { kEnc = 0, kEncRed = 1, kDec = 2, kDecRed = 3 };
 
-constexpr int kCWarps = 16;                 // consumer warps
-constexpr int kCThreads = 32 * kCWarps;
+// CW = consumer warps per CTA (template; 16). A measured negative result: an 8-warp, 56 KB
+// "lite" configuration meant to share each SM with a slice-GEMM CTA (overlapping the g_x/g_ex
+// decode with the g_w GEMM on two streams) ran 137 us alone and the pair 215 us vs 165 us
+// sequential, so the backward stays sequential.
 // Consumer groups taking alternate units: two 8-warp groups for the plain transforms (their
 // per-unit math is short, so two units in flight hide its latency), one 16-warp group for the
 // fused reductions (more math per unit: splitting it 16 ways wins).
-constexpr int kSThreads = kCThreads + 32;   // + producer warp
 constexpr int kMaxStages = 16;
 constexpr uint32_t kRowPad = 64;            // matrix rows: 16-word bank shift per row
 
@@ -44,7 +45,7 @@ template <int MODE> constexpr bool has_rows() { return MODE != kDec; }
 template <int MODE> constexpr bool has_planes_in() { return MODE != kEnc; }
 template <int MODE> constexpr bool is_enc() { return MODE == kEnc || MODE == kEncRed; }
 template <int MODE> constexpr bool has_red() { return MODE == kEncRed || MODE == kDecRed; }
-template <int MODE> constexpr int groups_of() { return has_red<MODE>() ? 1 : 2; }
+template <int MODE, int CW> constexpr int groups_of() { return has_red<MODE>() || CW < 16 ? 1 : 2; }
 
 // Plane element types: float, __nv_bfloat16, or F24 (kF24 of stl_internal.h: a 16-bit high
 // plane set + an 8-bit low plane set, moved as two boxes).
@@ -70,8 +71,8 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-template <int MODE, typename ZT, int kT>
-inline Layout make_layout(int P, int Pb) {
+template <int MODE, typename ZT, int kT, int CW>
+inline Layout make_layout(int P, int Pb, uint32_t budget) {
   // Pb >= P: planes of the input box (the TMA zero-fills planes P..Pb-1, so the consumers'
   // plane loops need no bounds checks)
   Layout L{};
@@ -88,9 +89,8 @@ inline Layout make_layout(int P, int Pb) {
     L.out_bytes = rup(4 * L.out_stride, 1024);
   }
   L.red_bytes = 0;  // the final per-warp reduction partials reuse the (drained) stage ring
-  static const uint32_t budget = env_int("STL_STREAM_SMEM_KB", 212) * 1024;
   static const uint32_t max_st = env_int("STL_STREAM_STAGES", 8);
-  const uint32_t fixed = 2 * groups_of<MODE>() * L.out_bytes + L.red_bytes;
+  const uint32_t fixed = 2 * groups_of<MODE, CW>() * L.out_bytes + L.red_bytes;
   uint32_t ns = (budget - fixed) / L.stage_bytes;
   if (ns > max_st) ns = max_st;
   L.nstages = ns > kMaxStages ? kMaxStages : (ns < 2 ? 2 : ns);
@@ -147,8 +147,9 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, uint32_t src,
       "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+template <int NT>
 __device__ __forceinline__ void cbar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kCThreads) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 // barrier of one consumer group of NT threads (ids 2, 3)
 template <int NT>
@@ -221,8 +222,8 @@ __device__ __forceinline__ uint32_t pl_off(int P, int p, int t) {
 
 // ------------------------------------------------------------------ the kernel
 // MT = number of 16-plane groups (ceil(P / 16)), a template so every plane loop unrolls.
-template <int MODE, typename ZT, int MT, int kT>
-__global__ void __launch_bounds__(kSThreads, 1)
+template <int MODE, typename ZT, int MT, int kT, int CW>
+__global__ void __launch_bounds__(32 * CW + 32, 1)
     k_stream(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_in2,
              const __grid_constant__ CUtensorMap tm_out,
              StreamArgs args, Layout L) {
@@ -239,8 +240,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
   const uint32_t s_out = s_stages + L.nstages * L.stage_bytes;
   float* s_red = reinterpret_cast<float*>(smem);  // after the unit loop only
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.nstages * L.stage_bytes +
-                                               2 * groups_of<MODE>() * L.out_bytes + L.red_bytes);
-  constexpr int kGroups = groups_of<MODE>();
+                                               2 * groups_of<MODE, CW>() * L.out_bytes + L.red_bytes);
+  constexpr int kCWarps = CW;
+  constexpr int kCThreads = 32 * CW;
+  constexpr int kGroups = groups_of<MODE, CW>();
   constexpr int kGWarps = kCWarps / kGroups;  // warps per group
   constexpr int kGThreads = 32 * kGWarps;
   uint64_t* empty = full + kMaxStages;
@@ -667,7 +670,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
   if constexpr (has_red<MODE>()) {
     // per-warp fragments -> smem (the stage ring, once every warp is done with it) ->
     // fixed-order sum over warps -> this CTA's partial
-    cbar();
+    cbar<kCThreads>();
     float* mine = s_red + warp * P * 16;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
@@ -683,7 +686,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
           mine[p1 * 16 + c + 1] = R[mt][nt][3];
         }
       }
-    cbar();
+    cbar<kCThreads>();
     const int n = P * 16;
     for (int o = ctid; o < n; o += kCThreads) {
       float s = s_red[o];
@@ -732,11 +735,11 @@ bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_
   return r == CUDA_SUCCESS;
 }
 
-template <int MODE, typename ZT, int MT, int kT>
+template <int MODE, typename ZT, int MT, int kT, int CW>
 cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
-                      cudaStream_t s) {
+                      cudaStream_t s, uint32_t budget) {
   a.Pb = ((a.P + 7) / 8) * 8;
-  const Layout L = make_layout<MODE, ZT, kT>(a.P, a.Pb);
+  const Layout L = make_layout<MODE, ZT, kT, CW>(a.P, a.Pb, budget);
   CUtensorMap tin{}, tin2{}, tout{};
   if (has_planes_in<MODE>() && !plane_tmap(&tin, planes_in, zhi<ZT>(), a.P, a.Pb, a.br, a.bc, kT))
     return cudaErrorNotSupported;
@@ -746,7 +749,7 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
     return cudaErrorNotSupported;
   if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.P, a.br, a.bc, kT))
     return cudaErrorNotSupported;
-  auto k = k_stream<MODE, ZT, MT, kT>;
+  auto k = k_stream<MODE, ZT, MT, kT, CW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(L.total));
   if (e != cudaSuccess) return e;
@@ -766,7 +769,7 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   if (grid < 1) return cudaSuccess;
   const uint64_t t0 = 0;
   (void)t0;
-  k<<<static_cast<int>(grid), kSThreads, L.total, s>>>(tin, tin2, tout, a, L);
+  k<<<static_cast<int>(grid), 32 * CW + 32, L.total, s>>>(tin, tin2, tout, a, L);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (a.dbg) {
@@ -788,13 +791,14 @@ template <int MODE, typename ZT, int MT>
 cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                      cudaStream_t s) {
   static const int force_t = env_int("STL_STREAM_T", 0);
+  static const uint32_t budget = env_int("STL_STREAM_SMEM_KB", 212) * 1024;
   const int pb = ((a.P + 7) / 8) * 8;
-  const Layout L512 = make_layout<MODE, ZT, 512>(a.P, pb);
+  const Layout L512 = make_layout<MODE, ZT, 512, 16>(a.P, pb, budget);
   const bool use512 = force_t ? force_t == 512
-                              : (L512.nstages >= 2 * groups_of<MODE>() && L512.total <= 227 * 1024 &&
+                              : (L512.nstages >= 2 * groups_of<MODE, 16>() && L512.total <= 227 * 1024 &&
                                  a.bc >= 512);
-  if (use512) return launch_mt<MODE, ZT, MT, 512>(a, planes_in, planes_out, red_out, s);
-  return launch_mt<MODE, ZT, MT, 256>(a, planes_in, planes_out, red_out, s);
+  if (use512) return launch_mt<MODE, ZT, MT, 512, 16>(a, planes_in, planes_out, red_out, s, budget);
+  return launch_mt<MODE, ZT, MT, 256, 16>(a, planes_in, planes_out, red_out, s, budget);
 }
 
 template <int MODE, typename ZT>
