@@ -7,6 +7,34 @@
 
 namespace stl {
 
+// Programmatic dependent launch: the hot-path kernels (streaming transforms, CTA-pair GEMM,
+// partial sums) are launched with cudaLaunchAttributeProgrammaticStreamSerialization and call
+// griddep_wait() before touching global memory, so each one's CTAs can be scheduled and run
+// their prologue (barrier init, TMEM alloc, descriptor prefetch) while the previous kernel
+// drains. STL_PDL=0 disables the attribute.
+bool pdl_enabled();
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // kF24: an fp32 quantity rounded to 24 bits (RNE) and stored as two plane sets — the high
 // 16 bits of every element (2 bytes each) followed by the next 8 bits (1 byte each) — so a
 // tensor of n elements occupies 3n bytes; value = as_float(hi << 16 | lo << 8), ~2^-16 relative.

@@ -338,10 +338,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, kTmemCols);
+  griddep_launch_dependents();
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // operands of this launch are complete (PDL)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -604,8 +606,7 @@ cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
   static const int nostore = getenv("STL_GEMM_NOSTORE") ? atoi(getenv("STL_GEMM_NOSTORE")) : 0;
   EpiArgs ea{pb.c, 0, nostore, 0, pb.r, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
              static_cast<__nv_bfloat16*>(pb.c2)};
-  kern<<<grid, kThreads, smem, s>>>(ta, tb, tc, tc2, ea);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, ta, tb, tc, tc2, ea);
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -628,6 +629,14 @@ bool make_bf16_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("STL_PDL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
 }
 
 int sm_count() {

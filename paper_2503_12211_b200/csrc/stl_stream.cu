@@ -264,12 +264,14 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     }
     ptx::fence_mbar_init();
   }
+  griddep_launch_dependents();
   if (warp == kCWarps && lane == 0) {
     if constexpr (has_planes_in<MODE>()) ptx::prefetch_tmap(&tm_in);
     if constexpr (kZ24) ptx::prefetch_tmap(&tm_in2);
     if constexpr (is_enc<MODE>()) ptx::prefetch_tmap(&tm_out);
   }
   __syncthreads();
+  griddep_wait();  // inputs of this launch are complete (PDL)
 
   if (warp == kCWarps) {
     // ---------------------------------------------------------------- producer
@@ -769,8 +771,8 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   if (grid < 1) return cudaSuccess;
   const uint64_t t0 = 0;
   (void)t0;
-  k<<<static_cast<int>(grid), 32 * CW + 32, L.total, s>>>(tin, tin2, tout, a, L);
-  e = cudaGetLastError();
+  e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(32 * CW + 32), L.total, s, tin, tin2,
+                 tout, a, L);
   if (e != cudaSuccess) return e;
   if (a.dbg) {
     unsigned long long h[4 * 1024];

@@ -451,6 +451,8 @@ __global__ void __launch_bounds__(256) k_sum_partials_tree(const float* __restri
                                                            int nblocks, int n,
                                                            float* __restrict__ out) {
   __shared__ float s[256];
+  griddep_launch_dependents();
+  griddep_wait();  // the partials of the preceding launch are complete (PDL)
   const int o = blockIdx.x;
   float v = 0.f;
   for (int b = threadIdx.x; b < nblocks; b += 256) v += partial[static_cast<int64_t>(b) * n + o];
@@ -538,8 +540,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 }  // namespace
 
 cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t s) {
-  k_sum_partials_tree<<<n, 256, 0, s>>>(partial, nblocks, n, out);
-  return cudaGetLastError();
+  return launch_pdl(k_sum_partials_tree, dim3(n), dim3(256), 0, s, partial, nblocks, n, out);
 }
 
 // Fast-path dispatch; returns cudaErrorNotSupported when the generic kernels must be used.
