@@ -419,203 +419,213 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     ptx::mbar_wait(&full[stage], phase);
     const uint64_t t_w1 = args.dbg ? ptx::globaltimer_ns() : 0;
 
-    if (args.nocompute) {
-    } else if constexpr (is_enc<MODE>()) {
-      // C^T[p][tile] = E . X^T per 8-tile n-tile. B: b0 = X[tile][c 2q, 2q+1] (row q>>1),
-      // b1 = row 2 + (q>>1). Banks: 16 (q>>1) + 2g + (q&1) -> conflict-free. C: plane 16m+g
-      // (c0, c1) / 16m+g+8 (c2, c3), tiles 8nt+2q, +1, into the swizzled plane box: the 8 planes
-      // g land in 8 different 16-byte chunks -> conflict-free.
-      const int nnt = Tw == kT ? kT / 8 : (Tw >> 3);  // full units: compile-time bounds
-#pragma unroll
-      for (int k = 0; k < kNK; ++k) {
-        if (wl + kGWarps * k < nnt) {
-          const uint32_t xb = rows + xoff + 64 * kGWarps * k;
-          const uint32_t b0 = lds32(xb), b1 = lds32(xb + 2 * RS);
-#pragma unroll
-          for (int m = 0; m < MT; ++m) {
-            float c[4] = {0.f, 0.f, 0.f, 0.f};
-            mma(c, fh[m][0], fh[m][1], fh[m][2], fh[m][3], b0, b1);
-            mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0, b1);
-            const uint32_t o = buf + soff[k] + 16 * m * 128;
-            if (m < MT - 1 || lastp0) sts32(o, pack2(c[0], c[1]));
-            if (m < MT - 1 || lastp1) sts32(o + 8 * 128, pack2(c[2], c[3]));
+    // The unit's math. Full units (Tw == kT) take a copy with compile-time bounds so the
+    // compiler can interleave the warp's independent m-tiles / k-steps.
+    auto unit_math = [&](auto full_tag) {
+      constexpr bool kFull = decltype(full_tag)::value;
+      if constexpr (is_enc<MODE>()) {
+        // C^T[p][tile] = E . X^T per 8-tile n-tile. B: b0 = X[tile][c 2q, 2q+1] (row q>>1),
+        // b1 = row 2 + (q>>1). Banks: 16 (q>>1) + 2g + (q&1) -> conflict-free. C: plane 16m+g
+        // (c0, c1) / 16m+g+8 (c2, c3), tiles 8nt+2q, +1, into the swizzled plane box: the 8 planes
+        // g land in 8 different 16-byte chunks -> conflict-free.
+        const int nnt = kFull ? kT / 8 : (Tw >> 3);
+  #pragma unroll
+        for (int k = 0; k < kNK; ++k) {
+          if (kFull || wl + kGWarps * k < nnt) {
+            const uint32_t xb = rows + xoff + 64 * kGWarps * k;
+            const uint32_t b0 = lds32(xb), b1 = lds32(xb + 2 * RS);
+  #pragma unroll
+            for (int m = 0; m < MT; ++m) {
+              float c[4] = {0.f, 0.f, 0.f, 0.f};
+              mma(c, fh[m][0], fh[m][1], fh[m][2], fh[m][3], b0, b1);
+              mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0, b1);
+              const uint32_t o = buf + soff[k] + 16 * m * 128;
+              if (m < MT - 1 || lastp0) sts32(o, pack2(c[0], c[1]));
+              if (m < MT - 1 || lastp1) sts32(o + 8 * 128, pack2(c[2], c[3]));
+            }
           }
         }
-      }
-    } else {
-      // C[tile][c] = Z^T . D per 16-tile m-tile; rows g / g+8 <-> tiles 2g / 2g+1 so each
-      // plane load is one 8-byte (fp32) or 4-byte (bf16) access; with the swizzle XOR a
-      // half-warp's loads hit 32 distinct banks.
-      const int nmt = Tw == kT ? kT / 16 : (Tw >> 4);
-#pragma unroll
-      for (int k = 0; k < kMK; ++k) {
-        if (wl + kGWarps * k < nmt) {
-          float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-          if constexpr (kTf32) {
-            // m16n8k8 tf32 per 8 planes: rows g / g+8 = tiles t0 / t0+1, k = q / q+4 = planes
-            // 8s+2q / 8s+2q+1: a0 a1 = Z[8s+2q][t0, t0+1] (one 8-byte or F24 load), a2 a3 =
-            // Z[8s+2q+1][t0, t0+1].
-#pragma unroll
-            for (int s8 = 0; s8 < KS8; ++s8) {
-              if (8 * s8 >= Pb) break;  // warp-uniform; planes P..Pb-1 are zero in the box
-              float2 v[2];
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const uint32_t ad = planes + da[k][h] + 8 * s8 * 128;
-                if constexpr (kZ24) v[h] = f24x2(lds32(ad), lds16(planes + dal[k][h] + 8 * s8 * 128));
-                else v[h] = lds64f(ad);
-              }
-              const uint32_t a0 = tf32_rna(v[0].x), a1 = tf32_rna(v[0].y);
-              const uint32_t a2 = tf32_rna(v[1].x), a3 = tf32_rna(v[1].y);
-#pragma unroll
-              for (int nt = 0; nt < 2; ++nt) mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
-            }
-          } else {
-#pragma unroll
-          for (int ks = 0; ks < MT; ++ks) {
-            float v[4][2];  // planes 16ks + 2q + {0, 1, 8, 9} at tiles t0, t0 + 1
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t ad = planes + da[k][j & 1] + (16 * ks + 8 * (j >> 1)) * 128;
-              if (ks < MT - 1 || dok[j]) {
-                if constexpr (kZ24) {
-                  const float2 f = f24x2(lds32(ad), lds16(planes + dal[k][j & 1] + (16 * ks + 8 * (j >> 1)) * 128));
-                  v[j][0] = f.x;
-                  v[j][1] = f.y;
-                } else if constexpr (ZSZ == 4) {
-                  const float2 f = lds64f(ad);
-                  v[j][0] = f.x;
-                  v[j][1] = f.y;
-                } else {
-                  const uint32_t w = lds32(ad);
-                  const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
-                  v[j][0] = f.x;
-                  v[j][1] = f.y;
-                }
-              } else {
-                v[j][0] = v[j][1] = 0.f;
-              }
-            }
-            // a0 = (row g = tile t0: planes 2q, 2q+1), a1 = row g+8 = tile t0+1, a2/a3: +8
-            if constexpr (ZSZ == 4 || kZ24) {
-              uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
-              split2(v[0][0], v[1][0], h0, l0);
-              split2(v[0][1], v[1][1], h1, l1);
-              split2(v[2][0], v[3][0], h2, l2);
-              split2(v[2][1], v[3][1], h3, l3);
-#pragma unroll
-              for (int nt = 0; nt < 2; ++nt) {
-                const uint32_t bh0 = fh[ks][2 * nt], bh1 = fh[ks][2 * nt + 1];
-                mma(acc[nt], h0, h1, h2, h3, bh0, bh1);
-                mma(acc[nt], l0, l1, l2, l3, bh0, bh1);
-                mma(acc[nt], h0, h1, h2, h3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
-              }
-            } else {
-              const uint32_t a0 = pack2(v[0][0], v[1][0]), a1 = pack2(v[0][1], v[1][1]);
-              const uint32_t a2 = pack2(v[2][0], v[3][0]), a3 = pack2(v[2][1], v[3][1]);
-#pragma unroll
-              for (int nt = 0; nt < 2; ++nt) {
-                mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
-                mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
-              }
-            }
-          }
-          }  // bf16 planes
-          // acc[nt][0,1] -> tile t0, c = 8nt + 2q (+1): row a = 2nt + (q>>1), col b = 2(q&1).
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            const uint32_t o = buf + ooff + 128 * kGWarps * k + 2 * nt * RS;
-            sts32(o, pack2(acc[nt][0], acc[nt][1]));
-            sts32(o + 8, pack2(acc[nt][2], acc[nt][3]));
-          }
-        }
-      }
-    }
-    if (has_red<MODE>() && !args.nocompute) {
-      // R[p][c] += sum over 16-tile k-steps of Z[p][tile] X[tile][c] (A = Z: M = p; B = X: N = c).
-      // B: b0 = (X[t0+2q][c], X[t0+2q+1][c]), b1 = tiles + 8, c = 8nt + g, 16-bit loads
-      // (words 16 (c>>2) + 4q + ((c&3)>>1): distinct). A: Z[p][t0+2q, +1] / [t0+2q+8, +9].
-      const int nks = Tw == kT ? kT / 16 : (Tw >> 4);
-#pragma unroll
-      for (int k = 0; k < kMK; ++k) {
-        if (wl + kGWarps * k < nks) {
-          uint32_t b[2][2], bx[2][2][2];
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            const uint32_t base = rows + rb[nt] + 128 * kGWarps * k;
-            const uint32_t x0 = lds16(base), x1 = lds16(base + 8), x8 = lds16(base + 64),
-                           x9 = lds16(base + 72);
-            b[nt][0] = pair16(x0, x1);
-            b[nt][1] = pair16(x8, x9);
-            bx[nt][0][0] = x0 << 16;
-            bx[nt][0][1] = x1 << 16;
-            bx[nt][1][0] = x8 << 16;
-            bx[nt][1][1] = x9 << 16;
-          }
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const bool ok0 = mt < MT - 1 || lastp0, ok1 = mt < MT - 1 || lastp1;
-            const uint32_t z0 = planes + ra0[k] + 16 * mt * 128, z2 = planes + ra2[k] + 16 * mt * 128;
+      } else {
+        // C[tile][c] = Z^T . D per 16-tile m-tile; rows g / g+8 <-> tiles 2g / 2g+1 so each
+        // plane load is one 8-byte (fp32) or 4-byte (bf16) access; with the swizzle XOR a
+        // half-warp's loads hit 32 distinct banks.
+        const int nmt = kFull ? kT / 16 : (Tw >> 4);
+  #pragma unroll
+        for (int k = 0; k < kMK; ++k) {
+          if (kFull || wl + kGWarps * k < nmt) {
+            float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
             if constexpr (kTf32) {
-              // two m16n8k8 tf32 steps (tiles t0..t0+7, t0+8..t0+15): rows g / g+8 = planes,
-              // k = q / q+4 = tiles 2q / 2q+1 of the step; B = X as fp32 (bf16 << 16, exact).
-#pragma unroll
-              for (int hh = 0; hh < 2; ++hh) {
-                const uint32_t za = hh ? z2 : z0;
-                // planes 16mt+g (< Pb) and 16mt+g+8 (may pass Pb in the last group: load a
-                // valid row, select zero)
-                const bool in1 = mt < MT - 1 || okb1;
-                const uint32_t d1 = in1 ? 1024u : 0u;
-                float2 v0, v1;
-                if constexpr (kZ24) {
-                  const uint32_t la = planes + (hh ? ra2l[k] : ra0l[k]) + 16 * mt * 128;
-                  v0 = f24x2(lds32(za), lds16(la));
-                  v1 = f24x2(lds32(za + d1), lds16(la + d1));
-                } else {
-                  v0 = lds64f(za);
-                  v1 = lds64f(za + d1);
+              // m16n8k8 tf32 per 8 planes: rows g / g+8 = tiles t0 / t0+1, k = q / q+4 = planes
+              // 8s+2q / 8s+2q+1: a0 a1 = Z[8s+2q][t0, t0+1] (one 8-byte or F24 load), a2 a3 =
+              // Z[8s+2q+1][t0, t0+1].
+  #pragma unroll
+              for (int s8 = 0; s8 < KS8; ++s8) {
+                if (8 * s8 >= Pb) break;  // warp-uniform; planes P..Pb-1 are zero in the box
+                float2 v[2];
+  #pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const uint32_t ad = planes + da[k][h] + 8 * s8 * 128;
+                  if constexpr (kZ24) v[h] = f24x2(lds32(ad), lds16(planes + dal[k][h] + 8 * s8 * 128));
+                  else v[h] = lds64f(ad);
                 }
-                if (!in1) v1 = make_float2(0.f, 0.f);
-                const uint32_t a0 = tf32_rna(v0.x), a1 = tf32_rna(v1.x);
-                const uint32_t a2 = tf32_rna(v0.y), a3 = tf32_rna(v1.y);
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
-                  mma_tf32(R[mt][nt], a0, a1, a2, a3, bx[nt][hh][0], bx[nt][hh][1]);
+                const uint32_t a0 = tf32_rna(v[0].x), a1 = tf32_rna(v[0].y);
+                const uint32_t a2 = tf32_rna(v[1].x), a3 = tf32_rna(v[1].y);
+  #pragma unroll
+                for (int nt = 0; nt < 2; ++nt) mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
               }
-            } else if constexpr (ZSZ == 2 && !kZ24) {
-              const uint32_t a0 = ok0 ? lds32(z0) : 0u, a2 = ok0 ? lds32(z2) : 0u;
-              const uint32_t a1 = ok1 ? lds32(z0 + 1024) : 0u, a3 = ok1 ? lds32(z2 + 1024) : 0u;
-#pragma unroll
-              for (int nt = 0; nt < 2; ++nt) mma(R[mt][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
             } else {
-              const float2 zero = make_float2(0.f, 0.f);
-              float2 v0, v1, v2, v3;
-              if constexpr (kZ24) {
-                const uint32_t l0 = planes + ra0l[k] + 16 * mt * 128, l2 = planes + ra2l[k] + 16 * mt * 128;
-                v0 = ok0 ? f24x2(lds32(z0), lds16(l0)) : zero;
-                v2 = ok0 ? f24x2(lds32(z2), lds16(l2)) : zero;
-                v1 = ok1 ? f24x2(lds32(z0 + 1024), lds16(l0 + 1024)) : zero;
-                v3 = ok1 ? f24x2(lds32(z2 + 1024), lds16(l2 + 1024)) : zero;
-              } else {
-                v0 = ok0 ? lds64f(z0) : zero;
-                v2 = ok0 ? lds64f(z2) : zero;
-                v1 = ok1 ? lds64f(z0 + 1024) : zero;
-                v3 = ok1 ? lds64f(z2 + 1024) : zero;
+  #pragma unroll
+            for (int ks = 0; ks < MT; ++ks) {
+              float v[4][2];  // planes 16ks + 2q + {0, 1, 8, 9} at tiles t0, t0 + 1
+  #pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t ad = planes + da[k][j & 1] + (16 * ks + 8 * (j >> 1)) * 128;
+                if (ks < MT - 1 || dok[j]) {
+                  if constexpr (kZ24) {
+                    const float2 f = f24x2(lds32(ad), lds16(planes + dal[k][j & 1] + (16 * ks + 8 * (j >> 1)) * 128));
+                    v[j][0] = f.x;
+                    v[j][1] = f.y;
+                  } else if constexpr (ZSZ == 4) {
+                    const float2 f = lds64f(ad);
+                    v[j][0] = f.x;
+                    v[j][1] = f.y;
+                  } else {
+                    const uint32_t w = lds32(ad);
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+                    v[j][0] = f.x;
+                    v[j][1] = f.y;
+                  }
+                } else {
+                  v[j][0] = v[j][1] = 0.f;
+                }
               }
-              uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
-              split2(v0.x, v0.y, h0, l0);
-              split2(v1.x, v1.y, h1, l1);
-              split2(v2.x, v2.y, h2, l2);
-              split2(v3.x, v3.y, h3, l3);
-#pragma unroll
-              for (int nt = 0; nt < 2; ++nt) {
-                mma(R[mt][nt], h0, h1, h2, h3, b[nt][0], b[nt][1]);
-                mma(R[mt][nt], l0, l1, l2, l3, b[nt][0], b[nt][1]);
+              // a0 = (row g = tile t0: planes 2q, 2q+1), a1 = row g+8 = tile t0+1, a2/a3: +8
+              if constexpr (ZSZ == 4 || kZ24) {
+                uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
+                split2(v[0][0], v[1][0], h0, l0);
+                split2(v[0][1], v[1][1], h1, l1);
+                split2(v[2][0], v[3][0], h2, l2);
+                split2(v[2][1], v[3][1], h3, l3);
+  #pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                  const uint32_t bh0 = fh[ks][2 * nt], bh1 = fh[ks][2 * nt + 1];
+                  mma(acc[nt], h0, h1, h2, h3, bh0, bh1);
+                  mma(acc[nt], l0, l1, l2, l3, bh0, bh1);
+                  mma(acc[nt], h0, h1, h2, h3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
+                }
+              } else {
+                const uint32_t a0 = pack2(v[0][0], v[1][0]), a1 = pack2(v[0][1], v[1][1]);
+                const uint32_t a2 = pack2(v[2][0], v[3][0]), a3 = pack2(v[2][1], v[3][1]);
+  #pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                  mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
+                  mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
+                }
+              }
+            }
+            }  // bf16 planes
+            // acc[nt][0,1] -> tile t0, c = 8nt + 2q (+1): row a = 2nt + (q>>1), col b = 2(q&1).
+  #pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const uint32_t o = buf + ooff + 128 * kGWarps * k + 2 * nt * RS;
+              sts32(o, pack2(acc[nt][0], acc[nt][1]));
+              sts32(o + 8, pack2(acc[nt][2], acc[nt][3]));
+            }
+          }
+        }
+      }
+      if constexpr (has_red<MODE>()) {
+        // R[p][c] += sum over 16-tile k-steps of Z[p][tile] X[tile][c] (A = Z: M = p; B = X: N = c).
+        // B: b0 = (X[t0+2q][c], X[t0+2q+1][c]), b1 = tiles + 8, c = 8nt + g, 16-bit loads
+        // (words 16 (c>>2) + 4q + ((c&3)>>1): distinct). A: Z[p][t0+2q, +1] / [t0+2q+8, +9].
+        const int nks = kFull ? kT / 16 : (Tw >> 4);
+  #pragma unroll
+        for (int k = 0; k < kMK; ++k) {
+          if (kFull || wl + kGWarps * k < nks) {
+            uint32_t b[2][2], bx[2][2][2];
+  #pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const uint32_t base = rows + rb[nt] + 128 * kGWarps * k;
+              const uint32_t x0 = lds16(base), x1 = lds16(base + 8), x8 = lds16(base + 64),
+                             x9 = lds16(base + 72);
+              b[nt][0] = pair16(x0, x1);
+              b[nt][1] = pair16(x8, x9);
+              bx[nt][0][0] = x0 << 16;
+              bx[nt][0][1] = x1 << 16;
+              bx[nt][1][0] = x8 << 16;
+              bx[nt][1][1] = x9 << 16;
+            }
+  #pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              const bool ok0 = mt < MT - 1 || lastp0, ok1 = mt < MT - 1 || lastp1;
+              const uint32_t z0 = planes + ra0[k] + 16 * mt * 128, z2 = planes + ra2[k] + 16 * mt * 128;
+              if constexpr (kTf32) {
+                // two m16n8k8 tf32 steps (tiles t0..t0+7, t0+8..t0+15): rows g / g+8 = planes,
+                // k = q / q+4 = tiles 2q / 2q+1 of the step; B = X as fp32 (bf16 << 16, exact).
+  #pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                  const uint32_t za = hh ? z2 : z0;
+                  // planes 16mt+g (< Pb) and 16mt+g+8 (may pass Pb in the last group: load a
+                  // valid row, select zero)
+                  const bool in1 = mt < MT - 1 || okb1;
+                  const uint32_t d1 = in1 ? 1024u : 0u;
+                  float2 v0, v1;
+                  if constexpr (kZ24) {
+                    const uint32_t la = planes + (hh ? ra2l[k] : ra0l[k]) + 16 * mt * 128;
+                    v0 = f24x2(lds32(za), lds16(la));
+                    v1 = f24x2(lds32(za + d1), lds16(la + d1));
+                  } else {
+                    v0 = lds64f(za);
+                    v1 = lds64f(za + d1);
+                  }
+                  if (!in1) v1 = make_float2(0.f, 0.f);
+                  const uint32_t a0 = tf32_rna(v0.x), a1 = tf32_rna(v1.x);
+                  const uint32_t a2 = tf32_rna(v0.y), a3 = tf32_rna(v1.y);
+  #pragma unroll
+                  for (int nt = 0; nt < 2; ++nt)
+                    mma_tf32(R[mt][nt], a0, a1, a2, a3, bx[nt][hh][0], bx[nt][hh][1]);
+                }
+              } else if constexpr (ZSZ == 2 && !kZ24) {
+                const uint32_t a0 = ok0 ? lds32(z0) : 0u, a2 = ok0 ? lds32(z2) : 0u;
+                const uint32_t a1 = ok1 ? lds32(z0 + 1024) : 0u, a3 = ok1 ? lds32(z2 + 1024) : 0u;
+  #pragma unroll
+                for (int nt = 0; nt < 2; ++nt) mma(R[mt][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
+              } else {
+                const float2 zero = make_float2(0.f, 0.f);
+                float2 v0, v1, v2, v3;
+                if constexpr (kZ24) {
+                  const uint32_t l0 = planes + ra0l[k] + 16 * mt * 128, l2 = planes + ra2l[k] + 16 * mt * 128;
+                  v0 = ok0 ? f24x2(lds32(z0), lds16(l0)) : zero;
+                  v2 = ok0 ? f24x2(lds32(z2), lds16(l2)) : zero;
+                  v1 = ok1 ? f24x2(lds32(z0 + 1024), lds16(l0 + 1024)) : zero;
+                  v3 = ok1 ? f24x2(lds32(z2 + 1024), lds16(l2 + 1024)) : zero;
+                } else {
+                  v0 = ok0 ? lds64f(z0) : zero;
+                  v2 = ok0 ? lds64f(z2) : zero;
+                  v1 = ok1 ? lds64f(z0 + 1024) : zero;
+                  v3 = ok1 ? lds64f(z2 + 1024) : zero;
+                }
+                uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
+                split2(v0.x, v0.y, h0, l0);
+                split2(v1.x, v1.y, h1, l1);
+                split2(v2.x, v2.y, h2, l2);
+                split2(v3.x, v3.y, h3, l3);
+  #pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                  mma(R[mt][nt], h0, h1, h2, h3, b[nt][0], b[nt][1]);
+                  mma(R[mt][nt], l0, l1, l2, l3, b[nt][0], b[nt][1]);
+                }
               }
             }
           }
         }
       }
+    };
+    if (args.nocompute) {
+    } else if (Tw == kT) {
+      unit_math(std::true_type{});
+    } else {
+      unit_math(std::false_type{});
     }
 
     __syncwarp();
