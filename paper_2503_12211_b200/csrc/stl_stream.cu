@@ -189,9 +189,10 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 // F24 pair: high halves of two elements (one 32-bit word) + their low bytes (one 16-bit word)
+// (lo2 is zero-extended from 16 bits, so its byte 2 supplies the zero low byte: one PRMT each)
 __device__ __forceinline__ float2 f24x2(uint32_t hi2, uint32_t lo2) {
-  return make_float2(__uint_as_float((hi2 << 16) | ((lo2 & 0xFFu) << 8)),
-                     __uint_as_float((hi2 & 0xFFFF0000u) | (lo2 & 0xFF00u)));
+  return make_float2(__uint_as_float(__byte_perm(lo2, hi2, 0x5402)),
+                     __uint_as_float(__byte_perm(lo2, hi2, 0x7612)));
 }
 // two bf16 from (lo16 of a, lo16 of b) -> packed pair
 __device__ __forceinline__ uint32_t pair16(uint32_t a, uint32_t b) { return a | (b << 16); }
