@@ -38,6 +38,7 @@ struct EpiArgs {
   int r;
   int M, N, K;
   __nv_bfloat16* c2;  // optional bf16 copy of C (the forward's training cache)
+  unsigned long long* dbg;  // probe: per-cluster MMA-thread wait timers [2] (ns), or null
 };
 
 template <int BN>
@@ -272,13 +273,13 @@ struct Smem2 {
   static constexpr uint32_t kABytes = 128 * kBK * 2;
   static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
   static constexpr uint32_t kRing = kStages * (kABytes + kBBytes);
-  // epilogue staging per warp and buffer, 32 rows x 32 columns:
+  // epilogue staging, two buffers of 128 rows (the CTA's TMEM lanes) x 32 columns, written by
+  // the 4 epilogue warps and stored with one TMA op per plane set:
   //   primary (fp32 128 B rows, or F24 high 64 B rows) + secondary (bf16 64 B rows / F24 low 32 B)
-  static constexpr uint32_t kStageF = OUT == kOutF24 ? 32 * 64 : 32 * 128;
-  static constexpr uint32_t kStageH = OUT == kOutF32Bf16 ? 32 * 64 : (OUT == kOutF24 ? 32 * 32 : 0);
+  static constexpr uint32_t kStageF = OUT == kOutF24 ? 128 * 64 : 128 * 128;
+  static constexpr uint32_t kStageH = OUT == kOutF32Bf16 ? 128 * 64 : (OUT == kOutF24 ? 128 * 32 : 0);
   static constexpr uint32_t kBufBytes = kStageF + kStageH;
-  static constexpr uint32_t kWarpStage = 2 * kBufBytes;
-  static constexpr uint32_t kBarOffset = kRing + 4 * kWarpStage;
+  static constexpr uint32_t kBarOffset = kRing + 2 * kBufBytes;
   static constexpr uint32_t kTotal = kBarOffset + 512 + 1024;
 };
 
@@ -395,12 +396,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int tile = cluster; tile < total; tile += nclusters, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
+        const uint64_t t0 = args.dbg ? ptx::globaltimer_ns() : 0;
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
+        if (args.dbg) args.dbg[2 * cluster] += ptx::globaltimer_ns() - t0;
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
+          const uint64_t t1 = args.dbg ? ptx::globaltimer_ns() : 0;
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (args.dbg) args.dbg[2 * cluster + 1] += ptx::globaltimer_ns() - t1;
           const uint32_t a_addr = ptx::smem_u32(sA + stage * S::kABytes);
           const uint32_t b_addr = ptx::smem_u32(sB + stage * S::kBBytes);
 #pragma unroll
@@ -422,10 +427,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
-    // TMEM -> registers -> 128B-swizzled smem (32 rows x 32 fp32 per warp and chunk) -> TMA
-    // bulk store; TMA clips rows >= M / cols >= N. Two staging buffers per warp.
+    // TMEM -> registers -> swizzled smem staging of the CTA's 128 rows x 32 columns (each warp
+    // writes its 32 TMEM lanes) -> one TMA store per plane set and chunk, issued by one thread
+    // after a 128-thread barrier (few, large TMA ops: the TMA unit also feeds the mainloop).
+    // TMA clips rows >= M / cols >= N. Two staging buffers.
     const int q = warp & 3;
-    uint8_t* stage_base = smem + S::kRing + q * S::kWarpStage;
+    const bool issuer = warp == 4 && lane == 0;
+    const int r = q * 32 + lane;  // staging row = TMEM lane
     int chunk_no = 0;
     int it = 0;
     for (int tile = cluster; tile < total; tile += nclusters, ++it) {
@@ -437,20 +445,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row0 = mb * 256 + static_cast<int>(rank) * 128 + q * 32;
+      const int row_base = mb * 256 + static_cast<int>(rank) * 128;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32, ++chunk_no) {
         uint32_t v[32];
         __syncwarp();
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c,
                                 v);
-        const int buf = chunk_no & 1;
-        uint8_t* sf = stage_base + buf * S::kBufBytes;
-        // the TMA store that last read this buffer (two chunks ago) must be done reading
-        if (lane == 0) ptx::bulk_wait_read<1>();
-        __syncwarp();
+        uint8_t* sf = smem + S::kRing + (chunk_no & 1) * S::kBufBytes;
         ptx::tmem_ld_wait();
-        if (nb * BN + c < N && row0 < M && !args.nostore) {
+        const bool active = nb * BN + c < N && row_base < M && !args.nostore;  // CTA-uniform
+        if (active) {
           if constexpr (OUT == kOutF24) {
             // high 16 bits: 64 B rows, 64B-swizzled; low 8 bits: 32 B rows, 32B-swizzled
             uint8_t* sh = sf + S::kStageF;
@@ -465,16 +470,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              *reinterpret_cast<uint4*>(sf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+              *reinterpret_cast<uint4*>(sf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
                   make_uint4(hw[4 * j], hw[4 * j + 1], hw[4 * j + 2], hw[4 * j + 3]);
 #pragma unroll
             for (int j = 0; j < 2; ++j)
-              *reinterpret_cast<uint4*>(sh + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4)) =
+              *reinterpret_cast<uint4*>(sh + r * 32 + ((j ^ ((r >> 2) & 1)) << 4)) =
                   make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
           } else {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              *reinterpret_cast<float4*>(sf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+              *reinterpret_cast<float4*>(sf + r * 128 + ((j ^ (r & 7)) << 4)) =
                   make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
           }
@@ -489,24 +494,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                                          __uint_as_float(v[8 * j + 2 * e + 1]));
                 w[e] = *reinterpret_cast<uint32_t*>(&h);
               }
-              *reinterpret_cast<uint4*>(sh + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+              *reinterpret_cast<uint4*>(sh + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
                   make_uint4(w[0], w[1], w[2], w[3]);
             }
           }
           ptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            ptx::tma_store_3d(&tmC, sf, nb * BN + c, row0, p);
-            if constexpr (OUT != kOutF32) ptx::tma_store_3d(&tmC2, sf + S::kStageF, nb * BN + c, row0, p);
-            ptx::bulk_commit();
-          }
+        }
+        // the previous chunk's store must be done reading the other buffer (written next chunk)
+        if (issuer) ptx::bulk_wait_read<0>();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (issuer && active) {
+          ptx::tma_store_3d(&tmC, sf, nb * BN + c, row_base, p);
+          if constexpr (OUT != kOutF32) ptx::tma_store_3d(&tmC2, sf + S::kStageF, nb * BN + c, row_base, p);
+          ptx::bulk_commit();
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
     }
-    if (lane == 0) ptx::bulk_wait_all();
+    if (issuer) ptx::bulk_wait_all();
   }
 
   ptx::tc_fence_before();
@@ -554,20 +561,20 @@ cudaError_t launch_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   const int64_t tiles = r * ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
   EpiArgs ea{pb.c, pb.c_dtype == kBF16 ? 1 : 0, 0, 0, pb.r, static_cast<int>(M), static_cast<int>(N),
-             static_cast<int>(K), static_cast<__nv_bfloat16*>(pb.c2)};
+             static_cast<int>(K), static_cast<__nv_bfloat16*>(pb.c2), nullptr};
   kern<<<grid, kThreads, smem, s>>>(ta, tb, ea);
   return cudaGetLastError();
 }
 
 
-// 3-D (N, M, r) store map for 32 x 32 output chunks: es = 4 (fp32, 128B swizzle),
+// 3-D (N, M, r) store map for 128-row x 32-column output chunks: es = 4 (fp32, 128B swizzle),
 // 2 (16-bit, 64B swizzle) or 1 (8-bit, 32B swizzle).
 bool make_out_tmap(CUtensorMap* m, const void* base, int es, uint64_t N, uint64_t M, uint64_t r) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {N, M, r};
   cuuint64_t strides[2] = {N * es, N * M * es};
-  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t box[3] = {32, 128, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   const CUtensorMapDataType dt = es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                  : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -605,8 +612,26 @@ cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
   static const int nostore = getenv("STL_GEMM_NOSTORE") ? atoi(getenv("STL_GEMM_NOSTORE")) : 0;
   EpiArgs ea{pb.c, 0, nostore, 0, pb.r, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
-             static_cast<__nv_bfloat16*>(pb.c2)};
-  return launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, ta, tb, tc, tc2, ea);
+             static_cast<__nv_bfloat16*>(pb.c2), nullptr};
+  static const bool dbg_on = getenv("STL_GEMM_DEBUG") != nullptr;
+  static unsigned long long* dbg = nullptr;
+  if (dbg_on && !dbg) cudaMalloc(&dbg, 2 * 256 * sizeof(unsigned long long));
+  if (dbg_on) {
+    cudaMemsetAsync(dbg, 0, 2 * 256 * sizeof(unsigned long long), s);
+    ea.dbg = dbg;
+  }
+  cudaError_t le = launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, ta, tb, tc, tc2, ea);
+  if (dbg_on) {
+    unsigned long long h[512];
+    const int nc = grid / 2;
+    cudaMemcpyAsync(h, dbg, sizeof(unsigned long long) * 2 * nc, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double te = 0, tf = 0;
+    for (int i = 0; i < nc; ++i) { te += h[2 * i]; tf += h[2 * i + 1]; }
+    fprintf(stderr, "[gemm dbg] OUT=%d M=%d N=%d K=%d tiles/cluster=%.2f MMA-thread avg us: wait tempty=%.1f wait full=%.1f\n",
+            OUT, int(M), int(N), int(K), double(tiles) / nc, te / nc / 1e3, tf / nc / 1e3);
+  }
+  return le;
 }
 
 template <int BN, bool A_MN, bool B_MN>
