@@ -85,7 +85,9 @@ STL_API int stl_decode(const void* enc, int dtype_in, int64_t block_rows, int64_
  * _slice_products (snf_operator.py:107-116):  C_p = A_p @ B_p for p = 0..r-1.
  * A: a_layout STL_K_MAJOR -> planes (r, M, K); STL_MN_MAJOR -> planes (r, K, M).
  * B: b_layout STL_K_MAJOR -> planes (r, N, K); STL_MN_MAJOR -> planes (r, K, N).
- * C: planes (r, M, N) of dtype_c (STL_F32 keeps the slice accumulators exact in fp32).
+ * C: planes (r, M, N) of dtype_c (STL_F32 keeps the slice accumulators exact in fp32;
+ *    STL_F24 — bf16 operands, M > 128, N % 16 == 0, 16-byte aligned — writes them rounded to
+ *    24 bits as 3*r*M*N bytes: the high 16 bits of every element, then the next 8 bits).
  * dtype_ab = STL_BF16 runs the tcgen05/TMEM tensor-core kernel (when the contiguous dims are
  * multiples of 8); STL_F32 runs the fp32 FFMA kernel (TF32 would miss the 1e-5 fp32 bar).
  */

@@ -139,7 +139,10 @@ int stl_decode(const void* enc, int dtype_in, int64_t block_rows, int64_t block_
 int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_layout, void* c,
                    int dtype_c, int dtype_ab, int r, int64_t M, int64_t N, int64_t K,
                    void* stream) {
-  if (!valid_dtype(dtype_c) || !valid_dtype(dtype_ab)) return fail(STL_ERR_VALUE, "invalid dtype");
+  if ((!valid_dtype(dtype_c) && dtype_c != STL_F24) || !valid_dtype(dtype_ab))
+    return fail(STL_ERR_VALUE, "invalid dtype");
+  if (dtype_c == STL_F24 && dtype_ab != STL_BF16)
+    return fail(STL_ERR_UNSUPPORTED, "F24 slice products need bf16 operands");
   if (r < 0 || M < 0 || N < 0 || K < 0) return fail(STL_ERR_SHAPE, "negative extent");
   if ((a_layout != 0 && a_layout != 1) || (b_layout != 0 && b_layout != 1))
     return fail(STL_ERR_VALUE, "invalid operand layout");

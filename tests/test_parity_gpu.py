@@ -156,6 +156,30 @@ def test_slice_gemm_tc_layouts(al, bl, shape):
     assert errb <= 5e-3, float(errb)
 
 
+@pytest.mark.parametrize("al,bl", [(0, 0), (1, 1), (0, 1)])
+@pytest.mark.parametrize("shape", [(3, 256, 128, 64), (2, 520, 272, 136), (24, 512, 256, 512)])
+def test_slice_gemm_f24_output(al, bl, shape):
+    """F24 slice products (CTA-pair epilogue): bit-exact RNE-24 of the fp32 products of the
+    same kernel, and ~2^-17 relative to the f64 product."""
+    r, M, N, K = shape
+    g = torch.Generator(device="cpu").manual_seed(M + N + K + 5 * al + bl)
+    A = torch.randn((r, M, K), generator=g).to(torch.bfloat16)
+    B = torch.randn((r, K, N), generator=g).to(torch.bfloat16)
+    a_dev = (A if al == 0 else A.transpose(1, 2)).contiguous().to(DEV)
+    b_dev = (B.transpose(1, 2) if bl == 0 else B).contiguous().to(DEV)
+    c32 = _gemm(a_dev, al, b_dev, bl, M, N, K, r)
+    c24 = torch.empty((3 * r * M * N,), dtype=torch.uint8, device=DEV)
+    _lib.check(_lib.load().stl_slice_gemm(a_dev.data_ptr(), al, b_dev.data_ptr(), bl,
+                                          c24.data_ptr(), _lib.STL_F24, _lib.STL_BF16, r, M, N, K,
+                                          torch.cuda.current_stream().cuda_stream))
+    got = stl.unpack_slice_products(c24, r, M, N)
+    u = c32.view(torch.int32)
+    rne = ((u + 0x7F + ((u >> 8) & 1)) & ~0xFF).view(torch.float32)
+    assert torch.equal(got, rne)
+    ref = torch.bmm(A.double(), B.double())
+    assert (got.cpu().double() - ref).norm() / ref.norm() <= 2e-5
+
+
 @pytest.mark.parametrize("shape", [(3, 37, 29, 13), (2, 64, 64, 64), (24, 256, 256, 256)])
 def test_slice_gemm_simt_fp32(shape):
     r, M, N, K = shape
