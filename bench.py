@@ -402,17 +402,37 @@ def main() -> None:
         del wf, xf, uf, sf, yf, wdf, ydf
         torch.cuda.empty_cache()
 
-        # ---- e2e: public API (StlLinear autograd) with pinned host inputs, copies timed
+        # ---- e2e: public API (StlLinear autograd) with pinned host inputs, copies timed.
+        # Double-buffered: step i's compute overlaps the H2D copy of step i+1's inputs on a copy
+        # stream (a data-loader prefetch). Exactly one input copy per timed step is issued and
+        # consumed inside the timed region (the pipeline is primed in the first timed step and
+        # the last step does not prefetch).
         mod = stl.StlLinear(snf, w_planes.clone())
         x_h = x.cpu().pin_memory()
         gy_h = gy.cpu().pin_memory()
-        x_d = torch.empty_like(x)
-        gy_d = torch.empty_like(gy)
+        bufs = [(torch.empty_like(x), torch.empty_like(gy)) for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_free = [torch.cuda.Event() for _ in range(2)]
+        copy_s = torch.cuda.Stream(dev)
         out_h = torch.empty((2, R, T * T), dtype=torch.float32).pin_memory()
+        pipe = {"i": 0, "left": 0}
+
+        def issue_copy(slot):
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_event(ev_free[slot])        # the step that last read it is done
+                bufs[slot][0].copy_(x_h, non_blocking=True)
+                bufs[slot][1].copy_(gy_h, non_blocking=True)
+                ev_in[slot].record(copy_s)
 
         def e2e_step():
-            x_d.copy_(x_h, non_blocking=True)
-            gy_d.copy_(gy_h, non_blocking=True)
+            i, slot = pipe["i"], pipe["i"] % 2
+            if i == 0:
+                issue_copy(slot)
+            if pipe["left"] > 1:
+                issue_copy(1 - slot)                     # prefetch step i+1
+            cs = torch.cuda.current_stream(dev)
+            cs.wait_event(ev_in[slot])
+            x_d, gy_d = bufs[slot]
             xin = x_d.detach().requires_grad_(True)
             mod.zero_grad(set_to_none=True)
             out = mod(xin)
@@ -421,17 +441,28 @@ def main() -> None:
                 dist.all_reduce(mod.w_planes.grad)
             out_h[0].copy_(mod.e_x.grad, non_blocking=True)
             out_h[1].copy_(mod.d.grad, non_blocking=True)
+            ev_free[slot].record(cs)
+            pipe["i"] += 1
+            pipe["left"] -= 1
+
+        def e2e_run(n):
+            pipe.update(i=0, left=n)
+            return lambda: e2e_step()
 
         steps_e = max(args.steps // 4, 10)
+        run = e2e_run(args.warmup)
         for _ in range(args.warmup):
-            e2e_step()
-        e2e_ms = timed(e2e_step, steps_e) / steps_e
+            run()
+        torch.cuda.synchronize(dev)
+        e2e_ms = timed(e2e_run(steps_e), steps_e) / steps_e
         line["e2e"] = {"value": world * dense_equiv_flops() / (e2e_ms * 1e-3) / 1e12,
                        "unit": UNIT, "ms_per_step": e2e_ms,
                        "h2d_bytes_per_step": x_h.numel() * 2 + gy_h.numel() * 2,
                        "d2h_bytes_per_step": out_h.numel() * 4,
+                       "h2d_GBs": (x_h.numel() + gy_h.numel()) * 2 / (e2e_ms * 1e-3) / 1e9,
                        "path": "StlLinear (autograd) forward+backward, pinned host X and dY "
-                               "copied in, encoder/decoder grads copied out each step"}
+                               "copied in (double-buffered on a copy stream), encoder/decoder "
+                               "grads copied out each step"}
 
     # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on a bounded sample
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
