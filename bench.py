@@ -182,12 +182,17 @@ def main() -> None:
     ap.add_argument("--cpu-rows", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip cuBLAS / 8192^3 / e2e legs")
+    ap.add_argument("--no-t2t", action="store_true", help="skip the T2T-ViT-7 training leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks for exercising the multi-rank path on a one-GPU box: every rank on cuda:0, gloo
+    if os.environ.get("STL_BENCH_SAME_DEVICE"):
+        local = 0
+    backend = os.environ.get("STL_BENCH_BACKEND", "nccl")
 
     if args.impl == "reference":
         run_reference(args, rank)
@@ -204,7 +209,7 @@ def main() -> None:
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     lib = _lib.load()
     peaks = load_peaks()
 
@@ -362,21 +367,24 @@ def main() -> None:
                              "cublas_tflops": dense_equiv_flops() / (dense_ms * 1e-3) / 1e12}
         del wd, yd, gxd, gwd
 
-        # ---- north-star forward: 8192^3 bf16, t=4, r=24, STL forward vs cuBLAS forward
+        # ---- north-star forward: 8192^3 bf16, t=4, r=24, STL forward vs cuBLAS forward.
+        # Under torchrun (configs[4]) the 8192 token rows are sharded over the ranks with no
+        # collective (rows of Y depend only on the same rows of X); time = max over ranks.
         n3 = 8192
+        m_loc = n3 // world
         wf = stl.weights_to_planes(
             stl.encode_tiles(torch.randn((n3, n3), device=dev) / n3 ** 0.5, snf.e_w, T),
             dtype=torch.bfloat16)
-        xf = torch.randn((n3, n3), device=dev).to(torch.bfloat16)
-        uf = torch.empty((R, n3 // T, n3 // T), dtype=torch.bfloat16, device=dev)
-        sf = torch.empty((int(lib.stl_forward_scratch_bytes(n3, n3, n3, T, R, _lib.STL_BF16)),),
+        xf = torch.randn((m_loc, n3), device=dev).to(torch.bfloat16)
+        uf = torch.empty((R, m_loc // T, n3 // T), dtype=torch.bfloat16, device=dev)
+        sf = torch.empty((int(lib.stl_forward_scratch_bytes(m_loc, n3, n3, T, R, _lib.STL_BF16)),),
                          dtype=torch.uint8, device=dev)
-        yf = torch.empty((n3, n3), dtype=torch.bfloat16, device=dev)
+        yf = torch.empty((m_loc, n3), dtype=torch.bfloat16, device=dev)
         wdf = torch.randn((n3, n3), device=dev).to(torch.bfloat16)
-        ydf = torch.empty((n3, n3), device=dev, dtype=torch.bfloat16)
+        ydf = torch.empty((m_loc, n3), device=dev, dtype=torch.bfloat16)
 
         def fwd8192():
-            _lib.check(lib.stl_forward(xf.data_ptr(), n3, n3, n3, wf.data_ptr(), n3,
+            _lib.check(lib.stl_forward(xf.data_ptr(), m_loc, n3, n3, wf.data_ptr(), n3,
                                        snf.e_x.data_ptr(), snf.d.data_ptr(), T, R, _lib.STL_BF16,
                                        yf.data_ptr(), n3, uf.data_ptr(), None, sf.data_ptr(),
                                        sf.numel(), stream))
@@ -391,11 +399,12 @@ def main() -> None:
         gemm_f = [ms for name, ms, _ in recs_f
                   if name in ("slice_gemm_tcgen05", "slice_gemm_decode_fused")]
         cub_f = timed(lambda: torch.matmul(xf, wdf, out=ydf), steps_f) / steps_f
-        cost_f = stl.LayerCost(n3, n3, n3, T, R, 2)
+        cost_f = stl.LayerCost(m_loc, n3, n3, T, R, 2)
         gf_ms = sum(gemm_f) / max(len(gemm_f), 1)
         line["north_star_fwd_8192"] = {
             "stl_ms": stl_f, "cublas_ms": cub_f, "speedup": cub_f / stl_f, "target": 1.8,
             "dense_equiv_tflops": 2 * n3 ** 3 / (stl_f * 1e-3) / 1e12,
+            "m_sharded_over": world, "rows_per_rank": m_loc,
             "gemm_ms": gf_ms, "gemm_tflops": cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12,
             "gemm_frac_of_burst": cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12 / peaks["bf16_burst"],
         }
@@ -463,6 +472,31 @@ def main() -> None:
                        "path": "StlLinear (autograd) forward+backward, pinned host X and dY "
                                "copied in (double-buffered on a copy stream), encoder/decoder "
                                "grads copied out each step"}
+
+    # ---- configs[3] / configs[4]: T2T-ViT-7 training step with STL projections (trunk qkv,
+    # proj, fc1, fc2 as STL r=24), synthetic 224x224, batch 256 per GPU, AdamW, gradient
+    # all-reduce under torchrun; the dense nn.Linear model is timed the same way.
+    if not args.no_extras and not args.no_t2t:
+        from paper_2503_12211_b200 import t2t_vit
+
+        res = {}
+        for name, use_stl in (("stl_r24", True), ("dense", False)):
+            torch.manual_seed(0)
+            model = t2t_vit.T2TViT7(stl=use_stl, r=R, device=dev)
+            opt = torch.optim.AdamW(model.parameters(), lr=1e-3, weight_decay=0.05)
+            gen = torch.Generator(device=dev).manual_seed(rank)
+            img = torch.randn(256, 3, 224, 224, device=dev, generator=gen)
+            lab = torch.randint(0, 1000, (256,), device=dev, generator=gen)
+            for _ in range(3):
+                t2t_vit.train_step(model, opt, img, lab, allreduce=world > 1)
+            ms = timed(lambda: t2t_vit.train_step(model, opt, img, lab, allreduce=world > 1), 5) / 5
+            res[name] = {"ms_per_step": ms, "images_per_s": world * 256 / (ms * 1e-3),
+                         "params": sum(p.numel() for p in model.parameters())}
+            del model, opt, img, lab
+            torch.cuda.empty_cache()
+        line["t2t_vit7_train"] = {"batch_per_gpu": 256, **res,
+                                  "note": "synthetic 224x224; STL layers memory-bound at these "
+                                          "widths (K, N <= 768), see DESIGN"}
 
     # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on a bounded sample
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
