@@ -1,0 +1,75 @@
+"""The HBM-streaming t = 4 transforms (stl_stream.cu) over their configuration space, against
+the CPU oracle: encode / decode of bf16 data with partial units (tile columns not a multiple of
+the 512-tile unit), ranks that are not multiples of 8 or 16 (zero-padded plane boxes), every
+plane group count (r up to 64), and the fused reductions (g_d, g_ex) through the layer backward
+in all three slice-product formats (F24, fp32, bf16 cache)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2503_12211_b200 as stl
+from paper_2503_12211_b200 import _lib
+from oracle import stl_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def bf(a):
+    t = torch.tensor(a, dtype=torch.float32).to(torch.bfloat16)
+    return t.cuda(), t.double().numpy()
+
+
+def rel(got, ref):
+    g = got.double().cpu().numpy() if isinstance(got, torch.Tensor) else np.asarray(got, float)
+    return np.linalg.norm(g - ref) / max(np.linalg.norm(ref), 1e-30)
+
+
+@pytest.mark.parametrize("rows,cols", [(64, 2304), (36, 256), (8, 4096), (128, 512)])
+@pytest.mark.parametrize("r", [5, 20, 24, 40, 64])
+def test_encode_decode_bf16(rows, cols, r):
+    """bf16 matrix -> bf16 planes -> bf16 matrix (units: 512 tiles; 2304/4 = 576 = 512 + 64)."""
+    rng = O.make_rng(rows * 31 + cols + r)
+    e_x, _, d = O.random_gaussian_init(4, r, rng, scale=0.5)
+    m_dev, m64 = bf(rng.standard_normal((rows, cols)))
+    enc = stl.encode_tiles(m_dev, e_x, 4)                     # (rows/4, cols/4, r) view
+    ref_enc = O.encode_tiles(m64, e_x, 4)
+    assert rel(enc, ref_enc) <= 5e-3                            # bf16 output rounding
+    enc_dev, enc64 = bf(ref_enc)
+    dec = stl.decode_tiles(enc_dev.permute(2, 0, 1).contiguous().permute(1, 2, 0), d, 4)
+    assert dec.dtype == torch.bfloat16
+    assert rel(dec, O.decode_tiles(enc64, d, 4)) <= 5e-3
+
+
+@pytest.mark.parametrize("M,K,N,r,fmt", [
+    (1024, 512, 512, 24, "f24"),     # F24 slice products (N/4 % 128 == 0)
+    (1024, 512, 768, 24, "bf16"),    # N/4 = 192: fp32 products + bf16 cache
+    (1024, 2304, 512, 20, "f24"),    # partial 512-tile units in K, r not a multiple of 8
+    (768, 256, 1024, 13, "f24"),     # r = 13: one plane group, zero-padded to 16 in the box
+    (1024, 512, 512, 32, "nof24"),   # F24 disabled (stl_set_fusion bit 4): fp32 products, bf16 cache
+])
+def test_layer_fwd_bwd_formats(M, K, N, r, fmt):
+    t = 4
+    rng = O.make_rng(M + K + N + r)
+    e_x, e_w, d = O.random_gaussian_init(t, r, rng, scale=0.5)
+    x_dev, x64 = bf(rng.standard_normal((M, K)))
+    w_dev, w64 = bf(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
+    gy_dev, gy64 = bf(rng.standard_normal((M, N)))
+    layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
+    try:
+        _lib.load().stl_set_fusion(16 if fmt == "nof24" else 0)
+        y, cache = stl._layer_forward_cached(layer, x_dev)
+        grads = stl._layer_backward(layer, cache, gy_dev)
+        torch.cuda.synchronize()
+    finally:
+        _lib.load().stl_set_fusion(0)
+    nbytes = cache.y_enc.numel() * cache.y_enc.element_size()
+    assert nbytes == {"f24": 3, "bf16": 2, "nof24": 2}[fmt] * r * (M // 4) * (N // 4)
+    y_ref, cache_ref = O.layer_forward_cached(x64, w64, e_x, d, t)
+    assert rel(y, y_ref) <= 1e-2
+    y_enc = stl.unpack_slice_products(cache.y_enc, r, M // 4, N // 4)
+    tol_enc = {"f24": 2e-3, "bf16": 5e-3, "nof24": 5e-3}[fmt]      # u is bf16 in all formats
+    assert rel(y_enc, cache_ref[2].transpose(2, 0, 1)) <= tol_enc
+    refs = O.layer_backward(w64, e_x, d, cache_ref, gy64, t)
+    for name, g, ref in zip(("g_ex", "g_d", "g_w", "g_x"), grads, refs):
+        assert rel(g, ref) <= 1e-2, (name, rel(g, ref))
