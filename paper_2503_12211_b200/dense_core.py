@@ -20,6 +20,19 @@ class ShapeError(ValueError):
     """Operand shapes are incompatible or a matrix is not tileable."""
 
 
+# Condition-number ceiling above which a normal-equation system counts as singular
+# (dense_core.py:27).
+SINGULAR_COND_LIMIT = 1e12
+
+
+class SingularSystemError(ValueError):
+    """A linear system is numerically singular; carries a condition estimate (dense_core.py:34-40)."""
+
+    def __init__(self, message: str, cond: float | None = None):
+        super().__init__(message)
+        self.cond = cond
+
+
 COMPUTE_DTYPES = (torch.float32, torch.bfloat16)
 
 # The reference rejects non-finite inputs on every API call (dense_core.py:47-48). The check
