@@ -305,17 +305,22 @@ def main() -> None:
     p_bytes = 3 if int(lib.stl_cache_bytes(M, K, N, T, R, _lib.STL_BF16)) == 3 * R * bi * bj else 4
     cost = stl.LayerCost(M, K, N, T, R, 2, p_bytes)
     gem = kern.get("slice_gemm_tcgen05", {"ms": float("nan"), "calls": 1})
-    gemm_ms = gem["ms"] / max(gem["calls"], 1)
-    gemm_tflops = cost.gemm_flops() / (gemm_ms * 1e-3) / 1e12
+    # the step's three slice-GEMMs (y_enc forward; g_w and g_u backward, one grouped launch when
+    # eligible) -> FLOP-weighted rate over all of the step's GEMM launches
+    gemm_ms_step = gem["ms"] / args.steps
+    gemm_flops_step = 3 * cost.gemm_flops()
+    gemm_tflops = gemm_flops_step / (gemm_ms_step * 1e-3) / 1e12
     traffic = None
     tp = ROOT / "profiles" / "gemm_traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get("bytes_per_launch")
-    roofline = {"kernel": "slice_gemm_tc2_kernel (CTA-pair tcgen05 slice GEMM; mean of the step's "
-                          "3 launches)", "bound": "tensor", "achieved": gemm_tflops,
-                "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
+    roofline = {"kernel": "slice_gemm_tc2_kernel (CTA-pair tcgen05 slice GEMM; the step's 3 "
+                          "slice-GEMMs over its launches, FLOP-weighted)", "bound": "tensor",
+                "achieved": gemm_tflops, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
                 "frac": gemm_tflops / peaks["bf16_sustained"], "traffic": traffic,
-                "flops_per_launch": cost.gemm_flops(), "ms_per_launch": gemm_ms,
+                "traffic_of": "one forward slice-GEMM launch (ncu dram bytes)",
+                "flops_per_step": gemm_flops_step, "ms_per_step": gemm_ms_step,
+                "launches_per_step": gem["calls"] / args.steps,
                 "peak_source": peaks["source"] + ", sustained bf16"}
     breakdown = {}
     step_kernel_ms = sum(v["ms"] for v in kern.values()) / args.steps

@@ -291,18 +291,37 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
   }
   if (st) return st;
   // g_w^T_p (N/t x K/t) = g_enc_p^T (N/t x M/t) . u_p (M/t x K/t): both operands MN-major.
-  if (g_w) {
+  // g_u_p (M/t x K/t) = g_enc_p (M/t x N/t) . W_p (N/t x K/t): B is N-major. F24 on the bf16
+  // path (3 of the 4 bytes of g_u_ws used).
+  const int gu_dt = f24_products(bi, bk, bj, t, r, dtype) ? stl::kF24 : STL_F32;
+  bool gw_done = false, gu_done = false;
+  if (g_w && (g_x || g_ex) && bi > 0 && bk > 0 && bj > 0 && r > 0) {
+    // both slice-GEMMs in one persistent launch (g_w first: its K = M/t is the longer one)
+    stl::SliceGemmProblem pw{g_enc_ws, STL_MN_MAJOR, x_enc, STL_MN_MAJOR, g_w, STL_F32, dtype,
+                             r, bj, bk, bi};
+    stl::SliceGemmProblem pu{g_enc_ws, STL_K_MAJOR, w_enc, STL_MN_MAJOR, g_u_ws, gu_dt, dtype,
+                             r, bi, bk, bj};
+    Prof prof("slice_gemm_tcgen05", s);
+    cudaError_t e = stl::slice_gemm_tc_group(pw, pu, s);
+    if (e == cudaSuccess) {
+      gw_done = gu_done = true;
+    } else if (e != cudaErrorNotSupported) {
+      return check_cuda(e, "grouped slice_gemm launch");
+    } else {
+      (void)cudaGetLastError();
+    }
+  }
+  if (g_w && !gw_done) {
     st = run_gemm(g_enc_ws, STL_MN_MAJOR, x_enc, STL_MN_MAJOR, g_w, STL_F32, dtype, r, bj, bk,
                   bi, s);
     if (st) return st;
   }
   if (g_x || g_ex) {
-    // g_u_p (M/t x K/t) = g_enc_p (M/t x N/t) . W_p (N/t x K/t): B is N-major. F24 on the bf16
-    // path (3 of the 4 bytes of g_u_ws used).
-    const int gu_dt = f24_products(bi, bk, bj, t, r, dtype) ? stl::kF24 : STL_F32;
-    st = run_gemm(g_enc_ws, STL_K_MAJOR, w_enc, STL_MN_MAJOR, g_u_ws, gu_dt, dtype, r, bi, bk,
-                  bj, s);
-    if (st) return st;
+    if (!gu_done) {
+      st = run_gemm(g_enc_ws, STL_K_MAJOR, w_enc, STL_MN_MAJOR, g_u_ws, gu_dt, dtype, r, bi, bk,
+                    bj, s);
+      if (st) return st;
+    }
     if (g_x) {
       Prof prof(g_ex ? "decode_gu+g_ex" : "decode_gu", s, g_ex ? 2 : 1);
       st = check_cuda(stl::planes_to_tiles(g_u_ws, gu_dt, r, bi, bk, t, e_x, g_x, dtype, ld_gx,

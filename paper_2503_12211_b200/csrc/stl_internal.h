@@ -79,6 +79,10 @@ cudaError_t cast_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t
 // tcgen05 path (bf16 operands, aligned shapes). Returns cudaError_t-like code, 0 = ok.
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s);
 bool slice_gemm_tc_supported(const SliceGemmProblem& pb);
+// Two problems with the same r in one persistent CTA-pair launch (problem 0's tiles first);
+// cudaErrorNotSupported when the pair (kinds, alignment) is not covered -> launch separately.
+cudaError_t slice_gemm_tc_group(const SliceGemmProblem& p0, const SliceGemmProblem& p1,
+                                cudaStream_t s);
 // F24 output (c_dtype = kF24) is produced by the CTA-pair kernel only.
 bool slice_gemm_f24_supported(const SliceGemmProblem& pb);
 // SIMT path (fp32 or bf16 operands, any shape).

@@ -266,20 +266,35 @@ __global__ void __launch_bounds__(kThreads, 1)
 // (c + 2 * r * M * N bytes), 3 bytes per element at ~2^-16 relative precision.
 enum OutMode { kOutF32 = 0, kOutF32Bf16 = 1, kOutF24 = 2 };
 
-template <int BN, int OUT>
+// Per-problem compile-time traits of the pair kernel: operand majorness and output mode.
+template <bool A_MN_, bool B_MN_, int OUT_>
+struct GemmKind {
+  static constexpr bool A_MN = A_MN_, B_MN = B_MN_;
+  static constexpr int OUT = OUT_;
+};
+
+// Epilogue staging of one output mode: 128 rows (the CTA's TMEM lanes) x 32 columns, a primary
+// part (fp32 128 B rows, or F24 high 64 B rows) and a secondary part at kSecOff (bf16 64 B rows,
+// or F24 low 32 B rows).
+template <int OUT>
+struct OutStage {
+  static constexpr uint32_t kSecOff = OUT == kOutF24 ? 128 * 64 : 128 * 128;
+  static constexpr uint32_t kBytes =
+      kSecOff + (OUT == kOutF32Bf16 ? 128 * 64 : (OUT == kOutF24 ? 128 * 32 : 0));
+};
+
+template <int BN, int OUT0, int OUT1>
 struct Smem2 {
   // ring depth chosen so ring + epilogue staging fits the 227 KB opt-in limit
-  static constexpr int kStages = BN == 256 ? (OUT == kOutF32Bf16 ? 5 : 6) : (OUT == kOutF32Bf16 ? 7 : 8);
+  static constexpr bool kDual = OUT0 == kOutF32Bf16 || OUT1 == kOutF32Bf16;
+  static constexpr int kStages = BN == 256 ? (kDual ? 5 : 6) : (kDual ? 7 : 8);
   static constexpr uint32_t kABytes = 128 * kBK * 2;
   static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
   static constexpr uint32_t kRing = kStages * (kABytes + kBBytes);
-  // epilogue staging, two buffers of 128 rows (the CTA's TMEM lanes) x 32 columns, written by
-  // the 4 epilogue warps and stored with one TMA op per plane set:
-  //   primary (fp32 128 B rows, or F24 high 64 B rows) + secondary (bf16 64 B rows / F24 low 32 B)
-  static constexpr uint32_t kStageF = OUT == kOutF24 ? 128 * 64 : 128 * 128;
-  static constexpr uint32_t kStageH = OUT == kOutF32Bf16 ? 128 * 64 : (OUT == kOutF24 ? 128 * 32 : 0);
-  static constexpr uint32_t kBufBytes = kStageF + kStageH;
-  static constexpr uint32_t kBarOffset = kRing + 2 * kBufBytes;
+  static constexpr uint32_t kBufBytes = OutStage<OUT0>::kBytes > OutStage<OUT1>::kBytes
+                                            ? OutStage<OUT0>::kBytes
+                                            : OutStage<OUT1>::kBytes;
+  static constexpr uint32_t kBarOffset = kRing + 2 * kBufBytes;  // two staging buffers
   static constexpr uint32_t kTotal = kBarOffset + 512 + 1024;
 };
 
@@ -289,15 +304,191 @@ __device__ __forceinline__ uint32_t rne24(float x) {
   return (u + 0x7Fu + ((u >> 8) & 1u)) & 0xFFFFFF00u;
 }
 
-template <int BN, bool A_MN, bool B_MN, int OUT>
+// A group of up to two slice-GEMM problems sharing r, run by one persistent launch: tiles
+// [0, total0) belong to problem 0, [total0, total) to problem 1 (the backward's g_w and g_u
+// GEMMs: one launch, one tail, and the longer-K problem scheduled first).
+struct GroupArgs {
+  int M[2], N[2], K[2];
+  int r;
+  int total0, total;
+  int nostore;
+  unsigned long long* dbg;
+};
+
+template <int BN>
+struct TileCoord {
+  int prob, p, mb, nb, num_kb;
+  __device__ __forceinline__ TileCoord(const GroupArgs& g, int tile) {
+    prob = tile >= g.total0 ? 1 : 0;
+    const int local = tile - (prob ? g.total0 : 0);
+    const int n_tiles = (g.N[prob] + BN - 1) / BN;
+    const int per_slice = ((g.M[prob] + 255) / 256) * n_tiles;
+    p = local / per_slice;
+    const int rem = local - p * per_slice;
+    mb = rem / n_tiles;
+    nb = rem - mb * n_tiles;
+    num_kb = (g.K[prob] + kBK - 1) / kBK;
+  }
+};
+
+// TMA producer for one tile (both CTAs: each loads its 128 rows of A and BN/2 columns of B).
+template <int BN, class Kd, class S>
+__device__ __forceinline__ void tc2_produce(const CUtensorMap* tmA, const CUtensorMap* tmB,
+                                            uint8_t* sA, uint8_t* sB, uint64_t* full,
+                                            uint64_t* empty, int& stage, uint32_t& phase,
+                                            const TileCoord<BN>& tc, uint32_t rank) {
+  const bool leader = rank == 0;
+  const int m0 = tc.mb * 256 + static_cast<int>(rank) * 128;
+  const int n0 = tc.nb * BN + static_cast<int>(rank) * (BN / 2);
+  for (int kb = 0; kb < tc.num_kb; ++kb) {
+    ptx::mbar_wait(&empty[stage], phase ^ 1);
+    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (S::kABytes + S::kBBytes));
+    uint8_t* a = sA + stage * S::kABytes;
+    uint8_t* b = sB + stage * S::kBBytes;
+    if constexpr (!Kd::A_MN) {
+      ptx::tma_load_3d_2sm(tmA, &full[stage], a, kb * kBK, m0, tc.p);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        ptx::tma_load_3d_2sm(tmA, &full[stage], a + j * (64 * kBK * 2), m0 + j * 64, kb * kBK,
+                             tc.p);
+    }
+    if constexpr (!Kd::B_MN) {
+      ptx::tma_load_3d_2sm(tmB, &full[stage], b, kb * kBK, n0, tc.p);
+    } else {
+#pragma unroll
+      for (int j = 0; j < BN / 128; ++j)
+        ptx::tma_load_3d_2sm(tmB, &full[stage], b + j * (64 * kBK * 2), n0 + j * 64, kb * kBK,
+                             tc.p);
+    }
+    if (!leader) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0));
+    if (++stage == S::kStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+// MMA issue for one tile (even CTA, one thread): num_kb x (kBK / 16) cta_group::2 MMAs.
+template <int BN, class Kd, class S>
+__device__ __forceinline__ void tc2_mma(uint8_t* sA, uint8_t* sB, uint64_t* full,
+                                        uint64_t* empty, int& stage, uint32_t& phase,
+                                        uint32_t d_tmem, int num_kb,
+                                        unsigned long long* dbg_full) {
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(256, BN, Kd::A_MN, Kd::B_MN);
+  for (int kb = 0; kb < num_kb; ++kb) {
+    const uint64_t t1 = dbg_full ? ptx::globaltimer_ns() : 0;
+    ptx::mbar_wait(&full[stage], phase);
+    ptx::tc_fence_after();
+    if (dbg_full) *dbg_full += ptx::globaltimer_ns() - t1;
+    const uint32_t a_addr = ptx::smem_u32(sA + stage * S::kABytes);
+    const uint32_t b_addr = ptx::smem_u32(sB + stage * S::kBBytes);
+#pragma unroll
+    for (int k = 0; k < kBK / 16; ++k) {
+      const uint64_t ad = Kd::A_MN ? ptx::smem_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
+                                   : ptx::smem_desc_sw128(a_addr + k * 32, 16, 1024);
+      const uint64_t bd = Kd::B_MN ? ptx::smem_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
+                                   : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
+      ptx::mma_bf16_ss_2sm(d_tmem, ad, bd, kIdesc, (kb | k) != 0 ? 1u : 0u);
+    }
+    ptx::mma_commit_2sm(&empty[stage]);
+    if (++stage == S::kStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+// Epilogue for one tile (4 warps per CTA): TMEM -> registers -> swizzled smem staging of the
+// CTA's 128 rows x 32 columns (each warp writes its 32 TMEM lanes) -> one TMA store per plane
+// set and chunk, issued by one thread after a 128-thread barrier (few, large TMA ops: the TMA
+// unit also feeds the mainloop). TMA clips rows >= M / cols >= N. Two staging buffers.
+template <int BN, class Kd, class S>
+__device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUtensorMap* tmC2,
+                                             uint8_t* stage_base, uint32_t tmem_acc,
+                                             int& chunk_no, const TileCoord<BN>& tc,
+                                             int row_base, int M, int N, bool nostore, int q,
+                                             int lane, bool issuer) {
+  constexpr int OUT = Kd::OUT;
+  constexpr uint32_t kSec = OutStage<OUT>::kSecOff;
+  const int r = q * 32 + lane;  // staging row = TMEM lane
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 32, ++chunk_no) {
+    uint32_t v[32];
+    __syncwarp();
+    ptx::tmem_ld_32x32b_x32(tmem_acc + c, v);
+    uint8_t* sf = stage_base + (chunk_no & 1) * S::kBufBytes;
+    ptx::tmem_ld_wait();
+    const bool active = tc.nb * BN + c < N && row_base < M && !nostore;  // CTA-uniform
+    if (active) {
+      if constexpr (OUT == kOutF24) {
+        // high 16 bits: 64 B rows, 64B-swizzled; low 8 bits: 32 B rows, 32B-swizzled
+        uint8_t* sh = sf + kSec;
+        uint32_t hw[16], lw[8];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint32_t a = rne24(__uint_as_float(v[2 * e])),
+                         b = rne24(__uint_as_float(v[2 * e + 1]));
+          hw[e] = (a >> 16) | (b & 0xFFFF0000u);
+          const uint32_t lo2 = ((a >> 8) & 0xFFu) | (b & 0xFF00u);  // two low bytes
+          if (e & 1) lw[e >> 1] |= lo2 << 16;
+          else lw[e >> 1] = lo2;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint4*>(sf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
+              make_uint4(hw[4 * j], hw[4 * j + 1], hw[4 * j + 2], hw[4 * j + 3]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          *reinterpret_cast<uint4*>(sh + r * 32 + ((j ^ ((r >> 2) & 1)) << 4)) =
+              make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(sf + r * 128 + ((j ^ (r & 7)) << 4)) =
+              make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                          __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+      }
+      if constexpr (OUT == kOutF32Bf16) {
+        uint8_t* sh = sf + kSec;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * e]),
+                                                     __uint_as_float(v[8 * j + 2 * e + 1]));
+            w[e] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          *reinterpret_cast<uint4*>(sh + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      ptx::fence_proxy_async_smem();
+    }
+    // the previous chunk's store must be done reading the other buffer (written next chunk)
+    if (issuer) ptx::bulk_wait_read<0>();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (issuer && active) {
+      ptx::tma_store_3d(tmC, sf, tc.nb * BN + c, row_base, tc.p);
+      if constexpr (OUT != kOutF32) ptx::tma_store_3d(tmC2, sf + kSec, tc.nb * BN + c, row_base, tc.p);
+      ptx::bulk_commit();
+    }
+  }
+}
+
+template <int BN, class K0, class K1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    slice_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA,
-                          const __grid_constant__ CUtensorMap tmB,
-                          const __grid_constant__ CUtensorMap tmC,
-                          const __grid_constant__ CUtensorMap tmC2, EpiArgs args) {
-  using S = Smem2<BN, OUT>;
+    slice_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA0,
+                          const __grid_constant__ CUtensorMap tmB0,
+                          const __grid_constant__ CUtensorMap tmC0,
+                          const __grid_constant__ CUtensorMap tmC20,
+                          const __grid_constant__ CUtensorMap tmA1,
+                          const __grid_constant__ CUtensorMap tmB1,
+                          const __grid_constant__ CUtensorMap tmC1,
+                          const __grid_constant__ CUtensorMap tmC21, GroupArgs args) {
+  using S = Smem2<BN, K0::OUT, K1::OUT>;
   constexpr int kSt = S::kStages;
-  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(256, BN, A_MN, B_MN);
   constexpr uint32_t kTmemCols = (2 * BN <= 256) ? 256 : 512;
 
   extern __shared__ uint8_t smem_raw[];
@@ -316,16 +507,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = ptx::cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-  const int M = args.M, N = args.N, K = args.K;
-  const int m_tiles = (M + 255) / 256;
-  const int n_tiles = (N + BN - 1) / BN;
-  const int per_slice = m_tiles * n_tiles;
-  const int total = args.r * per_slice;
-  const int num_kb = (K + kBK - 1) / kBK;
+  const int total = args.total;
 
   if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmA);
-    ptx::prefetch_tmap(&tmB);
+    ptx::prefetch_tmap(&tmA0);
+    ptx::prefetch_tmap(&tmB0);
+    if (args.total > args.total0) {
+      ptx::prefetch_tmap(&tmA1);
+      ptx::prefetch_tmap(&tmB1);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kSt; ++s) {
@@ -352,39 +542,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < total; tile += nclusters) {
-        const int p = tile / per_slice;
-        const int rem = tile - p * per_slice;
-        const int mb = rem / n_tiles;
-        const int nb = rem - mb * n_tiles;
-        const int m0 = mb * 256 + static_cast<int>(rank) * 128;
-        const int n0 = nb * BN + static_cast<int>(rank) * (BN / 2);
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (S::kABytes + S::kBBytes));
-          uint8_t* a = sA + stage * S::kABytes;
-          uint8_t* b = sB + stage * S::kBBytes;
-          if constexpr (!A_MN) {
-            ptx::tma_load_3d_2sm(&tmA, &full[stage], a, kb * kBK, m0, p);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-              ptx::tma_load_3d_2sm(&tmA, &full[stage], a + j * (64 * kBK * 2), m0 + j * 64,
-                                   kb * kBK, p);
-          }
-          if constexpr (!B_MN) {
-            ptx::tma_load_3d_2sm(&tmB, &full[stage], b, kb * kBK, n0, p);
-          } else {
-#pragma unroll
-            for (int j = 0; j < BN / 128; ++j)
-              ptx::tma_load_3d_2sm(&tmB, &full[stage], b + j * (64 * kBK * 2), n0 + j * 64,
-                                   kb * kBK, p);
-          }
-          if (!leader) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0));
-          if (++stage == kSt) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
+        const TileCoord<BN> tc(args, tile);
+        if (tc.prob == 0)
+          tc2_produce<BN, K0, S>(&tmA0, &tmB0, sA, sB, full, empty, stage, phase, tc, rank);
+        else
+          tc2_produce<BN, K1, S>(&tmA1, &tmB1, sA, sB, full, empty, stage, phase, tc, rank);
       }
     }
   } else if (warp == 1) {
@@ -393,7 +555,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      unsigned long long* dbg_full = args.dbg ? args.dbg + 2 * cluster + 1 : nullptr;
       for (int tile = cluster; tile < total; tile += nclusters, ++it) {
+        const TileCoord<BN> tc(args, tile);
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         const uint64_t t0 = args.dbg ? ptx::globaltimer_ns() : 0;
@@ -401,114 +565,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         if (args.dbg) args.dbg[2 * cluster] += ptx::globaltimer_ns() - t0;
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          const uint64_t t1 = args.dbg ? ptx::globaltimer_ns() : 0;
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          if (args.dbg) args.dbg[2 * cluster + 1] += ptx::globaltimer_ns() - t1;
-          const uint32_t a_addr = ptx::smem_u32(sA + stage * S::kABytes);
-          const uint32_t b_addr = ptx::smem_u32(sB + stage * S::kBBytes);
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t ad = A_MN ? ptx::smem_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
-                                     : ptx::smem_desc_sw128(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? ptx::smem_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
-                                     : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
-            ptx::mma_bf16_ss_2sm(d_tmem, ad, bd, kIdesc, (kb | k) != 0 ? 1u : 0u);
-          }
-          ptx::mma_commit_2sm(&empty[stage]);
-          if (++stage == kSt) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
+        if (tc.prob == 0)
+          tc2_mma<BN, K0, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb, dbg_full);
+        else
+          tc2_mma<BN, K1, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb, dbg_full);
         ptx::mma_commit_2sm(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
-    // TMEM -> registers -> swizzled smem staging of the CTA's 128 rows x 32 columns (each warp
-    // writes its 32 TMEM lanes) -> one TMA store per plane set and chunk, issued by one thread
-    // after a 128-thread barrier (few, large TMA ops: the TMA unit also feeds the mainloop).
-    // TMA clips rows >= M / cols >= N. Two staging buffers.
     const int q = warp & 3;
     const bool issuer = warp == 4 && lane == 0;
-    const int r = q * 32 + lane;  // staging row = TMEM lane
     int chunk_no = 0;
     int it = 0;
+    uint8_t* stage_base = smem + S::kRing;
     for (int tile = cluster; tile < total; tile += nclusters, ++it) {
-      const int p = tile / per_slice;
-      const int rem = tile - p * per_slice;
-      const int mb = rem / n_tiles;
-      const int nb = rem - mb * n_tiles;
+      const TileCoord<BN> tc(args, tile);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row_base = mb * 256 + static_cast<int>(rank) * 128;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32, ++chunk_no) {
-        uint32_t v[32];
-        __syncwarp();
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c,
-                                v);
-        uint8_t* sf = smem + S::kRing + (chunk_no & 1) * S::kBufBytes;
-        ptx::tmem_ld_wait();
-        const bool active = nb * BN + c < N && row_base < M && !args.nostore;  // CTA-uniform
-        if (active) {
-          if constexpr (OUT == kOutF24) {
-            // high 16 bits: 64 B rows, 64B-swizzled; low 8 bits: 32 B rows, 32B-swizzled
-            uint8_t* sh = sf + S::kStageF;
-            uint32_t hw[16], lw[8];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const uint32_t a = rne24(__uint_as_float(v[2 * e])), b = rne24(__uint_as_float(v[2 * e + 1]));
-              hw[e] = (a >> 16) | (b & 0xFFFF0000u);
-              const uint32_t lo2 = ((a >> 8) & 0xFFu) | (b & 0xFF00u);  // two low bytes
-              if (e & 1) lw[e >> 1] |= lo2 << 16;
-              else lw[e >> 1] = lo2;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              *reinterpret_cast<uint4*>(sf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
-                  make_uint4(hw[4 * j], hw[4 * j + 1], hw[4 * j + 2], hw[4 * j + 3]);
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-              *reinterpret_cast<uint4*>(sh + r * 32 + ((j ^ ((r >> 2) & 1)) << 4)) =
-                  make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              *reinterpret_cast<float4*>(sf + r * 128 + ((j ^ (r & 7)) << 4)) =
-                  make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                              __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-          }
-          if constexpr (OUT == kOutF32Bf16) {
-            uint8_t* sh = sf + S::kStageF;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint32_t w[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * e]),
-                                                         __uint_as_float(v[8 * j + 2 * e + 1]));
-                w[e] = *reinterpret_cast<uint32_t*>(&h);
-              }
-              *reinterpret_cast<uint4*>(sh + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
-                  make_uint4(w[0], w[1], w[2], w[3]);
-            }
-          }
-          ptx::fence_proxy_async_smem();
-        }
-        // the previous chunk's store must be done reading the other buffer (written next chunk)
-        if (issuer) ptx::bulk_wait_read<0>();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (issuer && active) {
-          ptx::tma_store_3d(&tmC, sf, nb * BN + c, row_base, p);
-          if constexpr (OUT != kOutF32) ptx::tma_store_3d(&tmC2, sf + S::kStageF, nb * BN + c, row_base, p);
-          ptx::bulk_commit();
-        }
-      }
+      const int row_base = tc.mb * 256 + static_cast<int>(rank) * 128;
+      const uint32_t tmem_acc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      if (tc.prob == 0)
+        tc2_epilogue<BN, K0, S>(&tmC0, &tmC20, stage_base, tmem_acc, chunk_no, tc, row_base,
+                                args.M[0], args.N[0], args.nostore, q, lane, issuer);
+      else
+        tc2_epilogue<BN, K1, S>(&tmC1, &tmC21, stage_base, tmem_acc, chunk_no, tc, row_base,
+                                args.M[1], args.N[1], args.nostore, q, lane, issuer);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
@@ -588,39 +672,69 @@ bool make_out_tmap(CUtensorMap* m, const void* base, int es, uint64_t N, uint64_
   return res == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN, int OUT>
-cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
-  CUtensorMap ta, tb, tc, tc2;
+struct Tc2Maps {
+  CUtensorMap a, b, c, c2;
+};
+
+template <int BN, class Kd>
+bool make_tc2_maps(const SliceGemmProblem& pb, Tc2Maps* m) {
   const uint64_t M = pb.M, N = pb.N, K = pb.K, r = pb.r;
-  bool ok = A_MN ? make_tmap(&ta, pb.a, M, K, r, kBK) : make_tmap(&ta, pb.a, K, M, r, 128);
-  ok = ok && (B_MN ? make_tmap(&tb, pb.b, N, K, r, kBK) : make_tmap(&tb, pb.b, K, N, r, BN / 2));
-  if (OUT == kOutF24) {
-    ok = ok && make_out_tmap(&tc, pb.c, 2, N, M, r) &&
-         make_out_tmap(&tc2, static_cast<uint8_t*>(pb.c) + 2 * r * M * N, 1, N, M, r);
+  bool ok = Kd::A_MN ? make_tmap(&m->a, pb.a, M, K, r, kBK) : make_tmap(&m->a, pb.a, K, M, r, 128);
+  ok = ok && (Kd::B_MN ? make_tmap(&m->b, pb.b, N, K, r, kBK)
+                       : make_tmap(&m->b, pb.b, K, N, r, BN / 2));
+  if (Kd::OUT == kOutF24) {
+    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r) &&
+         make_out_tmap(&m->c2, static_cast<uint8_t*>(pb.c) + 2 * r * M * N, 1, N, M, r);
   } else {
-    ok = ok && make_out_tmap(&tc, pb.c, 4, N, M, r);
-    if (OUT == kOutF32Bf16) ok = ok && make_out_tmap(&tc2, pb.c2, 2, N, M, r);
-    else tc2 = tc;
+    ok = ok && make_out_tmap(&m->c, pb.c, 4, N, M, r);
+    if (Kd::OUT == kOutF32Bf16) ok = ok && make_out_tmap(&m->c2, pb.c2, 2, N, M, r);
+    else m->c2 = m->c;
   }
+  return ok;
+}
+
+int64_t tc2_tiles(const SliceGemmProblem& pb, int BN) {
+  return static_cast<int64_t>(pb.r) * ((pb.M + 255) / 256) * ((pb.N + BN - 1) / BN);
+}
+
+// One persistent launch over np (1 or 2) problems of kinds K0, K1.
+template <int BN, class K0, class K1>
+cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
+  Tc2Maps m0, m1;
+  bool ok = make_tc2_maps<BN, K0>(pbs[0], &m0);
+  if (np > 1) ok = ok && make_tc2_maps<BN, K1>(pbs[1], &m1);
+  else m1 = m0;
   if (!ok) return cudaErrorInvalidValue;
-  auto kern = slice_gemm_tc2_kernel<BN, A_MN, B_MN, OUT>;
-  const int smem = Smem2<BN, OUT>::kTotal;
+  auto kern = slice_gemm_tc2_kernel<BN, K0, K1>;
+  const int smem = Smem2<BN, K0::OUT, K1::OUT>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int64_t tiles = r * ((M + 255) / 256) * ((N + BN - 1) / BN);
+  const int64_t t0 = tc2_tiles(pbs[0], BN);
+  const int64_t tiles = t0 + (np > 1 ? tc2_tiles(pbs[1], BN) : 0);
+  if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   const int pairs = sm_count() / 2;
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
   static const int nostore = getenv("STL_GEMM_NOSTORE") ? atoi(getenv("STL_GEMM_NOSTORE")) : 0;
-  EpiArgs ea{pb.c, 0, nostore, 0, pb.r, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
-             static_cast<__nv_bfloat16*>(pb.c2), nullptr};
+  GroupArgs ga{};
+  for (int i = 0; i < 2; ++i) {
+    const SliceGemmProblem& pb = pbs[i < np ? i : 0];
+    ga.M[i] = static_cast<int>(pb.M);
+    ga.N[i] = static_cast<int>(pb.N);
+    ga.K[i] = static_cast<int>(pb.K);
+  }
+  ga.r = pbs[0].r;
+  ga.total0 = static_cast<int>(t0);
+  ga.total = static_cast<int>(tiles);
+  ga.nostore = nostore;
   static const bool dbg_on = getenv("STL_GEMM_DEBUG") != nullptr;
   static unsigned long long* dbg = nullptr;
   if (dbg_on && !dbg) cudaMalloc(&dbg, 2 * 256 * sizeof(unsigned long long));
   if (dbg_on) {
     cudaMemsetAsync(dbg, 0, 2 * 256 * sizeof(unsigned long long), s);
-    ea.dbg = dbg;
+    ga.dbg = dbg;
   }
-  cudaError_t le = launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, ta, tb, tc, tc2, ea);
+  cudaError_t le = launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, m0.a, m0.b, m0.c, m0.c2,
+                              m1.a, m1.b, m1.c, m1.c2, ga);
   if (dbg_on) {
     unsigned long long h[512];
     const int nc = grid / 2;
@@ -628,16 +742,25 @@ cudaError_t launch_tc2(const SliceGemmProblem& pb, cudaStream_t s) {
     cudaStreamSynchronize(s);
     double te = 0, tf = 0;
     for (int i = 0; i < nc; ++i) { te += h[2 * i]; tf += h[2 * i + 1]; }
-    fprintf(stderr, "[gemm dbg] OUT=%d M=%d N=%d K=%d tiles/cluster=%.2f MMA-thread avg us: wait tempty=%.1f wait full=%.1f\n",
-            OUT, int(M), int(N), int(K), double(tiles) / nc, te / nc / 1e3, tf / nc / 1e3);
+    fprintf(stderr, "[gemm dbg] OUT=%d/%d np=%d M=%d N=%d K=%d tiles/cluster=%.2f MMA-thread avg us: wait tempty=%.1f wait full=%.1f\n",
+            K0::OUT, K1::OUT, np, ga.M[0], ga.N[0], ga.K[0], double(tiles) / nc, te / nc / 1e3,
+            tf / nc / 1e3);
   }
   return le;
 }
 
 template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch_tc2_any(const SliceGemmProblem& pb, cudaStream_t s) {
-  if (pb.c_dtype == kF24) return launch_tc2<BN, A_MN, B_MN, kOutF24>(pb, s);
-  return pb.c2 ? launch_tc2<BN, A_MN, B_MN, kOutF32Bf16>(pb, s) : launch_tc2<BN, A_MN, B_MN, kOutF32>(pb, s);
+  if (pb.c_dtype == kF24) {
+    using Kd = GemmKind<A_MN, B_MN, kOutF24>;
+    return launch_tc2_group<BN, Kd, Kd>(&pb, 1, s);
+  }
+  if (pb.c2) {
+    using Kd = GemmKind<A_MN, B_MN, kOutF32Bf16>;
+    return launch_tc2_group<BN, Kd, Kd>(&pb, 1, s);
+  }
+  using Kd = GemmKind<A_MN, B_MN, kOutF32>;
+  return launch_tc2_group<BN, Kd, Kd>(&pb, 1, s);
 }
 
 }  // namespace
@@ -693,6 +816,35 @@ bool slice_gemm_f24_supported(const SliceGemmProblem& pb) {
          (reinterpret_cast<uintptr_t>(pb.c) & 15) == 0 && getenv("STL_GEMM_1CTA") == nullptr;
 }
 
+namespace {
+// CTA-pair kernel: M > 128 and C stored with TMA (16-byte aligned rows).
+bool pair_eligible(const SliceGemmProblem& pb) {
+  return pb.M > 128 && (pb.c_dtype == kF32 || pb.c_dtype == kF24) && pb.N % 4 == 0 &&
+         (reinterpret_cast<uintptr_t>(pb.c) & 15) == 0 &&
+         (!pb.c2 || (pb.N % 8 == 0 && (reinterpret_cast<uintptr_t>(pb.c2) & 15) == 0));
+}
+}  // namespace
+
+cudaError_t slice_gemm_tc_group(const SliceGemmProblem& p0, const SliceGemmProblem& p1,
+                                cudaStream_t s) {
+  static const bool off = getenv("STL_GEMM_NOGROUP") != nullptr || getenv("STL_GEMM_1CTA");
+  if (off) return cudaErrorNotSupported;
+  const bool ok = slice_gemm_tc_supported(p0) && slice_gemm_tc_supported(p1) && p0.r == p1.r &&
+                  pair_eligible(p0) && pair_eligible(p1) && !p0.c2 && !p1.c2 &&
+                  p0.N > 128 && p1.N > 128 &&
+                  (p1.c_dtype != kF24 || slice_gemm_f24_supported(p1));
+  if (!ok) return cudaErrorNotSupported;
+  const SliceGemmProblem pbs[2] = {p0, p1};
+  // the backward's pair: g_w (A, B MN-major; fp32) with g_u (A K-major, B MN-major; F24/fp32)
+  if (p0.a_layout == 1 && p0.b_layout == 1 && p0.c_dtype == kF32 && p1.a_layout == 0 &&
+      p1.b_layout == 1) {
+    using K0 = GemmKind<true, true, kOutF32>;
+    if (p1.c_dtype == kF24) return launch_tc2_group<256, K0, GemmKind<false, true, kOutF24>>(pbs, 2, s);
+    return launch_tc2_group<256, K0, GemmKind<false, true, kOutF32>>(pbs, 2, s);
+  }
+  return cudaErrorNotSupported;
+}
+
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   const bool a_mn = pb.a_layout != 0, b_mn = pb.b_layout != 0;
   static const int force1 = [] {
@@ -702,11 +854,7 @@ cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   // The pair kernel stores C with TMA (fp32 output, 16-byte aligned rows); other cases use the
   // 1-CTA kernel's direct-store epilogue.
   if (pb.c_dtype == kF24 && !slice_gemm_f24_supported(pb)) return cudaErrorNotSupported;
-  const bool pair_ok = pb.M > 128 && !force1 && (pb.c_dtype == kF32 || pb.c_dtype == kF24) &&
-                       pb.N % 4 == 0 &&
-                       (reinterpret_cast<uintptr_t>(pb.c) & 15) == 0 &&
-                       (!pb.c2 || (pb.N % 8 == 0 && (reinterpret_cast<uintptr_t>(pb.c2) & 15) == 0));
-  if (pair_ok) {
+  if (!force1 && pair_eligible(pb)) {
     if (pb.N <= 128) {
       if (!a_mn && !b_mn) return launch_tc2_any<128, false, false>(pb, s);
       if (!a_mn && b_mn) return launch_tc2_any<128, false, true>(pb, s);
