@@ -156,6 +156,32 @@ STL_API int stl_fused_step(const float* x_prev, int64_t block_rows, int64_t bloc
                    float* out, void* mixed_ws, float* comp_ws, void* stream);
 
 /*
+ * Token-row plumbing for STL layers over (B, T, features) activations with T % t == 1 (the
+ * T2T-ViT-7 model's 197 tokens; no counterpart in the reference package,
+ * SPEC.md:8). The layer runs on Tp = T - 1 + t rows per sample (t - 1 null rows appended) and
+ * the last t output rows of each sample are folded into one with t learnable coefficients.
+ * One HBM pass each; activations bf16 row-major, features multiples of 8, 16-byte aligned.
+ *   stl_token_pad:   out (B, Tp, Cp) bf16 = x (B, T, C) of dtype_in, zero rows / columns.
+ *   stl_token_unpad: out (B, T, C) of dtype_out = g (B, Tp, Cp)[:, :T, :C].
+ *   stl_token_fold:  out (B, T, N) = y rows < T-1, row T-1 = sum_i fold[i] y[T-1+i]; + bias
+ *                    (bias: N fp32 or NULL; fold: t fp32, device pointers).
+ *   stl_token_fold_backward: g_y (B, Tp, N) from g_out (B, T, N) and y; g_bias_fold receives N
+ *                    bias gradients then t fold gradients (fixed-order sums; ws of
+ *                    stl_token_fold_ws_floats floats).
+ */
+STL_API int stl_token_pad(const void* x, int dtype_in, int64_t B, int64_t T, int64_t C, void* out,
+                          int64_t Tp, int64_t Cp, void* stream);
+STL_API int stl_token_unpad(const void* g, int64_t B, int64_t Tp, int64_t Cp, void* out,
+                            int dtype_out, int64_t T, int64_t C, void* stream);
+STL_API int stl_token_fold(const void* y, int64_t B, int64_t Tp, int64_t N, int t, const float* fold,
+                           const float* bias, void* out, int64_t T, void* stream);
+STL_API int64_t stl_token_fold_ws_floats(int64_t B, int64_t T, int64_t N, int t);
+STL_API int stl_token_fold_backward(const void* g_out, const void* y, int64_t B, int64_t Tp,
+                                    int64_t N, int t, const float* fold, int64_t T, void* g_y,
+                                    float* g_bias_fold, float* ws, int64_t ws_floats,
+                                    void* stream);
+
+/*
  * Launch profiler (no reference counterpart; B200 measurement aid). While enabled, every
  * kernel launch the library issues is bracketed by CUDA events on its own stream, so a caller
  * can attribute device time to kernels inside a timed region without a profiler attached.

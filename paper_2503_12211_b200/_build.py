@@ -19,7 +19,7 @@ LIB_NAME = "libstl_b200.so"
 LIB_PATH = PKG / LIB_NAME
 
 SOURCES = ["stl_capi.cu", "stl_slice_gemm.cu", "stl_transform.cu", "stl_transform4.cu",
-           "stl_fused_gemm.cu", "stl_transform_mma.cu", "stl_stream.cu"]
+           "stl_fused_gemm.cu", "stl_transform_mma.cu", "stl_stream.cu", "stl_tokens.cu"]
 HEADERS = ["sm100_ptx.cuh", "sm100_pair_pipeline.cuh", "stl_internal.h"]
 
 NVCC_FLAGS = [

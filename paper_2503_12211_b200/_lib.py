@@ -45,6 +45,15 @@ SIGNATURES = {
                       c_void_p, c_void_p], c_int),
     "stl_fused_step": ([c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int,
                         c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p], c_int),
+    "stl_token_pad": ([c_void_p, c_int, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64,
+                       c_void_p], c_int),
+    "stl_token_unpad": ([c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int, c_int64, c_int64,
+                         c_void_p], c_int),
+    "stl_token_fold": ([c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p,
+                        c_int64, c_void_p], c_int),
+    "stl_token_fold_ws_floats": ([c_int64, c_int64, c_int64, c_int], c_int64),
+    "stl_token_fold_backward": ([c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p,
+                                 c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p], c_int),
     "stl_profile_enable": ([c_int], c_int),
     "stl_profile_reset": ([], c_int),
     "stl_profile_count": ([], c_int),

@@ -301,14 +301,11 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
                              r, bj, bk, bi};
     stl::SliceGemmProblem pu{g_enc_ws, STL_K_MAJOR, w_enc, STL_MN_MAJOR, g_u_ws, gu_dt, dtype,
                              r, bi, bk, bj};
-    Prof prof("slice_gemm_tcgen05", s);
-    cudaError_t e = stl::slice_gemm_tc_group(pw, pu, s);
-    if (e == cudaSuccess) {
+    if (stl::slice_gemm_tc_group_supported(pw, pu)) {
+      Prof prof("slice_gemm_tcgen05", s);
+      st = check_cuda(stl::slice_gemm_tc_group(pw, pu, s), "grouped slice_gemm launch");
+      if (st) return st;
       gw_done = gu_done = true;
-    } else if (e != cudaErrorNotSupported) {
-      return check_cuda(e, "grouped slice_gemm launch");
-    } else {
-      (void)cudaGetLastError();
     }
   }
   if (g_w && !gw_done) {
@@ -334,6 +331,67 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
     if (st) return st;
   }
   return STL_OK;
+}
+
+namespace {
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+}  // namespace
+
+int stl_token_pad(const void* x, int dtype_in, int64_t B, int64_t T, int64_t C, void* out,
+                  int64_t Tp, int64_t Cp, void* stream) {
+  if (!valid_dtype(dtype_in)) return fail(STL_ERR_VALUE, "invalid dtype");
+  if (B < 0 || T < 0 || C < 0 || Tp < T || Cp < C)
+    return fail(STL_ERR_SHAPE, "pad (%lld, %lld, %lld) -> (%lld, %lld) shrinks", (long long)B,
+                (long long)T, (long long)C, (long long)Tp, (long long)Cp);
+  if (C % 8 || Cp % 8 || !al16(x) || !al16(out))
+    return fail(STL_ERR_UNSUPPORTED, "token pad needs feature counts %% 8 == 0, aligned buffers");
+  Prof prof("token_pad", as_stream(stream));
+  return check_cuda(stl::token_pad(x, dtype_in, B, T, C, out, Tp, Cp, as_stream(stream)),
+                    "token pad");
+}
+
+int stl_token_unpad(const void* g, int64_t B, int64_t Tp, int64_t Cp, void* out, int dtype_out,
+                    int64_t T, int64_t C, void* stream) {
+  if (!valid_dtype(dtype_out)) return fail(STL_ERR_VALUE, "invalid dtype");
+  if (B < 0 || T < 0 || C < 0 || Tp < T || Cp < C)
+    return fail(STL_ERR_SHAPE, "unpad target larger than the source");
+  if (C % 8 || Cp % 8 || !al16(g) || !al16(out))
+    return fail(STL_ERR_UNSUPPORTED, "token unpad needs feature counts %% 8 == 0, aligned buffers");
+  Prof prof("token_unpad", as_stream(stream));
+  return check_cuda(stl::token_unpad(g, B, Tp, Cp, out, dtype_out, T, C, as_stream(stream)),
+                    "token unpad");
+}
+
+int stl_token_fold(const void* y, int64_t B, int64_t Tp, int64_t N, int t, const float* fold,
+                   const float* bias, void* out, int64_t T, void* stream) {
+  if (B < 0 || N < 0 || T < 1 || t < 1 || t > stl::kFoldMaxT || Tp != T - 1 + t)
+    return fail(STL_ERR_SHAPE, "fold needs Tp = T - 1 + t (T=%lld, Tp=%lld, t=%d)", (long long)T,
+                (long long)Tp, t);
+  if (N % 8 || !al16(y) || !al16(out) || !al16(bias))
+    return fail(STL_ERR_UNSUPPORTED, "token fold needs N %% 8 == 0, aligned buffers");
+  Prof prof("token_fold", as_stream(stream));
+  return check_cuda(stl::token_fold(y, B, Tp, N, t, fold, bias, out, T, as_stream(stream)),
+                    "token fold");
+}
+
+int64_t stl_token_fold_ws_floats(int64_t B, int64_t T, int64_t N, int t) {
+  return stl::token_fold_ws_floats(B, T, N, t);
+}
+
+int stl_token_fold_backward(const void* g_out, const void* y, int64_t B, int64_t Tp, int64_t N,
+                            int t, const float* fold, int64_t T, void* g_y, float* g_bias_fold,
+                            float* ws, int64_t ws_floats, void* stream) {
+  if (B < 0 || N < 0 || T < 1 || t < 1 || t > stl::kFoldMaxT || Tp != T - 1 + t)
+    return fail(STL_ERR_SHAPE, "fold needs Tp = T - 1 + t (T=%lld, Tp=%lld, t=%d)", (long long)T,
+                (long long)Tp, t);
+  if (N % 8 || N > 8 * 1024 || !al16(g_out) || !al16(y) || !al16(g_y) || !al16(ws))
+    return fail(STL_ERR_UNSUPPORTED, "token fold backward needs N %% 8 == 0 (<= 8192), aligned buffers");
+  if (ws_floats < stl::token_fold_ws_floats(B, T, N, t))
+    return fail(STL_ERR_VALUE, "fold workspace too small");
+  Prof prof("token_fold_backward", as_stream(stream), 2);
+  return check_cuda(stl::token_fold_backward(g_out, y, B, Tp, N, t, fold, T, g_y, g_bias_fold, ws,
+                                             as_stream(stream)),
+                    "token fold backward");
 }
 
 int stl_fused_step(const float* x_prev, int64_t block_rows, int64_t block_k, const void* w_enc,

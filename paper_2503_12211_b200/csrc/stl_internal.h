@@ -81,6 +81,7 @@ cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s);
 bool slice_gemm_tc_supported(const SliceGemmProblem& pb);
 // Two problems with the same r in one persistent CTA-pair launch (problem 0's tiles first);
 // cudaErrorNotSupported when the pair (kinds, alignment) is not covered -> launch separately.
+bool slice_gemm_tc_group_supported(const SliceGemmProblem& p0, const SliceGemmProblem& p1);
 cudaError_t slice_gemm_tc_group(const SliceGemmProblem& p0, const SliceGemmProblem& p1,
                                 cudaStream_t s);
 // F24 output (c_dtype = kF24) is produced by the CTA-pair kernel only.
@@ -131,6 +132,21 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
 cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t s);
 cudaError_t compose_coefs(const float* a, const float* b, int r, int tt, float* out,
                           cudaStream_t s);
+
+// Token-row plumbing for T % t == 1 activations (stl_tokens.cu): pad to Tp = T - 1 + t rows
+// (bf16, zero rows/columns), its backward, the learnable fold of the last t rows (+ bias) and
+// its backward (d bias, d fold as N + t fixed-order sums). C, Cp, N multiples of 8.
+constexpr int kFoldMaxT = 8;
+cudaError_t token_pad(const void* x, int dtype_in, int64_t B, int64_t T, int64_t C, void* out,
+                      int64_t Tp, int64_t Cp, cudaStream_t s);
+cudaError_t token_unpad(const void* g, int64_t B, int64_t Tp, int64_t Cp, void* out,
+                        int dtype_out, int64_t T, int64_t C, cudaStream_t s);
+cudaError_t token_fold(const void* y, int64_t B, int64_t Tp, int64_t N, int t, const float* fold,
+                       const float* bias, void* out, int64_t T, cudaStream_t s);
+int64_t token_fold_ws_floats(int64_t B, int64_t T, int64_t N, int t);
+cudaError_t token_fold_backward(const void* gout, const void* y, int64_t B, int64_t Tp,
+                                int64_t N, int t, const float* fold, int64_t T, void* g_y,
+                                float* g_bias_fold, float* ws, cudaStream_t s);
 
 constexpr int kMaxRank = 64;          // upper bound on r handled by the transform kernels
 constexpr int kRedBlocks = 1024;      // max partial-sum blocks for the r x t^2 reductions

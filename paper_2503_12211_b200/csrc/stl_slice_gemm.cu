@@ -825,24 +825,25 @@ bool pair_eligible(const SliceGemmProblem& pb) {
 }
 }  // namespace
 
+bool slice_gemm_tc_group_supported(const SliceGemmProblem& p0, const SliceGemmProblem& p1) {
+  static const bool off = getenv("STL_GEMM_NOGROUP") != nullptr || getenv("STL_GEMM_1CTA");
+  if (off) return false;
+  // the instantiated pair: g_w (A, B MN-major; fp32) with g_u (A K-major, B MN-major; F24/fp32)
+  const bool kinds = p0.a_layout == 1 && p0.b_layout == 1 && p0.c_dtype == kF32 &&
+                     p1.a_layout == 0 && p1.b_layout == 1 &&
+                     (p1.c_dtype == kF32 || p1.c_dtype == kF24);
+  return kinds && slice_gemm_tc_supported(p0) && slice_gemm_tc_supported(p1) && p0.r == p1.r &&
+         pair_eligible(p0) && pair_eligible(p1) && !p0.c2 && !p1.c2 && p0.N > 128 &&
+         p1.N > 128 && (p1.c_dtype != kF24 || slice_gemm_f24_supported(p1));
+}
+
 cudaError_t slice_gemm_tc_group(const SliceGemmProblem& p0, const SliceGemmProblem& p1,
                                 cudaStream_t s) {
-  static const bool off = getenv("STL_GEMM_NOGROUP") != nullptr || getenv("STL_GEMM_1CTA");
-  if (off) return cudaErrorNotSupported;
-  const bool ok = slice_gemm_tc_supported(p0) && slice_gemm_tc_supported(p1) && p0.r == p1.r &&
-                  pair_eligible(p0) && pair_eligible(p1) && !p0.c2 && !p1.c2 &&
-                  p0.N > 128 && p1.N > 128 &&
-                  (p1.c_dtype != kF24 || slice_gemm_f24_supported(p1));
-  if (!ok) return cudaErrorNotSupported;
+  if (!slice_gemm_tc_group_supported(p0, p1)) return cudaErrorNotSupported;
   const SliceGemmProblem pbs[2] = {p0, p1};
-  // the backward's pair: g_w (A, B MN-major; fp32) with g_u (A K-major, B MN-major; F24/fp32)
-  if (p0.a_layout == 1 && p0.b_layout == 1 && p0.c_dtype == kF32 && p1.a_layout == 0 &&
-      p1.b_layout == 1) {
-    using K0 = GemmKind<true, true, kOutF32>;
-    if (p1.c_dtype == kF24) return launch_tc2_group<256, K0, GemmKind<false, true, kOutF24>>(pbs, 2, s);
-    return launch_tc2_group<256, K0, GemmKind<false, true, kOutF32>>(pbs, 2, s);
-  }
-  return cudaErrorNotSupported;
+  using K0 = GemmKind<true, true, kOutF32>;
+  if (p1.c_dtype == kF24) return launch_tc2_group<256, K0, GemmKind<false, true, kOutF24>>(pbs, 2, s);
+  return launch_tc2_group<256, K0, GemmKind<false, true, kOutF32>>(pbs, 2, s);
 }
 
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {

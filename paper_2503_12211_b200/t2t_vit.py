@@ -33,8 +33,9 @@ import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
+from . import _lib
 from .layer import StlLinearFunction
-from .snf_operator import encode_tiles, weights_to_planes
+from .snf_operator import _stream, encode_tiles, weights_to_planes
 from .strassen_basis import pruned_subset_init, random_gaussian_init, strassen_rank49
 
 
@@ -44,6 +45,78 @@ def make_triple(t: int, r: int, init: str, seed: int):
         full = strassen_rank49()
         return full if r == 49 else pruned_subset_init(full, r, rng)
     return random_gaussian_init(t, r, rng, scale=0.5)
+
+
+# The one-pass token plumbing kernels (TokenPad / TokenFold) are used whenever they apply;
+# False routes through the framework-op version (A/B tests).
+FUSED_TOKEN_PLUMBING = True
+
+
+def _dt(dtype: torch.dtype) -> int:
+    return _lib.STL_BF16 if dtype == torch.bfloat16 else _lib.STL_F32
+
+
+class TokenPad(torch.autograd.Function):
+    """(B, T, C) fp32/bf16 -> bf16 (B, Tp, Cp) with zero rows / columns in one pass
+    (stl_token_pad); backward = stl_token_unpad into the input's dtype."""
+
+    @staticmethod
+    def forward(ctx, x, Tp: int, Cp: int):
+        x = x.contiguous()
+        B, T, C = x.shape
+        out = torch.empty((B, Tp, Cp), dtype=torch.bfloat16, device=x.device)
+        _lib.check(_lib.load().stl_token_pad(x.data_ptr(), _dt(x.dtype), B, T, C, out.data_ptr(),
+                                             Tp, Cp, _stream(x.device)))
+        ctx.shape, ctx.dtype = (B, T, C), x.dtype
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        B, T, C = ctx.shape
+        g = g.to(torch.bfloat16).contiguous()
+        Tp, Cp = g.shape[1], g.shape[2]
+        out = torch.empty((B, T, C), dtype=ctx.dtype, device=g.device)
+        _lib.check(_lib.load().stl_token_unpad(g.data_ptr(), B, Tp, Cp, out.data_ptr(),
+                                               _dt(ctx.dtype), T, C, _stream(g.device)))
+        return out, None, None
+
+
+class TokenFold(torch.autograd.Function):
+    """(B, Tp, N) bf16 -> (B, T, N): the last t rows of each sample folded into one with the t
+    learnable coefficients, + bias, in one pass (stl_token_fold); the backward writes d y and
+    the fixed-order d bias / d fold sums in one pass plus a tree reduction."""
+
+    @staticmethod
+    def forward(ctx, y, fold, bias, T: int):
+        y = y.contiguous()
+        B, Tp, N = y.shape
+        t = fold.numel()
+        fold32 = fold.detach().float().contiguous()
+        b32 = bias.detach().float().contiguous() if bias is not None else None
+        out = torch.empty((B, T, N), dtype=torch.bfloat16, device=y.device)
+        _lib.check(_lib.load().stl_token_fold(y.data_ptr(), B, Tp, N, t, fold32.data_ptr(),
+                                              b32.data_ptr() if b32 is not None else None,
+                                              out.data_ptr(), T, _stream(y.device)))
+        ctx.save_for_backward(y, fold32)
+        ctx.T, ctx.has_bias = T, bias is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        y, fold32 = ctx.saved_tensors
+        B, Tp, N = y.shape
+        t, T = fold32.numel(), ctx.T
+        g = g.to(torch.bfloat16).contiguous()
+        lib = _lib.load()
+        gy = torch.empty_like(y)
+        ws_n = int(lib.stl_token_fold_ws_floats(B, T, N, t))
+        ws = torch.empty(ws_n, dtype=torch.float32, device=y.device)
+        sums = torch.empty(N + t, dtype=torch.float32, device=y.device)
+        _lib.check(lib.stl_token_fold_backward(g.data_ptr(), y.data_ptr(), B, Tp, N, t,
+                                               fold32.data_ptr(), T, gy.data_ptr(),
+                                               sums.data_ptr(), ws.data_ptr(), ws_n,
+                                               _stream(y.device)))
+        return gy, sums[N:], (sums[:N] if ctx.has_bias else None), None
 
 
 class StlTokenLinear(nn.Module):
@@ -75,6 +148,16 @@ class StlTokenLinear(nn.Module):
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         B, T, _ = x.shape
+        t = self.t
+        Tp = -(-T // t) * t
+        if (Tp != T and T % t == 1 and self.in_features % 8 == 0 and self.in_pad % 8 == 0
+                and self.out_features % 8 == 0 and x.is_cuda and FUSED_TOKEN_PLUMBING):
+            # one-pass plumbing kernels: pad+cast in, fold+bias out (stl_tokens.cu)
+            xp = TokenPad.apply(x, Tp, self.in_pad)
+            y = StlLinearFunction.apply(xp.reshape(B * Tp, self.in_pad),
+                                        self.w_planes.to(torch.bfloat16), self.e_x, self.d, t,
+                                        self.r)
+            return TokenFold.apply(y.reshape(B, Tp, self.out_features), self.fold, self.bias, T)
         x = x.to(torch.bfloat16)
         if self.in_pad != self.in_features:
             x = F.pad(x, (0, self.in_pad - self.in_features))

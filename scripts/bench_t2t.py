@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--r", type=int, default=24)
     ap.add_argument("--dense", action="store_true", help="dense nn.Linear baseline")
     ap.add_argument("--stl-t2t", action="store_true", help="STL in the T2T module too")
+    ap.add_argument("--no-fused-tokens", action="store_true",
+                    help="token pad/fold plumbing as framework ops (A/B)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -38,6 +40,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     torch.manual_seed(0)
+    t2t_vit.FUSED_TOKEN_PLUMBING = not args.no_fused_tokens
     model = t2t_vit.T2TViT7(stl=not args.dense, stl_t2t=args.stl_t2t and not args.dense, r=args.r,
                             device=dev)
     opt = torch.optim.AdamW(model.parameters(), lr=1e-3, weight_decay=0.05)

@@ -95,3 +95,62 @@ def test_t2t_vit7_train_step():
     losses = [float(t2t_vit.train_step(model, opt, img, labels)) for _ in range(3)]
     assert all(np.isfinite(losses)) and losses[-1] < losses[0]
     assert not torch.equal(before, model.blocks[0].fc1.w_planes.detach())
+
+
+@pytest.mark.gpu
+def test_token_kernels_match_framework_ops():
+    """stl_token_pad / unpad / fold / fold_backward against the same plumbing in torch ops."""
+    torch.manual_seed(1)
+    dev = torch.device("cuda")
+    B, T, C, N, t = 5, 197, 48, 64, 4
+    Tp = T - 1 + t
+    for dt in (torch.float32, torch.bfloat16):
+        x = torch.randn(B, T, C, device=dev, dtype=dt, requires_grad=True)
+        xp = t2t_vit.TokenPad.apply(x, Tp, 56)
+        ref = torch.nn.functional.pad(x.detach().to(torch.bfloat16), (0, 8, 0, Tp - T))
+        assert torch.equal(xp, ref)
+        g = torch.randn(B, Tp, 56, device=dev).to(torch.bfloat16)
+        xp.backward(g)
+        assert x.grad.dtype == dt and torch.equal(x.grad, g[:, :T, :C].to(dt))
+    y = torch.randn(B, Tp, N, device=dev).to(torch.bfloat16).requires_grad_(True)
+    fold = torch.randn(t, device=dev, requires_grad=True)
+    bias = torch.randn(N, device=dev, requires_grad=True)
+    out = t2t_vit.TokenFold.apply(y, fold, bias, T)
+    yr = y.detach().float().requires_grad_(True)
+    fr = fold.detach().clone().requires_grad_(True)
+    br = bias.detach().clone().requires_grad_(True)
+    last = torch.einsum("btn,t->bn", yr[:, T - 1:], fr)
+    ref = torch.cat([yr[:, :T - 1], last[:, None]], 1) + br
+    assert out.shape == (B, T, N)
+    assert ((out.float() - ref).abs() <= 1e-2 * ref.abs() + 1e-3).all()
+    go = torch.randn(B, T, N, device=dev).to(torch.bfloat16)
+    out.backward(go)
+    ref.backward(go.float())
+    assert ((y.grad.float() - yr.grad).abs() <= 1e-2 * yr.grad.abs() + 1e-3).all()
+    assert torch.allclose(fold.grad, fr.grad, rtol=1e-4, atol=1e-3)
+    assert torch.allclose(bias.grad, br.grad, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.gpu
+def test_stl_token_linear_fused_plumbing_matches_framework_ops():
+    torch.manual_seed(2)
+    lay = t2t_vit.StlTokenLinear(256, 512, t=4, r=24, seed=5)
+    with torch.no_grad():
+        lay.fold.copy_(torch.tensor([0.7, 0.2, -0.4, 0.3]))
+        lay.bias.normal_()
+    x0 = torch.randn(4, 197, 256, device="cuda")
+    gy = torch.randn(4, 197, 512, device="cuda").to(torch.bfloat16)
+    res = {}
+    for fused in (True, False):
+        t2t_vit.FUSED_TOKEN_PLUMBING = fused
+        try:
+            lay.zero_grad(set_to_none=True)
+            x = x0.clone().requires_grad_(True)
+            y = lay(x)
+            y.backward(gy)
+            res[fused] = [y.float(), x.grad, lay.fold.grad, lay.bias.grad, lay.e_x.grad,
+                          lay.d.grad, lay.w_planes.grad]
+        finally:
+            t2t_vit.FUSED_TOKEN_PLUMBING = True
+    for a, b in zip(res[True], res[False]):
+        assert ((a - b).norm() / b.norm()) < 5e-3
