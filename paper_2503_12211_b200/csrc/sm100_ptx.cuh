@@ -232,12 +232,25 @@ __device__ __forceinline__ void mma_bf16_ss_2sm(uint32_t tmem_d, uint64_t adesc,
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// Commit the pair's MMAs to the mbarrier at the same offset in both CTAs.
-__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+// Commit the pair's MMAs to the mbarrier at the same offset in the CTAs of `cta_mask`
+// (cluster ranks; default: the pair {0, 1}).
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t cta_mask = 3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(static_cast<uint16_t>(3))
+      "h"(cta_mask)
+      : "memory");
+}
+// 2-SM TMA load multicast to the CTAs of `cta_mask` (same smem offset in each); each
+// destination's transaction bytes land on the even CTA of that destination's pair.
+__device__ __forceinline__ void tma_load_3d_2sm_mc(const CUtensorMap* m, uint64_t* bar, void* dst,
+                                                   int32_t c0, int32_t c1, int32_t c2,
+                                                   uint16_t cta_mask) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2), "h"(cta_mask)
       : "memory");
 }
 

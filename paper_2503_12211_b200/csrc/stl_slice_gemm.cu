@@ -311,41 +311,57 @@ struct GroupArgs {
   int M[2], N[2], K[2];
   int r;
   int total0, total;
+  int offset0;  // problem 0's first cluster tile (a launch may cover a range of row blocks)
   int nostore;
   unsigned long long* dbg;
 };
 
-template <int BN>
+// A cluster is MC CTA pairs; its tile is MC adjacent 256 x BN tiles of one row block (the
+// pairs share the A rows, which are TMA-multicast between them when MC = 2). `pid` = the
+// pair's index in the cluster.
+template <int BN, int MC>
 struct TileCoord {
   int prob, p, mb, nb, num_kb;
-  __device__ __forceinline__ TileCoord(const GroupArgs& g, int tile) {
+  __device__ __forceinline__ TileCoord(const GroupArgs& g, int tile, int pid) {
     prob = tile >= g.total0 ? 1 : 0;
-    const int local = tile - (prob ? g.total0 : 0);
-    const int n_tiles = (g.N[prob] + BN - 1) / BN;
-    const int per_slice = ((g.M[prob] + 255) / 256) * n_tiles;
+    const int local = prob ? tile - g.total0 : tile + g.offset0;
+    const int n_sup = ((g.N[prob] + BN - 1) / BN + MC - 1) / MC;
+    const int per_slice = ((g.M[prob] + 255) / 256) * n_sup;
     p = local / per_slice;
     const int rem = local - p * per_slice;
-    mb = rem / n_tiles;
-    nb = rem - mb * n_tiles;
+    mb = rem / n_sup;
+    nb = (rem - mb * n_sup) * MC + pid;
     num_kb = (g.K[prob] + kBK - 1) / kBK;
   }
 };
 
 // TMA producer for one tile (both CTAs: each loads its 128 rows of A and BN/2 columns of B).
-template <int BN, class Kd, class S>
+template <int BN, int MC, class Kd, class S>
 __device__ __forceinline__ void tc2_produce(const CUtensorMap* tmA, const CUtensorMap* tmB,
                                             uint8_t* sA, uint8_t* sB, uint64_t* full,
                                             uint64_t* empty, int& stage, uint32_t& phase,
-                                            const TileCoord<BN>& tc, uint32_t rank) {
-  const bool leader = rank == 0;
-  const int m0 = tc.mb * 256 + static_cast<int>(rank) * 128;
-  const int n0 = tc.nb * BN + static_cast<int>(rank) * (BN / 2);
+                                            const TileCoord<BN, MC>& tc, uint32_t rank) {
+  const uint32_t prank = rank & 1u, pid = rank >> 1;
+  const bool leader = prank == 0;
+  // MC = 2: this CTA loads half of its A rows (64) and multicasts them to the same-rank CTA
+  // of the other pair, which loads the other half.
+  const uint16_t a_mask = static_cast<uint16_t>(prank ? 0xA : 0x5);
+  const int m0 = tc.mb * 256 + static_cast<int>(prank) * 128;
+  const int n0 = tc.nb * BN + static_cast<int>(prank) * (BN / 2);
   for (int kb = 0; kb < tc.num_kb; ++kb) {
     ptx::mbar_wait(&empty[stage], phase ^ 1);
     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (S::kABytes + S::kBBytes));
     uint8_t* a = sA + stage * S::kABytes;
     uint8_t* b = sB + stage * S::kBBytes;
-    if constexpr (!Kd::A_MN) {
+    if constexpr (MC == 2) {
+      const int j = static_cast<int>(pid);
+      if constexpr (!Kd::A_MN)
+        ptx::tma_load_3d_2sm_mc(tmA, &full[stage], a + j * (64 * kBK * 2), kb * kBK, m0 + j * 64,
+                                tc.p, a_mask);
+      else
+        ptx::tma_load_3d_2sm_mc(tmA, &full[stage], a + j * (64 * kBK * 2), m0 + j * 64, kb * kBK,
+                                tc.p, a_mask);
+    } else if constexpr (!Kd::A_MN) {
       ptx::tma_load_3d_2sm(tmA, &full[stage], a, kb * kBK, m0, tc.p);
     } else {
 #pragma unroll
@@ -361,7 +377,8 @@ __device__ __forceinline__ void tc2_produce(const CUtensorMap* tmA, const CUtens
         ptx::tma_load_3d_2sm(tmB, &full[stage], b + j * (64 * kBK * 2), n0 + j * 64, kb * kBK,
                              tc.p);
     }
-    if (!leader) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0));
+    if (!leader)
+      ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&full[stage]), rank & ~1u));
     if (++stage == S::kStages) {
       stage = 0;
       phase ^= 1;
@@ -370,11 +387,13 @@ __device__ __forceinline__ void tc2_produce(const CUtensorMap* tmA, const CUtens
 }
 
 // MMA issue for one tile (even CTA, one thread): num_kb x (kBK / 16) cta_group::2 MMAs.
-template <int BN, class Kd, class S>
+template <int BN, int MC, class Kd, class S>
 __device__ __forceinline__ void tc2_mma(uint8_t* sA, uint8_t* sB, uint64_t* full,
                                         uint64_t* empty, int& stage, uint32_t& phase,
                                         uint32_t d_tmem, int num_kb,
                                         unsigned long long* dbg_full) {
+  // a stage is free once every pair that reads it (all of them when A is multicast) is done
+  constexpr uint16_t kEmptyMask = MC == 2 ? 0xF : 0x3;
   constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(256, BN, Kd::A_MN, Kd::B_MN);
   for (int kb = 0; kb < num_kb; ++kb) {
     const uint64_t t1 = dbg_full ? ptx::globaltimer_ns() : 0;
@@ -391,7 +410,7 @@ __device__ __forceinline__ void tc2_mma(uint8_t* sA, uint8_t* sB, uint64_t* full
                                    : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
       ptx::mma_bf16_ss_2sm(d_tmem, ad, bd, kIdesc, (kb | k) != 0 ? 1u : 0u);
     }
-    ptx::mma_commit_2sm(&empty[stage]);
+    ptx::mma_commit_2sm(&empty[stage], kEmptyMask);
     if (++stage == S::kStages) {
       stage = 0;
       phase ^= 1;
@@ -403,10 +422,10 @@ __device__ __forceinline__ void tc2_mma(uint8_t* sA, uint8_t* sB, uint64_t* full
 // CTA's 128 rows x 32 columns (each warp writes its 32 TMEM lanes) -> one TMA store per plane
 // set and chunk, issued by one thread after a 128-thread barrier (few, large TMA ops: the TMA
 // unit also feeds the mainloop). TMA clips rows >= M / cols >= N. Two staging buffers.
-template <int BN, class Kd, class S>
+template <int BN, int MC, class Kd, class S>
 __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUtensorMap* tmC2,
                                              uint8_t* stage_base, uint32_t tmem_acc,
-                                             int& chunk_no, const TileCoord<BN>& tc,
+                                             int& chunk_no, const TileCoord<BN, MC>& tc,
                                              int row_base, int M, int N, bool nostore, int q,
                                              int lane, bool issuer) {
   constexpr int OUT = Kd::OUT;
@@ -477,8 +496,8 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
   }
 }
 
-template <int BN, class K0, class K1>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int BN, class K0, class K1, int MC>
+__global__ void __launch_bounds__(kThreads, 1)
     slice_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA0,
                           const __grid_constant__ CUtensorMap tmB0,
                           const __grid_constant__ CUtensorMap tmC0,
@@ -504,9 +523,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank();
-  const bool leader = rank == 0;
-  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const uint32_t rank = ptx::cluster_ctarank();  // 0 .. 2 MC - 1
+  const uint32_t prank = rank & 1u, pid = rank >> 1;
+  const bool leader = prank == 0;
+  const int cluster = blockIdx.x / (2 * MC), nclusters = gridDim.x / (2 * MC);
   const int total = args.total;
 
   if (warp == 0 && lane == 0) {
@@ -520,7 +540,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kSt; ++s) {
       ptx::mbar_init(&full[s], 2);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], MC);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
@@ -542,11 +562,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < total; tile += nclusters) {
-        const TileCoord<BN> tc(args, tile);
+        const TileCoord<BN, MC> tc(args, tile, pid);
         if (tc.prob == 0)
-          tc2_produce<BN, K0, S>(&tmA0, &tmB0, sA, sB, full, empty, stage, phase, tc, rank);
+          tc2_produce<BN, MC, K0, S>(&tmA0, &tmB0, sA, sB, full, empty, stage, phase, tc, rank);
         else
-          tc2_produce<BN, K1, S>(&tmA1, &tmB1, sA, sB, full, empty, stage, phase, tc, rank);
+          tc2_produce<BN, MC, K1, S>(&tmA1, &tmB1, sA, sB, full, empty, stage, phase, tc, rank);
       }
     }
   } else if (warp == 1) {
@@ -555,21 +575,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      unsigned long long* dbg_full = args.dbg ? args.dbg + 2 * cluster + 1 : nullptr;
+      const int dbg_slot = 2 * (cluster * MC + static_cast<int>(pid));
+      unsigned long long* dbg_full = args.dbg ? args.dbg + dbg_slot + 1 : nullptr;
       for (int tile = cluster; tile < total; tile += nclusters, ++it) {
-        const TileCoord<BN> tc(args, tile);
+        const TileCoord<BN, MC> tc(args, tile, pid);
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         const uint64_t t0 = args.dbg ? ptx::globaltimer_ns() : 0;
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        if (args.dbg) args.dbg[2 * cluster] += ptx::globaltimer_ns() - t0;
+        if (args.dbg) args.dbg[dbg_slot] += ptx::globaltimer_ns() - t0;
         const uint32_t d_tmem = tmem_base + acc * BN;
         if (tc.prob == 0)
-          tc2_mma<BN, K0, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb, dbg_full);
+          tc2_mma<BN, MC, K0, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb, dbg_full);
         else
-          tc2_mma<BN, K1, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb, dbg_full);
-        ptx::mma_commit_2sm(&tfull[acc]);
+          tc2_mma<BN, MC, K1, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb, dbg_full);
+        ptx::mma_commit_2sm(&tfull[acc], static_cast<uint16_t>(0x3u << (2 * pid)));
       }
     }
   } else if (warp >= 4) {
@@ -580,22 +601,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int it = 0;
     uint8_t* stage_base = smem + S::kRing;
     for (int tile = cluster; tile < total; tile += nclusters, ++it) {
-      const TileCoord<BN> tc(args, tile);
+      const TileCoord<BN, MC> tc(args, tile, pid);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row_base = tc.mb * 256 + static_cast<int>(rank) * 128;
+      const int row_base = tc.mb * 256 + static_cast<int>(prank) * 128;
       const uint32_t tmem_acc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       if (tc.prob == 0)
-        tc2_epilogue<BN, K0, S>(&tmC0, &tmC20, stage_base, tmem_acc, chunk_no, tc, row_base,
+        tc2_epilogue<BN, MC, K0, S>(&tmC0, &tmC20, stage_base, tmem_acc, chunk_no, tc, row_base,
                                 args.M[0], args.N[0], args.nostore, q, lane, issuer);
       else
-        tc2_epilogue<BN, K1, S>(&tmC1, &tmC21, stage_base, tmem_acc, chunk_no, tc, row_base,
+        tc2_epilogue<BN, MC, K1, S>(&tmC1, &tmC21, stage_base, tmem_acc, chunk_no, tc, row_base,
                                 args.M[1], args.N[1], args.nostore, q, lane, issuer);
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+      if (lane == 0)
+        ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), rank & ~1u));
     }
     if (issuer) ptx::bulk_wait_all();
   }
@@ -676,10 +698,12 @@ struct Tc2Maps {
   CUtensorMap a, b, c, c2;
 };
 
-template <int BN, class Kd>
+template <int BN, int MC, class Kd>
 bool make_tc2_maps(const SliceGemmProblem& pb, Tc2Maps* m) {
   const uint64_t M = pb.M, N = pb.N, K = pb.K, r = pb.r;
-  bool ok = Kd::A_MN ? make_tmap(&m->a, pb.a, M, K, r, kBK) : make_tmap(&m->a, pb.a, K, M, r, 128);
+  // K-major A: one 128-row box per CTA, or (MC = 2) a 64-row half multicast to both pairs
+  bool ok = Kd::A_MN ? make_tmap(&m->a, pb.a, M, K, r, kBK)
+                     : make_tmap(&m->a, pb.a, K, M, r, MC == 2 ? 64 : 128);
   ok = ok && (Kd::B_MN ? make_tmap(&m->b, pb.b, N, K, r, kBK)
                        : make_tmap(&m->b, pb.b, K, N, r, BN / 2));
   if (Kd::OUT == kOutF24) {
@@ -693,27 +717,62 @@ bool make_tc2_maps(const SliceGemmProblem& pb, Tc2Maps* m) {
   return ok;
 }
 
-int64_t tc2_tiles(const SliceGemmProblem& pb, int BN) {
-  return static_cast<int64_t>(pb.r) * ((pb.M + 255) / 256) * ((pb.N + BN - 1) / BN);
+// cluster tiles: MC adjacent 256 x BN tiles per cluster
+int64_t tc2_tiles(const SliceGemmProblem& pb, int BN, int MC) {
+  return static_cast<int64_t>(pb.r) * ((pb.M + 255) / 256) * (((pb.N + BN - 1) / BN + MC - 1) / MC);
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
 // One persistent launch over np (1 or 2) problems of kinds K0, K1.
-template <int BN, class K0, class K1>
-cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
+// Problem 0 may be restricted to the row-block units [ub, ue) (unit = one (slice, 256-row
+// block) of all its column tiles; ue < 0: all); `cap` limits the clusters (0: all co-resident).
+template <int BN, class K0, class K1, int MC>
+cudaError_t launch_tc2_group_mc(const SliceGemmProblem* pbs, int np, cudaStream_t s, int ub = 0,
+                                int ue = -1, int cap = 0) {
   Tc2Maps m0, m1;
-  bool ok = make_tc2_maps<BN, K0>(pbs[0], &m0);
-  if (np > 1) ok = ok && make_tc2_maps<BN, K1>(pbs[1], &m1);
+  bool ok = make_tc2_maps<BN, MC, K0>(pbs[0], &m0);
+  if (np > 1) ok = ok && make_tc2_maps<BN, MC, K1>(pbs[1], &m1);
   else m1 = m0;
   if (!ok) return cudaErrorInvalidValue;
-  auto kern = slice_gemm_tc2_kernel<BN, K0, K1>;
+  auto kern = slice_gemm_tc2_kernel<BN, K0, K1, MC>;
   const int smem = Smem2<BN, K0::OUT, K1::OUT>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int64_t t0 = tc2_tiles(pbs[0], BN);
-  const int64_t tiles = t0 + (np > 1 ? tc2_tiles(pbs[1], BN) : 0);
+  const int64_t n_sup0 = ((pbs[0].N + BN - 1) / BN + MC - 1) / MC;
+  const int64_t t0 = ue < 0 ? tc2_tiles(pbs[0], BN, MC) : (ue - ub) * n_sup0;
+  const int64_t tiles = t0 + (np > 1 ? tc2_tiles(pbs[1], BN, MC) : 0);
+  if (tiles <= 0) return cudaSuccess;
   if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-  const int pairs = sm_count() / 2;
-  const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * MC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  // persistent: as many clusters as can be co-resident (2 MC-CTA clusters need whole TPC groups)
+  static int max_clusters[3] = {0, 0, 0};
+  if (!max_clusters[MC]) {
+    cfg.gridDim = dim3(2 * MC * (sm_count() / (2 * MC)));
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0)
+      n = sm_count() / (2 * MC);
+    max_clusters[MC] = n;
+  }
+  int clusters = static_cast<int>(tiles < max_clusters[MC] ? tiles : max_clusters[MC]);
+  if (cap > 0 && clusters > cap) clusters = cap;
+  const int grid = 2 * MC * clusters;
+  cfg.gridDim = dim3(grid);
   static const int nostore = getenv("STL_GEMM_NOSTORE") ? atoi(getenv("STL_GEMM_NOSTORE")) : 0;
   GroupArgs ga{};
   for (int i = 0; i < 2; ++i) {
@@ -725,6 +784,7 @@ cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s
   ga.r = pbs[0].r;
   ga.total0 = static_cast<int>(t0);
   ga.total = static_cast<int>(tiles);
+  ga.offset0 = static_cast<int>(ub * n_sup0);
   ga.nostore = nostore;
   static const bool dbg_on = getenv("STL_GEMM_DEBUG") != nullptr;
   static unsigned long long* dbg = nullptr;
@@ -733,20 +793,31 @@ cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s
     cudaMemsetAsync(dbg, 0, 2 * 256 * sizeof(unsigned long long), s);
     ga.dbg = dbg;
   }
-  cudaError_t le = launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, m0.a, m0.b, m0.c, m0.c2,
-                              m1.a, m1.b, m1.c, m1.c2, ga);
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, m0.a, m0.b, m0.c, m0.c2, m1.a, m1.b, m1.c,
+                                      m1.c2, ga);
   if (dbg_on) {
     unsigned long long h[512];
-    const int nc = grid / 2;
+    const int nc = clusters * MC;
     cudaMemcpyAsync(h, dbg, sizeof(unsigned long long) * 2 * nc, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     double te = 0, tf = 0;
     for (int i = 0; i < nc; ++i) { te += h[2 * i]; tf += h[2 * i + 1]; }
-    fprintf(stderr, "[gemm dbg] OUT=%d/%d np=%d M=%d N=%d K=%d tiles/cluster=%.2f MMA-thread avg us: wait tempty=%.1f wait full=%.1f\n",
-            K0::OUT, K1::OUT, np, ga.M[0], ga.N[0], ga.K[0], double(tiles) / nc, te / nc / 1e3,
-            tf / nc / 1e3);
+    fprintf(stderr, "[gemm dbg] MC=%d clusters=%d OUT=%d/%d np=%d M=%d N=%d K=%d tiles/cluster=%.2f MMA-thread avg us: wait tempty=%.1f wait full=%.1f\n",
+            MC, clusters, K0::OUT, K1::OUT, np, ga.M[0], ga.N[0], ga.K[0], double(tiles) / nc,
+            te / nc / 1e3, tf / nc / 1e3);
   }
   return le;
+}
+
+// STL_GEMM_MC = 2 (opt-in): four-CTA clusters, two pairs sharing A by TMA multicast. Measured:
+// ~8% more work per SM, but only 33 such clusters are co-resident (clusters live inside a GPC:
+// 132 of 148 SMs), net -3%; running a pair-cluster launch beside it on the 16 left-over SMs
+// (second stream) gained nothing either. Default: pair clusters on all 148 SMs.
+template <int BN, class K0, class K1>
+cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
+  static const int mc = env_int("STL_GEMM_MC", 1);
+  if (mc == 2) return launch_tc2_group_mc<BN, K0, K1, 2>(pbs, np, s);
+  return launch_tc2_group_mc<BN, K0, K1, 1>(pbs, np, s);
 }
 
 template <int BN, bool A_MN, bool B_MN>

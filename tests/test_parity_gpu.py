@@ -452,3 +452,21 @@ def test_mma_transforms_match_ffma(M, K, N, r):
             a, b = outs[mode][i], outs[2 | 8 | 16][i]
             assert rel(a, b) <= 2e-3, (name, mode, rel(a, b))
             assert rel(a, refs[i]) <= BF16_TOL, (name, mode, rel(a, refs[i]))
+
+
+@pytest.mark.gpu
+def test_multicast_cluster_gemm_matches_bmm():
+    """The opt-in four-CTA (two pairs, A multicast) GEMM schedule against torch.bmm."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, STL_GEMM_MC="2")
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "gemm_check.py")],
+                         env=env, capture_output=True, text=True, timeout=300, check=True).stdout
+    rows = [json.loads(line) for line in out.splitlines() if line.startswith("{")]
+    assert len(rows) == 3
+    for row in rows:
+        assert not row["nan"] and row["rel_err"] < 1e-5, row
