@@ -21,7 +21,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -52,67 +51,84 @@ def load_peaks():
 
 
 # ----------------------------------------------------------------------------- clocks
+_SAMPLER_SRC = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+bus, path = sys.argv[1], sys.argv[2]
+try:
+    h = nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+except Exception:
+    h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[3]))
+fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+    getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+with open(path, "w") as f:
+    print(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM), flush=True)
+    while True:
+        f.write(f"{time.time():.6f} {nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)} {fn(h)}\n")
+        f.flush()
+        time.sleep(0.002)
+"""
+
+
 class ClockSampler:
-    """Polls NVML (SM clock, max clock, event reasons) every 2 ms in a thread."""
+    """Polls NVML (SM clock, event reasons) every 2 ms in a CHILD process — a thread of this
+    process would be starved by the launch loop holding the GIL — and keeps the samples taken
+    between start() and stop()."""
 
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device_index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        self._thr = None
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = self._handle(device_index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
-            self.nv = None
+        import subprocess
+        import tempfile
 
-    def _handle(self, idx):
         import torch
-        nv = self.nv
+        self.max_mhz, self.proc = None, None
+        self.path = tempfile.mktemp(prefix="stl_clocks_", suffix=".txt")
         try:
-            props = torch.cuda.get_device_properties(idx)
+            props = torch.cuda.get_device_properties(device_index)
             bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
-            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
-        except Exception:  # noqa: BLE001
-            return nv.nvmlDeviceGetHandleByIndex(idx)
-
-    def _reasons(self):
-        nv = self.nv
-        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
-        return fn(self.h)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                mask = self._reasons()
-                for bit, name in self.REASONS.items():
-                    if mask & bit:
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001
-                pass
-            time.sleep(0.002)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, bus, self.path,
+                                          str(device_index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            line = self.proc.stdout.readline()  # max clock: the sampler is running
+            self.max_mhz = int(line) if line.strip() else None
+            if self.max_mhz is None:
+                self.proc.kill()
+                self.proc = None
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self.proc = None
+        self.t0 = self.t1 = None
 
     def start(self):
-        if self.nv is not None:
-            self._thr = threading.Thread(target=self._run, daemon=True)
-            self._thr.start()
+        self.t0 = time.time()
 
     def stop(self):
-        if self._thr is not None:
-            self._stop.set()
-            self._thr.join()
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+        self.t1 = time.time()
+        samples, reasons = [], set()
+        if self.proc is not None:
+            time.sleep(0.005)
+            self.proc.kill()
+            self.proc.wait()
+            try:
+                with open(self.path) as f:
+                    for line in f:
+                        parts = line.split()
+                        if len(parts) != 3 or not (self.t0 <= float(parts[0]) <= self.t1):
+                            continue
+                        samples.append(int(parts[1]))
+                        for bit, name in self.REASONS.items():
+                            if int(parts[2]) & bit:
+                                reasons.add(name)
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
                     "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(samples)}
 
 
 # ----------------------------------------------------------------------------- CPU baseline
