@@ -105,8 +105,10 @@ STL_API int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_lay
  *                mode, see stl_cache_bytes);
  *   scratch: device workspace of at least stl_forward_scratch_bytes(...) bytes.
  *   M, K, N must be multiples of t (ShapeError otherwise, as the reference).
- * Default path: encode -> slice GEMM -> decode with fp32 slice products in `scratch`; with
- * stl_set_fusion bit 0, bf16 t = 4 runs the decode-fused tcgen05 kernel instead.
+ * Default path: encode -> slice GEMM -> decode with the slice products in `scratch` (fp32; on
+ * the bf16 t = 4 path bf16 planes when y_enc_cache is NULL — they only feed the decode — and
+ * F24 when the cache is kept); with stl_set_fusion bit 0, bf16 t = 4 runs the decode-fused
+ * tcgen05 kernel instead.
  */
 STL_API int64_t stl_forward_scratch_bytes(int64_t M, int64_t K, int64_t N, int t, int r,
                                           int dtype);
@@ -123,7 +125,8 @@ STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const
  * it is slower than encode + GEMM + decode today);
  * bit 1 = force the FFMA tile transforms instead of the tensor-core (mma.sync) ones;
  * bit 2 = also use the tensor-core decode (experimental); bit 3 = disable the streaming
- * (TMA-pipelined) transforms; bit 4 = keep fp32 slice products instead of F24. */
+ * (TMA-pipelined) transforms; bit 4 = keep fp32 slice products instead of F24; bit 5 = a
+ * cache-less bf16 forward keeps F24 slice products instead of bf16 ones. */
 STL_API int stl_set_fusion(int enabled);
 
 /*

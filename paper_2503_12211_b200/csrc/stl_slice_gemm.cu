@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Output modes of the pair kernel: fp32 C; fp32 C plus a bf16 copy (c2); or F24 — fp32 rounded
 // to 24 bits and stored as a 16-bit high plane set (c) followed by an 8-bit low plane set
 // (c + 2 * r * M * N bytes), 3 bytes per element at ~2^-16 relative precision.
-enum OutMode { kOutF32 = 0, kOutF32Bf16 = 1, kOutF24 = 2 };
+enum OutMode { kOutF32 = 0, kOutF32Bf16 = 1, kOutF24 = 2, kOutBf16 = 3 };
 
 // Per-problem compile-time traits of the pair kernel: operand majorness and output mode.
 template <bool A_MN_, bool B_MN_, int OUT_>
@@ -278,7 +278,8 @@ struct GemmKind {
 // or F24 low 32 B rows).
 template <int OUT>
 struct OutStage {
-  static constexpr uint32_t kSecOff = OUT == kOutF24 ? 128 * 64 : 128 * 128;
+  static constexpr uint32_t kSecOff =
+      OUT == kOutF24 ? 128 * 64 : (OUT == kOutBf16 ? 128 * 64 : 128 * 128);
   static constexpr uint32_t kBytes =
       kSecOff + (OUT == kOutF32Bf16 ? 128 * 64 : (OUT == kOutF24 ? 128 * 32 : 0));
 };
@@ -461,6 +462,20 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
         for (int j = 0; j < 2; ++j)
           *reinterpret_cast<uint4*>(sh + r * 32 + ((j ^ ((r >> 2) & 1)) << 4)) =
               make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
+      } else if constexpr (OUT == kOutBf16) {
+        // bf16 only: 64 B rows, 64B-swizzled
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * e]),
+                                                     __uint_as_float(v[8 * j + 2 * e + 1]));
+            w[e] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          *reinterpret_cast<uint4*>(sf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -490,7 +505,8 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (issuer && active) {
       ptx::tma_store_3d(tmC, sf, tc.nb * BN + c, row_base, tc.p);
-      if constexpr (OUT != kOutF32) ptx::tma_store_3d(tmC2, sf + kSec, tc.nb * BN + c, row_base, tc.p);
+      if constexpr (OUT == kOutF32Bf16 || OUT == kOutF24)
+        ptx::tma_store_3d(tmC2, sf + kSec, tc.nb * BN + c, row_base, tc.p);
       ptx::bulk_commit();
     }
   }
@@ -706,7 +722,10 @@ bool make_tc2_maps(const SliceGemmProblem& pb, Tc2Maps* m) {
                      : make_tmap(&m->a, pb.a, K, M, r, MC == 2 ? 64 : 128);
   ok = ok && (Kd::B_MN ? make_tmap(&m->b, pb.b, N, K, r, kBK)
                        : make_tmap(&m->b, pb.b, K, N, r, BN / 2));
-  if (Kd::OUT == kOutF24) {
+  if (Kd::OUT == kOutBf16) {
+    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r);
+    m->c2 = m->c;
+  } else if (Kd::OUT == kOutF24) {
     ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r) &&
          make_out_tmap(&m->c2, static_cast<uint8_t*>(pb.c) + 2 * r * M * N, 1, N, M, r);
   } else {
@@ -822,6 +841,10 @@ cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s
 
 template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch_tc2_any(const SliceGemmProblem& pb, cudaStream_t s) {
+  if (pb.c_dtype == kBF16) {
+    using Kd = GemmKind<A_MN, B_MN, kOutBf16>;
+    return launch_tc2_group<BN, Kd, Kd>(&pb, 1, s);
+  }
   if (pb.c_dtype == kF24) {
     using Kd = GemmKind<A_MN, B_MN, kOutF24>;
     return launch_tc2_group<BN, Kd, Kd>(&pb, 1, s);
@@ -890,7 +913,7 @@ bool slice_gemm_f24_supported(const SliceGemmProblem& pb) {
 namespace {
 // CTA-pair kernel: M > 128 and C stored with TMA (16-byte aligned rows).
 bool pair_eligible(const SliceGemmProblem& pb) {
-  return pb.M > 128 && (pb.c_dtype == kF32 || pb.c_dtype == kF24) && pb.N % 4 == 0 &&
+  return pb.M > 128 && pb.N % 4 == 0 && (pb.c_dtype != kBF16 || (pb.N % 8 == 0 && !pb.c2)) &&
          (reinterpret_cast<uintptr_t>(pb.c) & 15) == 0 &&
          (!pb.c2 || (pb.N % 8 == 0 && (reinterpret_cast<uintptr_t>(pb.c2) & 15) == 0));
 }

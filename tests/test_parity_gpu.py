@@ -400,7 +400,7 @@ def test_fused_decode_matches_unfused_and_oracle(M, K, N, r):
     w_dev, w64 = bf16_round(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
     layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
     try:
-        stl.set_fusion(False)
+        _lib.load().stl_set_fusion(32)  # unfused with fp32-class (F24 / fp32) slice products
         y_u = stl.stl_layer_forward(layer, x_dev)
         stl.set_fusion(True)  # the decode-fused kernel serves cache-free forwards
         y_f = stl.stl_layer_forward(layer, x_dev)
@@ -470,3 +470,29 @@ def test_multicast_cluster_gemm_matches_bmm():
     assert len(rows) == 3
     for row in rows:
         assert not row["nan"] and row["rel_err"] < 1e-5, row
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [0, 32])
+def test_inference_forward_product_formats(bits):
+    """Cache-less bf16 forward with bf16 slice products (default) and with F24 ones (bit 5),
+    both against the float64 restatement on the same bf16 inputs (bar 1e-2)."""
+    from paper_2503_12211_b200.snf_operator import _forward
+
+    dev = torch.device("cuda")
+    M, K, N, t, r = 1024, 768, 1536, 4, 24
+    snf = stl.random_gaussian_init(t, r, stl.make_rng(3), scale=0.5).to(dev)
+    g = torch.Generator(device=dev).manual_seed(3)
+    x = torch.randn((M, K), device=dev, generator=g).to(torch.bfloat16)
+    w0 = torch.randn((K, N), device=dev, generator=g) / K ** 0.5
+    w = stl.weights_to_planes(stl.encode_tiles(w0, snf.e_w, t).float(), dtype=torch.bfloat16)
+    xt = x.double().reshape(M // t, t, K // t, t).permute(0, 2, 1, 3).reshape(M // t, K // t, t * t)
+    prod = torch.einsum("ikp,pjk->ijp", xt @ snf.e_x.double().T, w.double())
+    yref = (prod @ snf.d.double()).reshape(M // t, N // t, t, t).permute(0, 2, 1, 3).reshape(M, N)
+    try:
+        _lib.load().stl_set_fusion(bits)
+        y = _forward(x, w, snf)
+    finally:
+        _lib.load().stl_set_fusion(0)
+    err = float((y.double() - yref).norm() / yref.norm())
+    assert err < 1e-2 and err < (4e-3 if bits == 0 else 3.5e-3), err
