@@ -318,7 +318,8 @@ def main() -> None:
         k["ms"] += ms
         k["calls"] += 1
         launches += n
-    p_bytes = 3 if int(lib.stl_cache_bytes(M, K, N, T, R, _lib.STL_BF16)) == 3 * R * bi * bj else 4
+    # bytes per stored slice product: the cache format (bf16 = 2, F24 = 3) on the bf16 path
+    p_bytes = int(lib.stl_cache_bytes(M, K, N, T, R, _lib.STL_BF16)) // (R * bi * bj)
     cost = stl.LayerCost(M, K, N, T, R, 2, p_bytes)
     gem = kern.get("slice_gemm_tcgen05", {"ms": float("nan"), "calls": 1})
     # the step's three slice-GEMMs (y_enc forward; g_w and g_u backward, one grouped launch when

@@ -151,23 +151,33 @@ int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_layout, voi
 
 namespace {
 bool g_fusion = false;  // decode-fused forward is opt-in until it beats the unfused path
-bool g_f24 = true;      // F24 slice products on the bf16 t = 4 path (stl_set_fusion bit 4 clears)
-// A cache-less (inference) bf16 forward writes its slice products as bf16 planes: they only
-// feed the decode, whose bf16 output rounding is of the same size (measured rel. error at
-// 8192^3: 2.9e-3 vs 2.4e-3 with F24, bar 1e-2; 7% faster). stl_set_fusion bit 5 keeps F24.
-bool g_bf16_infer = true;
+// Storage format of the fp32 slice products (forward y_enc / cache, backward g_u) on the bf16
+// t = 4 path, r <= 32: bf16 planes by default (2 B/element; they feed bf16-output decodes and
+// r x t^2 reductions over millions of tiles: measured rel. error of y at 8192^3 2.9e-3 vs
+// 2.4e-3 with F24, bar 1e-2); stl_set_fusion bit 5 = F24 (3 B), bit 4 = fp32 products with a
+// bf16 cache copy (the only format at r > 32: at r = 49, Strassen x Strassen, bf16 products
+// reach 9.6e-3 of the 1e-2 bar).
+enum ProdMode { kProdBf16 = 0, kProdF24 = 1, kProdF32 = 2 };
+int g_prod_mode = kProdBf16;
 
 bool fused_forward_shape(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
   if (!g_fusion || t != 4 || dtype != STL_BF16) return false;
   return stl::fused_decode_supported(t, r, M / t, N / t, K / t, dtype, nullptr, nullptr, 0);
 }
 
-// Slice products C (rows x cols tiles, contraction kt) in F24: the CTA-pair GEMM writes them and
-// the streaming transforms read them. A pure function of the shape, so the forward (writing the
-// y_enc cache) and the backward (reading it) agree on the cache format.
+// Format of the slice products C (rows x cols tiles, contraction kt): STL_BF16 / kF24 written
+// by the CTA-pair GEMM and read by the streaming transforms, or -1 = fp32 products (+ a cache
+// copy in the compute dtype). A pure function of the shape (and the mode), so the forward
+// (writing the y_enc cache) and the backward (reading it) agree on the cache format.
+int product_format(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype) {
+  if (g_prod_mode == kProdF32 || dtype != STL_BF16 || t != 4 || r > 32 || rows <= 128 ||
+      kt % 8)
+    return -1;
+  if (g_prod_mode == kProdF24) return cols % 128 == 0 ? stl::kF24 : -1;
+  return cols % 64 == 0 ? STL_BF16 : -1;
+}
 bool f24_products(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype) {
-  return g_f24 && dtype == STL_BF16 && t == 4 && r <= 32 && rows > 128 && cols % 128 == 0 &&
-         kt % 8 == 0;
+  return product_format(rows, cols, kt, t, r, dtype) == stl::kF24;
 }
 }  // namespace
 
@@ -183,8 +193,7 @@ int stl_set_fusion(int enabled) {
   stl::set_transform_mma((enabled & 2) == 0);         // bit 1 = force the FFMA transforms
   stl::set_transform_mma_decode((enabled & 4) != 0);  // bit 2 = mma decode (experimental)
   stl::set_transform_stream((enabled & 8) == 0);      // bit 3 = disable the streaming transforms
-  g_f24 = (enabled & 16) == 0;                        // bit 4 = fp32 slice products (no F24)
-  g_bf16_infer = (enabled & 32) == 0;                 // bit 5 = no bf16 products (inference)
+  g_prod_mode = (enabled & 16) ? kProdF32 : ((enabled & 32) ? kProdF24 : kProdBf16);
   return STL_OK;
 }
 
@@ -231,29 +240,18 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
                                              ld_y, dtype, nullptr, dtype, scratch, s),
                       "fused forward");
   }
-  // (same shapes as the F24 format, r <= 32: at r = 49 (Strassen x Strassen) the products'
-  // cancellation makes bf16 rounding reach 9.6e-3 of the 1e-2 bar, so fp32 products stay)
-  if (g_bf16_infer && !y_enc_cache && f24_products(bi, bj, bk, t, r, dtype)) {
-    // inference: the products only feed the decode -> bf16 planes (2 bytes per element)
-    if (scratch_bytes < 2 * static_cast<int64_t>(r) * bi * bj)
-      return fail(STL_ERR_VALUE, "scratch too small: %lld bytes", (long long)scratch_bytes);
-    st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, scratch, STL_BF16, dtype, r, bi, bj,
-                  bk, s);
-    if (st) return st;
-    Prof prof("decode_y", s);
-    return check_cuda(stl::planes_to_tiles(scratch, STL_BF16, r, bi, bj, t, d, y, dtype, ld_y,
-                                           nullptr, STL_F32, 0, nullptr, nullptr, s),
-                      "forward decode");
-  }
-  if (f24_products(bi, bj, bk, t, r, dtype)) {
-    // slice products in F24 straight into the cache (or scratch), decoded from there
+  const int pfmt = product_format(bi, bj, bk, t, r, dtype);
+  if (pfmt >= 0) {
+    // slice products (bf16 or F24) straight into the cache (or scratch), decoded from there
     void* prod = y_enc_cache ? y_enc_cache : scratch;
-    if (!y_enc_cache && scratch_bytes < 3 * static_cast<int64_t>(r) * bi * bj)
-      return fail(STL_ERR_VALUE, "scratch too small: %lld bytes", (long long)scratch_bytes);
-    st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, prod, stl::kF24, dtype, r, bi, bj, bk, s);
+    const int64_t need = static_cast<int64_t>(stl::dtype_size(pfmt)) * r * bi * bj;
+    if (!y_enc_cache && scratch_bytes < need)
+      return fail(STL_ERR_VALUE, "scratch too small: %lld < %lld bytes", (long long)scratch_bytes,
+                  (long long)need);
+    st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, prod, pfmt, dtype, r, bi, bj, bk, s);
     if (st) return st;
     Prof prof("decode_y", s);
-    return check_cuda(stl::planes_to_tiles(prod, stl::kF24, r, bi, bj, t, d, y, dtype, ld_y, nullptr,
+    return check_cuda(stl::planes_to_tiles(prod, pfmt, r, bi, bj, t, d, y, dtype, ld_y, nullptr,
                                            STL_F32, 0, nullptr, nullptr, s),
                       "forward decode");
   }
@@ -303,16 +301,17 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
   int st;
   {
     Prof prof(g_d ? "encode_gy+g_d" : "encode_gy", s, g_d ? 2 : 1);
-    const int cache_dt = f24_products(bi, bj, bk, t, r, dtype) ? stl::kF24 : dtype;
+    const int cache_dt = f24_products(bi, bj, bk, t, r, dtype) ? stl::kF24 : dtype;  // else bf16
     st = check_cuda(stl::tiles_to_planes(gy, dtype, ld_gy, bi, bj, t, d, r, g_enc_ws, dtype,
                                            g_d ? y_enc : nullptr, cache_dt, g_d, red_ws, s),
                       "backward encode(gy)");
   }
   if (st) return st;
   // g_w^T_p (N/t x K/t) = g_enc_p^T (N/t x M/t) . u_p (M/t x K/t): both operands MN-major.
-  // g_u_p (M/t x K/t) = g_enc_p (M/t x N/t) . W_p (N/t x K/t): B is N-major. F24 on the bf16
-  // path (3 of the 4 bytes of g_u_ws used).
-  const int gu_dt = f24_products(bi, bk, bj, t, r, dtype) ? stl::kF24 : STL_F32;
+  // g_u_p (M/t x K/t) = g_enc_p (M/t x N/t) . W_p (N/t x K/t): B is N-major. Stored in the
+  // slice-product format (bf16 / F24 on the bf16 path: 2 or 3 of the 4 bytes of g_u_ws used).
+  const int gu_fmt = product_format(bi, bk, bj, t, r, dtype);
+  const int gu_dt = gu_fmt >= 0 ? gu_fmt : STL_F32;
   bool gw_done = false, gu_done = false;
   if (g_w && (g_x || g_ex) && bi > 0 && bk > 0 && bj > 0 && r > 0) {
     // both slice-GEMMs in one persistent launch (g_w first: its K = M/t is the longer one)

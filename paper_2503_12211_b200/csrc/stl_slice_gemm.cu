@@ -925,7 +925,7 @@ bool slice_gemm_tc_group_supported(const SliceGemmProblem& p0, const SliceGemmPr
   // the instantiated pair: g_w (A, B MN-major; fp32) with g_u (A K-major, B MN-major; F24/fp32)
   const bool kinds = p0.a_layout == 1 && p0.b_layout == 1 && p0.c_dtype == kF32 &&
                      p1.a_layout == 0 && p1.b_layout == 1 &&
-                     (p1.c_dtype == kF32 || p1.c_dtype == kF24);
+                     (p1.c_dtype == kF32 || p1.c_dtype == kF24 || p1.c_dtype == kBF16);
   return kinds && slice_gemm_tc_supported(p0) && slice_gemm_tc_supported(p1) && p0.r == p1.r &&
          pair_eligible(p0) && pair_eligible(p1) && !p0.c2 && !p1.c2 && p0.N > 128 &&
          p1.N > 128 && (p1.c_dtype != kF24 || slice_gemm_f24_supported(p1));
@@ -937,6 +937,7 @@ cudaError_t slice_gemm_tc_group(const SliceGemmProblem& p0, const SliceGemmProbl
   const SliceGemmProblem pbs[2] = {p0, p1};
   using K0 = GemmKind<true, true, kOutF32>;
   if (p1.c_dtype == kF24) return launch_tc2_group<256, K0, GemmKind<false, true, kOutF24>>(pbs, 2, s);
+  if (p1.c_dtype == kBF16) return launch_tc2_group<256, K0, GemmKind<false, true, kOutBf16>>(pbs, 2, s);
   return launch_tc2_group<256, K0, GemmKind<false, true, kOutF32>>(pbs, 2, s);
 }
 

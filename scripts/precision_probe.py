@@ -28,7 +28,7 @@ for (M, K, N, R) in ((8192, 8192, 8192, 24), (8192, 4096, 4096, 24), (4096, 4096
     prod = torch.einsum("ikp,pjk->ijp", u, w.double())              # (bi, bj, r)
     yt = prod @ snf.d.double()                                     # (bi, bj, 16)
     yref = yt.reshape(rows // T, N // T, T, T).permute(0, 2, 1, 3).reshape(rows, N)
-    for bits in (32, 0):
+    for bits in (32, 0, 16):
         lib.stl_set_fusion(bits)
         y = _forward(x, w, snf)
         err = float((y[:rows].double() - yref).norm() / yref.norm())
@@ -41,6 +41,6 @@ for (M, K, N, R) in ((8192, 8192, 8192, 24), (8192, 4096, 4096, 24), (4096, 4096
             _forward(x, w, snf)
         e1.record()
         torch.cuda.synchronize()
-        print(json.dumps({"shape": [M, K, N], "r": R, "products": "F24/fp32" if bits else "bf16", "rel_err": err,
+        print(json.dumps({"shape": [M, K, N], "r": R, "products": {0: "bf16", 32: "F24", 16: "fp32"}[bits], "rel_err": err,
                           "ms": e0.elapsed_time(e1) / 20}))
 lib.stl_set_fusion(0)

@@ -434,8 +434,9 @@ def test_mma_transforms_match_ffma(M, K, N, r):
     outs = {}
     try:
         # 2|8|16: FFMA transforms, no streaming kernels, fp32 slice products;
-        # 4|8|16: register-mma transforms; 0: streaming transforms + F24 slice products
-        for mode in (2 | 8 | 16, 4 | 8 | 16, 0):
+        # 4|8|16: register-mma transforms; 32: streaming transforms + F24 slice products;
+        # 0 (default): streaming transforms + bf16 slice products
+        for mode in (2 | 8 | 16, 4 | 8 | 16, 32, 0):
             _lib.load().stl_set_fusion(mode)
             y, cache = stl._layer_forward_cached(layer, x_dev)
             y_enc = stl.unpack_slice_products(cache.y_enc, r, M // t, N // t)
@@ -448,9 +449,10 @@ def test_mma_transforms_match_ffma(M, K, N, r):
         tuple(O.layer_backward(w64, e_x, d, cache_ref, gy64, t))
     names = ("y", "u", "y_enc", "g_ex", "g_d", "g_w", "g_x")
     for i, name in enumerate(names):
-        for mode in (4 | 8 | 16, 0):
+        for mode in (4 | 8 | 16, 32, 0):
             a, b = outs[mode][i], outs[2 | 8 | 16][i]
-            assert rel(a, b) <= 2e-3, (name, mode, rel(a, b))
+            # bf16 slice products round y_enc / g_u once more (2^-9) than the fp32-class formats
+            assert rel(a, b) <= (5e-3 if mode == 0 else 2e-3), (name, mode, rel(a, b))
             assert rel(a, refs[i]) <= BF16_TOL, (name, mode, rel(a, refs[i]))
 
 

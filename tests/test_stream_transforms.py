@@ -42,11 +42,15 @@ def test_encode_decode_bf16(rows, cols, r):
 
 
 @pytest.mark.parametrize("M,K,N,r,fmt", [
-    (1024, 512, 512, 24, "f24"),     # F24 slice products (N/4 % 128 == 0)
-    (1024, 512, 768, 24, "bf16"),    # N/4 = 192: fp32 products + bf16 cache
+    (1024, 512, 512, 24, "bf16"),    # default: bf16 slice products (cache and g_u)
+    (1024, 512, 512, 24, "f24"),     # stl_set_fusion bit 5: F24 slice products (N/4 % 128 == 0)
+    (1024, 512, 768, 24, "bf16"),    # N/4 = 192: bf16 products need N/4 % 64 only
+    (1024, 512, 768, 24, "f24x"),    # bit 5 at N/4 = 192: F24 not eligible -> fp32 + bf16 cache
     (1024, 2304, 512, 20, "f24"),    # partial 512-tile units in K, r not a multiple of 8
+    (1024, 2304, 512, 20, "bf16"),
     (768, 256, 1024, 13, "f24"),     # r = 13: one plane group, zero-padded to 16 in the box
-    (1024, 512, 512, 32, "nof24"),   # F24 disabled (stl_set_fusion bit 4): fp32 products, bf16 cache
+    (768, 256, 1024, 13, "bf16"),
+    (1024, 512, 512, 32, "fp32"),    # stl_set_fusion bit 4: fp32 products, bf16 cache
 ])
 def test_layer_fwd_bwd_formats(M, K, N, r, fmt):
     t = 4
@@ -57,18 +61,18 @@ def test_layer_fwd_bwd_formats(M, K, N, r, fmt):
     gy_dev, gy64 = bf(rng.standard_normal((M, N)))
     layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
     try:
-        _lib.load().stl_set_fusion(16 if fmt == "nof24" else 0)
+        _lib.load().stl_set_fusion({"bf16": 0, "f24": 32, "f24x": 32, "fp32": 16}[fmt])
         y, cache = stl._layer_forward_cached(layer, x_dev)
         grads = stl._layer_backward(layer, cache, gy_dev)
         torch.cuda.synchronize()
     finally:
         _lib.load().stl_set_fusion(0)
     nbytes = cache.y_enc.numel() * cache.y_enc.element_size()
-    assert nbytes == {"f24": 3, "bf16": 2, "nof24": 2}[fmt] * r * (M // 4) * (N // 4)
+    assert nbytes == {"f24": 3, "bf16": 2, "f24x": 2, "fp32": 2}[fmt] * r * (M // 4) * (N // 4)
     y_ref, cache_ref = O.layer_forward_cached(x64, w64, e_x, d, t)
     assert rel(y, y_ref) <= 1e-2
     y_enc = stl.unpack_slice_products(cache.y_enc, r, M // 4, N // 4)
-    tol_enc = {"f24": 2e-3, "bf16": 5e-3, "nof24": 5e-3}[fmt]      # u is bf16 in all formats
+    tol_enc = {"f24": 2e-3, "bf16": 5e-3, "f24x": 5e-3, "fp32": 5e-3}[fmt]  # u is bf16 in all
     assert rel(y_enc, cache_ref[2].transpose(2, 0, 1)) <= tol_enc
     refs = O.layer_backward(w64, e_x, d, cache_ref, gy64, t)
     for name, g, ref in zip(("g_ex", "g_d", "g_w", "g_x"), grads, refs):
