@@ -105,16 +105,16 @@ STL_API int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_lay
  *                mode, see stl_cache_bytes);
  *   scratch: device workspace of at least stl_forward_scratch_bytes(...) bytes.
  *   M, K, N must be multiples of t (ShapeError otherwise, as the reference).
- * Default path: encode -> slice GEMM -> decode with the slice products in `scratch` (fp32; on
- * the bf16 t = 4 path bf16 planes when y_enc_cache is NULL — they only feed the decode — and
- * F24 when the cache is kept); with stl_set_fusion bit 0, bf16 t = 4 runs the decode-fused
- * tcgen05 kernel instead.
+ * Default path: encode -> slice GEMM -> decode with the slice products in y_enc_cache or
+ * `scratch` (fp32; on the bf16 t = 4 path with r <= 32 bf16 planes, F24 with stl_set_fusion
+ * bit 5); with stl_set_fusion bit 0, bf16 t = 4 runs the decode-fused tcgen05 kernel instead.
  */
 STL_API int64_t stl_forward_scratch_bytes(int64_t M, int64_t K, int64_t N, int t, int r,
                                           int dtype);
-/* Bytes of the forward cache y_enc (r, M/t, N/t): fp32 planes (dtype STL_F32); on the bf16
- * path STL_F24 planes (3 bytes per element) when t = 4, r <= 32, M/t > 128, N/t % 128 == 0 and
- * K/t % 8 == 0, else bf16 planes. stl_backward reads the cache in the same format. */
+/* Bytes of the forward cache y_enc (r, M/t, N/t): fp32 planes (dtype STL_F32); bf16 planes on
+ * the bf16 path — or, with stl_set_fusion bit 5, STL_F24 planes (3 bytes per element) when
+ * t = 4, r <= 32, M/t > 128, N/t % 128 == 0 and K/t % 8 == 0. stl_backward reads the cache in
+ * the same format. */
 STL_API int64_t stl_cache_bytes(int64_t M, int64_t K, int64_t N, int t, int r, int dtype);
 STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
                 const float* e_x, const float* d, int t, int r, int dtype, void* y, int64_t ld_y,
@@ -125,8 +125,8 @@ STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const
  * it is slower than encode + GEMM + decode today);
  * bit 1 = force the FFMA tile transforms instead of the tensor-core (mma.sync) ones;
  * bit 2 = also use the tensor-core decode (experimental); bit 3 = disable the streaming
- * (TMA-pipelined) transforms; bit 4 = keep fp32 slice products instead of F24; bit 5 = a
- * cache-less bf16 forward keeps F24 slice products instead of bf16 ones. */
+ * (TMA-pipelined) transforms; bit 4 = fp32 slice products (+ a bf16 cache copy); bit 5 = F24
+ * slice products instead of bf16 ones. */
 STL_API int stl_set_fusion(int enabled);
 
 /*
