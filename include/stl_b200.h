@@ -134,7 +134,9 @@ STL_API int stl_set_fusion(int enabled);
  *   g_d  = sum_{I,J} y_enc[I,J,p] gvy[I,J,c]      -> g_d  fp32 (r, t*t)
  *   g_enc = gvy @ d^T                              -> g_enc_ws planes (r, M/t, N/t) dtype
  *   g_w  = sum_I u[I,L,p] g_enc[I,J,p]             -> g_w  fp32 planes (r, N/t, K/t)
- *   g_u  = sum_J W[L,J,p] g_enc[I,J,p]             -> g_u_ws fp32 planes (r, M/t, K/t)
+ *   g_u  = sum_J W[L,J,p] g_enc[I,J,p]             -> g_u_ws (r, M/t, K/t): fp32 planes, or the
+ *                                                     slice-product format of y_enc (bf16/F24)
+ *                                                     in the first 2-3 bytes per element
  *   g_ex = sum_{I,L} g_u[I,L,p] vx[I,L,c]          -> g_ex fp32 (r, t*t)
  *   g_x  = untile(g_u @ e_x)                       -> g_x (M, K) ld_gx, dtype
  * Inputs: gy (M, N) ld_gy; x (M, K) ld_x (the layer input, vx); w_enc as in stl_forward;
