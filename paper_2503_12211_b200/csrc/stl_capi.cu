@@ -169,10 +169,14 @@ bool fused_forward_shape(int64_t M, int64_t K, int64_t N, int t, int r, int dtyp
 // by the CTA-pair GEMM and read by the streaming transforms, or -1 = fp32 products (+ a cache
 // copy in the compute dtype). A pure function of the shape (and the mode), so the forward
 // (writing the y_enc cache) and the backward (reading it) agree on the cache format.
-int product_format(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype) {
-  if (g_prod_mode == kProdF32 || dtype != STL_BF16 || t != 4 || r > 32 || rows <= 128 ||
-      kt % 8)
+// `inference`: a cache-less forward (no backward reads the products); there r in (32, 64]
+// (the Strassen x Strassen rank 49) uses F24 — fp32-class precision at 3 B — where the
+// reductions of the training path (r <= 32 only) do not run.
+int product_format(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype,
+                   bool inference = false) {
+  if (g_prod_mode == kProdF32 || dtype != STL_BF16 || t != 4 || rows <= 128 || kt % 8)
     return -1;
+  if (r > 32) return inference && r <= 64 && cols % 128 == 0 ? stl::kF24 : -1;
   if (g_prod_mode == kProdF24) return cols % 128 == 0 ? stl::kF24 : -1;
   return cols % 64 == 0 ? STL_BF16 : -1;
 }
@@ -240,7 +244,7 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
                                              ld_y, dtype, nullptr, dtype, scratch, s),
                       "fused forward");
   }
-  const int pfmt = product_format(bi, bj, bk, t, r, dtype);
+  const int pfmt = product_format(bi, bj, bk, t, r, dtype, y_enc_cache == nullptr);
   if (pfmt >= 0) {
     // slice products (bf16 or F24) straight into the cache (or scratch), decoded from there
     void* prod = y_enc_cache ? y_enc_cache : scratch;
