@@ -8,6 +8,7 @@ CPU fallback: if the shared library or a CUDA device is missing, every operator 
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import c_int, c_int64, c_void_p, c_char_p
 from pathlib import Path
 
@@ -69,7 +70,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path is not None else LIB_PATH
+    # STL_LIB: load another build of the library (A/B measurements)
+    p = Path(path) if path is not None else Path(os.environ.get("STL_LIB", LIB_PATH))
     if not p.exists():
         raise ImportError(
             f"STL CUDA library not found at {p}; build it with "

@@ -477,6 +477,24 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
             } else {
   #pragma unroll
             for (int ks = 0; ks < MT; ++ks) {
+              if constexpr (ZSZ == 2 && !kZ24) {
+                // bf16 planes: each 4-byte load holds one plane at tiles (t0, t0 + 1); the A
+                // fragments pair two planes at one tile, so regroup the halves with PRMT
+                uint32_t w[4];
+  #pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  w[j] = (ks < MT - 1 || dok[j])
+                             ? lds32(planes + da[k][j & 1] + (16 * ks + 8 * (j >> 1)) * 128)
+                             : 0u;
+                const uint32_t a0 = __byte_perm(w[0], w[1], 0x5410), a1 = __byte_perm(w[0], w[1], 0x7632);
+                const uint32_t a2 = __byte_perm(w[2], w[3], 0x5410), a3 = __byte_perm(w[2], w[3], 0x7632);
+  #pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                  mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
+                  mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
+                }
+                continue;
+              }
               float v[4][2];  // planes 16ks + 2q + {0, 1, 8, 9} at tiles t0, t0 + 1
   #pragma unroll
               for (int j = 0; j < 4; ++j) {
