@@ -35,9 +35,8 @@ enum Mode { kEnc = 0, kEncRed = 1, kDec = 2, kDecRed = 3 };
 // "lite" configuration meant to share each SM with a slice-GEMM CTA (overlapping the g_x/g_ex
 // decode with the g_w GEMM on two streams) ran 137 us alone and the pair 215 us vs 165 us
 // sequential, so the backward stays sequential.
-// Consumer groups taking alternate units: two 8-warp groups for the plain transforms (their
-// per-unit math is short, so two units in flight hide its latency), one 16-warp group for the
-// fused reductions (more math per unit: splitting it 16 ways wins).
+// Consumer groups taking alternate units: two 8-warp groups (two units' math in flight hides
+// latency; with bf16 slice products the fused reductions gain from it too: 1-2%).
 constexpr int kMaxStages = 16;
 constexpr uint32_t kRowPad = 64;            // matrix rows: 16-word bank shift per row
 
@@ -45,7 +44,7 @@ template <int MODE> constexpr bool has_rows() { return MODE != kDec; }
 template <int MODE> constexpr bool has_planes_in() { return MODE != kEnc; }
 template <int MODE> constexpr bool is_enc() { return MODE == kEnc || MODE == kEncRed; }
 template <int MODE> constexpr bool has_red() { return MODE == kEncRed || MODE == kDecRed; }
-template <int MODE, int CW> constexpr int groups_of() { return has_red<MODE>() || CW < 16 ? 1 : 2; }
+template <int MODE, int CW> constexpr int groups_of() { return CW < 16 ? 1 : 2; }
 
 // Plane element types: float, __nv_bfloat16, or F24 (kF24 of stl_internal.h: a 16-bit high
 // plane set + an 8-bit low plane set, moved as two boxes).
