@@ -312,7 +312,6 @@ struct GroupArgs {
   int M[2], N[2], K[2];
   int r;
   int total0, total;
-  int offset0;  // problem 0's first cluster tile (a launch may cover a range of row blocks)
   int nostore;
   unsigned long long* dbg;
 };
@@ -325,7 +324,7 @@ struct TileCoord {
   int prob, p, mb, nb, num_kb;
   __device__ __forceinline__ TileCoord(const GroupArgs& g, int tile, int pid) {
     prob = tile >= g.total0 ? 1 : 0;
-    const int local = prob ? tile - g.total0 : tile + g.offset0;
+    const int local = prob ? tile - g.total0 : tile;
     const int n_sup = ((g.N[prob] + BN - 1) / BN + MC - 1) / MC;
     const int per_slice = ((g.M[prob] + 255) / 256) * n_sup;
     p = local / per_slice;
@@ -747,11 +746,8 @@ int env_int(const char* name, int dflt) {
 }
 
 // One persistent launch over np (1 or 2) problems of kinds K0, K1.
-// Problem 0 may be restricted to the row-block units [ub, ue) (unit = one (slice, 256-row
-// block) of all its column tiles; ue < 0: all); `cap` limits the clusters (0: all co-resident).
 template <int BN, class K0, class K1, int MC>
-cudaError_t launch_tc2_group_mc(const SliceGemmProblem* pbs, int np, cudaStream_t s, int ub = 0,
-                                int ue = -1, int cap = 0) {
+cudaError_t launch_tc2_group_mc(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
   Tc2Maps m0, m1;
   bool ok = make_tc2_maps<BN, MC, K0>(pbs[0], &m0);
   if (np > 1) ok = ok && make_tc2_maps<BN, MC, K1>(pbs[1], &m1);
@@ -761,8 +757,7 @@ cudaError_t launch_tc2_group_mc(const SliceGemmProblem* pbs, int np, cudaStream_
   const int smem = Smem2<BN, K0::OUT, K1::OUT>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int64_t n_sup0 = ((pbs[0].N + BN - 1) / BN + MC - 1) / MC;
-  const int64_t t0 = ue < 0 ? tc2_tiles(pbs[0], BN, MC) : (ue - ub) * n_sup0;
+  const int64_t t0 = tc2_tiles(pbs[0], BN, MC);
   const int64_t tiles = t0 + (np > 1 ? tc2_tiles(pbs[1], BN, MC) : 0);
   if (tiles <= 0) return cudaSuccess;
   if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
@@ -788,8 +783,7 @@ cudaError_t launch_tc2_group_mc(const SliceGemmProblem* pbs, int np, cudaStream_
       n = sm_count() / (2 * MC);
     max_clusters[MC] = n;
   }
-  int clusters = static_cast<int>(tiles < max_clusters[MC] ? tiles : max_clusters[MC]);
-  if (cap > 0 && clusters > cap) clusters = cap;
+  const int clusters = static_cast<int>(tiles < max_clusters[MC] ? tiles : max_clusters[MC]);
   const int grid = 2 * MC * clusters;
   cfg.gridDim = dim3(grid);
   static const int nostore = getenv("STL_GEMM_NOSTORE") ? atoi(getenv("STL_GEMM_NOSTORE")) : 0;
@@ -803,7 +797,6 @@ cudaError_t launch_tc2_group_mc(const SliceGemmProblem* pbs, int np, cudaStream_
   ga.r = pbs[0].r;
   ga.total0 = static_cast<int>(t0);
   ga.total = static_cast<int>(tiles);
-  ga.offset0 = static_cast<int>(ub * n_sup0);
   ga.nostore = nostore;
   static const bool dbg_on = getenv("STL_GEMM_DEBUG") != nullptr;
   static unsigned long long* dbg = nullptr;

@@ -139,17 +139,21 @@ __global__ void k_token_fold(const __nv_bfloat16* __restrict__ y, int64_t B, int
 }
 
 
-// Backward of k_token_fold. Block `blk` owns output rows [blk*rpb, (blk+1)*rpb) and all N
-// columns (thread = 8 columns, blockDim.x = N / 8 rounded up to a warp multiple); it writes
-// g_y for its rows and its partial column sums of g_out (d bias) and, from the fold rows,
-// partial d fold[k] = sum_n g_out[b, T-1, n] y[b, T-1+k, n], to part[blk * (N + t) + ...].
+// Backward of k_token_fold. Block `blk` owns output rows [blk*rpb, (blk+1)*rpb); a thread owns
+// 8 columns (cpr = N / 8 rounded up to a warp multiple threads per row) of every ry-th row
+// (ry = the block's row lanes). It writes g_y for its rows; the block writes its partial column
+// sums of g_out (d bias: the row lanes summed in fixed order through shared memory) and, from
+// the fold rows, partial d fold[k] = sum_n g_out[b, T-1, n] y[b, T-1+k, n], to
+// part[blk * (N + t) + ...].
 __global__ void k_token_fold_bwd(const __nv_bfloat16* __restrict__ gout,
                                  const __nv_bfloat16* __restrict__ y, int64_t B, int64_t Tp,
                                  int64_t N, int t, const float* __restrict__ fold, int64_t T,
-                                 int64_t rpb, __nv_bfloat16* __restrict__ gy,
+                                 int64_t rpb, int cpr, __nv_bfloat16* __restrict__ gy,
                                  float* __restrict__ part) {
+  extern __shared__ float s_bias[];  // [row lanes][N]
   __shared__ float s_fold[32][kFoldMaxT];
-  const int64_t c0 = int64_t(threadIdx.x) * 8;
+  const int ry = threadIdx.x / cpr, nry = blockDim.x / cpr;
+  const int64_t c0 = int64_t(threadIdx.x - ry * cpr) * 8;
   const bool col_ok = c0 < N;
   const int64_t r0 = blockIdx.x * rpb;
   const int64_t r1 = min(r0 + rpb, B * T);
@@ -158,45 +162,44 @@ __global__ void k_token_fold_bwd(const __nv_bfloat16* __restrict__ gout,
 #pragma unroll
   for (int k = 0; k < kFoldMaxT; ++k) sf[k] = 0.f;
   if (col_ok) {
-    constexpr int kU = 4;  // rows in flight per thread
-    for (int64_t rb = r0; rb < r1; rb += kU) {
+    constexpr int kU = 2;  // rows in flight per thread
+    for (int64_t rb = r0 + ry; rb < r1; rb += kU * nry) {
       float gg[kU][8];
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (rb + u < r1) load8(gout + (rb + u) * N + c0, gg[u]);
+        if (rb + u * nry < r1) load8(gout + (rb + u * nry) * N + c0, gg[u]);
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-      const int64_t row = rb + u;
-      if (row >= r1) break;
-      const float* g = gg[u];
-      const int64_t b = row / T, j = row - b * T;
+        const int64_t row = rb + u * nry;
+        if (row >= r1) break;
+        const float* g = gg[u];
+        const int64_t b = row / T, j = row - b * T;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) sb[e] += g[e];
-      __nv_bfloat16* dst = gy + (b * Tp + j) * N + c0;
-      if (j != T - 1) {
-        store8(dst, g);
-      } else {
-        for (int k = 0; k < t; ++k) {
-          const float wk = fold[k];
-          float h[8], o[8];
-          load8(y + (b * Tp + j + k) * N + c0, h);
-          float acc = 0.f;
+        for (int e = 0; e < 8; ++e) sb[e] += g[e];
+        __nv_bfloat16* dst = gy + (b * Tp + j) * N + c0;
+        if (j != T - 1) {
+          store8(dst, g);
+        } else {
+          for (int k = 0; k < t; ++k) {
+            const float wk = fold[k];
+            float h[8], o[8];
+            load8(y + (b * Tp + j + k) * N + c0, h);
+            float acc = 0.f;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            o[e] = wk * g[e];
-            acc = fmaf(g[e], h[e], acc);
+            for (int e = 0; e < 8; ++e) {
+              o[e] = wk * g[e];
+              acc = fmaf(g[e], h[e], acc);
+            }
+#pragma unroll
+            for (int kk = 0; kk < kFoldMaxT; ++kk)
+              if (kk == k) sf[kk] += acc;
+            store8(dst + k * N, o);
           }
-#pragma unroll
-          for (int kk = 0; kk < kFoldMaxT; ++kk)
-            if (kk == k) sf[kk] += acc;
-          store8(dst + k * N, o);
         }
       }
-      }
     }
+    store8(s_bias + ry * N + c0, sb);
   }
-  float* out = part + blockIdx.x * (N + t);
-  if (col_ok) store8(out + c0, sb);
   // fold partials: warp shuffle reduction, then the block's warps in fixed order
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -207,6 +210,12 @@ __global__ void k_token_fold_bwd(const __nv_bfloat16* __restrict__ gout,
     if (lane == 0) s_fold[warp][k] = v;
   }
   __syncthreads();
+  float* out = part + blockIdx.x * (N + t);
+  for (int64_t c = threadIdx.x; c < N; c += blockDim.x) {
+    float v = s_bias[c];
+    for (int r = 1; r < nry; ++r) v += s_bias[r * N + c];
+    out[c] = v;
+  }
   if (threadIdx.x < t) {
     float v = 0.f;
     for (int w = 0; w < int(blockDim.x >> 5); ++w) v += s_fold[w][threadIdx.x];
@@ -276,10 +285,12 @@ cudaError_t token_fold_backward(const void* gout, const void* y, int64_t B, int6
   if (rows == 0 || N == 0) return cudaMemsetAsync(g_bias_fold, 0, sizeof(float) * (N + t), s);
   const int64_t nb = fold_blocks(rows);
   const int64_t rpb = (rows + nb - 1) / nb;
-  const int threads = static_cast<int>(((N / 8 + 31) / 32) * 32);
-  k_token_fold_bwd<<<static_cast<int>(nb), threads, 0, s>>>(
+  const int cpr = static_cast<int>(((N / 8 + 31) / 32) * 32);  // threads per row
+  const int nry = cpr >= 256 ? 1 : 256 / cpr;                    // row lanes per block
+  const size_t smem = sizeof(float) * nry * N;
+  k_token_fold_bwd<<<static_cast<int>(nb), cpr * nry, smem, s>>>(
       static_cast<const __nv_bfloat16*>(gout), static_cast<const __nv_bfloat16*>(y), B, Tp, N, t,
-      fold, T, rpb, static_cast<__nv_bfloat16*>(g_y), ws);
+      fold, T, rpb, cpr, static_cast<__nv_bfloat16*>(g_y), ws);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return sum_partials(ws, static_cast<int>(nb), static_cast<int>(N + t), g_bias_fold, s);
