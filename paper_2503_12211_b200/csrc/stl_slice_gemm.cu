@@ -273,13 +273,12 @@ struct GemmKind {
   static constexpr int OUT = OUT_;
 };
 
-// Epilogue staging of one output mode: 128 rows (the CTA's TMEM lanes) x 32 columns, a primary
-// part (fp32 128 B rows, or F24 high 64 B rows) and a secondary part at kSecOff (bf16 64 B rows,
-// or F24 low 32 B rows).
+// Epilogue staging of one output mode: 128 rows (the CTA's TMEM lanes) x 32 columns (64 for
+// bf16 output), a primary part (fp32 or bf16 128 B rows, or F24 high 64 B rows) and a secondary
+// part at kSecOff (the bf16 copy's 64 B rows, or F24 low 32 B rows).
 template <int OUT>
 struct OutStage {
-  static constexpr uint32_t kSecOff =
-      OUT == kOutF24 ? 128 * 64 : (OUT == kOutBf16 ? 128 * 64 : 128 * 128);
+  static constexpr uint32_t kSecOff = OUT == kOutF24 ? 128 * 64 : 128 * 128;
   static constexpr uint32_t kBytes =
       kSecOff + (OUT == kOutF32Bf16 ? 128 * 64 : (OUT == kOutF24 ? 128 * 32 : 0));
 };
@@ -431,11 +430,14 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
   constexpr int OUT = Kd::OUT;
   constexpr uint32_t kSec = OutStage<OUT>::kSecOff;
   const int r = q * 32 + lane;  // staging row = TMEM lane
+  // bf16 output drains 64 columns per chunk (128 B staging rows, half the barriers / stores)
+  constexpr int kCols = OUT == kOutBf16 ? 64 : 32;
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 32, ++chunk_no) {
-    uint32_t v[32];
+  for (int c = 0; c < BN; c += kCols, ++chunk_no) {
+    uint32_t v[32], v2[32];
     __syncwarp();
     ptx::tmem_ld_32x32b_x32(tmem_acc + c, v);
+    if constexpr (kCols == 64) ptx::tmem_ld_32x32b_x32(tmem_acc + c + 32, v2);
     uint8_t* sf = stage_base + (chunk_no & 1) * S::kBufBytes;
     ptx::tmem_ld_wait();
     const bool active = tc.nb * BN + c < N && row_base < M && !nostore;  // CTA-uniform
@@ -462,17 +464,18 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
           *reinterpret_cast<uint4*>(sh + r * 32 + ((j ^ ((r >> 2) & 1)) << 4)) =
               make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
       } else if constexpr (OUT == kOutBf16) {
-        // bf16 only: 64 B rows, 64B-swizzled
+        // bf16 only: 64 columns = 128 B rows, 128B-swizzled (16-byte chunk j at j ^ (r & 7))
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t* src = j < 4 ? v + 8 * j : v2 + 8 * (j - 4);
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * e]),
-                                                     __uint_as_float(v[8 * j + 2 * e + 1]));
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(src[2 * e]),
+                                                     __uint_as_float(src[2 * e + 1]));
             w[e] = *reinterpret_cast<uint32_t*>(&h);
           }
-          *reinterpret_cast<uint4*>(sf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
+          *reinterpret_cast<uint4*>(sf + r * 128 + ((j ^ (r & 7)) << 4)) =
               make_uint4(w[0], w[1], w[2], w[3]);
         }
       } else {
@@ -690,19 +693,21 @@ cudaError_t launch_tc(const SliceGemmProblem& pb, cudaStream_t s) {
 
 // 3-D (N, M, r) store map for 128-row x 32-column output chunks: es = 4 (fp32, 128B swizzle),
 // 2 (16-bit, 64B swizzle) or 1 (8-bit, 32B swizzle).
-bool make_out_tmap(CUtensorMap* m, const void* base, int es, uint64_t N, uint64_t M, uint64_t r) {
+bool make_out_tmap(CUtensorMap* m, const void* base, int es, uint64_t N, uint64_t M, uint64_t r,
+                   uint32_t cols = 32) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {N, M, r};
   cuuint64_t strides[2] = {N * es, N * M * es};
-  cuuint32_t box[3] = {32, 128, 1};
+  cuuint32_t box[3] = {cols, 128, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   const CUtensorMapDataType dt = es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                  : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                            : CU_TENSOR_MAP_DATA_TYPE_UINT8;
-  const CUtensorMapSwizzle sw = es == 4 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                : es == 2 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                          : CU_TENSOR_MAP_SWIZZLE_32B;
+  const uint32_t row_bytes = cols * es;  // the staging rows: 128, 64 or 32 bytes
+  const CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                  : CU_TENSOR_MAP_SWIZZLE_32B;
   CUresult res = fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -722,7 +727,7 @@ bool make_tc2_maps(const SliceGemmProblem& pb, Tc2Maps* m) {
   ok = ok && (Kd::B_MN ? make_tmap(&m->b, pb.b, N, K, r, kBK)
                        : make_tmap(&m->b, pb.b, K, N, r, BN / 2));
   if (Kd::OUT == kOutBf16) {
-    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r);
+    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r, 64);  // 64-column chunks, 128 B rows
     m->c2 = m->c;
   } else if (Kd::OUT == kOutF24) {
     ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r) &&
