@@ -815,8 +815,9 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   return cudaSuccess;
 }
 
-// 512-tile units whenever two pipeline stages fit in 200 KB (measured: longer bulk segments beat
-// deeper pipelines), else 256.
+// 512-tile units whenever two pipeline stages per consumer group fit (measured: longer bulk
+// segments beat deeper pipelines; the g_x / g_ex decode-reduction even with 3 stages: 47.7 vs
+// 55.9 us at config 2, while the g_enc / g_d encode-reduction is faster with 256), else 256.
 template <int MODE, typename ZT, int MT>
 cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                      cudaStream_t s) {
@@ -825,8 +826,8 @@ cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, floa
   const int pb = ((a.P + 7) / 8) * 8;
   const Layout L512 = make_layout<MODE, ZT, 512, 16>(a.P, pb, budget);
   const bool use512 = force_t ? force_t == 512
-                              : (L512.nstages >= 2 * groups_of<MODE, 16>() && L512.total <= 227 * 1024 &&
-                                 a.bc >= 512);
+                              : (L512.nstages >= (MODE == kDecRed ? 3u : 2u * groups_of<MODE, 16>()) &&
+                                 L512.total <= 227 * 1024 && a.bc >= 512);
   if (use512) return launch_mt<MODE, ZT, MT, 512, 16>(a, planes_in, planes_out, red_out, s, budget);
   return launch_mt<MODE, ZT, MT, 256, 16>(a, planes_in, planes_out, red_out, s, budget);
 }
