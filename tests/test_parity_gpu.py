@@ -346,6 +346,55 @@ def test_full_size_strassen49_equals_matmul_bf16():
     assert rel(got.float(), ref) <= BF16_TOL
 
 
+def test_full_size_backward_properties_bf16():
+    """BASELINE configs[1] shape, forward + backward: g_x rows depend only on the same rows of
+    gY (64-row slabs against the oracle), and g_w, g_d, g_ex are sums over token rows, so the
+    backward of the two halves of the batch must add up to the backward of the whole."""
+    t, r, M, K, N = 4, 24, 8192, 4096, 4096
+    rng = O.make_rng(5)
+    e_x, e_w, d = O.random_gaussian_init(t, r, rng, scale=0.5)
+    w_dev, w64 = bf16_round(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
+    layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
+    g = torch.Generator(device=DEV).manual_seed(6)
+    x = torch.randn((M, K), device=DEV, generator=g).to(torch.bfloat16)
+    gy = torch.randn((M, N), device=DEV, generator=g).to(torch.bfloat16)
+
+    def fwd_bwd(rows):
+        _, cache = stl._layer_forward_cached(layer, x[rows])
+        return [gr.float() for gr in stl._layer_backward(layer, cache, gy[rows])]
+
+    g_ex, g_d, g_w, g_x = fwd_bwd(slice(0, M))
+    for lo in (0, M - 64):
+        rows = slice(lo, lo + 64)
+        x64 = x[rows].double().cpu().numpy()
+        gy64 = gy[rows].double().cpu().numpy()
+        _, cache64 = O.layer_forward_cached(x64, w64, e_x, d, t)
+        ref_gx = O.layer_backward(w64, e_x, d, cache64, gy64, t)[3]
+        assert rel(g_x[rows], ref_gx) <= BF16_TOL
+    halves = [fwd_bwd(slice(0, M // 2)), fwd_bwd(slice(M // 2, M))]
+    for i, (name, full) in enumerate((("g_ex", g_ex), ("g_d", g_d), ("g_w", g_w))):
+        summed = halves[0][i] + halves[1][i]
+        assert rel(summed, full) <= 1e-4, (name, rel(summed, full))
+    assert torch.equal(torch.cat([halves[0][3], halves[1][3]]), g_x)
+
+
+def test_full_size_strassen49_backward_equals_matmul_bf16():
+    """With an exact triple the layer is Y = X W, so its input gradient is gY W^T: checked over
+    the whole output at M = 8192, K = N = 4096 (fp32 slice products at r = 49)."""
+    M, K, N = 8192, 4096, 4096
+    s49 = stl.strassen_rank49()
+    g = torch.Generator(device=DEV).manual_seed(7)
+    x = torch.randn((M, K), device=DEV, generator=g).to(torch.bfloat16)
+    gy = torch.randn((M, N), device=DEV, generator=g).to(torch.bfloat16)
+    w = (torch.randn((K, N), device=DEV, generator=g) / 64.0).to(torch.bfloat16)
+    w_enc = stl.encode_tiles(w.float(), s49.on(x.device).e_w, 4).to(torch.bfloat16)
+    layer = stl.StlLayer(s49, w_enc)
+    _, cache = stl._layer_forward_cached(layer, x)
+    g_x = stl._layer_backward(layer, cache, gy)[3]
+    ref = gy.float() @ w.float().T
+    assert rel(g_x.float(), ref) <= BF16_TOL
+
+
 # ----------------------------------------------------------------- errors / edge cases
 def test_errors_match_reference_classes():
     snf = stl.SnfTriple(4, 8, np.ones((8, 16)), np.ones((8, 16)), np.ones((8, 16)))
