@@ -180,6 +180,23 @@ int product_format(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dty
   if (g_prod_mode == kProdF24) return cols % 128 == 0 ? stl::kF24 : -1;
   return cols % 64 == 0 ? STL_BF16 : -1;
 }
+// Split-K factor for a tensor-core slice GEMM (M x N per slice, contraction K) whose output
+// tiles cannot fill the GPU: S divides K, K / S >= 512; 1 = no split. Used for g_w, whose
+// partials (r * S * M * N fp32) fit the g_u workspace (r * K * N fp32) when S * M <= K.
+int split_k_factor(int64_t M, int64_t N, int64_t K, int r, int dtype) {
+  if (dtype != STL_BF16 || M % 8 || N % 8 || (M * N) % 4) return 1;
+  const bool one_cta = M <= 128;  // 1-CTA tiles (128 x BN) vs CTA pairs (256 x BN)
+  const int64_t bn = N <= 128 ? 128 : 256;
+  const int64_t tiles = static_cast<int64_t>(r) * ((M + (one_cta ? 127 : 255)) / (one_cta ? 128 : 256)) *
+                        ((N + bn - 1) / bn);
+  const int64_t slots = one_cta ? stl::sm_count() : stl::sm_count() / 2;
+  int64_t want = slots / (tiles > 0 ? tiles : 1);
+  if (want > 16) want = 16;
+  for (int64_t S = want; S > 1; --S)
+    if (K % S == 0 && K / S >= 512 && S * M <= K) return static_cast<int>(S);
+  return 1;
+}
+
 bool f24_products(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype) {
   return product_format(rows, cols, kt, t, r, dtype) == stl::kF24;
 }
@@ -331,8 +348,21 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
     }
   }
   if (g_w && !gw_done) {
-    st = run_gemm(g_enc_ws, STL_MN_MAJOR, x_enc, STL_MN_MAJOR, g_w, STL_F32, dtype, r, bj, bk,
-                  bi, s);
+    // Few output tiles (narrow layers: M = N/t and N = K/t small, a long K = M/t): split the
+    // contraction over S consecutive row blocks — (r, bi, .) operands are exactly
+    // (r * S, bi / S, .) ones — into g_u_ws (free until the g_u GEMM) and sum the S partials
+    // in fixed order.
+    const int S = g_u_ws ? split_k_factor(bj, bk, bi, r, dtype) : 1;
+    if (S > 1) {
+      st = run_gemm(g_enc_ws, STL_MN_MAJOR, x_enc, STL_MN_MAJOR, g_u_ws, STL_F32, dtype, r * S,
+                    bj, bk, bi / S, s);
+      if (st) return st;
+      Prof prof("sum_splits", s);
+      st = check_cuda(stl::slice_gemm_sum_splits(g_u_ws, r, S, bj * bk, g_w, s), "split-K sum");
+    } else {
+      st = run_gemm(g_enc_ws, STL_MN_MAJOR, x_enc, STL_MN_MAJOR, g_w, STL_F32, dtype, r, bj, bk,
+                    bi, s);
+    }
     if (st) return st;
   }
   if (g_x || g_ex) {

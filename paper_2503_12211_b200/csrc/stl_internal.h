@@ -86,6 +86,9 @@ cudaError_t slice_gemm_tc_group(const SliceGemmProblem& p0, const SliceGemmProbl
                                 cudaStream_t s);
 // F24 output (c_dtype = kF24) is produced by the CTA-pair kernel only.
 bool slice_gemm_f24_supported(const SliceGemmProblem& pb);
+// out[p] = sum_s partial[p * S + s] over (r * S) fp32 slices of mn elements (split-K).
+cudaError_t slice_gemm_sum_splits(const float* partial, int r, int S, int64_t mn, float* out,
+                                  cudaStream_t s);
 // SIMT path (fp32 or bf16 operands, any shape).
 cudaError_t slice_gemm_simt(const SliceGemmProblem& pb, cudaStream_t s);
 

@@ -18,6 +18,7 @@
 // g_u = g_enc_p W_p^T and g_w = u_p^T g_enc_p), selected by the UMMA instruction descriptor.
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <mutex>
 #include "sm100_ptx.cuh"
 #include "stl_internal.h"
@@ -971,6 +972,40 @@ cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   if (!a_mn && b_mn) return launch_tc<256, false, true>(pb, s);
   if (a_mn && !b_mn) return launch_tc<256, true, false>(pb, s);
   return launch_tc<256, true, true>(pb, s);
+}
+
+// Split-K partial sums: out[p][i] = sum_s partial[p * S + s][i], fixed order (deterministic).
+namespace {
+__global__ void k_sum_splits(const float4* __restrict__ partial, int S, int64_t mn4, int64_t total4,
+                             float4* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p = i / mn4, o = i - p * mn4;
+    const float4* src = partial + p * S * mn4 + o;
+    float4 a = src[0];
+    for (int k = 1; k < S; ++k) {
+      const float4 b = src[k * mn4];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    out[i] = a;
+  }
+}
+}  // namespace
+
+cudaError_t slice_gemm_sum_splits(const float* partial, int r, int S, int64_t mn, float* out,
+                                  cudaStream_t s) {
+  if (mn % 4 || (reinterpret_cast<uintptr_t>(partial) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    return cudaErrorNotSupported;
+  const int64_t total4 = static_cast<int64_t>(r) * mn / 4;
+  if (total4 == 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((total4 + 255) / 256, int64_t(sm_count()) * 8);
+  k_sum_splits<<<static_cast<int>(blocks), 256, 0, s>>>(reinterpret_cast<const float4*>(partial),
+                                                        S, mn / 4, total4,
+                                                        reinterpret_cast<float4*>(out));
+  return cudaGetLastError();
 }
 
 // ==================================================================== SIMT slice GEMM

@@ -243,7 +243,10 @@ def test_encode_decode_bf16_and_fp32():
 
 
 # ----------------------------------------------------------------- layer backward (bf16)
-@pytest.mark.parametrize("M,K,N,r", [(1024, 512, 768, 24), (2048, 1024, 1024, 24), (512, 256, 256, 49)])
+@pytest.mark.parametrize("M,K,N,r", [(1024, 512, 768, 24), (2048, 1024, 1024, 24), (512, 256, 256, 49),
+                                     # narrow layers, long token axis: g_w runs split-K
+                                     # (1-CTA tiles, S = 4; CTA-pair tiles, S = 2)
+                                     (16384, 256, 256, 24), (12800, 256, 768, 24)])
 def test_layer_backward_bf16(M, K, N, r):
     t = 4
     rng = O.make_rng(M + r)
