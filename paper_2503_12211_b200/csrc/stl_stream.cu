@@ -107,7 +107,8 @@ struct StreamArgs {
   int P;
   int Pb;                    // planes in the (zero-padded) input plane box
   int64_t br, bc;
-  int64_t upr;               // units per tile row
+  int64_t upr;               // units per tile row (1 when R > 1)
+  int R;                     // tile rows per unit: kT / bc for narrow matrices (bc | kT), else 1
   int64_t nunits;
   int stg;                   // 1: consumers write outputs with st.global (else TMA/bulk stores)
   int nocompute;             // probe: skip the math (pure data movement)
@@ -255,6 +256,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   constexpr bool kZ24 = is_f24<ZT>();
   const uint32_t nunits = static_cast<uint32_t>(args.nunits);
   const uint32_t upr = static_cast<uint32_t>(args.upr);
+  const int urows = args.R;  // tile rows per unit
+  const uint32_t br = static_cast<uint32_t>(args.br);
   const uint32_t bc = static_cast<uint32_t>(args.bc);
 
   if (threadIdx.x == 0) {
@@ -281,9 +284,12 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
       const uint32_t stage = it % L.nstages;
       const uint32_t phase = (it / L.nstages) & 1;
-      const uint32_t I = u / upr;
-      const uint32_t J0 = (u - I * upr) * kT;
-      const uint32_t Tw = min(bc - J0, static_cast<uint32_t>(kT));
+      // a unit: tiles J0 .. J0 + kT - 1 of tile row I, or (R > 1) all bc tiles of the R tile
+      // rows I .. I + urows - 1 — the same smem layout (tile t of the unit at the same offsets)
+      const uint32_t I = urows > 1 ? u * urows : u / upr;
+      const uint32_t J0 = urows > 1 ? 0u : (u - I * upr) * kT;
+      const uint32_t nrows = urows > 1 ? min(static_cast<uint32_t>(urows), br - I) : 1u;
+      const uint32_t Tw = urows > 1 ? nrows * bc : min(bc - J0, static_cast<uint32_t>(kT));
       ptx::mbar_wait(&empty[stage], phase ^ 1);
       const uint32_t rows_b = has_rows<MODE>() ? Tw * 8 : 0;
       const uint32_t st = s_stages + stage * L.stage_bytes;
@@ -298,10 +304,18 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                       static_cast<int>(I));
       }
       if constexpr (has_rows<MODE>()) {
-        if (lane < 4)
+        if (urows > 1) {
+          // lane = 4 r + a: matrix row a of the unit's tile row r, appended after row r - 1's
+          const uint32_t r = lane >> 2, a = lane & 3;
+          if (r < nrows)
+            bulk_g2s(sbase + st + L.pl_bytes + a * L.row_stride + r * bc * 8,
+                     args.mat + (4 * static_cast<int64_t>(I + r) + a) * args.ldm, bc * 8,
+                     &full[stage]);
+        } else if (lane < 4) {
           bulk_g2s(sbase + st + L.pl_bytes + lane * L.row_stride,
                    args.mat + (4 * static_cast<int64_t>(I) + lane) * args.ldm + 4 * J0, rows_b,
                    &full[stage]);
+        }
       }
     }
     return;
@@ -409,9 +423,10 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
        u += kGroups * gridDim.x, it += kGroups) {
     const uint32_t stage = it % L.nstages;
     const uint32_t phase = (it / L.nstages) & 1;
-    const uint32_t I = u / upr;
-    const uint32_t J0 = (u - I * upr) * kT;
-    const int Tw = static_cast<int>(min(bc - J0, static_cast<uint32_t>(kT)));
+    const uint32_t I = urows > 1 ? u * urows : u / upr;
+    const uint32_t J0 = urows > 1 ? 0u : (u - I * upr) * kT;
+    const uint32_t nrows = urows > 1 ? min(static_cast<uint32_t>(urows), br - I) : 1u;
+    const int Tw = static_cast<int>(urows > 1 ? nrows * bc : min(bc - J0, static_cast<uint32_t>(kT)));
     const uint32_t buf = s_out + (grp * 2 + ((it / kGroups) & 1)) * L.out_bytes;
     const uint32_t planes = s_stages + stage * L.stage_bytes;
     const uint32_t rows = planes + L.pl_bytes;
@@ -690,7 +705,13 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
       } else {
         __nv_bfloat16* o =
             static_cast<__nv_bfloat16*>(args.out) + (4 * static_cast<int64_t>(I)) * args.ldo + 4 * J0;
-        if (lane < 4) bulk_s2g(o + lane * args.ldo, sbase + buf + lane * L.out_stride, Tw * 8);
+        if (urows > 1) {
+          const uint32_t r = lane >> 2, a = lane & 3;
+          if (r < nrows)
+            bulk_s2g(o + (4 * r + a) * args.ldo, sbase + buf + a * L.out_stride + r * bc * 8, bc * 8);
+        } else if (lane < 4) {
+          bulk_s2g(o + lane * args.ldo, sbase + buf + lane * L.out_stride, Tw * 8);
+        }
       }
       ptx::bulk_commit();
     }
@@ -729,7 +750,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 
 // 4-D plane map (W tiles, P planes, bc/W chunks, br rows) with box {W, P, kT/W, 1}, 128B swizzle.
 bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_t br, int64_t bc,
-                int kT) {
+                int kT, int R) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -748,8 +769,9 @@ bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_
                         static_cast<cuuint64_t>(br)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(br * bc * zsz), 128,
                            static_cast<cuuint64_t>(bc * zsz)};
+  // one unit: kT / W chunks of one tile row, or (R > 1) all bc / W chunks of R tile rows
   cuuint32_t box[4] = {static_cast<cuuint32_t>(W), static_cast<cuuint32_t>(Pb),
-                       static_cast<cuuint32_t>(kT / W), 1};
+                       static_cast<cuuint32_t>((R > 1 ? bc : kT) / W), static_cast<cuuint32_t>(R)};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, zsz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                   : zsz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8,
@@ -770,20 +792,29 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
                       cudaStream_t s, uint32_t budget) {
   a.Pb = ((a.P + 7) / 8) * 8;
   const Layout L = make_layout<MODE, ZT, kT, CW>(a.P, a.Pb, budget);
+  static const int stg = env_int("STL_STREAM_STG", 0);
+  static const int multirow = env_int("STL_STREAM_MULTIROW", 1);
+  // narrow matrices (bc < kT, bc | kT): a unit spans R = kT / bc whole tile rows (R <= 8: one
+  // producer lane per matrix row), so units stay full instead of bc / kT full
+  const int R = (multirow && !stg && a.bc < kT && kT % a.bc == 0 && kT / a.bc <= 8 &&
+                 (!is_f24<ZT>() || a.bc % 128 == 0))
+                    ? static_cast<int>(kT / a.bc)
+                    : 1;
+  a.R = R;
   CUtensorMap tin{}, tin2{}, tout{};
-  if (has_planes_in<MODE>() && !plane_tmap(&tin, planes_in, zhi<ZT>(), a.P, a.Pb, a.br, a.bc, kT))
+  if (has_planes_in<MODE>() &&
+      !plane_tmap(&tin, planes_in, zhi<ZT>(), a.P, a.Pb, a.br, a.bc, kT, R))
     return cudaErrorNotSupported;
   if (is_f24<ZT>() &&
       !plane_tmap(&tin2, static_cast<const uint8_t*>(planes_in) + 2 * a.P * a.br * a.bc, 1, a.P,
-                  a.Pb, a.br, a.bc, kT))
+                  a.Pb, a.br, a.bc, kT, R))
     return cudaErrorNotSupported;
-  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.P, a.br, a.bc, kT))
+  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.P, a.br, a.bc, kT, R))
     return cudaErrorNotSupported;
   auto k = k_stream<MODE, ZT, MT, kT, CW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(L.total));
   if (e != cudaSuccess) return e;
-  static const int stg = env_int("STL_STREAM_STG", 0);
   a.stg = stg;
   static const int noc = env_int("STL_STREAM_NOCOMPUTE", 0);
   a.nocompute = noc;
@@ -792,8 +823,8 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   if (dbg_on && !dbg) cudaMalloc(&dbg, 4 * 1024 * sizeof(unsigned long long));
   if (dbg_on) cudaMemsetAsync(dbg, 0, 4 * 1024 * sizeof(unsigned long long), s);
   a.dbg = dbg_on ? dbg : nullptr;
-  a.upr = (a.bc + kT - 1) / kT;  // kT: this launch's unit
-  a.nunits = a.br * a.upr;
+  a.upr = R > 1 ? 1 : (a.bc + kT - 1) / kT;  // kT: this launch's unit
+  a.nunits = R > 1 ? (a.br + R - 1) / R : a.br * a.upr;
   int64_t grid = sm_count();
   if (grid > a.nunits) grid = a.nunits;
   if (grid < 1) return cudaSuccess;

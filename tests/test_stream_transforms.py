@@ -25,10 +25,14 @@ def rel(got, ref):
     return np.linalg.norm(g - ref) / max(np.linalg.norm(ref), 1e-30)
 
 
-@pytest.mark.parametrize("rows,cols", [(64, 2304), (36, 256), (8, 4096), (128, 512)])
+# (36, 256), (148, 256), (128, 512), (52, 512): narrow matrices, units of 4 / 2 whole tile rows
+# with a partial last unit
+@pytest.mark.parametrize("rows,cols", [(64, 2304), (36, 256), (8, 4096), (128, 512), (148, 256),
+                                       (52, 512)])
 @pytest.mark.parametrize("r", [5, 20, 24, 40, 64])
 def test_encode_decode_bf16(rows, cols, r):
-    """bf16 matrix -> bf16 planes -> bf16 matrix (units: 512 tiles; 2304/4 = 576 = 512 + 64)."""
+    """bf16 matrix -> bf16 planes -> bf16 matrix (units: 512 tiles; 2304/4 = 576 = 512 + 64;
+    narrow matrices: 256-tile units of several tile rows)."""
     rng = O.make_rng(rows * 31 + cols + r)
     e_x, _, d = O.random_gaussian_init(4, r, rng, scale=0.5)
     m_dev, m64 = bf(rng.standard_normal((rows, cols)))
