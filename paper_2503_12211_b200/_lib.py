@@ -71,7 +71,7 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
     if _lib is not None and path is None:
         return _lib
     # STL_LIB: load another build of the library (A/B measurements)
-    p = Path(path) if path is not None else Path(os.environ.get("STL_LIB", LIB_PATH))
+    p = Path(path) if path is not None else Path(os.environ.get("STL_LIB") or LIB_PATH)
     if not p.exists():
         raise ImportError(
             f"STL CUDA library not found at {p}; build it with "
