@@ -93,7 +93,7 @@ inline Layout make_layout(int P, int Pb, uint32_t budget) {
   uint32_t ns = (budget - fixed) / L.stage_bytes;
   if (ns > max_st) ns = max_st;
   L.nstages = ns > kMaxStages ? kMaxStages : (ns < 2 ? 2 : ns);
-  L.total = L.nstages * L.stage_bytes + fixed + 2 * kMaxStages * 8 + 1024;  // + barriers, align
+  L.total = L.nstages * L.stage_bytes + fixed + 2 * kMaxStages * 8 + kMaxStages * 4 + 1024;  // + barriers, stage tags, align
   return L;
 }
 
@@ -248,6 +248,12 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   constexpr int kGWarps = kCWarps / kGroups;  // warps per group
   constexpr int kGThreads = 32 * kGWarps;
   uint64_t* empty = full + kMaxStages;
+  // stage tags: the unit a stage is being filled with, written by the producer once it owns the
+  // stage. With two consumer groups and an odd stage count a stage alternates between the
+  // groups, so a fast group can reach a stage's next use while the other group's fill of it is
+  // still in flight; the full barrier's parity alone would alias that to an older, completed
+  // phase. Consumers first wait for the tag, then for the barrier phase.
+  volatile uint32_t* stage_tag = reinterpret_cast<volatile uint32_t*>(empty + kMaxStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
@@ -264,6 +270,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     for (uint32_t s = 0; s < L.nstages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], kGWarps);
+      stage_tag[s] = 0xFFFFFFFFu;
     }
     ptx::fence_mbar_init();
   }
@@ -291,6 +298,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
       const uint32_t nrows = urows > 1 ? min(static_cast<uint32_t>(urows), br - I) : 1u;
       const uint32_t Tw = urows > 1 ? nrows * bc : min(bc - J0, static_cast<uint32_t>(kT));
       ptx::mbar_wait(&empty[stage], phase ^ 1);
+      if (lane == 0) stage_tag[stage] = it;  // before the expect_tx arrive (release) below
       const uint32_t rows_b = has_rows<MODE>() ? Tw * 8 : 0;
       const uint32_t st = s_stages + stage * L.stage_bytes;
       if (lane == 0) {
@@ -431,6 +439,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     const uint32_t planes = s_stages + stage * L.stage_bytes;
     const uint32_t rows = planes + L.pl_bytes;
     const uint64_t t_w0 = args.dbg ? ptx::globaltimer_ns() : 0;
+    while (stage_tag[stage] != it) {
+    }
     ptx::mbar_wait(&full[stage], phase);
     const uint64_t t_w1 = args.dbg ? ptx::globaltimer_ns() : 0;
 
