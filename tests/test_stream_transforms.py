@@ -81,3 +81,19 @@ def test_layer_fwd_bwd_formats(M, K, N, r, fmt):
     refs = O.layer_backward(w64, e_x, d, cache_ref, gy64, t)
     for name, g, ref in zip(("g_ex", "g_d", "g_w", "g_x"), grads, refs):
         assert rel(g, ref) <= 1e-2, (name, rel(g, ref))
+
+
+def test_stage_protocol_under_data_only_probe():
+    """Regression for the stage-reuse race (two consumer groups, odd stage counts): with the
+    STL_STREAM_NOCOMPUTE probe the consumers only move data, so a group runs far ahead of the
+    other; without the producer's per-stage unit tags this faulted within a few hundred
+    config-2 steps."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, STL_STREAM_NOCOMPUTE="1", STRESS_STEPS="300")
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "stress_step.py")],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "stress ok" in out.stdout, out.stderr[-2000:]
