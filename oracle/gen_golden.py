@@ -113,6 +113,22 @@ def main() -> None:
                      cost_model.io_fused_chain(n, t, r, 3, 2),
                      cost_model.flops_general(cost_model.ProblemShape(n, n // 2, n, t, r))])
     np.savez_compressed(OUT / "cost_model.npz", rows=np.array(rows, dtype=np.int64))
+    # 7. seeded streams of the remaining fixture helpers (dense_core.py:152-167,
+    #    strassen_basis.py:140-142) and instrumented FLOP counts (cost_model.py:150-187)
+    kids = st.spawn_rngs(5, 3)
+    counts = []
+    for (n, t, r) in ((8, 4, 16), (16, 4, 24), (8, 2, 7), (6, 1, 1)):
+        shape = cost_model.ProblemShape(n, n, n, t, r)
+        counts.append([n, t, r, cost_model.count_reference_flops(shape),
+                       cost_model.flops_general(shape)])
+    np.savez_compressed(
+        OUT / "streams.npz",
+        chain=strassen_basis.nested_subset_chain(st.make_rng(3)),
+        chain24=strassen_basis.nested_subset_chain(st.make_rng(11), 24),
+        gauss=st.gaussian_matrix(st.make_rng(4), 3, 5),
+        spawn=np.stack([k.standard_normal(4) for k in kids]),
+        unvec=st.unvec_tile(np.arange(16.0), 4),
+        counts=np.array(counts, dtype=np.int64))
     print(f"wrote golden fixtures to {OUT}")
 
 

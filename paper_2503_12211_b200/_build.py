@@ -47,20 +47,39 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+def _compile(src: Path, obj: Path) -> subprocess.CompletedProcess:
+    cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("STL_NVCC_EXTRA", "").split(), "-c", "-o",
+           str(obj), str(src), "-I", str(REPO / "include")]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every .cu into one shared library (skips if up to date)."""
+    """Compile every .cu (in parallel, one object each) and link one shared library (skips if
+    up to date)."""
     if not force and not _stale():
         return LIB_PATH
-    cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("STL_NVCC_EXTRA", "").split(), "-shared", "-o", str(LIB_PATH)]
-    cmd += [str(CSRC / s) for s in SOURCES]
-    cmd += ["-I", str(REPO / "include"), "-lcuda" if False else "-lcudart_static"]
-    proc = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    objs = [objdir / (Path(s).stem + ".o") for s in SOURCES]
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        procs = list(ex.map(lambda so: _compile(CSRC / so[0], so[1]), zip(SOURCES, objs)))
     log = PKG / "build.log"
-    log.write_text(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
-    if proc.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({proc.returncode}); see {log}\n{proc.stderr[-4000:]}")
+    text = "".join(" ".join(p.args) + "\n" + p.stdout + p.stderr for p in procs)
+    bad = [p for p in procs if p.returncode != 0]
+    if not bad:
+        link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
+                str(LIB_PATH), *map(str, objs), "-lcudart_static"]
+        lp = subprocess.run(link, capture_output=True, text=True)
+        text += " ".join(link) + "\n" + lp.stdout + lp.stderr
+        if lp.returncode != 0:
+            bad = [lp]
+    log.write_text(text)
+    if bad:
+        raise RuntimeError(f"nvcc failed ({bad[0].returncode}); see {log}\n{bad[0].stderr[-4000:]}")
     if verbose:
-        print(proc.stderr)
+        print(text)
     return LIB_PATH
 
 

@@ -242,6 +242,19 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
   if (M == 0 || N == 0) return STL_OK;
   int st;
   {
+    const int pf = product_format(bi, bj, bk, t, r, dtype, y_enc_cache == nullptr);
+    void* prod = y_enc_cache ? y_enc_cache : scratch;
+    if (pf == STL_BF16 && (y_enc_cache || scratch_bytes >= 2 * r * bi * bj) &&
+        stl::forward_banded_supported(r, bi, bk, bj, ld_x, ld_y, x, y, x_enc_ws, prod, w_enc,
+                                      e_x, d)) {
+      Prof prof("forward_banded", s, 4);
+      const cudaError_t e = stl::forward_banded(x, ld_x, w_enc, e_x, d, r, bi, bk, bj, x_enc_ws,
+                                                prod, y, ld_y, s);
+      if (e != cudaErrorNotSupported) return check_cuda(e, "banded forward");
+      // (nothing launched: the band-0 encode declined the shape; run the unbanded path)
+    }
+  }
+  {
     Prof prof("encode_x", s);
     st = check_cuda(stl::tiles_to_planes(x, dtype, ld_x, bi, bk, t, e_x, r, x_enc_ws, dtype,
                                          nullptr, STL_F32, nullptr, nullptr, s),

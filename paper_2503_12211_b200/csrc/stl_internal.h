@@ -58,13 +58,18 @@ struct SliceGemmProblem {
   int r;
   int64_t M, N, K;
   void* c2 = nullptr;  // optional bf16 copy of C (tcgen05 path only)
+  // Rows between consecutive slices of A (K-major) and C; 0 = M. A row band of taller planes:
+  // a, c point at the band's first row, M = band rows, m_stride = rows of the whole planes.
+  int64_t m_stride = 0;
 };
 
 int sm_count();
 
 // 3-D bf16 tensor map over `slices` contiguous (outer x inner) matrices, 128B swizzle.
+// slice_bytes: bytes between slices (0 = inner * outer * 2).
 bool make_bf16_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-                    uint64_t slices, uint32_t box_inner, uint32_t box_outer);
+                    uint64_t slices, uint32_t box_inner, uint32_t box_outer,
+                    uint64_t slice_bytes = 0);
 
 // Decode-fused slice GEMM (stl_fused_gemm.cu): y = decode(A_p . B_p, dec), t = 4, bf16.
 bool fused_decode_supported(int t, int r, int64_t M, int64_t N, int64_t K, int ab_dtype,
@@ -75,6 +80,16 @@ cudaError_t fused_gemm_decode(const void* a, const void* b, int b_layout, int r,
                               int y_dtype, void* cache, int cache_dtype, void* scratch,
                               cudaStream_t s);
 cudaError_t cast_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s);
+
+// Band-overlapped bf16 t = 4 forward with bf16 slice products (stl_slice_gemm.cu):
+// x (M x K, ldx) -> x_enc planes (r, bi, bk) -> y_enc planes (r, bi, bj) -> y (M x N, ldy), the
+// encode of band 1 and the decode of band 0 running beside the slice GEMMs of the other band.
+bool forward_banded_supported(int r, int64_t bi, int64_t bk, int64_t bj, int64_t ldx, int64_t ldy,
+                              const void* x, const void* y, const void* x_enc, const void* y_enc,
+                              const void* w_enc, const float* e_x, const float* d);
+cudaError_t forward_banded(const void* x, int64_t ldx, const void* w_enc, const float* e_x,
+                           const float* d, int r, int64_t bi, int64_t bk, int64_t bj,
+                           void* x_enc, void* y_enc, void* y, int64_t ldy, cudaStream_t s);
 
 // tcgen05 path (bf16 operands, aligned shapes). Returns cudaError_t-like code, 0 = ok.
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s);
@@ -124,13 +139,16 @@ cudaError_t planes_to_tiles_mma(const void* in, int idt, int Q, int64_t br, int6
 // HBM-streaming bulk-async t = 4 transforms (stl_stream.cu), tried first for t = 4;
 // cudaErrorNotSupported -> the kernels above. set_transform_stream(false) disables them.
 void set_transform_stream(bool on);
+// plane_rows: tile rows of the whole planes when (m / out, in / out) address a row band of
+// them (0 = br).
 cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
                                    const float* coef, int P, void* out, int odt, const void* rp,
-                                   int rdt, float* ro, float* rw, cudaStream_t s);
+                                   int rdt, float* ro, float* rw, cudaStream_t s,
+                                   int64_t plane_rows = 0);
 cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, int64_t bc,
                                    const float* coef, void* out, int odt, int64_t ldo,
                                    const void* rm, int rdt, int64_t ldr, float* ro, float* rw,
-                                   cudaStream_t s);
+                                   cudaStream_t s, int64_t plane_rows = 0);
 // out[o] = sum_b partial[b * n + o], deterministic fixed-order tree.
 cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t s);
 cudaError_t compose_coefs(const float* a, const float* b, int r, int tt, float* out,

@@ -422,10 +422,11 @@ __device__ __forceinline__ void tc2_mma(uint8_t* sA, uint8_t* sB, uint64_t* full
 // CTA's 128 rows x 32 columns (each warp writes its 32 TMEM lanes) -> one TMA store per plane
 // set and chunk, issued by one thread after a 128-thread barrier (few, large TMA ops: the TMA
 // unit also feeds the mainloop). TMA clips rows >= M / cols >= N. Two staging buffers.
-template <int BN, int MC, class Kd, class S>
+// BN = the accumulator's columns drained here; `col_base` = output column of its column 0.
+template <int BN, class Kd, class S>
 __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUtensorMap* tmC2,
                                              uint8_t* stage_base, uint32_t tmem_acc,
-                                             int& chunk_no, const TileCoord<BN, MC>& tc,
+                                             int& chunk_no, int p, int col_base,
                                              int row_base, int M, int N, bool nostore, int q,
                                              int lane, bool issuer) {
   constexpr int OUT = Kd::OUT;
@@ -441,7 +442,7 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
     if constexpr (kCols == 64) ptx::tmem_ld_32x32b_x32(tmem_acc + c + 32, v2);
     uint8_t* sf = stage_base + (chunk_no & 1) * S::kBufBytes;
     ptx::tmem_ld_wait();
-    const bool active = tc.nb * BN + c < N && row_base < M && !nostore;  // CTA-uniform
+    const bool active = col_base + c < N && row_base < M && !nostore;  // CTA-uniform
     if (active) {
       if constexpr (OUT == kOutF24) {
         // high 16 bits: 64 B rows, 64B-swizzled; low 8 bits: 32 B rows, 32B-swizzled
@@ -507,9 +508,9 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
     if (issuer) ptx::bulk_wait_read<0>();
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (issuer && active) {
-      ptx::tma_store_3d(tmC, sf, tc.nb * BN + c, row_base, tc.p);
+      ptx::tma_store_3d(tmC, sf, col_base + c, row_base, p);
       if constexpr (OUT == kOutF32Bf16 || OUT == kOutF24)
-        ptx::tma_store_3d(tmC2, sf + kSec, tc.nb * BN + c, row_base, tc.p);
+        ptx::tma_store_3d(tmC2, sf + kSec, col_base + c, row_base, p);
       ptx::bulk_commit();
     }
   }
@@ -628,10 +629,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row_base = tc.mb * 256 + static_cast<int>(prank) * 128;
       const uint32_t tmem_acc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       if (tc.prob == 0)
-        tc2_epilogue<BN, MC, K0, S>(&tmC0, &tmC20, stage_base, tmem_acc, chunk_no, tc, row_base,
+        tc2_epilogue<BN, K0, S>(&tmC0, &tmC20, stage_base, tmem_acc, chunk_no, tc.p, tc.nb * BN, row_base,
                                 args.M[0], args.N[0], args.nostore, q, lane, issuer);
       else
-        tc2_epilogue<BN, MC, K1, S>(&tmC1, &tmC21, stage_base, tmem_acc, chunk_no, tc, row_base,
+        tc2_epilogue<BN, K1, S>(&tmC1, &tmC21, stage_base, tmem_acc, chunk_no, tc.p, tc.nb * BN, row_base,
                                 args.M[1], args.N[1], args.nostore, q, lane, issuer);
       ptx::tc_fence_before();
       __syncwarp();
@@ -645,6 +646,468 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, kTmemCols);
+}
+
+// ==================================================================== wide CTA-pair variant
+// The slice GEMM at the bench shapes is bound by L2 -> SM operand traffic, not by the tensor
+// pipe (ncu, 24 x 2048^3: 6.9 KB of LTS traffic per L2 cycle, the practical cap, with the tensor
+// pipe 78% active; profiles/r02_l2probe.md). A 256 x 512 pair tile — two 256 x 256 halves
+// sharing one A box — moves 48 KB per CTA per 64-deep k-block for 8.4 MFLOP (175 FLOP/B)
+// instead of 32 KB for 4.2 MFLOP (128 FLOP/B): 27% less operand traffic per FLOP.
+// The two halves fill all 512 TMEM columns (D0 = columns 0-255, D1 = 256-511), so the
+// accumulator cannot be double-buffered. Instead the MMA issuer runs half 1 `lag` k-blocks
+// behind half 0: half 0 finishes `lag` k-blocks before half 1, the epilogue drains D0 while
+// the MMAs of half 1's last k-blocks run, and drains D1 while the next tile's half-0 MMAs of its
+// first `lag` k-blocks run — both drains overlap tensor work. A k-block's stage is released once
+// half 1 has consumed it, so `lag` + 1 stages are held by the MMA and the rest prefetch.
+// The wave-quantised tail is split: when the last partial wave holds at most half as many wide
+// tiles as there are pairs, those tiles run as two 256-wide half tiles each (D0 only).
+constexpr int kWStages = 4;
+
+template <int OUT0, int OUT1>
+struct SmemW {
+  static constexpr int kStages = kWStages;
+  static constexpr uint32_t kABytes = 128 * kBK * 2;     // this CTA's 128 A rows
+  static constexpr uint32_t kHBytes = 128 * kBK * 2;     // one half's 128 B columns
+  static constexpr uint32_t kBBytes = 2 * kHBytes;
+  static constexpr uint32_t kRing = kStages * (kABytes + kBBytes);
+  static constexpr uint32_t kBufBytes = OutStage<OUT0>::kBytes > OutStage<OUT1>::kBytes
+                                            ? OutStage<OUT0>::kBytes
+                                            : OutStage<OUT1>::kBytes;
+  static constexpr uint32_t kBarOffset = kRing + 2 * kBufBytes;
+  static constexpr uint32_t kTotal = kBarOffset + 512 + 1024;
+};
+
+struct WideArgs {
+  int M[2], N[2], K[2];
+  int r;
+  int total0;   // wide tiles of problem 0
+  int nwide;    // wide tiles of both problems
+  int nsplit;   // trailing wide tiles run as two half tiles each
+  int total;    // tiles scheduled: nwide - nsplit + 2 nsplit
+  int lag;      // k-blocks half 1 runs behind half 0 (0 .. kWStages - 2)
+  int nostore;
+  int rev;      // slices in descending order (the slices of the previous launch are L2-warm)
+};
+
+struct WTile {
+  int prob, p, mb, n0, nh, num_kb;
+  int hoff1;  // column offset of the second half (256), or of the single half of a split tile
+};
+
+__device__ __forceinline__ WTile wide_tile(const WideArgs& g, int tile) {
+  WTile w;
+  int wt = tile, half = -1;
+  const int first_split = g.nwide - g.nsplit;
+  if (tile >= first_split) {
+    wt = first_split + ((tile - first_split) >> 1);
+    half = (tile - first_split) & 1;
+  }
+  w.prob = wt >= g.total0 ? 1 : 0;
+  const int local = w.prob ? wt - g.total0 : wt;
+  const int N = g.N[w.prob];
+  const int n_sup = (N + 511) / 512;
+  const int per_slice = ((g.M[w.prob] + 255) / 256) * n_sup;
+  w.p = local / per_slice;
+  const int rem = local - w.p * per_slice;
+  if (g.rev) w.p = g.r - 1 - w.p;
+  w.mb = rem / n_sup;
+  const int nbw = rem - w.mb * n_sup;
+  w.n0 = nbw * 512 + (half > 0 ? 256 : 0);
+  w.nh = (half >= 0 || w.n0 + 256 >= N) ? 1 : 2;
+  w.hoff1 = 256;
+  w.num_kb = (g.K[w.prob] + kBK - 1) / kBK;
+  return w;
+}
+
+// TMA producer of one wide tile: per k-block this CTA's 128 A rows and, per half, its 128 B
+// columns (both CTAs issue; transaction bytes land on the even CTA's barrier).
+template <class Kd, class S>
+__device__ __forceinline__ void wide_produce(const CUtensorMap* tmA, const CUtensorMap* tmB,
+                                             uint8_t* sA, uint8_t* sB, uint64_t* full,
+                                             uint64_t* empty, uint32_t& kbg, const WTile& w,
+                                             uint32_t prank) {
+  const bool leader = prank == 0;
+  const int m0 = w.mb * 256 + static_cast<int>(prank) * 128;
+  for (int kb = 0; kb < w.num_kb; ++kb, ++kbg) {
+    const uint32_t stage = kbg % S::kStages, phase = (kbg / S::kStages) & 1;
+    ptx::mbar_wait(&empty[stage], phase ^ 1);
+    if (leader)
+      ptx::mbar_arrive_expect_tx(&full[stage], 2 * (S::kABytes + w.nh * S::kHBytes));
+    uint8_t* a = sA + stage * S::kABytes;
+    if constexpr (!Kd::A_MN) {
+      ptx::tma_load_3d_2sm(tmA, &full[stage], a, kb * kBK, m0, w.p);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        ptx::tma_load_3d_2sm(tmA, &full[stage], a + j * (64 * kBK * 2), m0 + j * 64, kb * kBK,
+                             w.p);
+    }
+    for (int h = 0; h < w.nh; ++h) {
+      uint8_t* b = sB + stage * S::kBBytes + h * S::kHBytes;
+      const int n = w.n0 + h * w.hoff1 + static_cast<int>(prank) * 128;
+      if constexpr (!Kd::B_MN) {
+        ptx::tma_load_3d_2sm(tmB, &full[stage], b, kb * kBK, n, w.p);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          ptx::tma_load_3d_2sm(tmB, &full[stage], b + j * (64 * kBK * 2), n + j * 64, kb * kBK,
+                               w.p);
+      }
+    }
+    if (!leader) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0u));
+  }
+}
+
+// The 4 pair MMAs (K = 16 each) of one k-block into one 256-column half.
+template <class Kd, class S>
+__device__ __forceinline__ void wide_mma_kblock(uint32_t a_addr, uint32_t b_addr, uint32_t d_tmem,
+                                                bool first) {
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(256, 256, Kd::A_MN, Kd::B_MN);
+#pragma unroll
+  for (int k = 0; k < kBK / 16; ++k) {
+    const uint64_t ad = Kd::A_MN ? ptx::smem_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
+                                 : ptx::smem_desc_sw128(a_addr + k * 32, 16, 1024);
+    const uint64_t bd = Kd::B_MN ? ptx::smem_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
+                                 : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
+    ptx::mma_bf16_ss_2sm(d_tmem, ad, bd, kIdesc, (first && k == 0) ? 0u : 1u);
+  }
+}
+
+// MMA issue of one wide tile (even CTA, one thread), half 1 `lag` k-blocks behind half 0.
+template <class Kd, class S>
+__device__ __forceinline__ void wide_mma(uint8_t* sA, uint8_t* sB, uint64_t* full, uint64_t* empty,
+                                         uint64_t* tfull, uint64_t* tempty, uint32_t& kbg,
+                                         uint32_t& n0, uint32_t& n1, uint32_t tmem_base,
+                                         const WTile& w, int lag) {
+  const int L = w.nh == 2 ? lag : 0;
+  const uint32_t kb0 = kbg;  // global k-block index of this tile's k-block 0
+  for (int j = 0; j < w.num_kb + L; ++j) {
+    if (j < w.num_kb) {
+      const uint32_t g = kb0 + j, stage = g % S::kStages;
+      ptx::mbar_wait(&full[stage], (g / S::kStages) & 1);
+      if (j == 0) ptx::mbar_wait(&tempty[0], (n0 & 1) ^ 1);
+      ptx::tc_fence_after();
+      wide_mma_kblock<Kd, S>(ptx::smem_u32(sA + stage * S::kABytes),
+                             ptx::smem_u32(sB + stage * S::kBBytes), tmem_base, j == 0);
+      if (w.nh == 1) ptx::mma_commit_2sm(&empty[stage], 0x3);
+      if (j == w.num_kb - 1) ptx::mma_commit_2sm(&tfull[0], 0x3);
+    }
+    const int kb = j - L;
+    if (w.nh == 2 && kb >= 0) {
+      const uint32_t g = kb0 + kb, stage = g % S::kStages;
+      if (L == 0) {
+        // (full already waited above for this k-block)
+      }
+      if (kb == 0) {
+        ptx::mbar_wait(&tempty[1], (n1 & 1) ^ 1);
+        ptx::tc_fence_after();
+      }
+      wide_mma_kblock<Kd, S>(ptx::smem_u32(sA + stage * S::kABytes),
+                             ptx::smem_u32(sB + stage * S::kBBytes + S::kHBytes),
+                             tmem_base + 256, kb == 0);
+      ptx::mma_commit_2sm(&empty[stage], 0x3);
+    }
+  }
+  if (w.nh == 2) {
+    ptx::mma_commit_2sm(&tfull[1], 0x3);
+    ++n1;
+  }
+  ++n0;
+  kbg = kb0 + w.num_kb;
+}
+
+// ------------------------------------------------------------ side transforms (band overlap)
+// The forward on row bands (DESIGN.md §4 K8): while the tensor cores run band b's slice GEMMs,
+// eight warps per CTA (2, 3 — idle in the GEMM pipeline — and 8 .. 13) encode band b+1 of X
+// (mode 1) or decode band b-1 of Y_enc (mode 2), straight from and to global memory (the ring
+// and the staging buffers fill shared memory). The math is the streaming kernels' own
+// mma.sync formulation (stl_stream.cu): the fp32 coefficients split hi + lo in registers,
+// m16n8k16 bf16 MMAs with fp32 accumulation, the same fragments and the same MMA order — so a
+// banded forward is bit-identical to the unbanded one. A unit is 64 consecutive tiles of one
+// tile row; a warp loads its fragments straight from global memory (4-byte loads: per
+// instruction two 64-byte runs (encode) or four 32-byte runs (decode)), and writes plane rows
+// as 16-byte runs (encode) or matrix rows as 128-byte runs (decode: one shuffle pairs the
+// column halves of each tile).
+constexpr int kSideWarps = 8;       // side warps per CTA: 2, 3 and 8 .. 13
+constexpr int kSideThreads = 32 * (6 + kSideWarps);
+struct SideArgs {
+  int mode;                    // 0 none, 1 encode, 2 decode
+  int P;                       // rank (<= 32)
+  const __nv_bfloat16* src;    // encode: X (row-major, ld); decode: Y_enc planes
+  __nv_bfloat16* dst;          // encode: X_enc planes;       decode: Y (row-major, ld)
+  const float* coef;           // e_x (encode) or d (decode): (P, 16) fp32, device
+  int64_t ld;                  // leading dim of the row-major matrix (elements)
+  int64_t plane_stride;        // elements between planes (all tile rows x bc)
+  int I0, I1;                  // tile rows [I0, I1) of this launch's side work
+  int bc;                      // tiles per row (multiple of 64)
+};
+
+__device__ __forceinline__ uint32_t side_pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void side_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  lo = side_pack2(x0 - hf.x, x1 - hf.y);
+}
+__device__ __forceinline__ void side_mma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t ld_nc32(const void* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// Encode: C^T[p][tile] = E . X^T per 8-tile n-tile (A = E: 16 planes x 16 c; B = X fragment:
+// b0 = X[tile 8n + g][c 2q, 2q+1] = row q>>1, b1 = row 2 + (q>>1)); planes 16m + g (+8).
+template <int MT>
+__device__ __forceinline__ void side_encode(const SideArgs& a, int wid, int nw, int lane) {
+  const int g = lane >> 2, q = lane & 3;
+  uint32_t fh[MT][4], fl[MT][4];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int p = 16 * m + g + 8 * (i & 1), c = 2 * q + 8 * (i >> 1);
+      const float e0 = p < a.P ? __ldg(a.coef + p * 16 + c) : 0.f;
+      const float e1 = p < a.P ? __ldg(a.coef + p * 16 + c + 1) : 0.f;
+      side_split2(e0, e1, fh[m][i], fl[m][i]);
+    }
+  const bool ok0 = 16 * (MT - 1) + g < a.P, ok1 = 16 * (MT - 1) + g + 8 < a.P;
+  const int upr = a.bc >> 6;
+  const int64_t units = static_cast<int64_t>(a.I1 - a.I0) * upr;
+  for (int64_t u = wid; u < units; u += nw) {
+    const int I = a.I0 + static_cast<int>(u / upr), J0 = static_cast<int>(u % upr) * 64;
+    const __nv_bfloat16* xr =
+        a.src + static_cast<int64_t>(4 * I + (q >> 1)) * a.ld + 4 * (J0 + g) + 2 * (q & 1);
+    uint32_t b0[8], b1[8];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      b0[n] = ld_nc32(xr + 32 * n);
+      b1[n] = ld_nc32(xr + 2 * a.ld + 32 * n);
+    }
+    __nv_bfloat16* o = a.dst + static_cast<int64_t>(I) * a.bc + J0 + 2 * q;
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        float c[4] = {0.f, 0.f, 0.f, 0.f};
+        side_mma(c, fh[m][0], fh[m][1], fh[m][2], fh[m][3], b0[n], b1[n]);
+        side_mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0[n], b1[n]);
+        __nv_bfloat16* op = o + (16 * m + g) * a.plane_stride + 8 * n;
+        if (m < MT - 1 || ok0) *reinterpret_cast<uint32_t*>(op) = side_pack2(c[0], c[1]);
+        if (m < MT - 1 || ok1)
+          *reinterpret_cast<uint32_t*>(op + 8 * a.plane_stride) = side_pack2(c[2], c[3]);
+      }
+  }
+}
+
+// Decode: C[tile][c] = Z^T . D per 16-tile m-tile; rows g / g+8 <-> tiles 2g / 2g+1, so each
+// plane load is one 4-byte access holding both tiles, regrouped into A fragments with PRMT.
+template <int MT>
+__device__ __forceinline__ void side_decode(const SideArgs& a, int wid, int nw, int lane) {
+  const int g = lane >> 2, q = lane & 3;
+  uint32_t fh[MT][4], fl[MT][4];
+#pragma unroll
+  for (int ks = 0; ks < MT; ++ks)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // i = nt * 2 + h
+      const int nt = i >> 1, h = i & 1, c = 8 * nt + g;
+      const int pa = 16 * ks + 2 * q + 8 * h, pb = pa + 1;
+      const float d0 = pa < a.P ? __ldg(a.coef + pa * 16 + c) : 0.f;
+      const float d1 = pb < a.P ? __ldg(a.coef + pb * 16 + c) : 0.f;
+      side_split2(d0, d1, fh[ks][i], fl[ks][i]);
+    }
+  bool dok[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) dok[j] = 16 * (MT - 1) + 2 * q + (j & 1) + 8 * (j >> 1) < a.P;
+  const int upr = a.bc >> 6;
+  const int64_t units = static_cast<int64_t>(a.I1 - a.I0) * upr;
+  for (int64_t u = wid; u < units; u += nw) {
+    const int I = a.I0 + static_cast<int>(u / upr), J0 = static_cast<int>(u % upr) * 64;
+    const __nv_bfloat16* zr = a.src + static_cast<int64_t>(I) * a.bc + J0 + 2 * g;
+    uint32_t w[4][MT][4];  // [m-tile][k-step][planes 2q, 2q+1, 2q+8, 2q+9]
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int ks = 0; ks < MT; ++ks)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pl = 16 * ks + 2 * q + (j & 1) + 8 * (j >> 1);
+          w[k][ks][j] = (ks < MT - 1 || dok[j]) ? ld_nc32(zr + pl * a.plane_stride + 16 * k) : 0u;
+        }
+    __nv_bfloat16* orow = a.dst + static_cast<int64_t>(4 * I) * a.ld + 4 * J0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int ks = 0; ks < MT; ++ks) {
+        const uint32_t* wk = w[k][ks];
+        const uint32_t a0 = __byte_perm(wk[0], wk[1], 0x5410), a1 = __byte_perm(wk[0], wk[1], 0x7632);
+        const uint32_t a2 = __byte_perm(wk[2], wk[3], 0x5410), a3 = __byte_perm(wk[2], wk[3], 0x7632);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          side_mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
+          side_mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
+        }
+      }
+      // acc[nt][0,1]: tile 2g, c = 8nt + 2q (+1) = row 2nt + (q>>1), cols 2(q&1) (+1);
+      // acc[nt][2,3]: tile 2g + 1. Pair the column halves with the q^1 lane: 8-byte stores.
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const uint32_t uu = side_pack2(acc[nt][0], acc[nt][1]), vv = side_pack2(acc[nt][2], acc[nt][3]);
+        const uint32_t send = (q & 1) ? uu : vv;
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
+        const int row = 2 * nt + (q >> 1);
+        const int tile = 16 * k + 2 * g + (q & 1);
+        const uint2 val = (q & 1) ? make_uint2(recv, vv) : make_uint2(uu, recv);
+        *reinterpret_cast<uint2*>(orow + row * a.ld + 4 * tile) = val;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void side_work(const SideArgs& a, int wid_in_cta, int warps_per_cta,
+                                          int lane) {
+  const int nw = warps_per_cta * gridDim.x;
+  const int wid = blockIdx.x * warps_per_cta + wid_in_cta;
+  const int mt = (a.P + 15) / 16;
+  if (a.mode == 1) {
+    if (mt == 1) side_encode<1>(a, wid, nw, lane);
+    else if (mt == 2) side_encode<2>(a, wid, nw, lane);
+  } else if (a.mode == 2) {
+    if (mt == 1) side_decode<1>(a, wid, nw, lane);
+    else if (mt == 2) side_decode<2>(a, wid, nw, lane);
+  }
+}
+
+template <class K0, class K1, bool SIDE>
+__global__ void __launch_bounds__(SIDE ? kSideThreads : kThreads, 1)
+    slice_gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA0,
+                           const __grid_constant__ CUtensorMap tmB0,
+                           const __grid_constant__ CUtensorMap tmC0,
+                           const __grid_constant__ CUtensorMap tmC20,
+                           const __grid_constant__ CUtensorMap tmA1,
+                           const __grid_constant__ CUtensorMap tmB1,
+                           const __grid_constant__ CUtensorMap tmC1,
+                           const __grid_constant__ CUtensorMap tmC21, WideArgs args,
+                           const __grid_constant__ SideArgs side) {
+  using S = SmemW<K0::OUT, K1::OUT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S::kStages * S::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty = full + S::kStages;
+  uint64_t* tfull = empty + S::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const uint32_t prank = rank & 1u;
+  const bool leader = prank == 0;
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int total = args.total;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA0);
+    ptx::prefetch_tmap(&tmB0);
+    if (args.nwide > args.total0) {
+      ptx::prefetch_tmap(&tmA1);
+      ptx::prefetch_tmap(&tmB1);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < S::kStages; ++s) {
+      ptx::mbar_init(&full[s], 2);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 8);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, 512);
+  griddep_launch_dependents();
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t kbg = 0;
+      for (int tile = cluster; tile < total; tile += nclusters) {
+        const WTile w = wide_tile(args, tile);
+        if (w.prob == 0)
+          wide_produce<K0, S>(&tmA0, &tmB0, sA, sB, full, empty, kbg, w, prank);
+        else
+          wide_produce<K1, S>(&tmA1, &tmB1, sA, sB, full, empty, kbg, w, prank);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      uint32_t kbg = 0, n0 = 0, n1 = 0;
+      for (int tile = cluster; tile < total; tile += nclusters) {
+        const WTile w = wide_tile(args, tile);
+        if (w.prob == 0)
+          wide_mma<K0, S>(sA, sB, full, empty, tfull, tempty, kbg, n0, n1, tmem_base, w, args.lag);
+        else
+          wide_mma<K1, S>(sA, sB, full, empty, tfull, tempty, kbg, n0, n1, tmem_base, w, args.lag);
+      }
+    }
+  } else if (warp == 2 || warp == 3 || warp >= 8) {
+    // side warps 2, 3, 8 .. 13 (two per SM sub-partition)
+    if constexpr (SIDE) side_work(side, warp >= 8 ? warp - 6 : warp - 2, kSideWarps, lane);
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const bool issuer = warp == 4 && lane == 0;
+    int chunk_no = 0;
+    uint32_t n0 = 0, n1 = 0;
+    uint8_t* stage_base = smem + S::kRing;
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    for (int tile = cluster; tile < total; tile += nclusters) {
+      const WTile w = wide_tile(args, tile);
+      const int row_base = w.mb * 256 + static_cast<int>(prank) * 128;
+      for (int h = 0; h < w.nh; ++h) {
+        const uint32_t n = h ? n1++ : n0++;
+        ptx::mbar_wait(&tfull[h], n & 1);
+        ptx::tc_fence_after();
+        const int col = w.n0 + h * w.hoff1;
+        if (w.prob == 0)
+          tc2_epilogue<256, K0, S>(&tmC0, &tmC20, stage_base, lane_base + h * 256, chunk_no, w.p,
+                                   col, row_base, args.M[0], args.N[0], args.nostore, q, lane,
+                                   issuer);
+        else
+          tc2_epilogue<256, K1, S>(&tmC1, &tmC21, stage_base, lane_base + h * 256, chunk_no, w.p,
+                                   col, row_base, args.M[1], args.N[1], args.nostore, q, lane,
+                                   issuer);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[h]), rank & ~1u));
+      }
+    }
+    if (issuer) ptx::bulk_wait_all();
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, 512);
 }
 
 // ------------------------------------------------------------------ host side
@@ -668,8 +1131,8 @@ EncodeTiledFn get_encode_fn() {
 }
 
 bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t slices,
-               uint32_t box_outer) {
-  return make_bf16_tmap(m, base, inner, outer, slices, 64, box_outer);
+               uint32_t box_outer, uint64_t slice_bytes = 0) {
+  return make_bf16_tmap(m, base, inner, outer, slices, 64, box_outer, slice_bytes);
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -695,11 +1158,11 @@ cudaError_t launch_tc(const SliceGemmProblem& pb, cudaStream_t s) {
 // 3-D (N, M, r) store map for 128-row x 32-column output chunks: es = 4 (fp32, 128B swizzle),
 // 2 (16-bit, 64B swizzle) or 1 (8-bit, 32B swizzle).
 bool make_out_tmap(CUtensorMap* m, const void* base, int es, uint64_t N, uint64_t M, uint64_t r,
-                   uint32_t cols = 32) {
+                   uint32_t cols = 32, uint64_t slice_rows = 0) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {N, M, r};
-  cuuint64_t strides[2] = {N * es, N * M * es};
+  cuuint64_t strides[2] = {N * es, N * (slice_rows ? slice_rows : M) * es};
   cuuint32_t box[3] = {cols, 128, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   const CUtensorMapDataType dt = es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
@@ -722,20 +1185,22 @@ struct Tc2Maps {
 template <int BN, int MC, class Kd>
 bool make_tc2_maps(const SliceGemmProblem& pb, Tc2Maps* m) {
   const uint64_t M = pb.M, N = pb.N, K = pb.K, r = pb.r;
+  const uint64_t ms = pb.m_stride ? pb.m_stride : M;  // rows between slices of A and C
+  if (pb.m_stride && Kd::A_MN) return false;
   // K-major A: one 128-row box per CTA, or (MC = 2) a 64-row half multicast to both pairs
   bool ok = Kd::A_MN ? make_tmap(&m->a, pb.a, M, K, r, kBK)
-                     : make_tmap(&m->a, pb.a, K, M, r, MC == 2 ? 64 : 128);
+                     : make_tmap(&m->a, pb.a, K, M, r, MC == 2 ? 64 : 128, ms * K * 2);
   ok = ok && (Kd::B_MN ? make_tmap(&m->b, pb.b, N, K, r, kBK)
                        : make_tmap(&m->b, pb.b, K, N, r, BN / 2));
   if (Kd::OUT == kOutBf16) {
-    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r, 64);  // 64-column chunks, 128 B rows
+    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r, 64, ms);  // 64-column chunks, 128 B rows
     m->c2 = m->c;
   } else if (Kd::OUT == kOutF24) {
-    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r) &&
-         make_out_tmap(&m->c2, static_cast<uint8_t*>(pb.c) + 2 * r * M * N, 1, N, M, r);
+    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r, 32, ms) &&
+         make_out_tmap(&m->c2, static_cast<uint8_t*>(pb.c) + 2 * r * ms * N, 1, N, M, r, 32, ms);
   } else {
-    ok = ok && make_out_tmap(&m->c, pb.c, 4, N, M, r);
-    if (Kd::OUT == kOutF32Bf16) ok = ok && make_out_tmap(&m->c2, pb.c2, 2, N, M, r);
+    ok = ok && make_out_tmap(&m->c, pb.c, 4, N, M, r, 32, ms);
+    if (Kd::OUT == kOutF32Bf16) ok = ok && make_out_tmap(&m->c2, pb.c2, 2, N, M, r, 32, ms);
     else m->c2 = m->c;
   }
   return ok;
@@ -827,6 +1292,81 @@ cudaError_t launch_tc2_group_mc(const SliceGemmProblem* pbs, int np, cudaStream_
   return le;
 }
 
+// Wide-tile launch (256 x 512 pair tiles) of np (1 or 2) problems; see slice_gemm_wide_kernel.
+int64_t wide_tiles(const SliceGemmProblem& pb) {
+  return static_cast<int64_t>(pb.r) * ((pb.M + 255) / 256) * ((pb.N + 511) / 512);
+}
+
+template <class K0, class K1, bool SIDE = false>
+cudaError_t launch_wide_group(const SliceGemmProblem* pbs, int np, cudaStream_t s,
+                              const SideArgs* side = nullptr, int rev = 0) {
+  Tc2Maps m0, m1;
+  bool ok = make_tc2_maps<256, 1, K0>(pbs[0], &m0);
+  if (np > 1) ok = ok && make_tc2_maps<256, 1, K1>(pbs[1], &m1);
+  else m1 = m0;
+  if (!ok) return cudaErrorInvalidValue;
+  auto kern = slice_gemm_wide_kernel<K0, K1, SIDE>;
+  const int smem = SmemW<K0::OUT, K1::OUT>::kTotal;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t t0 = wide_tiles(pbs[0]);
+  const int64_t nwide = t0 + (np > 1 ? wide_tiles(pbs[1]) : 0);
+  if (nwide <= 0) return cudaSuccess;
+  if (nwide >= (int64_t(1) << 30)) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.blockDim = dim3(SIDE ? kSideThreads : kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  static int max_clusters = 0;
+  if (!max_clusters) {
+    cfg.gridDim = dim3(2 * (sm_count() / 2));
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = sm_count() / 2;
+    max_clusters = n;
+  }
+  static const int lag = env_int("STL_GEMM_LAG", 1);
+  static const int nosplit = env_int("STL_GEMM_NOSPLIT", 0);
+  WideArgs wa{};
+  for (int i = 0; i < 2; ++i) {
+    const SliceGemmProblem& pb = pbs[i < np ? i : 0];
+    wa.M[i] = static_cast<int>(pb.M);
+    wa.N[i] = static_cast<int>(pb.N);
+    wa.K[i] = static_cast<int>(pb.K);
+  }
+  wa.r = pbs[0].r;
+  wa.total0 = static_cast<int>(t0);
+  wa.nwide = static_cast<int>(nwide);
+  const int clusters = static_cast<int>(nwide < max_clusters ? nwide : max_clusters);
+  const int rem = static_cast<int>(nwide % clusters);
+  // split the last partial wave into half tiles when they fit one wave
+  wa.nsplit = (!nosplit && rem > 0 && 2 * rem <= clusters) ? rem : 0;
+  wa.total = wa.nwide + wa.nsplit;
+  wa.lag = lag < 0 ? 0 : (lag > kWStages - 2 ? kWStages - 2 : lag);
+  static const int nostore = env_int("STL_GEMM_NOSTORE", 0);
+  wa.nostore = nostore;
+  wa.rev = np == 1 ? rev : 0;
+  cfg.gridDim = dim3(2 * clusters);
+  SideArgs sa{};
+  if (side) sa = *side;
+  return cudaLaunchKernelEx(&cfg, kern, m0.a, m0.b, m0.c, m0.c2, m1.a, m1.b, m1.c, m1.c2, wa, sa);
+}
+
+// Wide tiles for problems whose output is at least one wide tile across (N >= 512) and whose
+// output mode the wide kernel stages (fp32, bf16, F24; not the fp32 + bf16 copy).
+bool wide_eligible(const SliceGemmProblem& pb) {
+  static const int off = env_int("STL_GEMM_NOWIDE", 0);
+  return !off && pb.N >= 512 && pb.M > 128 && !pb.c2 && pb.c_dtype != kF32;
+}
+
 // STL_GEMM_MC = 2 (opt-in): four-CTA clusters, two pairs sharing A by TMA multicast. Measured:
 // ~8% more work per SM, but only 33 such clusters are co-resident (clusters live inside a GPC:
 // 132 of 148 SMs), net -3%; running a pair-cluster launch beside it on the 16 left-over SMs
@@ -840,6 +1380,18 @@ cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s
 
 template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch_tc2_any(const SliceGemmProblem& pb, cudaStream_t s) {
+  if (BN == 256 && wide_eligible(pb)) {
+    if (pb.c_dtype == kBF16) {
+      using Kd = GemmKind<A_MN, B_MN, kOutBf16>;
+      return launch_wide_group<Kd, Kd>(&pb, 1, s);
+    }
+    if (pb.c_dtype == kF24) {
+      using Kd = GemmKind<A_MN, B_MN, kOutF24>;
+      return launch_wide_group<Kd, Kd>(&pb, 1, s);
+    }
+    using Kd = GemmKind<A_MN, B_MN, kOutF32>;
+    return launch_wide_group<Kd, Kd>(&pb, 1, s);
+  }
   if (pb.c_dtype == kBF16) {
     using Kd = GemmKind<A_MN, B_MN, kOutBf16>;
     return launch_tc2_group<BN, Kd, Kd>(&pb, 1, s);
@@ -859,11 +1411,12 @@ cudaError_t launch_tc2_any(const SliceGemmProblem& pb, cudaStream_t s) {
 }  // namespace
 
 bool make_bf16_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-                    uint64_t slices, uint32_t box_inner, uint32_t box_outer) {
+                    uint64_t slices, uint32_t box_inner, uint32_t box_outer,
+                    uint64_t slice_bytes) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {inner, outer, slices};
-  cuuint64_t strides[2] = {inner * 2, inner * outer * 2};
+  cuuint64_t strides[2] = {inner * 2, slice_bytes ? slice_bytes : inner * outer * 2};
   cuuint32_t box[3] = {box_inner, box_outer, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult res = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
@@ -935,9 +1488,111 @@ cudaError_t slice_gemm_tc_group(const SliceGemmProblem& p0, const SliceGemmProbl
   if (!slice_gemm_tc_group_supported(p0, p1)) return cudaErrorNotSupported;
   const SliceGemmProblem pbs[2] = {p0, p1};
   using K0 = GemmKind<true, true, kOutF32>;
+  if (wide_eligible(p0) && wide_eligible(p1)) {
+    if (p1.c_dtype == kF24) return launch_wide_group<K0, GemmKind<false, true, kOutF24>>(pbs, 2, s);
+    if (p1.c_dtype == kBF16) return launch_wide_group<K0, GemmKind<false, true, kOutBf16>>(pbs, 2, s);
+    return launch_wide_group<K0, GemmKind<false, true, kOutF32>>(pbs, 2, s);
+  }
   if (p1.c_dtype == kF24) return launch_tc2_group<256, K0, GemmKind<false, true, kOutF24>>(pbs, 2, s);
   if (p1.c_dtype == kBF16) return launch_tc2_group<256, K0, GemmKind<false, true, kOutBf16>>(pbs, 2, s);
   return launch_tc2_group<256, K0, GemmKind<false, true, kOutF32>>(pbs, 2, s);
+}
+
+// ------------------------------------------------------------ band-overlapped forward
+namespace {
+bool al16p(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+}  // namespace
+
+bool forward_banded_supported(int r, int64_t bi, int64_t bk, int64_t bj, int64_t ldx, int64_t ldy,
+                              const void* x, const void* y, const void* x_enc, const void* y_enc,
+                              const void* w_enc, const float* e_x, const float* d) {
+  // measured a wash (profiles/r02_band_overlap_*.log): opt-in only
+  static const int on = env_int("STL_BAND", 0);
+  if (!on || env_int("STL_GEMM_NOWIDE", 0)) return false;
+  return r >= 1 && r <= 32 && bi >= 512 && bk % 64 == 0 && bk >= 256 && bj % 64 == 0 &&
+         bj >= 512 && bi < (int64_t(1) << 30) && ldx % 8 == 0 && ldy % 8 == 0 && al16p(x) &&
+         al16p(y) && al16p(x_enc) && al16p(y_enc) && al16p(w_enc) && al16p(e_x) && al16p(d) &&
+         get_encode_fn() != nullptr;
+}
+
+// encode(band 0) -> [slice GEMMs(band 0) | warps 2-3: encode(band 1)]
+//                -> [slice GEMMs(band 1) | warps 2-3: decode(band 0)] -> decode(band 1).
+// Bands are whole 256-row blocks of the tile grid; band 0 = the first half (STL_BAND0_MB
+// overrides). Two of the four transform passes run under the tensor-core work; the band-1
+// GEMM re-reads W_enc (its p-major order is reversed so the slices the band-0 GEMM read last
+// are still in L2).
+cudaError_t forward_banded(const void* x, int64_t ldx, const void* w_enc, const float* e_x,
+                           const float* d, int r, int64_t bi, int64_t bk, int64_t bj,
+                           void* x_enc, void* y_enc, void* y, int64_t ldy, cudaStream_t s) {
+  const int64_t nmb = (bi + 255) / 256;
+  static const int b0 = env_int("STL_BAND0_MB", 0);
+  int64_t mb0 = b0 > 0 ? b0 : nmb / 2;
+  if (mb0 < 1) mb0 = 1;
+  if (mb0 >= nmb) mb0 = nmb - 1;
+  const int64_t Ib = mb0 * 256;
+  // probes (timing only): STL_BAND_PROFILE prints per-launch times; STL_BAND_NOSIDE=1/2 drops
+  // the side encode / decode (wrong results)
+  static const int prof = env_int("STL_BAND_PROFILE", 0), noside = env_int("STL_BAND_NOSIDE", 0);
+  cudaEvent_t ev[5];
+  if (prof)
+    for (auto& v : ev) cudaEventCreate(&v);
+  if (prof) cudaEventRecord(ev[0], s);
+  const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
+  __nv_bfloat16* xe = static_cast<__nv_bfloat16*>(x_enc);
+  __nv_bfloat16* ye = static_cast<__nv_bfloat16*>(y_enc);
+  __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(y);
+  cudaError_t e = tiles_to_planes_stream(x, kBF16, ldx, Ib, bk, e_x, r, x_enc, kBF16, nullptr,
+                                         kBF16, nullptr, nullptr, s, bi);
+  if (e != cudaSuccess) return e;
+  if (prof) cudaEventRecord(ev[1], s);
+  using Kd = GemmKind<false, false, kOutBf16>;
+  SliceGemmProblem p0{x_enc, 0, w_enc, 0, y_enc, kBF16, kBF16, r, Ib, bj, bk};
+  p0.m_stride = bi;
+  SideArgs se{};
+  se.mode = 1;
+  se.P = r;
+  se.src = xb;
+  se.dst = xe;
+  se.coef = e_x;
+  se.ld = ldx;
+  se.plane_stride = bi * bk;
+  se.I0 = static_cast<int>(Ib);
+  se.I1 = static_cast<int>(bi);
+  se.bc = static_cast<int>(bk);
+  if (noside & 1) se.mode = 0;
+  e = launch_wide_group<Kd, Kd, true>(&p0, 1, s, &se);
+  if (e != cudaSuccess) return e;
+  if (prof) cudaEventRecord(ev[2], s);
+  SliceGemmProblem p1{xe + Ib * bk, 0, w_enc, 0, ye + Ib * bj, kBF16, kBF16, r, bi - Ib, bj, bk};
+  p1.m_stride = bi;
+  SideArgs sd{};
+  sd.mode = 2;
+  sd.P = r;
+  sd.src = ye;
+  sd.dst = yb;
+  sd.coef = d;
+  sd.ld = ldy;
+  sd.plane_stride = bi * bj;
+  sd.I0 = 0;
+  sd.I1 = static_cast<int>(Ib);
+  sd.bc = static_cast<int>(bj);
+  static const int rev = env_int("STL_BAND_REV", 1);
+  if (noside & 2) sd.mode = 0;
+  e = launch_wide_group<Kd, Kd, true>(&p1, 1, s, &sd, rev);
+  if (e != cudaSuccess) return e;
+  if (prof) cudaEventRecord(ev[3], s);
+  e = planes_to_tiles_stream(ye + Ib * bj, kBF16, r, bi - Ib, bj, d, yb + 4 * Ib * ldy, kBF16,
+                             ldy, nullptr, kBF16, 0, nullptr, nullptr, s, bi);
+  if (prof) {
+    cudaEventRecord(ev[4], s);
+    cudaEventSynchronize(ev[4]);
+    float t[4];
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    fprintf(stderr, "[band] mb0=%lld enc0 %.1f us | gemm0+enc1 %.1f | gemm1+dec0 %.1f | dec1 %.1f\n",
+            (long long)mb0, 1e3 * t[0], 1e3 * t[1], 1e3 * t[2], 1e3 * t[3]);
+    for (auto& v : ev) cudaEventDestroy(v);
+  }
+  return e;
 }
 
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {

@@ -110,6 +110,7 @@ struct StreamArgs {
   int64_t upr;               // units per tile row (1 when R > 1)
   int R;                     // tile rows per unit: kT / bc for narrow matrices (bc | kT), else 1
   int64_t nunits;
+  int64_t prow;              // tile rows between planes (>= br: a row band of taller planes)
   int stg;                   // 1: consumers write outputs with st.global (else TMA/bulk stores)
   int nocompute;             // probe: skip the math (pure data movement)
   unsigned long long* dbg;   // probe: per-CTA phase timers [grid][4] (ns), or null
@@ -760,7 +761,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 
 // 4-D plane map (W tiles, P planes, bc/W chunks, br rows) with box {W, P, kT/W, 1}, 128B swizzle.
 bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_t br, int64_t bc,
-                int kT, int R) {
+                int kT, int R, int64_t prow) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -777,7 +778,7 @@ bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_
   const uint64_t W = 128 / zsz;
   cuuint64_t dims[4] = {W, static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(bc / W),
                         static_cast<cuuint64_t>(br)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(br * bc * zsz), 128,
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(prow * bc * zsz), 128,
                            static_cast<cuuint64_t>(bc * zsz)};
   // one unit: kT / W chunks of one tile row, or (R > 1) all bc / W chunks of R tile rows
   cuuint32_t box[4] = {static_cast<cuuint32_t>(W), static_cast<cuuint32_t>(Pb),
@@ -812,14 +813,16 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
                     : 1;
   a.R = R;
   CUtensorMap tin{}, tin2{}, tout{};
+  if (a.prow < a.br) a.prow = a.br;
+  if (a.prow != a.br && (stg || R > 1)) return cudaErrorNotSupported;  // band: TMA, 1-row units
   if (has_planes_in<MODE>() &&
-      !plane_tmap(&tin, planes_in, zhi<ZT>(), a.P, a.Pb, a.br, a.bc, kT, R))
+      !plane_tmap(&tin, planes_in, zhi<ZT>(), a.P, a.Pb, a.br, a.bc, kT, R, a.prow))
     return cudaErrorNotSupported;
   if (is_f24<ZT>() &&
-      !plane_tmap(&tin2, static_cast<const uint8_t*>(planes_in) + 2 * a.P * a.br * a.bc, 1, a.P,
-                  a.Pb, a.br, a.bc, kT, R))
+      !plane_tmap(&tin2, static_cast<const uint8_t*>(planes_in) + 2 * a.P * a.prow * a.bc, 1, a.P,
+                  a.Pb, a.br, a.bc, kT, R, a.prow))
     return cudaErrorNotSupported;
-  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.P, a.br, a.bc, kT, R))
+  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.P, a.br, a.bc, kT, R, a.prow))
     return cudaErrorNotSupported;
   auto k = k_stream<MODE, ZT, MT, kT, CW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -897,7 +900,8 @@ void set_transform_stream(bool on) { g_use_stream = on; }
 // encode (+ g_d-style reduction): bf16 matrix -> bf16 planes; red planes bf16 or fp32.
 cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
                                    const float* coef, int P, void* out, int odt, const void* rp,
-                                   int rdt, float* ro, float* rw, cudaStream_t s) {
+                                   int rdt, float* ro, float* rw, cudaStream_t s,
+                                   int64_t plane_rows) {
   if (!g_use_stream || mdt != kBF16 || odt != kBF16 || bc % 64 || ldm % 8 || P < 1 || P > 64 ||
       !al16(m) || !al16(out))
     return cudaErrorNotSupported;
@@ -912,6 +916,7 @@ cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t 
   a.P = P;
   a.br = br;
   a.bc = bc;
+  a.prow = plane_rows;
   if (!rp) return launch<kEnc, __nv_bfloat16>(a, nullptr, out, nullptr, s);
   if (rdt == kBF16) return launch<kEncRed, __nv_bfloat16>(a, rp, out, ro, s);
   if (rdt == kF24) return launch<kEncRed, F24>(a, rp, out, ro, s);
@@ -922,7 +927,7 @@ cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t 
 cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, int64_t bc,
                                    const float* coef, void* out, int odt, int64_t ldo,
                                    const void* rm, int rdt, int64_t ldr, float* ro, float* rw,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, int64_t plane_rows) {
   if (!g_use_stream || odt != kBF16 || bc % 64 || ldo % 8 || Q < 1 || Q > 64 || !al16(in) ||
       !al16(out))
     return cudaErrorNotSupported;
@@ -939,6 +944,7 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
   a.P = Q;
   a.br = br;
   a.bc = bc;
+  a.prow = plane_rows;
   if (rm) {
     if (idt == kF32) return launch<kDecRed, float>(a, in, nullptr, ro, s);
     if (idt == kF24) return launch<kDecRed, F24>(a, in, nullptr, ro, s);

@@ -5,9 +5,11 @@ Mirrors the parts of ``strassen_tile.dense_core`` the hot path depends on:
 * ``ShapeError`` — same class name and ``ValueError`` base (dense_core.py:30-31);
 * ``as_matrix``  — coercion + non-finite rejection (dense_core.py:42-49), except that the GPU
   path computes in fp32 or bf16 instead of f64 (f64 input is cast to fp32);
-* ``tile_fibers`` / ``untile_fibers`` / ``vec_tile`` — the row-major t x t tile layout contract
-  (dense_core.py:86-119). These are pure index permutations (torch views/copies); the kernels
-  never materialise fibers, they read tiles straight from the row-major matrix.
+* ``tile_fibers`` / ``untile_fibers`` / ``vec_tile`` / ``unvec_tile`` — the row-major t x t tile
+  layout contract (dense_core.py:77-119). These are pure index permutations (torch views/copies);
+  the kernels never materialise fibers, they read tiles straight from the row-major matrix;
+* ``make_rng`` / ``spawn_rngs`` / ``gaussian_matrix`` — the seeded PCG64 streams the fixtures and
+  benchmarks draw from (dense_core.py:152-166), bit-identical to the reference's.
 """
 
 from __future__ import annotations
@@ -110,3 +112,31 @@ def vec_tile(m, block_row: int, block_col: int, t: int) -> torch.Tensor:
         raise ShapeError(f"tile index ({block_row},{block_col}) out of range for {rows}x{cols} grid")
     i, j = block_row * t, block_col * t
     return m[i : i + t, j : j + t].reshape(t * t).clone()
+
+
+def unvec_tile(v, t: int) -> torch.Tensor:
+    """Inverse of vec_tile: a length t*t vector back to a t x t tile (dense_core.py:90-95)."""
+    v = (v if isinstance(v, torch.Tensor) else to_tensor(v)).reshape(-1)
+    if v.shape[0] != t * t:
+        raise ShapeError(f"expected length {t * t}, got {v.shape[0]}")
+    return v.reshape(t, t).clone()
+
+
+def make_rng(seed: int) -> np.random.Generator:
+    """Seeded PCG64 generator; identical seeds give identical streams (dense_core.py:152-154)."""
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def spawn_rngs(seed: int, n: int) -> list[np.random.Generator]:
+    """n independent child generators split deterministically from one seed
+    (dense_core.py:157-160)."""
+    seq = np.random.SeedSequence(seed)
+    return [np.random.Generator(np.random.PCG64(child)) for child in seq.spawn(n)]
+
+
+def gaussian_matrix(rng: np.random.Generator, rows: int, cols: int) -> np.ndarray:
+    """rows x cols matrix of i.i.d. standard normal entries (dense_core.py:163-167); host numpy,
+    the same stream as the reference (move it to the GPU with ``to_tensor``)."""
+    if rows < 1 or cols < 1:
+        raise ShapeError(f"matrix dims must be >= 1, got {rows}x{cols}")
+    return rng.standard_normal((rows, cols))

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .dense_core import ShapeError
+from .dense_core import ShapeError, make_rng  # noqa: F401  (make_rng re-exported)
 from .snf_operator import SnfTriple
 
 
@@ -140,6 +140,7 @@ def random_gaussian_init(t: int, r: int, rng: np.random.Generator, scale: float 
     return SnfTriple(t, r, e_x, e_w, d)
 
 
-def make_rng(seed: int) -> np.random.Generator:
-    """Seeded PCG64 generator (dense_core.py:152-154)."""
-    return np.random.Generator(np.random.PCG64(seed))
+def nested_subset_chain(rng: np.random.Generator, size: int = 49) -> np.ndarray:
+    """A seeded permutation whose first-r prefixes form nested row subsets
+    (strassen_basis.py:140-142)."""
+    return rng.permutation(size)

@@ -40,6 +40,7 @@ import numpy as np
 import torch
 
 from .dense_core import SINGULAR_COND_LIMIT, ShapeError, SingularSystemError, default_device
+from .dense_core import spawn_rngs  # noqa: F401  (re-exported; dense_core.py:157-160)
 from .snf_operator import SnfTriple, encode_tiles
 from .strassen_basis import strassen_rank49
 
@@ -111,12 +112,6 @@ class Class0Result:
 
 
 # ------------------------------------------------------------------ helpers
-def spawn_rngs(seed: int, n: int) -> list[np.random.Generator]:
-    """n independent child generators split from one seed (dense_core.py:157-160)."""
-    seq = np.random.SeedSequence(seed)
-    return [np.random.Generator(np.random.PCG64(child)) for child in seq.spawn(n)]
-
-
 def _device(device) -> torch.device:
     return torch.device(device) if device is not None else default_device()
 

@@ -156,6 +156,35 @@ def test_slice_gemm_tc_layouts(al, bl, shape):
     assert errb <= 5e-3, float(errb)
 
 
+@pytest.mark.parametrize("al", [0, 1])
+@pytest.mark.parametrize("bl", [0, 1])
+@pytest.mark.parametrize("shape", [(10, 1024, 1024, 128), (10, 1000, 1000, 200), (3, 256, 512, 64),
+                                   (2, 264, 1544, 72)])
+def test_slice_gemm_wide_tiles(al, bl, shape):
+    """256 x 512 pair tiles (N >= 512): half 1 lagging half 0, the split tail wave (80 wide
+    tiles on 74 pairs -> 6 of them as half tiles), clipped second halves, K shorter than the lag;
+    fp32, bf16 and F24 outputs against f64."""
+    r, M, N, K = shape
+    g = torch.Generator(device="cpu").manual_seed(M + 3 * N + K + 2 * al + bl)
+    A = torch.randn((r, M, K), generator=g).to(torch.bfloat16)
+    B = torch.randn((r, K, N), generator=g).to(torch.bfloat16)
+    ref = torch.bmm(A.double(), B.double())
+    a_dev = (A if al == 0 else A.transpose(1, 2)).contiguous().to(DEV)
+    b_dev = (B.transpose(1, 2) if bl == 0 else B).contiguous().to(DEV)
+    c = _gemm(a_dev, al, b_dev, bl, M, N, K, r)
+    assert (c.cpu().double() - ref).norm() / ref.norm() <= 1e-5
+    cb = _gemm(a_dev, al, b_dev, bl, M, N, K, r, out_dtype=torch.bfloat16)
+    assert (cb.cpu().double() - ref).norm() / ref.norm() <= 5e-3
+    if N % 16 == 0:
+        c24 = torch.empty((3 * r * M * N,), dtype=torch.uint8, device=DEV)
+        _lib.check(_lib.load().stl_slice_gemm(a_dev.data_ptr(), al, b_dev.data_ptr(), bl,
+                                              c24.data_ptr(), _lib.STL_F24, _lib.STL_BF16, r, M,
+                                              N, K, torch.cuda.current_stream().cuda_stream))
+        u = c.view(torch.int32)
+        rne = ((u + 0x7F + ((u >> 8) & 1)) & ~0xFF).view(torch.float32)
+        assert torch.equal(stl.unpack_slice_products(c24, r, M, N), rne)
+
+
 @pytest.mark.parametrize("al,bl", [(0, 0), (1, 1), (0, 1)])
 @pytest.mark.parametrize("shape", [(3, 256, 128, 64), (2, 520, 272, 136), (24, 512, 256, 512)])
 def test_slice_gemm_f24_output(al, bl, shape):
@@ -222,6 +251,46 @@ def test_stl_batched_bf16(M, K, N, t, r, strassen):
     assert got.dtype == torch.bfloat16
     err = rel(got, ref)
     assert err <= BF16_TOL, err
+
+
+@pytest.mark.parametrize("M,K,N,r,init", [
+    (2048, 256, 2048, 24, "gaussian"),   # 2 row blocks: one per band
+    (4096, 512, 2048, 16, "gaussian"),
+    (3328, 256, 2560, 32, "gaussian"),   # ragged last row block, clipped second half tile
+    (2048, 512, 2048, 24, "subset"),     # the paper's training init: Strassen-49 row subset
+])
+def test_banded_forward_bf16(M, K, N, r, init):
+    """The band-overlapped forward (encode of band 1 / decode of band 0 in warps 2-3 of the
+    slice-GEMM launches, FFMA) against the f64 oracle over the whole output, cache-less and
+    with the training cache (whose slice products the backward then reads)."""
+    t = 4
+    rng = O.make_rng(M + K + r)
+    if init == "subset":
+        sub = stl.pruned_subset_init(stl.strassen_rank49(), r, stl.make_rng(7))
+        e_x, e_w, d = (getattr(sub, n).double().numpy() for n in ("e_x", "e_w", "d"))
+    else:
+        e_x, e_w, d = O.random_gaussian_init(t, r, rng, scale=0.5)
+    x_dev, x64 = bf16_round(rng.standard_normal((M, K)))
+    w_dev, w64 = bf16_round(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
+    snf = stl.SnfTriple(t, r, e_x, e_w, d)
+    ref = O.stl_batched(x64, w64, e_x, d, t)
+    got = stl.stl_batched(x_dev, w_dev, snf)
+    assert rel(got, ref) <= BF16_TOL
+    # bands agree separately (a wrong band would hide in the whole-matrix norm)
+    half = (M // 4 // 256 // 2) * 256 * 4
+    for rows in (slice(0, half), slice(half, M)):
+        assert rel(got[rows], ref[rows]) <= BF16_TOL
+    layer = stl.StlLayer(snf, w_dev)
+    y, cache = stl._layer_forward_cached(layer, x_dev)
+    assert torch.equal(y, got)
+    y_ref, cache_ref = O.layer_forward_cached(x64, w64, e_x, d, t)
+    prods = stl.unpack_slice_products(cache.y_enc, r, M // t, N // t)
+    assert rel(prods.permute(1, 2, 0), cache_ref[2]) <= BF16_TOL
+    gy_dev, gy64 = bf16_round(rng.standard_normal((M, N)))
+    grads = stl._layer_backward(layer, cache, gy_dev)
+    refs = O.layer_backward(w64, e_x, d, cache_ref, gy64, t)
+    for g_, r_, name in zip(grads, refs, ("g_ex", "g_d", "g_w", "g_x")):
+        assert rel(g_, r_) <= BF16_TOL, name
 
 
 def test_encode_decode_bf16_and_fp32():
