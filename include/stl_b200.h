@@ -96,38 +96,47 @@ STL_API int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_lay
                    void* stream);
 
 /*
+ * Slice-product storage format (the forward's y_enc cache and scratch, the backward's g_u): an
+ * explicit argument of the _ex entry points, never process state.
+ *   STL_PROD_AUTO: per shape. On the bf16 t = 4 tensor-core path (M/t > 128, K/t % 8 == 0):
+ *     bf16 planes for r <= 32 (N/t % 64 == 0); for r in (32, 64] fp32-class products — STL_F24
+ *     planes in a cache-less forward (N/t % 128 == 0), fp32 products with a bf16 cache copy in
+ *     training. Otherwise fp32 products (a cache in the compute dtype).
+ *   STL_BF16 / STL_F24 / STL_F32: force one (STL_ERR_VALUE when the shape cannot use it).
+ */
+#define STL_PROD_AUTO (-1)
+/* Format of the y_enc cache a training forward writes: STL_F32 (fp32 dtype), STL_BF16 or
+ * STL_F24; -1 with stl_last_error set when `prod` is unavailable for the shape. */
+STL_API int stl_cache_format(int64_t M, int64_t K, int64_t N, int t, int r, int dtype, int prod);
+/* Bytes of that cache (r, M/t, N/t) planes: 4, 2 or 3 bytes per element. stl_cache_bytes is the
+ * STL_PROD_AUTO case. */
+STL_API int64_t stl_cache_bytes_ex(int64_t M, int64_t K, int64_t N, int t, int r, int dtype,
+                                   int prod);
+STL_API int64_t stl_cache_bytes(int64_t M, int64_t K, int64_t N, int t, int r, int dtype);
+
+/*
  * stl_batched (snf_operator.py:156-172) / stl_layer_forward + _layer_forward_cached
  * (toy_network.py:74-92):  y = decode(slice_products(encode(x, e_x), w_enc), d).
  *   x: (M, K) ld_x, dtype;  w_enc: planes (r, N/t, K/t) of dtype;  y: (M, N) ld_y, dtype.
  *   x_enc_ws: planes (r, M/t, K/t) of dtype (also the cache `u`);
- *   y_enc_cache: NULL, or stl_cache_bytes(...) bytes receiving the slice products (the cache
- *                `y_enc` for stl_backward; fp32 planes in fp32 mode, F24 or bf16 planes in bf16
- *                mode, see stl_cache_bytes);
+ *   y_enc_cache: NULL, or stl_cache_bytes_ex(..., prod) bytes receiving the slice products in
+ *                the format stl_cache_format(..., prod) reports (the cache `y_enc` for
+ *                stl_backward_ex, which takes that format back as an argument);
  *   scratch: device workspace of at least stl_forward_scratch_bytes(...) bytes.
  *   M, K, N must be multiples of t (ShapeError otherwise, as the reference).
- * Default path: encode -> slice GEMM -> decode with the slice products in y_enc_cache or
- * `scratch` (fp32; on the bf16 t = 4 path with r <= 32 bf16 planes, F24 with stl_set_fusion
- * bit 5); with stl_set_fusion bit 0, bf16 t = 4 runs the decode-fused tcgen05 kernel instead.
+ * encode -> slice GEMM (tcgen05, bf16 / F24 / fp32 products) -> decode. stl_forward is
+ * stl_forward_ex with prod = STL_PROD_AUTO.
  */
 STL_API int64_t stl_forward_scratch_bytes(int64_t M, int64_t K, int64_t N, int t, int r,
                                           int dtype);
-/* Bytes of the forward cache y_enc (r, M/t, N/t): fp32 planes (dtype STL_F32); bf16 planes on
- * the bf16 path — or, with stl_set_fusion bit 5, STL_F24 planes (3 bytes per element) when
- * t = 4, r <= 32, M/t > 128, N/t % 128 == 0 and K/t % 8 == 0. stl_backward reads the cache in
- * the same format. */
-STL_API int64_t stl_cache_bytes(int64_t M, int64_t K, int64_t N, int t, int r, int dtype);
+STL_API int stl_forward_ex(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc,
+                           int64_t N, const float* e_x, const float* d, int t, int r, int dtype,
+                           void* y, int64_t ld_y, void* x_enc_ws, void* y_enc_cache, void* scratch,
+                           int64_t scratch_bytes, int prod, void* stream);
 STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
                 const float* e_x, const float* d, int t, int r, int dtype, void* y, int64_t ld_y,
                 void* x_enc_ws, void* y_enc_cache, void* scratch, int64_t scratch_bytes,
                 void* stream);
-
-/* A/B switches (host-only): bit 0 = enable the decode-fused forward (default off:
- * it is slower than encode + GEMM + decode today);
- * bit 1 = force the FFMA tile transforms instead of the tensor-core (mma.sync) ones;
- * bit 2 = also use the tensor-core decode (experimental); bit 3 = disable the streaming
- * (TMA-pipelined) transforms; bit 4 = fp32 slice products (+ a bf16 cache copy); bit 5 = F24
- * slice products instead of bf16 ones. */
-STL_API int stl_set_fusion(int enabled);
 
 /*
  * _layer_backward (toy_network.py:95-106), all seven formulas:
@@ -135,15 +144,25 @@ STL_API int stl_set_fusion(int enabled);
  *   g_enc = gvy @ d^T                              -> g_enc_ws planes (r, M/t, N/t) dtype
  *   g_w  = sum_I u[I,L,p] g_enc[I,J,p]             -> g_w  fp32 planes (r, N/t, K/t)
  *   g_u  = sum_J W[L,J,p] g_enc[I,J,p]             -> g_u_ws (r, M/t, K/t): fp32 planes, or the
- *                                                     slice-product format of y_enc (bf16/F24)
- *                                                     in the first 2-3 bytes per element
+ *                                                     products format `gu_prod` (bf16 / F24, in
+ *                                                     the first 2-3 bytes per element)
  *   g_ex = sum_{I,L} g_u[I,L,p] vx[I,L,c]          -> g_ex fp32 (r, t*t)
  *   g_x  = untile(g_u @ e_x)                       -> g_x (M, K) ld_gx, dtype
  * Inputs: gy (M, N) ld_gy; x (M, K) ld_x (the layer input, vx); w_enc as in stl_forward;
- * x_enc (= u) and y_enc (planes of dtype) from the forward cache. red_ws:
- * stl_reduce_workspace_floats floats.
- * Any of g_ex, g_d, g_w, g_x may be NULL to skip that gradient.
+ * x_enc (= u) and y_enc from the forward cache, y_enc_format = the format the forward wrote it
+ * in (stl_cache_format; a format this shape's forward cannot write -> STL_ERR_VALUE).
+ * gu_prod: STL_PROD_AUTO (the cache's format family: F24 cache -> F24 g_u where the shape
+ * allows, else the AUTO rule) or a forced format. red_ws: stl_reduce_workspace_floats floats.
+ * Any of g_ex, g_d, g_w, g_x may be NULL to skip that gradient, except that g_ex is fused with
+ * g_x (g_ex without g_x -> STL_ERR_VALUE). stl_backward = stl_backward_ex with the AUTO cache
+ * format and gu_prod = STL_PROD_AUTO.
  */
+STL_API int stl_backward_ex(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x,
+                            const void* w_enc, const float* e_x, const float* d,
+                            const void* x_enc, const void* y_enc, int y_enc_format, int64_t M,
+                            int64_t K, int64_t N, int t, int r, int dtype, float* g_ex, float* g_d,
+                            float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws, float* g_u_ws,
+                            float* red_ws, int gu_prod, void* stream);
 STL_API int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, const void* w_enc,
                  const float* e_x, const float* d, const void* x_enc, const void* y_enc,
                  int64_t M, int64_t K, int64_t N, int t, int r, int dtype, float* g_ex,

@@ -17,9 +17,12 @@ REPO = PKG.parent
 CSRC = PKG / "csrc"
 LIB_NAME = "libstl_b200.so"
 LIB_PATH = PKG / LIB_NAME
+# The probe build: the same sources with -DSTL_PROBES, whose STL_* environment switches
+# (scripts/) select A/B variants and timers. The product library never reads the environment.
+PROBE_LIB_PATH = PKG / "libstl_b200_probe.so"
 
 SOURCES = ["stl_capi.cu", "stl_slice_gemm.cu", "stl_transform.cu", "stl_transform4.cu",
-           "stl_fused_gemm.cu", "stl_transform_mma.cu", "stl_stream.cu", "stl_tokens.cu"]
+           "stl_transform_mma.cu", "stl_stream.cu", "stl_tokens.cu"]
 HEADERS = ["sm100_ptx.cuh", "sm100_pair_pipeline.cuh", "stl_internal.h"]
 
 NVCC_FLAGS = [
@@ -39,42 +42,51 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found (set NVCC or install CUDA 12.9)")
 
 
-def _stale() -> bool:
-    if not LIB_PATH.exists():
+def _stale(lib: Path) -> bool:
+    if not lib.exists():
         return True
-    t = LIB_PATH.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES + HEADERS] + [REPO / "include" / "stl_b200.h"]
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def _compile(src: Path, obj: Path) -> subprocess.CompletedProcess:
-    cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("STL_NVCC_EXTRA", "").split(), "-c", "-o",
-           str(obj), str(src), "-I", str(REPO / "include")]
+def _compile(src: Path, obj: Path, extra: list[str]) -> subprocess.CompletedProcess:
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, *os.environ.get("STL_NVCC_EXTRA", "").split(), "-c",
+           "-o", str(obj), str(src), "-I", str(REPO / "include")]
     return subprocess.run(cmd, capture_output=True, text=True)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every .cu (in parallel, one object each) and link one shared library (skips if
-    up to date)."""
-    if not force and not _stale():
-        return LIB_PATH
+def build(force: bool = False, verbose: bool = False, probes: bool = True) -> Path:
+    """Compile every .cu (in parallel, one object each) and link libstl_b200.so — and, with
+    `probes`, libstl_b200_probe.so (-DSTL_PROBES) — skipping libraries that are up to date."""
     from concurrent.futures import ThreadPoolExecutor
 
-    objdir = PKG / "build"
-    objdir.mkdir(exist_ok=True)
-    objs = [objdir / (Path(s).stem + ".o") for s in SOURCES]
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        procs = list(ex.map(lambda so: _compile(CSRC / so[0], so[1]), zip(SOURCES, objs)))
+    variants = [(LIB_PATH, PKG / "build", [])]
+    if probes:
+        variants.append((PROBE_LIB_PATH, PKG / "build" / "probe", ["-DSTL_PROBES"]))
+    todo = [v for v in variants if force or _stale(v[0])]
+    if not todo:
+        return LIB_PATH
+    jobs = []
+    for lib, objdir, extra in todo:
+        objdir.mkdir(parents=True, exist_ok=True)
+        for src in SOURCES:
+            jobs.append((CSRC / src, objdir / (Path(src).stem + ".o"), extra))
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 8)) as ex:
+        procs = list(ex.map(lambda j: _compile(*j), jobs))
     log = PKG / "build.log"
     text = "".join(" ".join(p.args) + "\n" + p.stdout + p.stderr for p in procs)
     bad = [p for p in procs if p.returncode != 0]
     if not bad:
-        link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
-                str(LIB_PATH), *map(str, objs), "-lcudart_static"]
-        lp = subprocess.run(link, capture_output=True, text=True)
-        text += " ".join(link) + "\n" + lp.stdout + lp.stderr
-        if lp.returncode != 0:
-            bad = [lp]
+        for lib, objdir, _ in todo:
+            objs = [str(objdir / (Path(src).stem + ".o")) for src in SOURCES]
+            link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
+                    str(lib), *objs, "-lcudart_static"]
+            lp = subprocess.run(link, capture_output=True, text=True)
+            text += " ".join(link) + "\n" + lp.stdout + lp.stderr
+            if lp.returncode != 0:
+                bad = [lp]
+                break
     log.write_text(text)
     if bad:
         raise RuntimeError(f"nvcc failed ({bad[0].returncode}); see {log}\n{bad[0].stderr[-4000:]}")

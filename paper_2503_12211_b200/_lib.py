@@ -15,10 +15,13 @@ from pathlib import Path
 from .dense_core import ShapeError
 
 LIB_PATH = Path(__file__).resolve().with_name("libstl_b200.so")
+# the probe build (-DSTL_PROBES: STL_* environment A/B switches), for scripts/ and one stress test
+PROBE_LIB_PATH = LIB_PATH.with_name("libstl_b200_probe.so")
 
 STL_F32 = 0
 STL_BF16 = 1
 STL_F24 = 2  # intermediate format of the bf16 path's fp32 slice products (see stl_cache_bytes)
+STL_PROD_AUTO = -1  # slice-product format chosen per shape (include/stl_b200.h)
 STL_K_MAJOR = 0
 STL_MN_MAJOR = 1
 
@@ -36,10 +39,19 @@ SIGNATURES = {
                         c_int64, c_int64, c_int64, c_void_p], c_int),
     "stl_forward_scratch_bytes": ([c_int64, c_int64, c_int64, c_int, c_int, c_int], c_int64),
     "stl_cache_bytes": ([c_int64, c_int64, c_int64, c_int, c_int, c_int], c_int64),
+    "stl_cache_bytes_ex": ([c_int64, c_int64, c_int64, c_int, c_int, c_int, c_int], c_int64),
+    "stl_cache_format": ([c_int64, c_int64, c_int64, c_int, c_int, c_int, c_int], c_int),
+    "stl_forward_ex": ([c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                        c_void_p, c_int, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p,
+                        c_void_p, c_int64, c_int, c_void_p], c_int),
+    "stl_backward_ex": ([c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                         c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int, c_int,
+                         c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+                         c_void_p, c_void_p, c_int, c_void_p], c_int),
     "stl_forward": ([c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                      c_int, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                      c_int64, c_void_p], c_int),
-    "stl_set_fusion": ([c_int], c_int),
+    
     "stl_backward": ([c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                       c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_int,
                       c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,

@@ -150,35 +150,47 @@ int stl_slice_gemm(const void* a, int a_layout, const void* b, int b_layout, voi
 }
 
 namespace {
-bool g_fusion = false;  // decode-fused forward is opt-in until it beats the unfused path
-// Storage format of the fp32 slice products (forward y_enc / cache, backward g_u) on the bf16
-// t = 4 path, r <= 32: bf16 planes by default (2 B/element; they feed bf16-output decodes and
-// r x t^2 reductions over millions of tiles: measured rel. error of y at 8192^3 2.9e-3 vs
-// 2.4e-3 with F24, bar 1e-2); stl_set_fusion bit 5 = F24 (3 B), bit 4 = fp32 products with a
-// bf16 cache copy (the only format at r > 32: at r = 49, Strassen x Strassen, bf16 products
-// reach 9.6e-3 of the 1e-2 bar).
-enum ProdMode { kProdBf16 = 0, kProdF24 = 1, kProdF32 = 2 };
-int g_prod_mode = kProdBf16;
-
-bool fused_forward_shape(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
-  if (!g_fusion || t != 4 || dtype != STL_BF16) return false;
-  return stl::fused_decode_supported(t, r, M / t, N / t, K / t, dtype, nullptr, nullptr, 0);
+// Storage format of the slice products (forward y_enc, backward g_u) — an explicit argument of
+// every call (STL_PROD_AUTO or a forced format), never process state, so stl_forward /
+// stl_backward are pure and re-entrant and the cache's format travels with the cache.
+// AUTO on the bf16 t = 4 path: bf16 planes (2 B/element; they feed bf16-output decodes and
+// r x t^2 reductions: measured rel. error of y at 8192^3 2.9e-3 vs 2.4e-3 with fp32-class
+// products, bar 1e-2) for r <= 32; above r = 32 (the Strassen x Strassen rank 49, where bf16
+// products reach 9.6e-3) fp32-class products: F24 in a cache-less forward, fp32 products with a
+// bf16 cache copy in training (the backward's fused reductions read bf16 or F24 at r <= 32).
+// Returns the products' format (STL_BF16, STL_F24, or -1 = fp32 products), or -2 when `prod`
+// forces a format the shape cannot use.
+constexpr int kFp32Products = -1, kBadFormat = -2;
+bool bf16_tc_path(int64_t rows, int64_t kt, int t, int dtype) {
+  return dtype == STL_BF16 && t == 4 && rows > 128 && kt % 8 == 0;
 }
-
-// Format of the slice products C (rows x cols tiles, contraction kt): STL_BF16 / kF24 written
-// by the CTA-pair GEMM and read by the streaming transforms, or -1 = fp32 products (+ a cache
-// copy in the compute dtype). A pure function of the shape (and the mode), so the forward
-// (writing the y_enc cache) and the backward (reading it) agree on the cache format.
-// `inference`: a cache-less forward (no backward reads the products); there r in (32, 64]
-// (the Strassen x Strassen rank 49) uses F24 — fp32-class precision at 3 B — where the
-// reductions of the training path (r <= 32 only) do not run.
-int product_format(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype,
-                   bool inference = false) {
-  if (g_prod_mode == kProdF32 || dtype != STL_BF16 || t != 4 || rows <= 128 || kt % 8)
-    return -1;
-  if (r > 32) return inference && r <= 64 && cols % 128 == 0 ? stl::kF24 : -1;
-  if (g_prod_mode == kProdF24) return cols % 128 == 0 ? stl::kF24 : -1;
-  return cols % 64 == 0 ? STL_BF16 : -1;
+int product_format(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype, int prod,
+                   bool inference) {
+  const bool tc = bf16_tc_path(rows, kt, t, dtype);
+  switch (prod) {
+    case STL_PROD_AUTO:
+      if (!tc) return kFp32Products;
+      if (r > 32) return inference && r <= 64 && cols % 128 == 0 ? stl::kF24 : kFp32Products;
+      return cols % 64 == 0 ? STL_BF16 : kFp32Products;
+    case STL_F32:
+      return kFp32Products;
+    case STL_BF16:
+      return tc && cols % 64 == 0 && (inference || r <= 32) ? STL_BF16 : kBadFormat;
+    case STL_F24:
+      return tc && cols % 128 == 0 && r <= (inference ? 64 : 32) ? stl::kF24 : kBadFormat;
+    default:
+      return kBadFormat;
+  }
+}
+// The y_enc cache of a training forward: the products' format, or the compute dtype when the
+// products are fp32 (a bf16 copy on the bf16 path).
+int cache_format(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype, int prod) {
+  const int pf = product_format(rows, cols, kt, t, r, dtype, prod, false);
+  return pf == kFp32Products ? dtype : pf;
+}
+int bad_format(int prod) {
+  return fail(STL_ERR_VALUE, "slice-product format %d is not available for this shape / dtype "
+              "(bf16 needs t = 4, r <= 32, N/t %% 64 == 0; F24 needs N/t %% 128 == 0)", prod);
 }
 // Split-K factor for a tensor-core slice GEMM (M x N per slice, contraction K) whose output
 // tiles cannot fill the GPU: S divides K, K / S >= 512; 1 = no split. Used for g_w, whose
@@ -196,39 +208,36 @@ int split_k_factor(int64_t M, int64_t N, int64_t K, int r, int dtype) {
     if (K % S == 0 && K / S >= 512 && S * M <= K) return static_cast<int>(S);
   return 1;
 }
-
-bool f24_products(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype) {
-  return product_format(rows, cols, kt, t, r, dtype) == stl::kF24;
-}
 }  // namespace
 
-int64_t stl_cache_bytes(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
-  if (t < 1 || r < 1 || M < 0 || K < 0 || N < 0) return 0;
-  const int64_t n = static_cast<int64_t>(r) * (M / t) * (N / t);
-  if (f24_products(M / t, N / t, K / t, t, r, dtype)) return 3 * n;
-  return n * (dtype == STL_BF16 ? 2 : 4);
+int stl_cache_format(int64_t M, int64_t K, int64_t N, int t, int r, int dtype, int prod) {
+  if (t < 1 || r < 1 || M < 0 || K < 0 || N < 0) return fail(STL_ERR_SHAPE, "invalid shape"), -1;
+  if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype"), -1;
+  const int f = cache_format(M / t, N / t, K / t, t, r, dtype, prod);
+  if (f == kBadFormat) return bad_format(prod), -1;
+  return f;
 }
 
-int stl_set_fusion(int enabled) {
-  g_fusion = (enabled & 1) != 0;
-  stl::set_transform_mma((enabled & 2) == 0);         // bit 1 = force the FFMA transforms
-  stl::set_transform_mma_decode((enabled & 4) != 0);  // bit 2 = mma decode (experimental)
-  stl::set_transform_stream((enabled & 8) == 0);      // bit 3 = disable the streaming transforms
-  g_prod_mode = (enabled & 16) ? kProdF32 : ((enabled & 32) ? kProdF24 : kProdBf16);
-  return STL_OK;
+int64_t stl_cache_bytes_ex(int64_t M, int64_t K, int64_t N, int t, int r, int dtype, int prod) {
+  if (t < 1 || r < 1 || M < 0 || K < 0 || N < 0 || !valid_dtype(dtype)) return 0;
+  const int f = cache_format(M / t, N / t, K / t, t, r, dtype, prod);
+  if (f == kBadFormat) return 0;
+  return static_cast<int64_t>(r) * (M / t) * (N / t) * static_cast<int64_t>(stl::dtype_size(f));
+}
+
+int64_t stl_cache_bytes(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
+  return stl_cache_bytes_ex(M, K, N, t, r, dtype, STL_PROD_AUTO);
 }
 
 int64_t stl_forward_scratch_bytes(int64_t M, int64_t K, int64_t N, int t, int r, int dtype) {
   if (t < 1 || r < 1 || M < 0 || K < 0 || N < 0) return 0;
-  if (fused_forward_shape(M, K, N, t, r, dtype))
-    return static_cast<int64_t>(stl::fused_decode_scratch_bytes(r, M / t, N / t));
   return static_cast<int64_t>(r) * (M / t) * (N / t) * 4;
 }
 
-int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
-                const float* e_x, const float* d, int t, int r, int dtype, void* y, int64_t ld_y,
-                void* x_enc_ws, void* y_enc_cache, void* scratch, int64_t scratch_bytes,
-                void* stream) {
+int stl_forward_ex(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
+                   const float* e_x, const float* d, int t, int r, int dtype, void* y,
+                   int64_t ld_y, void* x_enc_ws, void* y_enc_cache, void* scratch,
+                   int64_t scratch_bytes, int prod, void* stream) {
   if (int st = check_tr(t, r)) return st;
   if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype");
   if (M < 0 || K < 0 || N < 0) return fail(STL_ERR_SHAPE, "negative extent");
@@ -239,21 +248,10 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
   if (ld_x < K || ld_y < N) return fail(STL_ERR_SHAPE, "leading dimension too small");
   cudaStream_t s = as_stream(stream);
   const int64_t bi = M / t, bk = K / t, bj = N / t;
+  const int pfmt = product_format(bi, bj, bk, t, r, dtype, prod, y_enc_cache == nullptr);
+  if (pfmt == kBadFormat) return bad_format(prod);
   if (M == 0 || N == 0) return STL_OK;
   int st;
-  {
-    const int pf = product_format(bi, bj, bk, t, r, dtype, y_enc_cache == nullptr);
-    void* prod = y_enc_cache ? y_enc_cache : scratch;
-    if (pf == STL_BF16 && (y_enc_cache || scratch_bytes >= 2 * r * bi * bj) &&
-        stl::forward_banded_supported(r, bi, bk, bj, ld_x, ld_y, x, y, x_enc_ws, prod, w_enc,
-                                      e_x, d)) {
-      Prof prof("forward_banded", s, 4);
-      const cudaError_t e = stl::forward_banded(x, ld_x, w_enc, e_x, d, r, bi, bk, bj, x_enc_ws,
-                                                prod, y, ld_y, s);
-      if (e != cudaErrorNotSupported) return check_cuda(e, "banded forward");
-      // (nothing launched: the band-0 encode declined the shape; run the unbanded path)
-    }
-  }
   {
     Prof prof("encode_x", s);
     st = check_cuda(stl::tiles_to_planes(x, dtype, ld_x, bi, bk, t, e_x, r, x_enc_ws, dtype,
@@ -261,32 +259,19 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
                     "forward encode");
   }
   if (st) return st;
-  const bool fused = !y_enc_cache && fused_forward_shape(M, K, N, t, r, dtype) && bk > 0 &&
-                     ld_y % 8 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
-                     stl::fused_decode_supported(t, r, bi, bj, bk, dtype, x_enc_ws, w_enc, 0);
-  if (fused) {
-    const size_t need = stl::fused_decode_scratch_bytes(r, bi, bj);
-    if (scratch_bytes < static_cast<int64_t>(need))
-      return fail(STL_ERR_VALUE, "scratch too small: %lld < %lld bytes", (long long)scratch_bytes,
-                  (long long)need);
-    Prof prof("slice_gemm_decode_fused", s);
-    return check_cuda(stl::fused_gemm_decode(x_enc_ws, w_enc, STL_K_MAJOR, r, bi, bj, bk, d, y,
-                                             ld_y, dtype, nullptr, dtype, scratch, s),
-                      "fused forward");
-  }
-  const int pfmt = product_format(bi, bj, bk, t, r, dtype, y_enc_cache == nullptr);
   if (pfmt >= 0) {
     // slice products (bf16 or F24) straight into the cache (or scratch), decoded from there
-    void* prod = y_enc_cache ? y_enc_cache : scratch;
+    void* prod_buf = y_enc_cache ? y_enc_cache : scratch;
     const int64_t need = static_cast<int64_t>(stl::dtype_size(pfmt)) * r * bi * bj;
     if (!y_enc_cache && scratch_bytes < need)
       return fail(STL_ERR_VALUE, "scratch too small: %lld < %lld bytes", (long long)scratch_bytes,
                   (long long)need);
-    st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, prod, pfmt, dtype, r, bi, bj, bk, s);
+    st = run_gemm(x_enc_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, prod_buf, pfmt, dtype, r, bi, bj, bk,
+                  s);
     if (st) return st;
     Prof prof("decode_y", s);
-    return check_cuda(stl::planes_to_tiles(prod, pfmt, r, bi, bj, t, d, y, dtype, ld_y, nullptr,
-                                           STL_F32, 0, nullptr, nullptr, s),
+    return check_cuda(stl::planes_to_tiles(prod_buf, pfmt, r, bi, bj, t, d, y, dtype, ld_y,
+                                           nullptr, STL_F32, 0, nullptr, nullptr, s),
                       "forward decode");
   }
   float* yenc = nullptr;
@@ -318,36 +303,61 @@ int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w
   return st;
 }
 
-int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, const void* w_enc,
-                 const float* e_x, const float* d, const void* x_enc, const void* y_enc,
-                 int64_t M, int64_t K, int64_t N, int t, int r, int dtype, float* g_ex,
-                 float* g_d, float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws,
-                 float* g_u_ws, float* red_ws, void* stream) {
+int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const void* w_enc, int64_t N,
+                const float* e_x, const float* d, int t, int r, int dtype, void* y, int64_t ld_y,
+                void* x_enc_ws, void* y_enc_cache, void* scratch, int64_t scratch_bytes,
+                void* stream) {
+  return stl_forward_ex(x, M, K, ld_x, w_enc, N, e_x, d, t, r, dtype, y, ld_y, x_enc_ws,
+                        y_enc_cache, scratch, scratch_bytes, STL_PROD_AUTO, stream);
+}
+
+int stl_backward_ex(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, const void* w_enc,
+                    const float* e_x, const float* d, const void* x_enc, const void* y_enc,
+                    int y_enc_format, int64_t M, int64_t K, int64_t N, int t, int r, int dtype,
+                    float* g_ex, float* g_d, float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws,
+                    float* g_u_ws, float* red_ws, int gu_prod, void* stream) {
   if (int st = check_tr(t, r)) return st;
   if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype");
   if (M < 0 || K < 0 || N < 0 || M % t || K % t || N % t)
     return fail(STL_ERR_SHAPE, "tile size %d does not divide (M, K, N) = (%lld, %lld, %lld)", t,
                 (long long)M, (long long)K, (long long)N);
   if ((g_d || g_ex) && !red_ws) return fail(STL_ERR_VALUE, "reduction workspace required");
+  if (g_ex && !g_x) return fail(STL_ERR_VALUE, "g_ex needs the g_x output (it is fused with it)");
   cudaStream_t s = as_stream(stream);
   const int64_t bi = M / t, bk = K / t, bj = N / t;
+  // The cache format is the caller's record of what the forward wrote; it must be one this
+  // shape's forward can write (any forced format), else the bytes would be misread.
+  bool fmt_ok = y_enc_format == dtype;  // fp32 products (fp32 mode) or the bf16 copy
+  if (y_enc_format == stl::kF24 || (y_enc_format == STL_BF16 && dtype == STL_BF16))
+    fmt_ok = fmt_ok || product_format(bi, bj, bk, t, r, dtype, y_enc_format, false) == y_enc_format;
+  if (!fmt_ok)
+    return fail(STL_ERR_VALUE, "y_enc cache format %d cannot come from a forward of this shape "
+                "and dtype", y_enc_format);
+  // g_u products: the cache's format family by default (F24 cache -> F24 g_u when the shape
+  // allows it), else as requested.
+  int gu_fmt;
+  if (gu_prod == STL_PROD_AUTO && y_enc_format == stl::kF24) {
+    gu_fmt = product_format(bi, bk, bj, t, r, dtype, stl::kF24, false);
+    if (gu_fmt == kBadFormat) gu_fmt = kFp32Products;
+  } else {
+    gu_fmt = product_format(bi, bk, bj, t, r, dtype, gu_prod, false);
+    if (gu_fmt == kBadFormat) return bad_format(gu_prod);
+  }
+  const int gu_dt = gu_fmt >= 0 ? gu_fmt : STL_F32;
   // gvy -> g_enc (planes), fused with g_d = sum y_enc (x) gvy.
   int st;
   {
     Prof prof(g_d ? "encode_gy+g_d" : "encode_gy", s, g_d ? 2 : 1);
-    const int cache_dt = f24_products(bi, bj, bk, t, r, dtype) ? stl::kF24 : dtype;  // else bf16
     st = check_cuda(stl::tiles_to_planes(gy, dtype, ld_gy, bi, bj, t, d, r, g_enc_ws, dtype,
-                                           g_d ? y_enc : nullptr, cache_dt, g_d, red_ws, s),
-                      "backward encode(gy)");
+                                         g_d ? y_enc : nullptr, y_enc_format, g_d, red_ws, s),
+                    "backward encode(gy)");
   }
   if (st) return st;
   // g_w^T_p (N/t x K/t) = g_enc_p^T (N/t x M/t) . u_p (M/t x K/t): both operands MN-major.
-  // g_u_p (M/t x K/t) = g_enc_p (M/t x N/t) . W_p (N/t x K/t): B is N-major. Stored in the
-  // slice-product format (bf16 / F24 on the bf16 path: 2 or 3 of the 4 bytes of g_u_ws used).
-  const int gu_fmt = product_format(bi, bk, bj, t, r, dtype);
-  const int gu_dt = gu_fmt >= 0 ? gu_fmt : STL_F32;
+  // g_u_p (M/t x K/t) = g_enc_p (M/t x N/t) . W_p (N/t x K/t): B is N-major. Stored in gu_dt
+  // (bf16 / F24 on the bf16 path: 2 or 3 of the 4 bytes of g_u_ws used).
   bool gw_done = false, gu_done = false;
-  if (g_w && (g_x || g_ex) && bi > 0 && bk > 0 && bj > 0 && r > 0) {
+  if (g_w && g_x && bi > 0 && bk > 0 && bj > 0 && r > 0) {
     // both slice-GEMMs in one persistent launch (g_w first: its K = M/t is the longer one)
     stl::SliceGemmProblem pw{g_enc_ws, STL_MN_MAJOR, x_enc, STL_MN_MAJOR, g_w, STL_F32, dtype,
                              r, bj, bk, bi};
@@ -378,24 +388,32 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
     }
     if (st) return st;
   }
-  if (g_x || g_ex) {
+  if (g_x) {
     if (!gu_done) {
       st = run_gemm(g_enc_ws, STL_K_MAJOR, w_enc, STL_MN_MAJOR, g_u_ws, gu_dt, dtype, r, bi, bk,
                     bj, s);
       if (st) return st;
     }
-    if (g_x) {
-      Prof prof(g_ex ? "decode_gu+g_ex" : "decode_gu", s, g_ex ? 2 : 1);
-      st = check_cuda(stl::planes_to_tiles(g_u_ws, gu_dt, r, bi, bk, t, e_x, g_x, dtype, ld_gx,
-                                           g_ex ? x : nullptr, dtype, ld_x, g_ex, red_ws, s),
-                      "backward decode(g_u)");
-    } else {
-      // g_ex only: reduction without the g_x store is not specialised; write g_x to scratch.
-      return fail(STL_ERR_UNSUPPORTED, "g_ex without g_x is not supported");
-    }
+    Prof prof(g_ex ? "decode_gu+g_ex" : "decode_gu", s, g_ex ? 2 : 1);
+    st = check_cuda(stl::planes_to_tiles(g_u_ws, gu_dt, r, bi, bk, t, e_x, g_x, dtype, ld_gx,
+                                         g_ex ? x : nullptr, dtype, ld_x, g_ex, red_ws, s),
+                    "backward decode(g_u)");
     if (st) return st;
   }
   return STL_OK;
+}
+
+int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, const void* w_enc,
+                 const float* e_x, const float* d, const void* x_enc, const void* y_enc,
+                 int64_t M, int64_t K, int64_t N, int t, int r, int dtype, float* g_ex,
+                 float* g_d, float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws,
+                 float* g_u_ws, float* red_ws, void* stream) {
+  if (int st = check_tr(t, r)) return st;
+  if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype");
+  const int fmt = t > 0 ? cache_format(M / t, N / t, K / t, t, r, dtype, STL_PROD_AUTO) : dtype;
+  return stl_backward_ex(gy, ld_gy, x, ld_x, w_enc, e_x, d, x_enc, y_enc, fmt, M, K, N, t, r, dtype,
+                         g_ex, g_d, g_w, g_x, ld_gx, g_enc_ws, g_u_ws, red_ws, STL_PROD_AUTO,
+                         stream);
 }
 
 namespace {

@@ -1,5 +1,6 @@
 // stl_internal.h — shared declarations between the STL CUDA translation units.
 #pragma once
+#include <cstdlib>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -41,6 +42,20 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 // Used for the bf16 path's fp32 slice products (forward cache y_enc, backward g_u).
 enum Dtype : int { kF32 = 0, kBF16 = 1, kF24 = 2 };
 
+// Measurement probes (the STL_* environment switches used by scripts/ for A/B runs: stage
+// counts, store-less mainloops, disabled tile shapes, ...) exist only in the probe build of the
+// library (libstl_b200_probe.so, compiled with -DSTL_PROBES). The product library never reads
+// the environment: probe_env returns the default there.
+inline int probe_env(const char* name, int dflt) {
+#ifdef STL_PROBES
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
+}
+
 inline size_t dtype_size(int dt) { return dt == kBF16 ? 2 : (dt == kF24 ? 3 : 4); }
 
 // Operand layouts of one slice-GEMM batch C_p = A_p · B_p (p = 0..r-1), all slices contiguous.
@@ -71,25 +86,8 @@ bool make_bf16_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
                     uint64_t slices, uint32_t box_inner, uint32_t box_outer,
                     uint64_t slice_bytes = 0);
 
-// Decode-fused slice GEMM (stl_fused_gemm.cu): y = decode(A_p . B_p, dec), t = 4, bf16.
-bool fused_decode_supported(int t, int r, int64_t M, int64_t N, int64_t K, int ab_dtype,
-                            const void* a, const void* b, int b_layout);
-size_t fused_decode_scratch_bytes(int r, int64_t M, int64_t N);
-cudaError_t fused_gemm_decode(const void* a, const void* b, int b_layout, int r, int64_t M,
-                              int64_t N, int64_t K, const float* dec, void* y, int64_t ldy,
-                              int y_dtype, void* cache, int cache_dtype, void* scratch,
-                              cudaStream_t s);
 cudaError_t cast_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s);
 
-// Band-overlapped bf16 t = 4 forward with bf16 slice products (stl_slice_gemm.cu):
-// x (M x K, ldx) -> x_enc planes (r, bi, bk) -> y_enc planes (r, bi, bj) -> y (M x N, ldy), the
-// encode of band 1 and the decode of band 0 running beside the slice GEMMs of the other band.
-bool forward_banded_supported(int r, int64_t bi, int64_t bk, int64_t bj, int64_t ldx, int64_t ldy,
-                              const void* x, const void* y, const void* x_enc, const void* y_enc,
-                              const void* w_enc, const float* e_x, const float* d);
-cudaError_t forward_banded(const void* x, int64_t ldx, const void* w_enc, const float* e_x,
-                           const float* d, int r, int64_t bi, int64_t bk, int64_t bj,
-                           void* x_enc, void* y_enc, void* y, int64_t ldy, cudaStream_t s);
 
 // tcgen05 path (bf16 operands, aligned shapes). Returns cudaError_t-like code, 0 = ok.
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s);
@@ -126,19 +124,13 @@ cudaError_t tiles_to_planes4(const void* m, int mdt, int64_t ldm, int64_t br, in
 cudaError_t planes_to_tiles4(const void* in, int idt, int Q, int64_t br, int64_t bc,
                              const float* coef, void* out, int odt, int64_t ldo, const void* rm,
                              int rdt, int64_t ldr, float* ro, float* rw, cudaStream_t s);
-// Tensor-core (mma.sync) t = 4 transforms (stl_transform_mma.cu); set_transform_mma(false)
-// routes t = 4 to the FFMA kernels (A/B testing).
-void set_transform_mma(bool on);
-void set_transform_mma_decode(bool on);
+// Tensor-core (mma.sync) t = 4 encode (stl_transform_mma.cu): the fallback for shapes the
+// streaming encode declines (tile columns not a multiple of 64, e.g. T2T-ViT's 144).
 cudaError_t tiles_to_planes_mma(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
                                 const float* coef, int P, void* out, int odt, const void* rp,
                                 int rdt, float* ro, float* rw, cudaStream_t s);
-cudaError_t planes_to_tiles_mma(const void* in, int idt, int Q, int64_t br, int64_t bc,
-                                const float* coef, void* out, int odt, int64_t ldo, const void* rm,
-                                int rdt, int64_t ldr, float* ro, float* rw, cudaStream_t s);
 // HBM-streaming bulk-async t = 4 transforms (stl_stream.cu), tried first for t = 4;
-// cudaErrorNotSupported -> the kernels above. set_transform_stream(false) disables them.
-void set_transform_stream(bool on);
+// cudaErrorNotSupported -> the kernels above. The only readers of F24 planes.
 // plane_rows: tile rows of the whole planes when (m / out, in / out) address a row band of
 // them (0 = br).
 cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,

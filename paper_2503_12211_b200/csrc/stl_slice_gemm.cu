@@ -39,7 +39,6 @@ struct EpiArgs {
   int r;
   int M, N, K;
   __nv_bfloat16* c2;  // optional bf16 copy of C (the forward's training cache)
-  unsigned long long* dbg;  // probe: per-cluster MMA-thread wait timers [2] (ns), or null
 };
 
 template <int BN>
@@ -313,39 +312,32 @@ struct GroupArgs {
   int r;
   int total0, total;
   int nostore;
-  unsigned long long* dbg;
 };
 
-// A cluster is MC CTA pairs; its tile is MC adjacent 256 x BN tiles of one row block (the
-// pairs share the A rows, which are TMA-multicast between them when MC = 2). `pid` = the
-// pair's index in the cluster.
-template <int BN, int MC>
+// Tile `tile` of a group: problem, slice, 256-row block, BN-column block.
+template <int BN>
 struct TileCoord {
   int prob, p, mb, nb, num_kb;
-  __device__ __forceinline__ TileCoord(const GroupArgs& g, int tile, int pid) {
+  __device__ __forceinline__ TileCoord(const GroupArgs& g, int tile) {
     prob = tile >= g.total0 ? 1 : 0;
     const int local = prob ? tile - g.total0 : tile;
-    const int n_sup = ((g.N[prob] + BN - 1) / BN + MC - 1) / MC;
-    const int per_slice = ((g.M[prob] + 255) / 256) * n_sup;
+    const int n_tiles = (g.N[prob] + BN - 1) / BN;
+    const int per_slice = ((g.M[prob] + 255) / 256) * n_tiles;
     p = local / per_slice;
     const int rem = local - p * per_slice;
-    mb = rem / n_sup;
-    nb = (rem - mb * n_sup) * MC + pid;
+    mb = rem / n_tiles;
+    nb = rem - mb * n_tiles;
     num_kb = (g.K[prob] + kBK - 1) / kBK;
   }
 };
 
 // TMA producer for one tile (both CTAs: each loads its 128 rows of A and BN/2 columns of B).
-template <int BN, int MC, class Kd, class S>
+template <int BN, class Kd, class S>
 __device__ __forceinline__ void tc2_produce(const CUtensorMap* tmA, const CUtensorMap* tmB,
                                             uint8_t* sA, uint8_t* sB, uint64_t* full,
                                             uint64_t* empty, int& stage, uint32_t& phase,
-                                            const TileCoord<BN, MC>& tc, uint32_t rank) {
-  const uint32_t prank = rank & 1u, pid = rank >> 1;
+                                            const TileCoord<BN>& tc, uint32_t prank) {
   const bool leader = prank == 0;
-  // MC = 2: this CTA loads half of its A rows (64) and multicasts them to the same-rank CTA
-  // of the other pair, which loads the other half.
-  const uint16_t a_mask = static_cast<uint16_t>(prank ? 0xA : 0x5);
   const int m0 = tc.mb * 256 + static_cast<int>(prank) * 128;
   const int n0 = tc.nb * BN + static_cast<int>(prank) * (BN / 2);
   for (int kb = 0; kb < tc.num_kb; ++kb) {
@@ -353,15 +345,7 @@ __device__ __forceinline__ void tc2_produce(const CUtensorMap* tmA, const CUtens
     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (S::kABytes + S::kBBytes));
     uint8_t* a = sA + stage * S::kABytes;
     uint8_t* b = sB + stage * S::kBBytes;
-    if constexpr (MC == 2) {
-      const int j = static_cast<int>(pid);
-      if constexpr (!Kd::A_MN)
-        ptx::tma_load_3d_2sm_mc(tmA, &full[stage], a + j * (64 * kBK * 2), kb * kBK, m0 + j * 64,
-                                tc.p, a_mask);
-      else
-        ptx::tma_load_3d_2sm_mc(tmA, &full[stage], a + j * (64 * kBK * 2), m0 + j * 64, kb * kBK,
-                                tc.p, a_mask);
-    } else if constexpr (!Kd::A_MN) {
+    if constexpr (!Kd::A_MN) {
       ptx::tma_load_3d_2sm(tmA, &full[stage], a, kb * kBK, m0, tc.p);
     } else {
 #pragma unroll
@@ -377,8 +361,7 @@ __device__ __forceinline__ void tc2_produce(const CUtensorMap* tmA, const CUtens
         ptx::tma_load_3d_2sm(tmB, &full[stage], b + j * (64 * kBK * 2), n0 + j * 64, kb * kBK,
                              tc.p);
     }
-    if (!leader)
-      ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&full[stage]), rank & ~1u));
+    if (!leader) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0u));
     if (++stage == S::kStages) {
       stage = 0;
       phase ^= 1;
@@ -387,19 +370,14 @@ __device__ __forceinline__ void tc2_produce(const CUtensorMap* tmA, const CUtens
 }
 
 // MMA issue for one tile (even CTA, one thread): num_kb x (kBK / 16) cta_group::2 MMAs.
-template <int BN, int MC, class Kd, class S>
+template <int BN, class Kd, class S>
 __device__ __forceinline__ void tc2_mma(uint8_t* sA, uint8_t* sB, uint64_t* full,
                                         uint64_t* empty, int& stage, uint32_t& phase,
-                                        uint32_t d_tmem, int num_kb,
-                                        unsigned long long* dbg_full) {
-  // a stage is free once every pair that reads it (all of them when A is multicast) is done
-  constexpr uint16_t kEmptyMask = MC == 2 ? 0xF : 0x3;
+                                        uint32_t d_tmem, int num_kb) {
   constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(256, BN, Kd::A_MN, Kd::B_MN);
   for (int kb = 0; kb < num_kb; ++kb) {
-    const uint64_t t1 = dbg_full ? ptx::globaltimer_ns() : 0;
     ptx::mbar_wait(&full[stage], phase);
     ptx::tc_fence_after();
-    if (dbg_full) *dbg_full += ptx::globaltimer_ns() - t1;
     const uint32_t a_addr = ptx::smem_u32(sA + stage * S::kABytes);
     const uint32_t b_addr = ptx::smem_u32(sB + stage * S::kBBytes);
 #pragma unroll
@@ -410,7 +388,7 @@ __device__ __forceinline__ void tc2_mma(uint8_t* sA, uint8_t* sB, uint64_t* full
                                    : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
       ptx::mma_bf16_ss_2sm(d_tmem, ad, bd, kIdesc, (kb | k) != 0 ? 1u : 0u);
     }
-    ptx::mma_commit_2sm(&empty[stage], kEmptyMask);
+    ptx::mma_commit_2sm(&empty[stage], 0x3);
     if (++stage == S::kStages) {
       stage = 0;
       phase ^= 1;
@@ -516,7 +494,7 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
   }
 }
 
-template <int BN, class K0, class K1, int MC>
+template <int BN, class K0, class K1>
 __global__ void __launch_bounds__(kThreads, 1)
     slice_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA0,
                           const __grid_constant__ CUtensorMap tmB0,
@@ -543,10 +521,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank();  // 0 .. 2 MC - 1
-  const uint32_t prank = rank & 1u, pid = rank >> 1;
+  const uint32_t prank = ptx::cluster_ctarank();  // 0 (leader: issues the pair MMAs) or 1
   const bool leader = prank == 0;
-  const int cluster = blockIdx.x / (2 * MC), nclusters = gridDim.x / (2 * MC);
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
   const int total = args.total;
 
   if (warp == 0 && lane == 0) {
@@ -560,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kSt; ++s) {
       ptx::mbar_init(&full[s], 2);
-      ptx::mbar_init(&empty[s], MC);
+      ptx::mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
@@ -582,11 +559,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < total; tile += nclusters) {
-        const TileCoord<BN, MC> tc(args, tile, pid);
+        const TileCoord<BN> tc(args, tile);
         if (tc.prob == 0)
-          tc2_produce<BN, MC, K0, S>(&tmA0, &tmB0, sA, sB, full, empty, stage, phase, tc, rank);
+          tc2_produce<BN, K0, S>(&tmA0, &tmB0, sA, sB, full, empty, stage, phase, tc, prank);
         else
-          tc2_produce<BN, MC, K1, S>(&tmA1, &tmB1, sA, sB, full, empty, stage, phase, tc, rank);
+          tc2_produce<BN, K1, S>(&tmA1, &tmB1, sA, sB, full, empty, stage, phase, tc, prank);
       }
     }
   } else if (warp == 1) {
@@ -595,22 +572,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      const int dbg_slot = 2 * (cluster * MC + static_cast<int>(pid));
-      unsigned long long* dbg_full = args.dbg ? args.dbg + dbg_slot + 1 : nullptr;
       for (int tile = cluster; tile < total; tile += nclusters, ++it) {
-        const TileCoord<BN, MC> tc(args, tile, pid);
+        const TileCoord<BN> tc(args, tile);
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
-        const uint64_t t0 = args.dbg ? ptx::globaltimer_ns() : 0;
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        if (args.dbg) args.dbg[dbg_slot] += ptx::globaltimer_ns() - t0;
         const uint32_t d_tmem = tmem_base + acc * BN;
         if (tc.prob == 0)
-          tc2_mma<BN, MC, K0, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb, dbg_full);
+          tc2_mma<BN, K0, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb);
         else
-          tc2_mma<BN, MC, K1, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb, dbg_full);
-        ptx::mma_commit_2sm(&tfull[acc], static_cast<uint16_t>(0x3u << (2 * pid)));
+          tc2_mma<BN, K1, S>(sA, sB, full, empty, stage, phase, d_tmem, tc.num_kb);
+        ptx::mma_commit_2sm(&tfull[acc], 0x3);
       }
     }
   } else if (warp >= 4) {
@@ -621,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;
     uint8_t* stage_base = smem + S::kRing;
     for (int tile = cluster; tile < total; tile += nclusters, ++it) {
-      const TileCoord<BN, MC> tc(args, tile, pid);
+      const TileCoord<BN> tc(args, tile);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -637,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0)
-        ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), rank & ~1u));
+        ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0u));
     }
     if (issuer) ptx::bulk_wait_all();
   }
@@ -687,7 +660,6 @@ struct WideArgs {
   int total;    // tiles scheduled: nwide - nsplit + 2 nsplit
   int lag;      // k-blocks half 1 runs behind half 0 (0 .. kWStages - 2)
   int nostore;
-  int rev;      // slices in descending order (the slices of the previous launch are L2-warm)
 };
 
 struct WTile {
@@ -710,7 +682,6 @@ __device__ __forceinline__ WTile wide_tile(const WideArgs& g, int tile) {
   const int per_slice = ((g.M[w.prob] + 255) / 256) * n_sup;
   w.p = local / per_slice;
   const int rem = local - w.p * per_slice;
-  if (g.rev) w.p = g.r - 1 - w.p;
   w.mb = rem / n_sup;
   const int nbw = rem - w.mb * n_sup;
   w.n0 = nbw * 512 + (half > 0 ? 256 : 0);
@@ -817,180 +788,8 @@ __device__ __forceinline__ void wide_mma(uint8_t* sA, uint8_t* sB, uint64_t* ful
   kbg = kb0 + w.num_kb;
 }
 
-// ------------------------------------------------------------ side transforms (band overlap)
-// The forward on row bands (DESIGN.md §4 K8): while the tensor cores run band b's slice GEMMs,
-// eight warps per CTA (2, 3 — idle in the GEMM pipeline — and 8 .. 13) encode band b+1 of X
-// (mode 1) or decode band b-1 of Y_enc (mode 2), straight from and to global memory (the ring
-// and the staging buffers fill shared memory). The math is the streaming kernels' own
-// mma.sync formulation (stl_stream.cu): the fp32 coefficients split hi + lo in registers,
-// m16n8k16 bf16 MMAs with fp32 accumulation, the same fragments and the same MMA order — so a
-// banded forward is bit-identical to the unbanded one. A unit is 64 consecutive tiles of one
-// tile row; a warp loads its fragments straight from global memory (4-byte loads: per
-// instruction two 64-byte runs (encode) or four 32-byte runs (decode)), and writes plane rows
-// as 16-byte runs (encode) or matrix rows as 128-byte runs (decode: one shuffle pairs the
-// column halves of each tile).
-constexpr int kSideWarps = 8;       // side warps per CTA: 2, 3 and 8 .. 13
-constexpr int kSideThreads = 32 * (6 + kSideWarps);
-struct SideArgs {
-  int mode;                    // 0 none, 1 encode, 2 decode
-  int P;                       // rank (<= 32)
-  const __nv_bfloat16* src;    // encode: X (row-major, ld); decode: Y_enc planes
-  __nv_bfloat16* dst;          // encode: X_enc planes;       decode: Y (row-major, ld)
-  const float* coef;           // e_x (encode) or d (decode): (P, 16) fp32, device
-  int64_t ld;                  // leading dim of the row-major matrix (elements)
-  int64_t plane_stride;        // elements between planes (all tile rows x bc)
-  int I0, I1;                  // tile rows [I0, I1) of this launch's side work
-  int bc;                      // tiles per row (multiple of 64)
-};
-
-__device__ __forceinline__ uint32_t side_pack2(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-__device__ __forceinline__ void side_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
-  const float2 hf = __bfloat1622float2(h);
-  hi = *reinterpret_cast<uint32_t*>(&h);
-  lo = side_pack2(x0 - hf.x, x1 - hf.y);
-}
-__device__ __forceinline__ void side_mma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                         uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t ld_nc32(const void* p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-
-// Encode: C^T[p][tile] = E . X^T per 8-tile n-tile (A = E: 16 planes x 16 c; B = X fragment:
-// b0 = X[tile 8n + g][c 2q, 2q+1] = row q>>1, b1 = row 2 + (q>>1)); planes 16m + g (+8).
-template <int MT>
-__device__ __forceinline__ void side_encode(const SideArgs& a, int wid, int nw, int lane) {
-  const int g = lane >> 2, q = lane & 3;
-  uint32_t fh[MT][4], fl[MT][4];
-#pragma unroll
-  for (int m = 0; m < MT; ++m)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int p = 16 * m + g + 8 * (i & 1), c = 2 * q + 8 * (i >> 1);
-      const float e0 = p < a.P ? __ldg(a.coef + p * 16 + c) : 0.f;
-      const float e1 = p < a.P ? __ldg(a.coef + p * 16 + c + 1) : 0.f;
-      side_split2(e0, e1, fh[m][i], fl[m][i]);
-    }
-  const bool ok0 = 16 * (MT - 1) + g < a.P, ok1 = 16 * (MT - 1) + g + 8 < a.P;
-  const int upr = a.bc >> 6;
-  const int64_t units = static_cast<int64_t>(a.I1 - a.I0) * upr;
-  for (int64_t u = wid; u < units; u += nw) {
-    const int I = a.I0 + static_cast<int>(u / upr), J0 = static_cast<int>(u % upr) * 64;
-    const __nv_bfloat16* xr =
-        a.src + static_cast<int64_t>(4 * I + (q >> 1)) * a.ld + 4 * (J0 + g) + 2 * (q & 1);
-    uint32_t b0[8], b1[8];
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      b0[n] = ld_nc32(xr + 32 * n);
-      b1[n] = ld_nc32(xr + 2 * a.ld + 32 * n);
-    }
-    __nv_bfloat16* o = a.dst + static_cast<int64_t>(I) * a.bc + J0 + 2 * q;
-#pragma unroll
-    for (int n = 0; n < 8; ++n)
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        float c[4] = {0.f, 0.f, 0.f, 0.f};
-        side_mma(c, fh[m][0], fh[m][1], fh[m][2], fh[m][3], b0[n], b1[n]);
-        side_mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0[n], b1[n]);
-        __nv_bfloat16* op = o + (16 * m + g) * a.plane_stride + 8 * n;
-        if (m < MT - 1 || ok0) *reinterpret_cast<uint32_t*>(op) = side_pack2(c[0], c[1]);
-        if (m < MT - 1 || ok1)
-          *reinterpret_cast<uint32_t*>(op + 8 * a.plane_stride) = side_pack2(c[2], c[3]);
-      }
-  }
-}
-
-// Decode: C[tile][c] = Z^T . D per 16-tile m-tile; rows g / g+8 <-> tiles 2g / 2g+1, so each
-// plane load is one 4-byte access holding both tiles, regrouped into A fragments with PRMT.
-template <int MT>
-__device__ __forceinline__ void side_decode(const SideArgs& a, int wid, int nw, int lane) {
-  const int g = lane >> 2, q = lane & 3;
-  uint32_t fh[MT][4], fl[MT][4];
-#pragma unroll
-  for (int ks = 0; ks < MT; ++ks)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {  // i = nt * 2 + h
-      const int nt = i >> 1, h = i & 1, c = 8 * nt + g;
-      const int pa = 16 * ks + 2 * q + 8 * h, pb = pa + 1;
-      const float d0 = pa < a.P ? __ldg(a.coef + pa * 16 + c) : 0.f;
-      const float d1 = pb < a.P ? __ldg(a.coef + pb * 16 + c) : 0.f;
-      side_split2(d0, d1, fh[ks][i], fl[ks][i]);
-    }
-  bool dok[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) dok[j] = 16 * (MT - 1) + 2 * q + (j & 1) + 8 * (j >> 1) < a.P;
-  const int upr = a.bc >> 6;
-  const int64_t units = static_cast<int64_t>(a.I1 - a.I0) * upr;
-  for (int64_t u = wid; u < units; u += nw) {
-    const int I = a.I0 + static_cast<int>(u / upr), J0 = static_cast<int>(u % upr) * 64;
-    const __nv_bfloat16* zr = a.src + static_cast<int64_t>(I) * a.bc + J0 + 2 * g;
-    uint32_t w[4][MT][4];  // [m-tile][k-step][planes 2q, 2q+1, 2q+8, 2q+9]
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int ks = 0; ks < MT; ++ks)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int pl = 16 * ks + 2 * q + (j & 1) + 8 * (j >> 1);
-          w[k][ks][j] = (ks < MT - 1 || dok[j]) ? ld_nc32(zr + pl * a.plane_stride + 16 * k) : 0u;
-        }
-    __nv_bfloat16* orow = a.dst + static_cast<int64_t>(4 * I) * a.ld + 4 * J0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-      for (int ks = 0; ks < MT; ++ks) {
-        const uint32_t* wk = w[k][ks];
-        const uint32_t a0 = __byte_perm(wk[0], wk[1], 0x5410), a1 = __byte_perm(wk[0], wk[1], 0x7632);
-        const uint32_t a2 = __byte_perm(wk[2], wk[3], 0x5410), a3 = __byte_perm(wk[2], wk[3], 0x7632);
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          side_mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
-          side_mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
-        }
-      }
-      // acc[nt][0,1]: tile 2g, c = 8nt + 2q (+1) = row 2nt + (q>>1), cols 2(q&1) (+1);
-      // acc[nt][2,3]: tile 2g + 1. Pair the column halves with the q^1 lane: 8-byte stores.
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const uint32_t uu = side_pack2(acc[nt][0], acc[nt][1]), vv = side_pack2(acc[nt][2], acc[nt][3]);
-        const uint32_t send = (q & 1) ? uu : vv;
-        const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
-        const int row = 2 * nt + (q >> 1);
-        const int tile = 16 * k + 2 * g + (q & 1);
-        const uint2 val = (q & 1) ? make_uint2(recv, vv) : make_uint2(uu, recv);
-        *reinterpret_cast<uint2*>(orow + row * a.ld + 4 * tile) = val;
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void side_work(const SideArgs& a, int wid_in_cta, int warps_per_cta,
-                                          int lane) {
-  const int nw = warps_per_cta * gridDim.x;
-  const int wid = blockIdx.x * warps_per_cta + wid_in_cta;
-  const int mt = (a.P + 15) / 16;
-  if (a.mode == 1) {
-    if (mt == 1) side_encode<1>(a, wid, nw, lane);
-    else if (mt == 2) side_encode<2>(a, wid, nw, lane);
-  } else if (a.mode == 2) {
-    if (mt == 1) side_decode<1>(a, wid, nw, lane);
-    else if (mt == 2) side_decode<2>(a, wid, nw, lane);
-  }
-}
-
-template <class K0, class K1, bool SIDE>
-__global__ void __launch_bounds__(SIDE ? kSideThreads : kThreads, 1)
+template <class K0, class K1>
+__global__ void __launch_bounds__(kThreads, 1)
     slice_gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA0,
                            const __grid_constant__ CUtensorMap tmB0,
                            const __grid_constant__ CUtensorMap tmC0,
@@ -998,8 +797,7 @@ __global__ void __launch_bounds__(SIDE ? kSideThreads : kThreads, 1)
                            const __grid_constant__ CUtensorMap tmA1,
                            const __grid_constant__ CUtensorMap tmB1,
                            const __grid_constant__ CUtensorMap tmC1,
-                           const __grid_constant__ CUtensorMap tmC21, WideArgs args,
-                           const __grid_constant__ SideArgs side) {
+                           const __grid_constant__ CUtensorMap tmC21, WideArgs args) {
   using S = SmemW<K0::OUT, K1::OUT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -1069,9 +867,6 @@ __global__ void __launch_bounds__(SIDE ? kSideThreads : kThreads, 1)
           wide_mma<K1, S>(sA, sB, full, empty, tfull, tempty, kbg, n0, n1, tmem_base, w, args.lag);
       }
     }
-  } else if (warp == 2 || warp == 3 || warp >= 8) {
-    // side warps 2, 3, 8 .. 13 (two per SM sub-partition)
-    if constexpr (SIDE) side_work(side, warp >= 8 ? warp - 6 : warp - 2, kSideWarps, lane);
   } else if (warp >= 4) {
     const int q = warp & 3;
     const bool issuer = warp == 4 && lane == 0;
@@ -1149,7 +944,7 @@ cudaError_t launch_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   const int64_t tiles = r * ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
   EpiArgs ea{pb.c, pb.c_dtype == kBF16 ? 1 : 0, 0, 0, pb.r, static_cast<int>(M), static_cast<int>(N),
-             static_cast<int>(K), static_cast<__nv_bfloat16*>(pb.c2), nullptr};
+             static_cast<int>(K), static_cast<__nv_bfloat16*>(pb.c2)};
   kern<<<grid, kThreads, smem, s>>>(ta, tb, ea);
   return cudaGetLastError();
 }
@@ -1182,82 +977,78 @@ struct Tc2Maps {
   CUtensorMap a, b, c, c2;
 };
 
-template <int BN, int MC, class Kd>
+template <int BN, class Kd>
 bool make_tc2_maps(const SliceGemmProblem& pb, Tc2Maps* m) {
   const uint64_t M = pb.M, N = pb.N, K = pb.K, r = pb.r;
-  const uint64_t ms = pb.m_stride ? pb.m_stride : M;  // rows between slices of A and C
-  if (pb.m_stride && Kd::A_MN) return false;
-  // K-major A: one 128-row box per CTA, or (MC = 2) a 64-row half multicast to both pairs
-  bool ok = Kd::A_MN ? make_tmap(&m->a, pb.a, M, K, r, kBK)
-                     : make_tmap(&m->a, pb.a, K, M, r, MC == 2 ? 64 : 128, ms * K * 2);
+  // K-major A: one 128-row box per CTA
+  bool ok = Kd::A_MN ? make_tmap(&m->a, pb.a, M, K, r, kBK) : make_tmap(&m->a, pb.a, K, M, r, 128);
   ok = ok && (Kd::B_MN ? make_tmap(&m->b, pb.b, N, K, r, kBK)
                        : make_tmap(&m->b, pb.b, K, N, r, BN / 2));
   if (Kd::OUT == kOutBf16) {
-    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r, 64, ms);  // 64-column chunks, 128 B rows
+    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r, 64);  // 64-column chunks, 128 B rows
     m->c2 = m->c;
   } else if (Kd::OUT == kOutF24) {
-    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r, 32, ms) &&
-         make_out_tmap(&m->c2, static_cast<uint8_t*>(pb.c) + 2 * r * ms * N, 1, N, M, r, 32, ms);
+    ok = ok && make_out_tmap(&m->c, pb.c, 2, N, M, r) &&
+         make_out_tmap(&m->c2, static_cast<uint8_t*>(pb.c) + 2 * r * M * N, 1, N, M, r);
   } else {
-    ok = ok && make_out_tmap(&m->c, pb.c, 4, N, M, r, 32, ms);
-    if (Kd::OUT == kOutF32Bf16) ok = ok && make_out_tmap(&m->c2, pb.c2, 2, N, M, r, 32, ms);
+    ok = ok && make_out_tmap(&m->c, pb.c, 4, N, M, r);
+    if (Kd::OUT == kOutF32Bf16) ok = ok && make_out_tmap(&m->c2, pb.c2, 2, N, M, r);
     else m->c2 = m->c;
   }
   return ok;
 }
 
-// cluster tiles: MC adjacent 256 x BN tiles per cluster
-int64_t tc2_tiles(const SliceGemmProblem& pb, int BN, int MC) {
-  return static_cast<int64_t>(pb.r) * ((pb.M + 255) / 256) * (((pb.N + BN - 1) / BN + MC - 1) / MC);
+int64_t tc2_tiles(const SliceGemmProblem& pb, int BN) {
+  return static_cast<int64_t>(pb.r) * ((pb.M + 255) / 256) * ((pb.N + BN - 1) / BN);
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
+// Launch config of the persistent CTA-pair kernels: clusters of 2 (one TPC), as many as can be
+// co-resident, programmatic dependent launch.
+struct PairLaunch {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  PairLaunch(int smem, cudaStream_t s) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  }
+  template <class Kern>
+  int max_clusters(Kern kern) {
+    cfg.gridDim = dim3(2 * (sm_count() / 2));
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = sm_count() / 2;
+    return n;
+  }
+};
 
 // One persistent launch over np (1 or 2) problems of kinds K0, K1.
-template <int BN, class K0, class K1, int MC>
-cudaError_t launch_tc2_group_mc(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
+template <int BN, class K0, class K1>
+cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
   Tc2Maps m0, m1;
-  bool ok = make_tc2_maps<BN, MC, K0>(pbs[0], &m0);
-  if (np > 1) ok = ok && make_tc2_maps<BN, MC, K1>(pbs[1], &m1);
+  bool ok = make_tc2_maps<BN, K0>(pbs[0], &m0);
+  if (np > 1) ok = ok && make_tc2_maps<BN, K1>(pbs[1], &m1);
   else m1 = m0;
   if (!ok) return cudaErrorInvalidValue;
-  auto kern = slice_gemm_tc2_kernel<BN, K0, K1, MC>;
+  auto kern = slice_gemm_tc2_kernel<BN, K0, K1>;
   const int smem = Smem2<BN, K0::OUT, K1::OUT>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int64_t t0 = tc2_tiles(pbs[0], BN, MC);
-  const int64_t tiles = t0 + (np > 1 ? tc2_tiles(pbs[1], BN, MC) : 0);
+  const int64_t t0 = tc2_tiles(pbs[0], BN);
+  const int64_t tiles = t0 + (np > 1 ? tc2_tiles(pbs[1], BN) : 0);
   if (tiles <= 0) return cudaSuccess;
   if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2 * MC;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  // persistent: as many clusters as can be co-resident (2 MC-CTA clusters need whole TPC groups)
-  static int max_clusters[3] = {0, 0, 0};
-  if (!max_clusters[MC]) {
-    cfg.gridDim = dim3(2 * MC * (sm_count() / (2 * MC)));
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0)
-      n = sm_count() / (2 * MC);
-    max_clusters[MC] = n;
-  }
-  const int clusters = static_cast<int>(tiles < max_clusters[MC] ? tiles : max_clusters[MC]);
-  const int grid = 2 * MC * clusters;
-  cfg.gridDim = dim3(grid);
-  static const int nostore = getenv("STL_GEMM_NOSTORE") ? atoi(getenv("STL_GEMM_NOSTORE")) : 0;
+  PairLaunch L(smem, s);
+  static const int max_clusters = L.max_clusters(kern);
+  const int clusters = static_cast<int>(tiles < max_clusters ? tiles : max_clusters);
+  L.cfg.gridDim = dim3(2 * clusters);
   GroupArgs ga{};
   for (int i = 0; i < 2; ++i) {
     const SliceGemmProblem& pb = pbs[i < np ? i : 0];
@@ -1268,28 +1059,8 @@ cudaError_t launch_tc2_group_mc(const SliceGemmProblem* pbs, int np, cudaStream_
   ga.r = pbs[0].r;
   ga.total0 = static_cast<int>(t0);
   ga.total = static_cast<int>(tiles);
-  ga.nostore = nostore;
-  static const bool dbg_on = getenv("STL_GEMM_DEBUG") != nullptr;
-  static unsigned long long* dbg = nullptr;
-  if (dbg_on && !dbg) cudaMalloc(&dbg, 2 * 256 * sizeof(unsigned long long));
-  if (dbg_on) {
-    cudaMemsetAsync(dbg, 0, 2 * 256 * sizeof(unsigned long long), s);
-    ga.dbg = dbg;
-  }
-  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, m0.a, m0.b, m0.c, m0.c2, m1.a, m1.b, m1.c,
-                                      m1.c2, ga);
-  if (dbg_on) {
-    unsigned long long h[512];
-    const int nc = clusters * MC;
-    cudaMemcpyAsync(h, dbg, sizeof(unsigned long long) * 2 * nc, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    double te = 0, tf = 0;
-    for (int i = 0; i < nc; ++i) { te += h[2 * i]; tf += h[2 * i + 1]; }
-    fprintf(stderr, "[gemm dbg] MC=%d clusters=%d OUT=%d/%d np=%d M=%d N=%d K=%d tiles/cluster=%.2f MMA-thread avg us: wait tempty=%.1f wait full=%.1f\n",
-            MC, clusters, K0::OUT, K1::OUT, np, ga.M[0], ga.N[0], ga.K[0], double(tiles) / nc,
-            te / nc / 1e3, tf / nc / 1e3);
-  }
-  return le;
+  ga.nostore = probe_env("STL_GEMM_NOSTORE", 0);
+  return cudaLaunchKernelEx(&L.cfg, kern, m0.a, m0.b, m0.c, m0.c2, m1.a, m1.b, m1.c, m1.c2, ga);
 }
 
 // Wide-tile launch (256 x 512 pair tiles) of np (1 or 2) problems; see slice_gemm_wide_kernel.
@@ -1297,15 +1068,14 @@ int64_t wide_tiles(const SliceGemmProblem& pb) {
   return static_cast<int64_t>(pb.r) * ((pb.M + 255) / 256) * ((pb.N + 511) / 512);
 }
 
-template <class K0, class K1, bool SIDE = false>
-cudaError_t launch_wide_group(const SliceGemmProblem* pbs, int np, cudaStream_t s,
-                              const SideArgs* side = nullptr, int rev = 0) {
+template <class K0, class K1>
+cudaError_t launch_wide_group(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
   Tc2Maps m0, m1;
-  bool ok = make_tc2_maps<256, 1, K0>(pbs[0], &m0);
-  if (np > 1) ok = ok && make_tc2_maps<256, 1, K1>(pbs[1], &m1);
+  bool ok = make_tc2_maps<256, K0>(pbs[0], &m0);
+  if (np > 1) ok = ok && make_tc2_maps<256, K1>(pbs[1], &m1);
   else m1 = m0;
   if (!ok) return cudaErrorInvalidValue;
-  auto kern = slice_gemm_wide_kernel<K0, K1, SIDE>;
+  auto kern = slice_gemm_wide_kernel<K0, K1>;
   const int smem = SmemW<K0::OUT, K1::OUT>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -1313,28 +1083,8 @@ cudaError_t launch_wide_group(const SliceGemmProblem* pbs, int np, cudaStream_t 
   const int64_t nwide = t0 + (np > 1 ? wide_tiles(pbs[1]) : 0);
   if (nwide <= 0) return cudaSuccess;
   if (nwide >= (int64_t(1) << 30)) return cudaErrorInvalidValue;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.blockDim = dim3(SIDE ? kSideThreads : kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  static int max_clusters = 0;
-  if (!max_clusters) {
-    cfg.gridDim = dim3(2 * (sm_count() / 2));
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = sm_count() / 2;
-    max_clusters = n;
-  }
-  static const int lag = env_int("STL_GEMM_LAG", 1);
-  static const int nosplit = env_int("STL_GEMM_NOSPLIT", 0);
+  PairLaunch L(smem, s);
+  static const int max_clusters = L.max_clusters(kern);
   WideArgs wa{};
   for (int i = 0; i < 2; ++i) {
     const SliceGemmProblem& pb = pbs[i < np ? i : 0];
@@ -1348,34 +1098,20 @@ cudaError_t launch_wide_group(const SliceGemmProblem* pbs, int np, cudaStream_t 
   const int clusters = static_cast<int>(nwide < max_clusters ? nwide : max_clusters);
   const int rem = static_cast<int>(nwide % clusters);
   // split the last partial wave into half tiles when they fit one wave
-  wa.nsplit = (!nosplit && rem > 0 && 2 * rem <= clusters) ? rem : 0;
+  wa.nsplit = (!probe_env("STL_GEMM_NOSPLIT", 0) && rem > 0 && 2 * rem <= clusters) ? rem : 0;
   wa.total = wa.nwide + wa.nsplit;
+  const int lag = probe_env("STL_GEMM_LAG", 1);  // measured: 0 ~ 1 > 2 (r02_wide_tiles.log)
   wa.lag = lag < 0 ? 0 : (lag > kWStages - 2 ? kWStages - 2 : lag);
-  static const int nostore = env_int("STL_GEMM_NOSTORE", 0);
-  wa.nostore = nostore;
-  wa.rev = np == 1 ? rev : 0;
-  cfg.gridDim = dim3(2 * clusters);
-  SideArgs sa{};
-  if (side) sa = *side;
-  return cudaLaunchKernelEx(&cfg, kern, m0.a, m0.b, m0.c, m0.c2, m1.a, m1.b, m1.c, m1.c2, wa, sa);
+  wa.nostore = probe_env("STL_GEMM_NOSTORE", 0);
+  L.cfg.gridDim = dim3(2 * clusters);
+  return cudaLaunchKernelEx(&L.cfg, kern, m0.a, m0.b, m0.c, m0.c2, m1.a, m1.b, m1.c, m1.c2, wa);
 }
 
 // Wide tiles for problems whose output is at least one wide tile across (N >= 512) and whose
 // output mode the wide kernel stages (fp32, bf16, F24; not the fp32 + bf16 copy).
 bool wide_eligible(const SliceGemmProblem& pb) {
-  static const int off = env_int("STL_GEMM_NOWIDE", 0);
-  return !off && pb.N >= 512 && pb.M > 128 && !pb.c2 && pb.c_dtype != kF32;
-}
-
-// STL_GEMM_MC = 2 (opt-in): four-CTA clusters, two pairs sharing A by TMA multicast. Measured:
-// ~8% more work per SM, but only 33 such clusters are co-resident (clusters live inside a GPC:
-// 132 of 148 SMs), net -3%; running a pair-cluster launch beside it on the 16 left-over SMs
-// (second stream) gained nothing either. Default: pair clusters on all 148 SMs.
-template <int BN, class K0, class K1>
-cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
-  static const int mc = env_int("STL_GEMM_MC", 1);
-  if (mc == 2) return launch_tc2_group_mc<BN, K0, K1, 2>(pbs, np, s);
-  return launch_tc2_group_mc<BN, K0, K1, 1>(pbs, np, s);
+  return !probe_env("STL_GEMM_NOWIDE", 0) && pb.N >= 512 && pb.M > 128 && !pb.c2 &&
+         pb.c_dtype != kF32;
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -1427,8 +1163,7 @@ bool make_bf16_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
 
 bool pdl_enabled() {
   static const bool on = [] {
-    const char* e = getenv("STL_PDL");
-    return e ? atoi(e) != 0 : true;
+    return probe_env("STL_PDL", 1) != 0;
   }();
   return on;
 }
@@ -1459,7 +1194,7 @@ bool slice_gemm_tc_supported(const SliceGemmProblem& pb) {
 
 bool slice_gemm_f24_supported(const SliceGemmProblem& pb) {
   return slice_gemm_tc_supported(pb) && pb.M > 128 && pb.N % 16 == 0 && !pb.c2 &&
-         (reinterpret_cast<uintptr_t>(pb.c) & 15) == 0 && getenv("STL_GEMM_1CTA") == nullptr;
+         (reinterpret_cast<uintptr_t>(pb.c) & 15) == 0 && !probe_env("STL_GEMM_1CTA", 0);
 }
 
 namespace {
@@ -1472,7 +1207,7 @@ bool pair_eligible(const SliceGemmProblem& pb) {
 }  // namespace
 
 bool slice_gemm_tc_group_supported(const SliceGemmProblem& p0, const SliceGemmProblem& p1) {
-  static const bool off = getenv("STL_GEMM_NOGROUP") != nullptr || getenv("STL_GEMM_1CTA");
+  const bool off = probe_env("STL_GEMM_NOGROUP", 0) || probe_env("STL_GEMM_1CTA", 0);
   if (off) return false;
   // the instantiated pair: g_w (A, B MN-major; fp32) with g_u (A K-major, B MN-major; F24/fp32)
   const bool kinds = p0.a_layout == 1 && p0.b_layout == 1 && p0.c_dtype == kF32 &&
@@ -1498,109 +1233,9 @@ cudaError_t slice_gemm_tc_group(const SliceGemmProblem& p0, const SliceGemmProbl
   return launch_tc2_group<256, K0, GemmKind<false, true, kOutF32>>(pbs, 2, s);
 }
 
-// ------------------------------------------------------------ band-overlapped forward
-namespace {
-bool al16p(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-}  // namespace
-
-bool forward_banded_supported(int r, int64_t bi, int64_t bk, int64_t bj, int64_t ldx, int64_t ldy,
-                              const void* x, const void* y, const void* x_enc, const void* y_enc,
-                              const void* w_enc, const float* e_x, const float* d) {
-  // measured a wash (profiles/r02_band_overlap_*.log): opt-in only
-  static const int on = env_int("STL_BAND", 0);
-  if (!on || env_int("STL_GEMM_NOWIDE", 0)) return false;
-  return r >= 1 && r <= 32 && bi >= 512 && bk % 64 == 0 && bk >= 256 && bj % 64 == 0 &&
-         bj >= 512 && bi < (int64_t(1) << 30) && ldx % 8 == 0 && ldy % 8 == 0 && al16p(x) &&
-         al16p(y) && al16p(x_enc) && al16p(y_enc) && al16p(w_enc) && al16p(e_x) && al16p(d) &&
-         get_encode_fn() != nullptr;
-}
-
-// encode(band 0) -> [slice GEMMs(band 0) | warps 2-3: encode(band 1)]
-//                -> [slice GEMMs(band 1) | warps 2-3: decode(band 0)] -> decode(band 1).
-// Bands are whole 256-row blocks of the tile grid; band 0 = the first half (STL_BAND0_MB
-// overrides). Two of the four transform passes run under the tensor-core work; the band-1
-// GEMM re-reads W_enc (its p-major order is reversed so the slices the band-0 GEMM read last
-// are still in L2).
-cudaError_t forward_banded(const void* x, int64_t ldx, const void* w_enc, const float* e_x,
-                           const float* d, int r, int64_t bi, int64_t bk, int64_t bj,
-                           void* x_enc, void* y_enc, void* y, int64_t ldy, cudaStream_t s) {
-  const int64_t nmb = (bi + 255) / 256;
-  static const int b0 = env_int("STL_BAND0_MB", 0);
-  int64_t mb0 = b0 > 0 ? b0 : nmb / 2;
-  if (mb0 < 1) mb0 = 1;
-  if (mb0 >= nmb) mb0 = nmb - 1;
-  const int64_t Ib = mb0 * 256;
-  // probes (timing only): STL_BAND_PROFILE prints per-launch times; STL_BAND_NOSIDE=1/2 drops
-  // the side encode / decode (wrong results)
-  static const int prof = env_int("STL_BAND_PROFILE", 0), noside = env_int("STL_BAND_NOSIDE", 0);
-  cudaEvent_t ev[5];
-  if (prof)
-    for (auto& v : ev) cudaEventCreate(&v);
-  if (prof) cudaEventRecord(ev[0], s);
-  const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
-  __nv_bfloat16* xe = static_cast<__nv_bfloat16*>(x_enc);
-  __nv_bfloat16* ye = static_cast<__nv_bfloat16*>(y_enc);
-  __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(y);
-  cudaError_t e = tiles_to_planes_stream(x, kBF16, ldx, Ib, bk, e_x, r, x_enc, kBF16, nullptr,
-                                         kBF16, nullptr, nullptr, s, bi);
-  if (e != cudaSuccess) return e;
-  if (prof) cudaEventRecord(ev[1], s);
-  using Kd = GemmKind<false, false, kOutBf16>;
-  SliceGemmProblem p0{x_enc, 0, w_enc, 0, y_enc, kBF16, kBF16, r, Ib, bj, bk};
-  p0.m_stride = bi;
-  SideArgs se{};
-  se.mode = 1;
-  se.P = r;
-  se.src = xb;
-  se.dst = xe;
-  se.coef = e_x;
-  se.ld = ldx;
-  se.plane_stride = bi * bk;
-  se.I0 = static_cast<int>(Ib);
-  se.I1 = static_cast<int>(bi);
-  se.bc = static_cast<int>(bk);
-  if (noside & 1) se.mode = 0;
-  e = launch_wide_group<Kd, Kd, true>(&p0, 1, s, &se);
-  if (e != cudaSuccess) return e;
-  if (prof) cudaEventRecord(ev[2], s);
-  SliceGemmProblem p1{xe + Ib * bk, 0, w_enc, 0, ye + Ib * bj, kBF16, kBF16, r, bi - Ib, bj, bk};
-  p1.m_stride = bi;
-  SideArgs sd{};
-  sd.mode = 2;
-  sd.P = r;
-  sd.src = ye;
-  sd.dst = yb;
-  sd.coef = d;
-  sd.ld = ldy;
-  sd.plane_stride = bi * bj;
-  sd.I0 = 0;
-  sd.I1 = static_cast<int>(Ib);
-  sd.bc = static_cast<int>(bj);
-  static const int rev = env_int("STL_BAND_REV", 1);
-  if (noside & 2) sd.mode = 0;
-  e = launch_wide_group<Kd, Kd, true>(&p1, 1, s, &sd, rev);
-  if (e != cudaSuccess) return e;
-  if (prof) cudaEventRecord(ev[3], s);
-  e = planes_to_tiles_stream(ye + Ib * bj, kBF16, r, bi - Ib, bj, d, yb + 4 * Ib * ldy, kBF16,
-                             ldy, nullptr, kBF16, 0, nullptr, nullptr, s, bi);
-  if (prof) {
-    cudaEventRecord(ev[4], s);
-    cudaEventSynchronize(ev[4]);
-    float t[4];
-    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
-    fprintf(stderr, "[band] mb0=%lld enc0 %.1f us | gemm0+enc1 %.1f | gemm1+dec0 %.1f | dec1 %.1f\n",
-            (long long)mb0, 1e3 * t[0], 1e3 * t[1], 1e3 * t[2], 1e3 * t[3]);
-    for (auto& v : ev) cudaEventDestroy(v);
-  }
-  return e;
-}
-
 cudaError_t slice_gemm_tc(const SliceGemmProblem& pb, cudaStream_t s) {
   const bool a_mn = pb.a_layout != 0, b_mn = pb.b_layout != 0;
-  static const int force1 = [] {
-    const char* e = getenv("STL_GEMM_1CTA");
-    return e ? atoi(e) : 0;
-  }();
+  const int force1 = probe_env("STL_GEMM_1CTA", 0);
   // The pair kernel stores C with TMA (fp32 output, 16-byte aligned rows); other cases use the
   // 1-CTA kernel's direct-store epilogue.
   if (pb.c_dtype == kF24 && !slice_gemm_f24_supported(pb)) return cudaErrorNotSupported;

@@ -65,10 +65,6 @@ struct Layout {
 
 __host__ __device__ inline uint32_t rup(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
 
 template <int MODE, typename ZT, int kT, int CW>
 inline Layout make_layout(int P, int Pb, uint32_t budget) {
@@ -88,7 +84,7 @@ inline Layout make_layout(int P, int Pb, uint32_t budget) {
     L.out_bytes = rup(4 * L.out_stride, 1024);
   }
   L.red_bytes = 0;  // the final per-warp reduction partials reuse the (drained) stage ring
-  static const uint32_t max_st = env_int("STL_STREAM_STAGES", 8);
+  static const uint32_t max_st = probe_env("STL_STREAM_STAGES", 8);
   const uint32_t fixed = 2 * groups_of<MODE, CW>() * L.out_bytes + L.red_bytes;
   uint32_t ns = (budget - fixed) / L.stage_bytes;
   if (ns > max_st) ns = max_st;
@@ -803,8 +799,8 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
                       cudaStream_t s, uint32_t budget) {
   a.Pb = ((a.P + 7) / 8) * 8;
   const Layout L = make_layout<MODE, ZT, kT, CW>(a.P, a.Pb, budget);
-  static const int stg = env_int("STL_STREAM_STG", 0);
-  static const int multirow = env_int("STL_STREAM_MULTIROW", 1);
+  static const int stg = probe_env("STL_STREAM_STG", 0);
+  static const int multirow = probe_env("STL_STREAM_MULTIROW", 1);
   // narrow matrices (bc < kT, bc | kT): a unit spans R = kT / bc whole tile rows (R <= 8: one
   // producer lane per matrix row), so units stay full instead of bc / kT full
   const int R = (multirow && !stg && a.bc < kT && kT % a.bc == 0 && kT / a.bc <= 8 &&
@@ -829,9 +825,9 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
                                        static_cast<int>(L.total));
   if (e != cudaSuccess) return e;
   a.stg = stg;
-  static const int noc = env_int("STL_STREAM_NOCOMPUTE", 0);
+  static const int noc = probe_env("STL_STREAM_NOCOMPUTE", 0);
   a.nocompute = noc;
-  static const int dbg_on = env_int("STL_STREAM_DEBUG", 0);
+  static const int dbg_on = probe_env("STL_STREAM_DEBUG", 0);
   static unsigned long long* dbg = nullptr;
   if (dbg_on && !dbg) cudaMalloc(&dbg, 4 * 1024 * sizeof(unsigned long long));
   if (dbg_on) cudaMemsetAsync(dbg, 0, 4 * 1024 * sizeof(unsigned long long), s);
@@ -865,8 +861,8 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
 template <int MODE, typename ZT, int MT>
 cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                      cudaStream_t s) {
-  static const int force_t = env_int("STL_STREAM_T", 0);
-  static const uint32_t budget = env_int("STL_STREAM_SMEM_KB", 212) * 1024;
+  static const int force_t = probe_env("STL_STREAM_T", 0);
+  static const uint32_t budget = probe_env("STL_STREAM_SMEM_KB", 212) * 1024;
   const int pb = ((a.P + 7) / 8) * 8;
   const Layout L512 = make_layout<MODE, ZT, 512, 16>(a.P, pb, budget);
   const bool use512 = force_t ? force_t == 512
@@ -894,15 +890,12 @@ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
 
-bool g_use_stream = true;
-void set_transform_stream(bool on) { g_use_stream = on; }
-
 // encode (+ g_d-style reduction): bf16 matrix -> bf16 planes; red planes bf16 or fp32.
 cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
                                    const float* coef, int P, void* out, int odt, const void* rp,
                                    int rdt, float* ro, float* rw, cudaStream_t s,
                                    int64_t plane_rows) {
-  if (!g_use_stream || mdt != kBF16 || odt != kBF16 || bc % 64 || ldm % 8 || P < 1 || P > 64 ||
+  if (mdt != kBF16 || odt != kBF16 || bc % 64 || ldm % 8 || P < 1 || P > 64 ||
       !al16(m) || !al16(out))
     return cudaErrorNotSupported;
   if (rp && (P > 32 || !al16(rp) || !ro || !rw || (rdt == kF24 && bc % 128)))
@@ -928,7 +921,7 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
                                    const float* coef, void* out, int odt, int64_t ldo,
                                    const void* rm, int rdt, int64_t ldr, float* ro, float* rw,
                                    cudaStream_t s, int64_t plane_rows) {
-  if (!g_use_stream || odt != kBF16 || bc % 64 || ldo % 8 || Q < 1 || Q > 64 || !al16(in) ||
+  if (odt != kBF16 || bc % 64 || ldo % 8 || Q < 1 || Q > 64 || !al16(in) ||
       !al16(out))
     return cudaErrorNotSupported;
   if (rm && (rdt != kBF16 || Q > 32 || ldr % 8 || !al16(rm) || !ro || !rw))

@@ -380,11 +380,10 @@ cudaError_t p2t_dispatch(const void* in, int idt, int Q, int64_t br, int64_t bc,
 
 }  // namespace
 
-bool g_use_mma = true;
-bool g_use_mma_decode = false;  // mma decode is slower than FFMA today (scattered stores)
-void set_transform_mma(bool on) { g_use_mma = on; }
-void set_transform_mma_decode(bool on) { g_use_mma_decode = on; }
-
+// Dispatch: the streaming kernels first (t = 4, aligned bf16), then the t = 4 register /
+// tensor-core fallbacks, then the generic tile-size-templated FFMA kernels. F24 planes (a bf16
+// path intermediate) are read by the streaming kernels only: if they decline, fail loudly
+// instead of reading the 3-byte format as fp32.
 cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br, int64_t bc,
                             int t, const float* coef, int P, void* out, int out_dtype,
                             const void* red_planes, int red_dtype, float* red_out,
@@ -395,14 +394,13 @@ cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br,
                                            red_planes, red_dtype, red_out, red_ws, s);
     if (e != cudaErrorNotSupported) return e;
   }
-  if (t == 4 && g_use_mma) {
+  if (red_planes && red_dtype == kF24) return cudaErrorNotSupported;
+  if (t == 4) {
     cudaError_t e = tiles_to_planes_mma(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype,
                                         red_planes, red_dtype, red_out, red_ws, s);
     if (e != cudaErrorNotSupported) return e;
-  }
-  if (t == 4) {
-    cudaError_t e = tiles_to_planes4(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes,
-                                     red_dtype, red_out, red_ws, s);
+    e = tiles_to_planes4(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, red_planes,
+                         red_dtype, red_out, red_ws, s);
     if (e != cudaErrorNotSupported) return e;
   }
   switch (t) {
@@ -424,11 +422,7 @@ cudaError_t planes_to_tiles(const void* in, int in_dtype, int Q, int64_t br, int
                                            red_m, red_dtype, ldr, red_out, red_ws, s);
     if (e != cudaErrorNotSupported) return e;
   }
-  if (t == 4 && g_use_mma && g_use_mma_decode) {
-    cudaError_t e = planes_to_tiles_mma(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m,
-                                        red_dtype, ldr, red_out, red_ws, s);
-    if (e != cudaErrorNotSupported) return e;
-  }
+  if (in_dtype == kF24) return cudaErrorNotSupported;
   if (t == 4) {
     cudaError_t e = planes_to_tiles4(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m,
                                      red_dtype, ldr, red_out, red_ws, s);

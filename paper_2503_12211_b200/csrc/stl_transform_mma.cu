@@ -1,9 +1,10 @@
-// stl_transform_mma.cu — t = 4 tile transforms on the tensor cores (warp-level mma.sync).
+// stl_transform_mma.cu — t = 4 encode on the tensor cores (warp-level mma.sync), the fallback
+// of the streaming encode (stl_stream.cu) for tile-column counts that are not multiples of 64
+// (the T2T-ViT-7 layers).
 //
 // The per-tile change of basis is a GEMM with a tiny inner dimension:
 //   encode  (encode_tiles, snf_operator.py:80-85):  C[tile][p] = sum_c X[tile][c] * E[p][c]
-//   decode  (decode_tiles, snf_operator.py:88-96):  C[tile][c] = sum_p Z[p][tile] * D[p][c]
-//   g_d / g_ex (toy_network.py:100,104):            R[p][c]   = sum_tiles Z[p][tile] * X[tile][c]
+//   g_d (toy_network.py:100):                       R[p][c]   = sum_tiles Z[p][tile] * X[tile][c]
 // On CUDA cores these cost r FMAs per element (~43 us of FFMA at 8192^2, as much as the HBM
 // time), so they run as m16n8k16 bf16 MMAs with fp32 accumulation, leaving the kernels
 // HBM-bound. Operands are loaded straight from global memory in fragment layout:
@@ -234,144 +235,6 @@ __global__ void __launch_bounds__(kThreadsM)
   if constexpr (RED) R.finish(sred, P, red_partial);
 }
 
-// ---------------------------------------------------------------------------------------------
-// decode: Q planes (fp32 or bf16) -> tiles. RED: g_ex += Z (x) X' (X' = bf16 matrix).
-template <typename Tz, typename Tout, bool RED, int KST>
-__global__ void __launch_bounds__(kThreadsM)
-    k_decode_mma(const Tz* __restrict__ z, int Q, int64_t br, int64_t bc,
-                 const float* __restrict__ coef, Tout* __restrict__ out, int64_t ldo,
-                 const __nv_bfloat16* __restrict__ xr, int64_t ldr, float* __restrict__ red_partial) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int kOutStride = 128 + (sizeof(Tout) == 2 ? 8 : 4);  // padded staged output row
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  Tout* ostage = reinterpret_cast<Tout*>(smem) + warp * 4 * kOutStride;
-  float* sred = reinterpret_cast<float*>(smem + kWarpsM * 4 * kOutStride * sizeof(Tout));
-  // D as B fragments (K = p, N = c): b0 = D[16ks+2q, +1][c], b1 = D[16ks+2q+8, +9][c], c = 8nt+g
-  uint32_t bh[KST][2][2], bl[KST][2][2];
-#pragma unroll
-  for (int ks = 0; ks < KST; ++ks)
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = 16 * ks + 2 * q + 8 * h, c = 8 * nt + g;
-        const float d0 = p < Q ? coef[p * 16 + c] : 0.f;
-        const float d1 = p + 1 < Q ? coef[(p + 1) * 16 + c] : 0.f;
-        split2(d0, d1, bh[ks][nt][h], bl[ks][nt][h]);
-      }
-  RedAcc R;
-  R.zero();
-  const int64_t ntiles = br * bc;
-  const int64_t tasks_per_row = (bc + kTaskTiles - 1) / kTaskTiles;
-  const int64_t ntasks = br * tasks_per_row;
-  for (int64_t task = static_cast<int64_t>(blockIdx.x) * kWarpsM + warp; task < ntasks;
-       task += static_cast<int64_t>(gridDim.x) * kWarpsM) {
-    const int64_t I = task / tasks_per_row;
-    const int64_t J0 = (task - I * tasks_per_row) * kTaskTiles;
-    const int64_t rem_mt = (bc - J0) >> 4;
-    const int nmt = rem_mt < kMtPerTask ? static_cast<int>(rem_mt) : kMtPerTask;
-    const Tz* zrow = z + I * bc + J0;
-    // 32-tile groups; M rows permuted so thread (g, q) owns tiles 4g .. 4g+3 of the group:
-    // m-tile A rows g, g+8 <-> tiles 4g, 4g+1; m-tile B rows g, g+8 <-> tiles 4g+2, 4g+3.
-    const int ngroups = nmt >> 1;
-    for (int gp = 0; gp < ngroups; gp += 2) {
-      // issue the loads of two 32-tile groups before any math (memory-level parallelism)
-      float vv[2][KST][4][4];  // [group][k-step][plane 2q, 2q+1, 2q+8, 2q+9][tile 4g + i]
-#pragma unroll
-      for (int gg = 0; gg < 2; ++gg) {
-        const bool gok = gp + gg < ngroups;
-        const Tz* zt = zrow + 32 * (gp + gg) + 4 * g;
-#pragma unroll
-        for (int ks = 0; ks < KST; ++ks)
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int p = 16 * ks + 2 * q + (h & 1) + 8 * (h >> 1);
-            float* v = vv[gg][ks][h];
-            if (gok && p < Q) {
-              if constexpr (sizeof(Tz) == 2) {
-                const uint2 u = *reinterpret_cast<const uint2*>(zt + p * ntiles);
-                const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-                const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-                v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
-              } else {
-                const float4 f = *reinterpret_cast<const float4*>(zt + p * ntiles);
-                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-              }
-            } else {
-              v[0] = v[1] = v[2] = v[3] = 0.f;
-            }
-          }
-      }
-#pragma unroll
-      for (int gg = 0; gg < 2; ++gg) {
-      const int gi = gp + gg;
-      if (gi >= ngroups) break;
-      float acc[2][2][4] = {};  // [m-tile A/B][n-tile][frag]
-#pragma unroll
-      for (int ks = 0; ks < KST; ++ks) {
-        float (&v)[4][4] = vv[gg][ks];
-#pragma unroll
-        for (int m = 0; m < 2; ++m) {
-          // a0 = (tile 4g+2m, planes 2q, 2q+1), a1 = (tile 4g+2m+1, ...), a2/a3: planes 2q+8, +9
-          const int t0 = 2 * m, t1 = 2 * m + 1;
-          if constexpr (sizeof(Tz) == 2) {
-            const uint32_t a0 = pack2(v[0][t0], v[1][t0]), a1 = pack2(v[0][t1], v[1][t1]);
-            const uint32_t a2 = pack2(v[2][t0], v[3][t0]), a3 = pack2(v[2][t1], v[3][t1]);
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-              mma(acc[m][nt], a0, a1, a2, a3, bh[ks][nt][0], bh[ks][nt][1]);
-              mma(acc[m][nt], a0, a1, a2, a3, bl[ks][nt][0], bl[ks][nt][1]);
-            }
-          } else {
-            uint32_t h0, l0, h1, l1, h2, l2, h3, l3;
-            split2(v[0][t0], v[1][t0], h0, l0);
-            split2(v[0][t1], v[1][t1], h1, l1);
-            split2(v[2][t0], v[3][t0], h2, l2);
-            split2(v[2][t1], v[3][t1], h3, l3);
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-              mma(acc[m][nt], h0, h1, h2, h3, bh[ks][nt][0], bh[ks][nt][1]);
-              mma(acc[m][nt], l0, l1, l2, l3, bh[ks][nt][0], bh[ks][nt][1]);
-              mma(acc[m][nt], h0, h1, h2, h3, bl[ks][nt][0], bl[ks][nt][1]);
-            }
-          }
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int m = 0; m < 2; ++m)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          const int a = 2 * nt + (q >> 1), b = 2 * (q & 1);
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            Tout* d = ostage + a * kOutStride + (4 * g + 2 * m + t) * 4 + b;
-            if constexpr (sizeof(Tout) == 2)
-              *reinterpret_cast<uint32_t*>(d) = pack2(acc[m][nt][2 * t], acc[m][nt][2 * t + 1]);
-            else
-              *reinterpret_cast<float2*>(d) = make_float2(acc[m][nt][2 * t], acc[m][nt][2 * t + 1]);
-          }
-        }
-      __syncwarp();
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        Tout* dst = out + (I * 4 + a) * ldo + (J0 + 32 * gi) * 4 + 4 * lane;
-        const Tout* src = ostage + a * kOutStride + 4 * lane;
-        if constexpr (sizeof(Tout) == 2)
-          *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(src);
-        else
-          *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
-      }
-      if constexpr (RED) {
-        const __nv_bfloat16* xg = xr + I * 4 * ldr + (J0 + 32 * gi) * 4;
-        R.step(zrow + 32 * gi, ntiles, Q, xg, ldr);
-        R.step(zrow + 32 * gi + 16, ntiles, Q, xg + 64, ldr);
-      }
-      }
-    }
-  }
-  if constexpr (RED) R.finish(sred, Q, red_partial);
-}
 
 int grid_m(int64_t ntasks, int cap) {
   int64_t g = (ntasks + kWarpsM - 1) / kWarpsM;
@@ -404,35 +267,6 @@ cudaError_t launch_enc(const void* m, int64_t ldm, int64_t br, int64_t bc, const
   return cudaGetLastError();
 }
 
-template <typename Tz, typename Tout, bool RED, int KST>
-cudaError_t launch_dec_k(const void* in, int Q, int64_t br, int64_t bc, const float* coef,
-                         void* out, int64_t ldo, const void* rm, int64_t ldr, float* ro, float* rw,
-                         cudaStream_t s) {
-  constexpr int kOutStride = 128 + (sizeof(Tout) == 2 ? 8 : 4);
-  const size_t smem = kWarpsM * 4 * kOutStride * sizeof(Tout) + (RED ? kWarpsM * Q * 16 * 4 : 0);
-  auto k = k_decode_mma<Tz, Tout, RED, KST>;
-  if (cudaError_t e = set_smem(k, smem)) return e;
-  const int64_t ntasks = br * ((bc + kTaskTiles - 1) / kTaskTiles);
-  const int grid = grid_m(ntasks, sm_count() * (RED ? 4 : 8));
-  k<<<grid, kThreadsM, smem, s>>>(static_cast<const Tz*>(in), Q, br, bc, coef,
-                                  static_cast<Tout*>(out), ldo,
-                                  static_cast<const __nv_bfloat16*>(rm), ldr, rw);
-  if (RED) return sum_partials(rw, grid, Q * 16, ro, s);
-  return cudaGetLastError();
-}
-
-template <typename Tz, typename Tout, bool RED>
-cudaError_t launch_dec(const void* in, int Q, int64_t br, int64_t bc, const float* coef, void* out,
-                       int64_t ldo, const void* rm, int64_t ldr, float* ro, float* rw,
-                       cudaStream_t s) {
-  switch ((Q + 15) / 16) {
-    case 1: return launch_dec_k<Tz, Tout, RED, 1>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
-    case 2: return launch_dec_k<Tz, Tout, RED, 2>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
-    case 3: return launch_dec_k<Tz, Tout, RED, 3>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
-    default: return launch_dec_k<Tz, Tout, RED, 4>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
-  }
-}
-
 }  // namespace
 
 // Tensor-core encode: bf16 X, t = 4, bc % 16 == 0. Returns cudaErrorNotSupported otherwise.
@@ -452,22 +286,6 @@ cudaError_t tiles_to_planes_mma(const void* m, int mdt, int64_t ldm, int64_t br,
   if (rdt == kBF16)
     return launch_enc<float, __nv_bfloat16, true>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
   return launch_enc<float, float, true>(m, ldm, br, bc, coef, P, out, rp, ro, rw, s);
-}
-
-// Tensor-core decode: t = 4, bc % 16 == 0, output bf16 (fp32 output keeps the FFMA path so
-// the fp32 parity mode stays full precision); RED needs a bf16 second matrix.
-cudaError_t planes_to_tiles_mma(const void* in, int idt, int Q, int64_t br, int64_t bc,
-                                const float* coef, void* out, int odt, int64_t ldo, const void* rm,
-                                int rdt, int64_t ldr, float* ro, float* rw, cudaStream_t s) {
-  if (odt != kBF16 || bc % 32 || ldo % 8 || Q > 64 || !al16(in) || !al16(out))
-    return cudaErrorNotSupported;
-  if (rm && (rdt != kBF16 || Q > 32 || ldr % 8 || !al16(rm))) return cudaErrorNotSupported;
-  if (idt == kF32) {
-    if (rm) return launch_dec<float, __nv_bfloat16, true>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
-    return launch_dec<float, __nv_bfloat16, false>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
-  }
-  if (rm) return launch_dec<__nv_bfloat16, __nv_bfloat16, true>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
-  return launch_dec<__nv_bfloat16, __nv_bfloat16, false>(in, Q, br, bc, coef, out, ldo, rm, ldr, ro, rw, s);
 }
 
 }  // namespace stl

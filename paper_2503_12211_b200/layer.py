@@ -3,7 +3,8 @@
 Mirror of the hot-path part of ``strassen_tile.toy_network`` (toy_network.py:45-106):
 ``StlLayer``, ``stl_layer_forward``, ``_layer_forward_cached`` and ``_layer_backward`` keep the
 reference's names, argument order, ShapeError checks and return conventions; the arithmetic is
-``stl_forward`` / ``stl_backward`` of the C ABI. On top of that, ``StlLinear`` packages the same
+``stl_forward_ex`` / ``stl_backward_ex`` of the C ABI (the cache's slice-product format is
+recorded by its dtype and passed to the backward explicitly). On top of that, ``StlLinear`` packages the same
 kernels as a ``torch.autograd.Function`` / ``nn.Module`` for training (the DP path of bench.py).
 
 Weights are held in the native slice-major layout ``w_planes`` (r, out_tiles, in_tiles); the
@@ -18,7 +19,7 @@ import torch
 
 from . import _lib
 from .dense_core import ShapeError, as_matrix, to_tensor
-from .snf_operator import SnfTriple, _dt, _forward, _stream, as_triple
+from .snf_operator import SnfTriple, _dt, _forward, _stream, as_triple, cache_dtype_format
 
 
 class StlLayer:
@@ -86,10 +87,13 @@ def stl_layer_forward(layer: StlLayer, x) -> torch.Tensor:
     return _forward(x, layer.w_planes, layer.snf)
 
 
-def _layer_forward_cached(layer: StlLayer, x):
-    """Forward plus the (vx, u, y_enc) cache (toy_network.py:86-92)."""
+def _layer_forward_cached(layer: StlLayer, x, *, products=None):
+    """Forward plus the (vx, u, y_enc) cache (toy_network.py:86-92).
+
+    `products` (keyword, not in the reference): force the slice-product format of the cache
+    (torch.bfloat16, "f24", torch.float32; default per shape, include/stl_b200.h)."""
     x = _check_input(layer, x)
-    y, u, y_enc = _forward(x, layer.w_planes, layer.snf, keep_cache=True)
+    y, u, y_enc = _forward(x, layer.w_planes, layer.snf, keep_cache=True, products=products)
     return y, LayerCache(x, u, y_enc)
 
 
@@ -115,11 +119,12 @@ def backward_raw(snf: SnfTriple, w_planes: torch.Tensor, cache: LayerCache, gy: 
     def ptr(tns):
         return tns.data_ptr() if tns is not None else None
 
-    _lib.check(lib.stl_backward(
+    # the cache carries its format (its dtype); the backward is told, never guesses
+    _lib.check(lib.stl_backward_ex(
         gy.data_ptr(), gy.stride(0), x.data_ptr(), x.stride(0), w_planes.data_ptr(),
-        snf.e_x.data_ptr(), snf.d.data_ptr(), u.data_ptr(), y_enc.data_ptr(), M, K, N, t, r,
-        _dt(x.dtype), ptr(g_ex), ptr(g_d), ptr(g_w), ptr(g_x), K, g_enc.data_ptr(), ptr(g_u),
-        ptr(red), _stream(dev)))
+        snf.e_x.data_ptr(), snf.d.data_ptr(), u.data_ptr(), y_enc.data_ptr(),
+        cache_dtype_format(y_enc), M, K, N, t, r, _dt(x.dtype), ptr(g_ex), ptr(g_d), ptr(g_w),
+        ptr(g_x), K, g_enc.data_ptr(), ptr(g_u), ptr(red), _lib.STL_PROD_AUTO, _stream(dev)))
     return g_ex, g_d, g_w, g_x
 
 
@@ -195,8 +200,15 @@ class StlLinear(torch.nn.Module):
         return cls(layer.snf, layer.w_planes)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        if x.shape[0] % self.t or x.shape[1] != self.w_planes.shape[2] * self.t:
+        if x.ndim != 2 or x.shape[0] % self.t or x.shape[1] != self.w_planes.shape[2] * self.t:
             raise ShapeError(f"input {tuple(x.shape)} incompatible with STL layer "
                              f"(t={self.t}, in_dim={self.w_planes.shape[2] * self.t})")
+        if self.w_planes.ndim != 3 or self.w_planes.shape[0] != self.r:
+            raise ShapeError(f"w_planes must be (r={self.r}, N/t, K/t), "
+                             f"got {tuple(self.w_planes.shape)}")
+        # the kernels compute in the weights' dtype (e.g. fp32 activations under a bf16 layer,
+        # or autocast output): cast the input, never reinterpret its bytes
+        if x.dtype != self.w_planes.dtype:
+            x = x.to(self.w_planes.dtype)
         return StlLinearFunction.apply(x.contiguous(), self.w_planes, self.e_x, self.d, self.t,
                                        self.r)

@@ -218,9 +218,36 @@ def forward_scratch(M: int, K: int, N: int, t: int, r: int, dtype: torch.dtype,
     return torch.empty((max(nbytes, 1),), dtype=torch.uint8, device=device)
 
 
-def cache_bytes(M: int, K: int, N: int, t: int, r: int, dtype: torch.dtype) -> int:
-    """Bytes of the forward cache y_enc (stl_cache_bytes)."""
-    return int(_lib.load().stl_cache_bytes(M, K, N, t, r, _dt(dtype)))
+def _prod(products) -> int:
+    """Slice-product format argument: None = per shape (STL_PROD_AUTO), or torch.bfloat16 /
+    "f24" / torch.float32 to force one (include/stl_b200.h)."""
+    if products is None:
+        return _lib.STL_PROD_AUTO
+    if products == "f24":
+        return _lib.STL_F24
+    return _dt(products)
+
+
+def cache_format(M: int, K: int, N: int, t: int, r: int, dtype: torch.dtype, products=None) -> int:
+    """Format of the y_enc cache a training forward writes (stl_cache_format): STL_F32,
+    STL_BF16 or STL_F24; ValueError when the forced `products` format cannot be used."""
+    f = int(_lib.load().stl_cache_format(M, K, N, t, r, _dt(dtype), _prod(products)))
+    if f < 0:
+        _lib.check(2)
+    return f
+
+
+def cache_bytes(M: int, K: int, N: int, t: int, r: int, dtype: torch.dtype, products=None) -> int:
+    """Bytes of the forward cache y_enc (stl_cache_bytes_ex)."""
+    return int(_lib.load().stl_cache_bytes_ex(M, K, N, t, r, _dt(dtype), _prod(products)))
+
+
+def cache_dtype_format(y_enc: torch.Tensor) -> int:
+    """The format a y_enc cache tensor holds — the cache carries it in its dtype: uint8 = F24
+    bytes, bfloat16 = bf16 planes, float32 = fp32 planes."""
+    if y_enc.dtype == torch.uint8:
+        return _lib.STL_F24
+    return _dt(y_enc.dtype)
 
 
 def unpack_slice_products(y_enc: torch.Tensor, r: int, rows: int, cols: int) -> torch.Tensor:
@@ -237,40 +264,44 @@ def unpack_slice_products(y_enc: torch.Tensor, r: int, rows: int, cols: int) -> 
     return ((hi << 16) | (lo << 8)).view(torch.float32).reshape(r, rows, cols)
 
 
-def _forward(x: torch.Tensor, w_planes: torch.Tensor, snf: SnfTriple, keep_cache: bool = False):
+def _forward(x: torch.Tensor, w_planes: torch.Tensor, snf: SnfTriple, keep_cache: bool = False,
+             products=None):
     """Shared forward launch: returns y (and the (u, y_enc) cache when keep_cache).
 
-    y_enc is fp32 planes (fp32 mode), or on the bf16 path a uint8 F24 buffer or bf16 planes
-    (stl_cache_bytes decides); unpack_slice_products gives fp32 planes for any of them."""
+    y_enc is fp32 planes (fp32 mode), or on the bf16 path bf16 planes or a uint8 F24 buffer
+    (cache_format decides; the tensor's dtype records it for the backward);
+    unpack_slice_products gives fp32 planes for any of them. `products`: see _prod."""
     t, r = snf.t, snf.r
     M, K = x.shape
+    if w_planes.dtype != x.dtype:
+        raise ValueError(f"weights dtype {w_planes.dtype} != input dtype {x.dtype}")
+    if w_planes.ndim != 3 or w_planes.shape[0] != r:
+        raise ShapeError(f"weight planes must be (r={r}, N/t, K/t), got {tuple(w_planes.shape)}")
     bk, bj = w_planes.shape[2], w_planes.shape[1]
     if bk * t != K:
         raise ShapeError(f"x tiling {(M // t, K // t)} incompatible with weights {(bk, bj)}")
     N = bj * t
     dev = x.device
     snf.on(dev)
+    prod = _prod(products)
     u = torch.empty((r, M // t, bk), dtype=x.dtype, device=dev)
     y_enc = None
     if keep_cache:
-        nbytes = cache_bytes(M, K, N, t, r, x.dtype)
-        if nbytes == 3 * r * (M // t) * bj:
-            y_enc = torch.empty((nbytes,), dtype=torch.uint8, device=dev)
+        fmt = cache_format(M, K, N, t, r, x.dtype, products)
+        if fmt == _lib.STL_F24:
+            y_enc = torch.empty((3 * r * (M // t) * bj,), dtype=torch.uint8, device=dev)
         else:
-            y_enc = torch.empty((r, M // t, bj), dtype=x.dtype, device=dev)
+            y_enc = torch.empty((r, M // t, bj),
+                                dtype=torch.bfloat16 if fmt == _lib.STL_BF16 else torch.float32,
+                                device=dev)
     y = torch.empty((M, N), dtype=x.dtype, device=dev)
     scratch = forward_scratch(M, K, N, t, r, x.dtype, dev)
-    _lib.check(_lib.load().stl_forward(
+    _lib.check(_lib.load().stl_forward_ex(
         x.data_ptr(), M, K, x.stride(0), w_planes.data_ptr(), N, snf.e_x.data_ptr(),
         snf.d.data_ptr(), t, r, _dt(x.dtype), y.data_ptr(), y.stride(0), u.data_ptr(),
         y_enc.data_ptr() if y_enc is not None else None, scratch.data_ptr(), scratch.numel(),
-        _stream(dev)))
+        prod, _stream(dev)))
     return (y, u, y_enc) if keep_cache else y
-
-
-def set_fusion(enabled: bool) -> None:
-    """Enable/disable the decode-fused kernels (A/B testing; default on)."""
-    _lib.load().stl_set_fusion(1 if enabled else 0)
 
 
 def stl_batched(x, w_encoded, snf) -> torch.Tensor:

@@ -1,5 +1,5 @@
 """Cache-less forward accuracy and time: bf16 slice products (default) vs F24 / fp32 products
-(stl_set_fusion bit 5) at BASELINE shapes; error vs a float64 restatement on the same bf16
+(forced with stl_forward_ex) at BASELINE shapes; error vs a float64 restatement on the same bf16
 inputs."""
 import json
 import os
@@ -28,19 +28,20 @@ for (M, K, N, R) in ((8192, 8192, 8192, 24), (8192, 4096, 4096, 24), (4096, 4096
     prod = torch.einsum("ikp,pjk->ijp", u, w.double())              # (bi, bj, r)
     yt = prod @ snf.d.double()                                     # (bi, bj, 16)
     yref = yt.reshape(rows // T, N // T, T, T).permute(0, 2, 1, 3).reshape(rows, N)
-    for bits in (32, 0, 16):
-        lib.stl_set_fusion(bits)
-        y = _forward(x, w, snf)
+    for name, prod in (("F24", "f24"), ("auto", None), ("fp32", torch.float32)):
+        try:
+            y = _forward(x, w, snf, products=prod)
+        except ValueError:
+            continue
         err = float((y[:rows].double() - yref).norm() / yref.norm())
         for _ in range(3):
-            _forward(x, w, snf)
+            _forward(x, w, snf, products=prod)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(20):
-            _forward(x, w, snf)
+            _forward(x, w, snf, products=prod)
         e1.record()
         torch.cuda.synchronize()
-        print(json.dumps({"shape": [M, K, N], "r": R, "products": {0: "bf16", 32: "F24", 16: "fp32"}[bits], "rel_err": err,
+        print(json.dumps({"shape": [M, K, N], "r": R, "products": name, "rel_err": err,
                           "ms": e0.elapsed_time(e1) / 20}))
-lib.stl_set_fusion(0)

@@ -1,6 +1,7 @@
 #!/bin/bash
 # L2-boundness probe of the slice GEMM: timings (+ mainloop-only) and ncu of ours vs cuBLAS.
 mkdir -p gpurun_out
+export STL_LIB=paper_2503_12211_b200/libstl_b200_probe.so  # STL_* switches: probe build
 tag=${1:-l2probe}
 {
 nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv

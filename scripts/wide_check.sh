@@ -1,6 +1,7 @@
 #!/bin/bash
 # wide-tile slice GEMM: parity tests + timing at the north-star shape (lag / split variants)
 mkdir -p gpurun_out
+export STL_LIB=paper_2503_12211_b200/libstl_b200_probe.so  # STL_* switches: probe build
 tag=${1:-wide}
 {
 timeout 900 python -m pytest tests/test_parity_gpu.py -q -x -p no:cacheprovider -k "slice_gemm or layer_backward or stl_batched or full_size" 2>&1 | tail -5

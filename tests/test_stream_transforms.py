@@ -47,14 +47,13 @@ def test_encode_decode_bf16(rows, cols, r):
 
 @pytest.mark.parametrize("M,K,N,r,fmt", [
     (1024, 512, 512, 24, "bf16"),    # default: bf16 slice products (cache and g_u)
-    (1024, 512, 512, 24, "f24"),     # stl_set_fusion bit 5: F24 slice products (N/4 % 128 == 0)
+    (1024, 512, 512, 24, "f24"),     # forced F24 slice products (N/4 % 128 == 0)
     (1024, 512, 768, 24, "bf16"),    # N/4 = 192: bf16 products need N/4 % 64 only
-    (1024, 512, 768, 24, "f24x"),    # bit 5 at N/4 = 192: F24 not eligible -> fp32 + bf16 cache
     (1024, 2304, 512, 20, "f24"),    # partial 512-tile units in K, r not a multiple of 8
     (1024, 2304, 512, 20, "bf16"),
     (768, 256, 1024, 13, "f24"),     # r = 13: one plane group, zero-padded to 16 in the box
     (768, 256, 1024, 13, "bf16"),
-    (1024, 512, 512, 32, "fp32"),    # stl_set_fusion bit 4: fp32 products, bf16 cache
+    (1024, 512, 512, 32, "fp32"),    # forced fp32 products, bf16 cache copy
 ])
 def test_layer_fwd_bwd_formats(M, K, N, r, fmt):
     t = 4
@@ -64,23 +63,52 @@ def test_layer_fwd_bwd_formats(M, K, N, r, fmt):
     w_dev, w64 = bf(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
     gy_dev, gy64 = bf(rng.standard_normal((M, N)))
     layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
-    try:
-        _lib.load().stl_set_fusion({"bf16": 0, "f24": 32, "f24x": 32, "fp32": 16}[fmt])
-        y, cache = stl._layer_forward_cached(layer, x_dev)
-        grads = stl._layer_backward(layer, cache, gy_dev)
-        torch.cuda.synchronize()
-    finally:
-        _lib.load().stl_set_fusion(0)
+    products = {"bf16": None, "f24": "f24", "fp32": torch.float32}[fmt]
+    y, cache = stl._layer_forward_cached(layer, x_dev, products=products)
+    grads = stl._layer_backward(layer, cache, gy_dev)
+    torch.cuda.synchronize()
     nbytes = cache.y_enc.numel() * cache.y_enc.element_size()
-    assert nbytes == {"f24": 3, "bf16": 2, "f24x": 2, "fp32": 2}[fmt] * r * (M // 4) * (N // 4)
+    assert nbytes == {"f24": 3, "bf16": 2, "fp32": 2}[fmt] * r * (M // 4) * (N // 4)
     y_ref, cache_ref = O.layer_forward_cached(x64, w64, e_x, d, t)
     assert rel(y, y_ref) <= 1e-2
     y_enc = stl.unpack_slice_products(cache.y_enc, r, M // 4, N // 4)
-    tol_enc = {"f24": 2e-3, "bf16": 5e-3, "f24x": 5e-3, "fp32": 5e-3}[fmt]  # u is bf16 in all
+    tol_enc = {"f24": 2e-3, "bf16": 5e-3, "fp32": 5e-3}[fmt]  # u is bf16 in all
     assert rel(y_enc, cache_ref[2].transpose(2, 0, 1)) <= tol_enc
     refs = O.layer_backward(w64, e_x, d, cache_ref, gy64, t)
     for name, g, ref in zip(("g_ex", "g_d", "g_w", "g_x"), grads, refs):
         assert rel(g, ref) <= 1e-2, (name, rel(g, ref))
+
+
+def test_cache_format_is_explicit():
+    """The cache's format is an argument, not process state: a format the shape cannot use is
+    a ValueError (forward), and a backward told a format the forward could not have written
+    fails instead of misreading the bytes (include/stl_b200.h stl_backward_ex)."""
+    t, r, M, K, N = 4, 24, 1024, 512, 768  # N/4 = 192: bf16 products yes, F24 no
+    rng = O.make_rng(9)
+    e_x, e_w, d = O.random_gaussian_init(t, r, rng, scale=0.5)
+    x_dev, _ = bf(rng.standard_normal((M, K)))
+    w_dev, _ = bf(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
+    layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
+    with pytest.raises(ValueError):
+        stl._layer_forward_cached(layer, x_dev, products="f24")
+    assert stl.cache_format(M, K, N, t, r, torch.bfloat16) == _lib.STL_BF16
+    assert stl.cache_format(M, K, N, t, r, torch.float32) == _lib.STL_F32
+    y, cache = stl._layer_forward_cached(layer, x_dev)
+    lib = _lib.load()
+    dev = x_dev.device
+    bi, bk, bj = M // t, K // t, N // t
+    g_enc = torch.empty((r, bi, bj), dtype=torch.bfloat16, device=dev)
+    g_u = torch.empty((r, bi, bk), dtype=torch.float32, device=dev)
+    g_x = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
+    snf = layer.snf.on(dev)
+    for bad in (_lib.STL_F24, _lib.STL_F32, 7):
+        st = lib.stl_backward_ex(
+            x_dev.data_ptr(), K, x_dev.data_ptr(), K, layer.w_planes.data_ptr(),
+            snf.e_x.data_ptr(), snf.d.data_ptr(), cache.u.data_ptr(), cache.y_enc.data_ptr(), bad,
+            M, K, N, t, r, _lib.STL_BF16, None, None, None, g_x.data_ptr(), K, g_enc.data_ptr(),
+            g_u.data_ptr(), None, _lib.STL_PROD_AUTO, torch.cuda.current_stream().cuda_stream)
+        assert st == 2, bad  # STL_ERR_VALUE
+    torch.cuda.synchronize()
 
 
 def test_stage_protocol_under_data_only_probe():
@@ -93,7 +121,37 @@ def test_stage_protocol_under_data_only_probe():
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, STL_STREAM_NOCOMPUTE="1", STRESS_STEPS="300")
+    # the probe switch lives in the probe build of the library only
+    env = dict(os.environ, STL_LIB=str(_lib.PROBE_LIB_PATH), STL_STREAM_NOCOMPUTE="1",
+               STRESS_STEPS="300")
     out = subprocess.run([sys.executable, os.path.join(root, "scripts", "stress_step.py")],
                          env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "stress ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_stage_protocol_bitwise_repeat_with_compute():
+    """The same race with the math on: config-2 steps whose reductions run two consumer groups
+    over odd stage counts (decode_gu+g_ex: 3 stages, encode_gy+g_d: 7) must reproduce every
+    gradient bit for bit across repeated steps (a stale-stage read would change values without
+    faulting)."""
+    from paper_2503_12211_b200.layer import LayerCache, backward_raw
+    from paper_2503_12211_b200.snf_operator import _forward
+
+    T, R, M, K, N = 4, 24, 8192, 4096, 4096
+    dev = torch.device("cuda")
+    snf = stl.random_gaussian_init(T, R, stl.make_rng(0), scale=0.5).to(dev)
+    g = torch.Generator(device=dev).manual_seed(4)
+    w = (torch.randn((R, N // T, K // T), device=dev, generator=g) * 0.03).to(torch.bfloat16)
+    x = torch.randn((M, K), device=dev, generator=g).to(torch.bfloat16)
+    gy = torch.randn((M, N), device=dev, generator=g).to(torch.bfloat16)
+    first = None
+    for _ in range(40):
+        y, u, ye = _forward(x, w, snf, keep_cache=True)
+        grads = backward_raw(snf, w, LayerCache(x, u, ye), gy)
+        out = [y] + [gr for gr in grads]
+        if first is None:
+            first = [o.clone() for o in out]
+        else:
+            for a, b in zip(out, first):
+                assert torch.equal(a, b)
+    torch.cuda.synchronize()
