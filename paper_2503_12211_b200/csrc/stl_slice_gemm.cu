@@ -621,290 +621,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, kTmemCols);
 }
 
-// ==================================================================== wide CTA-pair variant
-// The slice GEMM at the bench shapes is bound by L2 -> SM operand traffic, not by the tensor
-// pipe (ncu, 24 x 2048^3: 6.9 KB of LTS traffic per L2 cycle, the practical cap, with the tensor
-// pipe 78% active; profiles/r02_l2probe.md). A 256 x 512 pair tile — two 256 x 256 halves
-// sharing one A box — moves 48 KB per CTA per 64-deep k-block for 8.4 MFLOP (175 FLOP/B)
-// instead of 32 KB for 4.2 MFLOP (128 FLOP/B): 27% less operand traffic per FLOP.
-// The two halves fill all 512 TMEM columns (D0 = columns 0-255, D1 = 256-511), so the
-// accumulator cannot be double-buffered. Instead the MMA issuer runs half 1 `lag` k-blocks
-// behind half 0: half 0 finishes `lag` k-blocks before half 1, the epilogue drains D0 while
-// the MMAs of half 1's last k-blocks run, and drains D1 while the next tile's half-0 MMAs of its
-// first `lag` k-blocks run — both drains overlap tensor work. A k-block's stage is released once
-// half 1 has consumed it, so `lag` + 1 stages are held by the MMA and the rest prefetch.
-// The wave-quantised tail is split: when the last partial wave holds at most half as many wide
-// tiles as there are pairs, those tiles run as two 256-wide half tiles each (D0 only).
-constexpr int kWStages = 4;
-
-template <int OUT0, int OUT1>
-struct SmemW {
-  static constexpr int kStages = kWStages;
-  static constexpr uint32_t kABytes = 128 * kBK * 2;     // this CTA's 128 A rows
-  static constexpr uint32_t kHBytes = 128 * kBK * 2;     // one half's 128 B columns
-  static constexpr uint32_t kBBytes = 2 * kHBytes;
-  static constexpr uint32_t kRing = kStages * (kABytes + kBBytes);
-  static constexpr uint32_t kBufBytes = OutStage<OUT0>::kBytes > OutStage<OUT1>::kBytes
-                                            ? OutStage<OUT0>::kBytes
-                                            : OutStage<OUT1>::kBytes;
-  static constexpr uint32_t kBarOffset = kRing + 2 * kBufBytes;
-  static constexpr uint32_t kTotal = kBarOffset + 512 + 1024;
-};
-
-struct WideArgs {
-  int M[2], N[2], K[2];
-  int r;
-  int total0;   // wide tiles of problem 0
-  int nwide;    // wide tiles of both problems
-  int nsplit;   // trailing wide tiles run as two half tiles each
-  int total;    // tiles scheduled: nwide - nsplit + 2 nsplit
-  int lag;      // k-blocks half 1 runs behind half 0 (0 .. kWStages - 2)
-  int nostore;
-};
-
-struct WTile {
-  int prob, p, mb, n0, nh, num_kb;
-  int hoff1;  // column offset of the second half (256), or of the single half of a split tile
-};
-
-__device__ __forceinline__ WTile wide_tile(const WideArgs& g, int tile) {
-  WTile w;
-  int wt = tile, half = -1;
-  const int first_split = g.nwide - g.nsplit;
-  if (tile >= first_split) {
-    wt = first_split + ((tile - first_split) >> 1);
-    half = (tile - first_split) & 1;
-  }
-  w.prob = wt >= g.total0 ? 1 : 0;
-  const int local = w.prob ? wt - g.total0 : wt;
-  const int N = g.N[w.prob];
-  const int n_sup = (N + 511) / 512;
-  const int per_slice = ((g.M[w.prob] + 255) / 256) * n_sup;
-  w.p = local / per_slice;
-  const int rem = local - w.p * per_slice;
-  w.mb = rem / n_sup;
-  const int nbw = rem - w.mb * n_sup;
-  w.n0 = nbw * 512 + (half > 0 ? 256 : 0);
-  w.nh = (half >= 0 || w.n0 + 256 >= N) ? 1 : 2;
-  w.hoff1 = 256;
-  w.num_kb = (g.K[w.prob] + kBK - 1) / kBK;
-  return w;
-}
-
-// TMA producer of one wide tile: per k-block this CTA's 128 A rows and, per half, its 128 B
-// columns (both CTAs issue; transaction bytes land on the even CTA's barrier).
-template <class Kd, class S>
-__device__ __forceinline__ void wide_produce(const CUtensorMap* tmA, const CUtensorMap* tmB,
-                                             uint8_t* sA, uint8_t* sB, uint64_t* full,
-                                             uint64_t* empty, uint32_t& kbg, const WTile& w,
-                                             uint32_t prank) {
-  const bool leader = prank == 0;
-  const int m0 = w.mb * 256 + static_cast<int>(prank) * 128;
-  for (int kb = 0; kb < w.num_kb; ++kb, ++kbg) {
-    const uint32_t stage = kbg % S::kStages, phase = (kbg / S::kStages) & 1;
-    ptx::mbar_wait(&empty[stage], phase ^ 1);
-    if (leader)
-      ptx::mbar_arrive_expect_tx(&full[stage], 2 * (S::kABytes + w.nh * S::kHBytes));
-    uint8_t* a = sA + stage * S::kABytes;
-    if constexpr (!Kd::A_MN) {
-      ptx::tma_load_3d_2sm(tmA, &full[stage], a, kb * kBK, m0, w.p);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-        ptx::tma_load_3d_2sm(tmA, &full[stage], a + j * (64 * kBK * 2), m0 + j * 64, kb * kBK,
-                             w.p);
-    }
-    for (int h = 0; h < w.nh; ++h) {
-      uint8_t* b = sB + stage * S::kBBytes + h * S::kHBytes;
-      const int n = w.n0 + h * w.hoff1 + static_cast<int>(prank) * 128;
-      if constexpr (!Kd::B_MN) {
-        ptx::tma_load_3d_2sm(tmB, &full[stage], b, kb * kBK, n, w.p);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-          ptx::tma_load_3d_2sm(tmB, &full[stage], b + j * (64 * kBK * 2), n + j * 64, kb * kBK,
-                               w.p);
-      }
-    }
-    if (!leader) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0u));
-  }
-}
-
-// The 4 pair MMAs (K = 16 each) of one k-block into one 256-column half.
-template <class Kd, class S>
-__device__ __forceinline__ void wide_mma_kblock(uint32_t a_addr, uint32_t b_addr, uint32_t d_tmem,
-                                                bool first) {
-  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(256, 256, Kd::A_MN, Kd::B_MN);
-#pragma unroll
-  for (int k = 0; k < kBK / 16; ++k) {
-    const uint64_t ad = Kd::A_MN ? ptx::smem_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
-                                 : ptx::smem_desc_sw128(a_addr + k * 32, 16, 1024);
-    const uint64_t bd = Kd::B_MN ? ptx::smem_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
-                                 : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
-    ptx::mma_bf16_ss_2sm(d_tmem, ad, bd, kIdesc, (first && k == 0) ? 0u : 1u);
-  }
-}
-
-// MMA issue of one wide tile (even CTA, one thread), half 1 `lag` k-blocks behind half 0.
-template <class Kd, class S>
-__device__ __forceinline__ void wide_mma(uint8_t* sA, uint8_t* sB, uint64_t* full, uint64_t* empty,
-                                         uint64_t* tfull, uint64_t* tempty, uint32_t& kbg,
-                                         uint32_t& n0, uint32_t& n1, uint32_t tmem_base,
-                                         const WTile& w, int lag) {
-  const int L = w.nh == 2 ? lag : 0;
-  const uint32_t kb0 = kbg;  // global k-block index of this tile's k-block 0
-  for (int j = 0; j < w.num_kb + L; ++j) {
-    if (j < w.num_kb) {
-      const uint32_t g = kb0 + j, stage = g % S::kStages;
-      ptx::mbar_wait(&full[stage], (g / S::kStages) & 1);
-      if (j == 0) ptx::mbar_wait(&tempty[0], (n0 & 1) ^ 1);
-      ptx::tc_fence_after();
-      wide_mma_kblock<Kd, S>(ptx::smem_u32(sA + stage * S::kABytes),
-                             ptx::smem_u32(sB + stage * S::kBBytes), tmem_base, j == 0);
-      if (w.nh == 1) ptx::mma_commit_2sm(&empty[stage], 0x3);
-      if (j == w.num_kb - 1) ptx::mma_commit_2sm(&tfull[0], 0x3);
-    }
-    const int kb = j - L;
-    if (w.nh == 2 && kb >= 0) {
-      const uint32_t g = kb0 + kb, stage = g % S::kStages;
-      if (L == 0) {
-        // (full already waited above for this k-block)
-      }
-      if (kb == 0) {
-        ptx::mbar_wait(&tempty[1], (n1 & 1) ^ 1);
-        ptx::tc_fence_after();
-      }
-      wide_mma_kblock<Kd, S>(ptx::smem_u32(sA + stage * S::kABytes),
-                             ptx::smem_u32(sB + stage * S::kBBytes + S::kHBytes),
-                             tmem_base + 256, kb == 0);
-      ptx::mma_commit_2sm(&empty[stage], 0x3);
-    }
-  }
-  if (w.nh == 2) {
-    ptx::mma_commit_2sm(&tfull[1], 0x3);
-    ++n1;
-  }
-  ++n0;
-  kbg = kb0 + w.num_kb;
-}
-
-template <class K0, class K1>
-__global__ void __launch_bounds__(kThreads, 1)
-    slice_gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA0,
-                           const __grid_constant__ CUtensorMap tmB0,
-                           const __grid_constant__ CUtensorMap tmC0,
-                           const __grid_constant__ CUtensorMap tmC20,
-                           const __grid_constant__ CUtensorMap tmA1,
-                           const __grid_constant__ CUtensorMap tmB1,
-                           const __grid_constant__ CUtensorMap tmC1,
-                           const __grid_constant__ CUtensorMap tmC21, WideArgs args) {
-  using S = SmemW<K0::OUT, K1::OUT>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + S::kStages * S::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
-  uint64_t* empty = full + S::kStages;
-  uint64_t* tfull = empty + S::kStages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank();
-  const uint32_t prank = rank & 1u;
-  const bool leader = prank == 0;
-  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
-  const int total = args.total;
-
-  if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmA0);
-    ptx::prefetch_tmap(&tmB0);
-    if (args.nwide > args.total0) {
-      ptx::prefetch_tmap(&tmA1);
-      ptx::prefetch_tmap(&tmB1);
-    }
-  }
-  if (warp == 1 && lane == 0) {
-    for (int s = 0; s < S::kStages; ++s) {
-      ptx::mbar_init(&full[s], 2);
-      ptx::mbar_init(&empty[s], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 8);
-    }
-    ptx::fence_mbar_init();
-  }
-  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, 512);
-  griddep_launch_dependents();
-  ptx::tc_fence_before();
-  ptx::cluster_sync();
-  ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  griddep_wait();
-
-  if (warp == 0) {
-    if (lane == 0) {
-      uint32_t kbg = 0;
-      for (int tile = cluster; tile < total; tile += nclusters) {
-        const WTile w = wide_tile(args, tile);
-        if (w.prob == 0)
-          wide_produce<K0, S>(&tmA0, &tmB0, sA, sB, full, empty, kbg, w, prank);
-        else
-          wide_produce<K1, S>(&tmA1, &tmB1, sA, sB, full, empty, kbg, w, prank);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      uint32_t kbg = 0, n0 = 0, n1 = 0;
-      for (int tile = cluster; tile < total; tile += nclusters) {
-        const WTile w = wide_tile(args, tile);
-        if (w.prob == 0)
-          wide_mma<K0, S>(sA, sB, full, empty, tfull, tempty, kbg, n0, n1, tmem_base, w, args.lag);
-        else
-          wide_mma<K1, S>(sA, sB, full, empty, tfull, tempty, kbg, n0, n1, tmem_base, w, args.lag);
-      }
-    }
-  } else if (warp >= 4) {
-    const int q = warp & 3;
-    const bool issuer = warp == 4 && lane == 0;
-    int chunk_no = 0;
-    uint32_t n0 = 0, n1 = 0;
-    uint8_t* stage_base = smem + S::kRing;
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    for (int tile = cluster; tile < total; tile += nclusters) {
-      const WTile w = wide_tile(args, tile);
-      const int row_base = w.mb * 256 + static_cast<int>(prank) * 128;
-      for (int h = 0; h < w.nh; ++h) {
-        const uint32_t n = h ? n1++ : n0++;
-        ptx::mbar_wait(&tfull[h], n & 1);
-        ptx::tc_fence_after();
-        const int col = w.n0 + h * w.hoff1;
-        if (w.prob == 0)
-          tc2_epilogue<256, K0, S>(&tmC0, &tmC20, stage_base, lane_base + h * 256, chunk_no, w.p,
-                                   col, row_base, args.M[0], args.N[0], args.nostore, q, lane,
-                                   issuer);
-        else
-          tc2_epilogue<256, K1, S>(&tmC1, &tmC21, stage_base, lane_base + h * 256, chunk_no, w.p,
-                                   col, row_base, args.M[1], args.N[1], args.nostore, q, lane,
-                                   issuer);
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0)
-          ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[h]), rank & ~1u));
-      }
-    }
-    if (issuer) ptx::bulk_wait_all();
-  }
-
-  ptx::tc_fence_before();
-  ptx::cluster_sync();
-  ptx::tc_fence_after();
-  if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, 512);
-}
-
 // ------------------------------------------------------------------ host side
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1060,74 +776,14 @@ cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s
   ga.total0 = static_cast<int>(t0);
   ga.total = static_cast<int>(tiles);
   ga.nostore = probe_env("STL_GEMM_NOSTORE", 0);
+  if (probe_env("STL_GEMM_VERBOSE", 0))
+    fprintf(stderr, "[tc2] max_clusters=%d clusters=%d tiles=%d BN=%d smem=%d\n", max_clusters,
+            clusters, ga.total, BN, smem);
   return cudaLaunchKernelEx(&L.cfg, kern, m0.a, m0.b, m0.c, m0.c2, m1.a, m1.b, m1.c, m1.c2, ga);
-}
-
-// Wide-tile launch (256 x 512 pair tiles) of np (1 or 2) problems; see slice_gemm_wide_kernel.
-int64_t wide_tiles(const SliceGemmProblem& pb) {
-  return static_cast<int64_t>(pb.r) * ((pb.M + 255) / 256) * ((pb.N + 511) / 512);
-}
-
-template <class K0, class K1>
-cudaError_t launch_wide_group(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
-  Tc2Maps m0, m1;
-  bool ok = make_tc2_maps<256, K0>(pbs[0], &m0);
-  if (np > 1) ok = ok && make_tc2_maps<256, K1>(pbs[1], &m1);
-  else m1 = m0;
-  if (!ok) return cudaErrorInvalidValue;
-  auto kern = slice_gemm_wide_kernel<K0, K1>;
-  const int smem = SmemW<K0::OUT, K1::OUT>::kTotal;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  const int64_t t0 = wide_tiles(pbs[0]);
-  const int64_t nwide = t0 + (np > 1 ? wide_tiles(pbs[1]) : 0);
-  if (nwide <= 0) return cudaSuccess;
-  if (nwide >= (int64_t(1) << 30)) return cudaErrorInvalidValue;
-  PairLaunch L(smem, s);
-  static const int max_clusters = L.max_clusters(kern);
-  WideArgs wa{};
-  for (int i = 0; i < 2; ++i) {
-    const SliceGemmProblem& pb = pbs[i < np ? i : 0];
-    wa.M[i] = static_cast<int>(pb.M);
-    wa.N[i] = static_cast<int>(pb.N);
-    wa.K[i] = static_cast<int>(pb.K);
-  }
-  wa.r = pbs[0].r;
-  wa.total0 = static_cast<int>(t0);
-  wa.nwide = static_cast<int>(nwide);
-  const int clusters = static_cast<int>(nwide < max_clusters ? nwide : max_clusters);
-  const int rem = static_cast<int>(nwide % clusters);
-  // split the last partial wave into half tiles when they fit one wave
-  wa.nsplit = (!probe_env("STL_GEMM_NOSPLIT", 0) && rem > 0 && 2 * rem <= clusters) ? rem : 0;
-  wa.total = wa.nwide + wa.nsplit;
-  const int lag = probe_env("STL_GEMM_LAG", 1);  // measured: 0 ~ 1 > 2 (r02_wide_tiles.log)
-  wa.lag = lag < 0 ? 0 : (lag > kWStages - 2 ? kWStages - 2 : lag);
-  wa.nostore = probe_env("STL_GEMM_NOSTORE", 0);
-  L.cfg.gridDim = dim3(2 * clusters);
-  return cudaLaunchKernelEx(&L.cfg, kern, m0.a, m0.b, m0.c, m0.c2, m1.a, m1.b, m1.c, m1.c2, wa);
-}
-
-// Wide tiles for problems whose output is at least one wide tile across (N >= 512) and whose
-// output mode the wide kernel stages (fp32, bf16, F24; not the fp32 + bf16 copy).
-bool wide_eligible(const SliceGemmProblem& pb) {
-  return !probe_env("STL_GEMM_NOWIDE", 0) && pb.N >= 512 && pb.M > 128 && !pb.c2 &&
-         pb.c_dtype != kF32;
 }
 
 template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch_tc2_any(const SliceGemmProblem& pb, cudaStream_t s) {
-  if (BN == 256 && wide_eligible(pb)) {
-    if (pb.c_dtype == kBF16) {
-      using Kd = GemmKind<A_MN, B_MN, kOutBf16>;
-      return launch_wide_group<Kd, Kd>(&pb, 1, s);
-    }
-    if (pb.c_dtype == kF24) {
-      using Kd = GemmKind<A_MN, B_MN, kOutF24>;
-      return launch_wide_group<Kd, Kd>(&pb, 1, s);
-    }
-    using Kd = GemmKind<A_MN, B_MN, kOutF32>;
-    return launch_wide_group<Kd, Kd>(&pb, 1, s);
-  }
   if (pb.c_dtype == kBF16) {
     using Kd = GemmKind<A_MN, B_MN, kOutBf16>;
     return launch_tc2_group<BN, Kd, Kd>(&pb, 1, s);
@@ -1223,11 +879,6 @@ cudaError_t slice_gemm_tc_group(const SliceGemmProblem& p0, const SliceGemmProbl
   if (!slice_gemm_tc_group_supported(p0, p1)) return cudaErrorNotSupported;
   const SliceGemmProblem pbs[2] = {p0, p1};
   using K0 = GemmKind<true, true, kOutF32>;
-  if (wide_eligible(p0) && wide_eligible(p1)) {
-    if (p1.c_dtype == kF24) return launch_wide_group<K0, GemmKind<false, true, kOutF24>>(pbs, 2, s);
-    if (p1.c_dtype == kBF16) return launch_wide_group<K0, GemmKind<false, true, kOutBf16>>(pbs, 2, s);
-    return launch_wide_group<K0, GemmKind<false, true, kOutF32>>(pbs, 2, s);
-  }
   if (p1.c_dtype == kF24) return launch_tc2_group<256, K0, GemmKind<false, true, kOutF24>>(pbs, 2, s);
   if (p1.c_dtype == kBF16) return launch_tc2_group<256, K0, GemmKind<false, true, kOutBf16>>(pbs, 2, s);
   return launch_tc2_group<256, K0, GemmKind<false, true, kOutF32>>(pbs, 2, s);

@@ -156,35 +156,6 @@ def test_slice_gemm_tc_layouts(al, bl, shape):
     assert errb <= 5e-3, float(errb)
 
 
-@pytest.mark.parametrize("al", [0, 1])
-@pytest.mark.parametrize("bl", [0, 1])
-@pytest.mark.parametrize("shape", [(10, 1024, 1024, 128), (10, 1000, 1000, 200), (3, 256, 512, 64),
-                                   (2, 264, 1544, 72)])
-def test_slice_gemm_wide_tiles(al, bl, shape):
-    """256 x 512 pair tiles (N >= 512): half 1 lagging half 0, the split tail wave (80 wide
-    tiles on 74 pairs -> 6 of them as half tiles), clipped second halves, K shorter than the lag;
-    fp32, bf16 and F24 outputs against f64."""
-    r, M, N, K = shape
-    g = torch.Generator(device="cpu").manual_seed(M + 3 * N + K + 2 * al + bl)
-    A = torch.randn((r, M, K), generator=g).to(torch.bfloat16)
-    B = torch.randn((r, K, N), generator=g).to(torch.bfloat16)
-    ref = torch.bmm(A.double(), B.double())
-    a_dev = (A if al == 0 else A.transpose(1, 2)).contiguous().to(DEV)
-    b_dev = (B.transpose(1, 2) if bl == 0 else B).contiguous().to(DEV)
-    c = _gemm(a_dev, al, b_dev, bl, M, N, K, r)
-    assert (c.cpu().double() - ref).norm() / ref.norm() <= 1e-5
-    cb = _gemm(a_dev, al, b_dev, bl, M, N, K, r, out_dtype=torch.bfloat16)
-    assert (cb.cpu().double() - ref).norm() / ref.norm() <= 5e-3
-    if N % 16 == 0:
-        c24 = torch.empty((3 * r * M * N,), dtype=torch.uint8, device=DEV)
-        _lib.check(_lib.load().stl_slice_gemm(a_dev.data_ptr(), al, b_dev.data_ptr(), bl,
-                                              c24.data_ptr(), _lib.STL_F24, _lib.STL_BF16, r, M,
-                                              N, K, torch.cuda.current_stream().cuda_stream))
-        u = c.view(torch.int32)
-        rne = ((u + 0x7F + ((u >> 8) & 1)) & ~0xFF).view(torch.float32)
-        assert torch.equal(stl.unpack_slice_products(c24, r, M, N), rne)
-
-
 @pytest.mark.parametrize("al,bl", [(0, 0), (1, 1), (0, 1)])
 @pytest.mark.parametrize("shape", [(3, 256, 128, 64), (2, 520, 272, 136), (24, 512, 256, 512)])
 def test_slice_gemm_f24_output(al, bl, shape):
@@ -254,15 +225,15 @@ def test_stl_batched_bf16(M, K, N, t, r, strassen):
 
 
 @pytest.mark.parametrize("M,K,N,r,init", [
-    (2048, 256, 2048, 24, "gaussian"),   # 2 row blocks: one per band
+    (2048, 256, 2048, 24, "gaussian"),
     (4096, 512, 2048, 16, "gaussian"),
-    (3328, 256, 2560, 32, "gaussian"),   # ragged last row block, clipped second half tile
+    (3328, 256, 2560, 32, "gaussian"),   # ragged last 256-row block
     (2048, 512, 2048, 24, "subset"),     # the paper's training init: Strassen-49 row subset
 ])
-def test_banded_forward_bf16(M, K, N, r, init):
-    """The band-overlapped forward (encode of band 1 / decode of band 0 in warps 2-3 of the
-    slice-GEMM launches, FFMA) against the f64 oracle over the whole output, cache-less and
-    with the training cache (whose slice products the backward then reads)."""
+def test_forward_backward_bf16_whole_output(M, K, N, r, init):
+    """Default bf16 path (bf16 slice products) against the f64 oracle over the whole output
+    and in two row slabs, cache-less and with the training cache whose slice products the
+    backward then reads; the Strassen-subset r = 24 encoders are the paper's training init."""
     t = 4
     rng = O.make_rng(M + K + r)
     if init == "subset":
