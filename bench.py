@@ -187,6 +187,52 @@ def run_reference(args, rank: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def rank_sweep(stl, lib, _lib, dev, stream, peaks, timed, n=8192, iters=5):
+    """BASELINE configs[2]: forward at n^3, t in {2, 4}, r in {16, 24, 32, 49 (Strassen x
+    Strassen)}; per point the forward time, its slice-GEMM rate against the burst bf16 peak and
+    the transforms' HBM rate against the copy bandwidth (library profiler attribution)."""
+    import torch
+
+    x = torch.randn((n, n), device=dev).to(torch.bfloat16)
+    out = []
+    for t in (2, 4):
+        for r in (16, 24, 32, 49):
+            if r == 49 and t != 4:
+                continue
+            snf = (stl.strassen_rank49() if r == 49 else
+                   stl.random_gaussian_init(t, r, stl.make_rng(0), scale=0.5)).to(dev)
+            w = (torch.randn((r, n // t, n // t), device=dev) * 0.02).to(torch.bfloat16)
+            u = torch.empty((r, n // t, n // t), dtype=torch.bfloat16, device=dev)
+            sb = int(lib.stl_forward_scratch_bytes(n, n, n, t, r, _lib.STL_BF16))
+            scratch = torch.empty((sb,), dtype=torch.uint8, device=dev)
+            y = torch.empty((n, n), dtype=torch.bfloat16, device=dev)
+
+            def fwd():
+                _lib.check(lib.stl_forward(x.data_ptr(), n, n, n, w.data_ptr(), n,
+                                           snf.e_x.data_ptr(), snf.d.data_ptr(), t, r,
+                                           _lib.STL_BF16, y.data_ptr(), n, u.data_ptr(), None,
+                                           scratch.data_ptr(), sb, stream))
+
+            fwd()
+            ms = timed(fwd, iters) / iters
+            timed(fwd, iters, profile=True)
+            recs = _lib.profile_records()
+            g_ms = sum(m for nm, m, _ in recs if nm.startswith("slice_gemm")) / iters
+            x_ms = sum(m for nm, m, _ in recs if nm in ("encode_x", "decode_y")) / iters
+            p_bytes = 2 if (t == 4 and r <= 32) else (3 if t == 4 else 4)  # bf16 / F24 / fp32
+            cost = stl.LayerCost(n, n, n, t, r, 2, p_bytes)
+            g_tf = cost.gemm_flops() / (g_ms * 1e-3) / 1e12
+            xf_gbs = (cost.encode_bytes() + cost.decode_bytes()) / (x_ms * 1e-3) / 1e9
+            out.append({"t": t, "r": r, "init": "strassen49" if r == 49 else "gaussian",
+                        "fwd_ms": ms, "slice_gemm_tflops": g_tf,
+                        "gemm_frac_of_burst": g_tf / peaks["bf16_burst"],
+                        "transforms_GBs": xf_gbs, "transforms_hbm_frac": xf_gbs / peaks["hbm_gbs"],
+                        "dense_over_stl_flops": 2 * n ** 3 / cost.forward_flops()})
+            del w, u, scratch, y
+            torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main() -> None:
     ap = argparse.ArgumentParser()
@@ -195,10 +241,11 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("stl", "reference"), default="stl")
     ap.add_argument("--ref-rows", type=int, default=128)
-    ap.add_argument("--cpu-rows", type=int, default=512)
+    ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip cuBLAS / 8192^3 / e2e legs")
     ap.add_argument("--no-t2t", action="store_true", help="skip the T2T-ViT-7 training leg")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[2] rank sweep")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -258,19 +305,33 @@ def main() -> None:
                       device=dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
 
+    cache_fmt = int(lib.stl_cache_format(M, K, N, T, R, _lib.STL_BF16, _lib.STL_PROD_AUTO))
+    side = torch.cuda.Stream(dev)          # DP: g_w all-reduce beside the g_x / g_ex decode
+    gw_ready = torch.cuda.Event()
+    gw_ready.record()
+    gw_done = torch.cuda.Event()
+
     def stl_step(allreduce: bool):
         _lib.check(lib.stl_forward(x.data_ptr(), M, K, K, w_planes.data_ptr(), N,
                                    snf.e_x.data_ptr(), snf.d.data_ptr(), T, R, _lib.STL_BF16,
                                    y.data_ptr(), N, u.data_ptr(), y_enc.data_ptr(),
                                    fwd_scratch.data_ptr(), fwd_scratch.numel(), stream))
-        _lib.check(lib.stl_backward(gy.data_ptr(), N, x.data_ptr(), K, w_planes.data_ptr(),
-                                    snf.e_x.data_ptr(), snf.d.data_ptr(), u.data_ptr(),
-                                    y_enc.data_ptr(), M, K, N, T, R, _lib.STL_BF16,
-                                    g_ex.data_ptr(), g_d.data_ptr(), g_w.data_ptr(),
-                                    g_x.data_ptr(), K, g_enc.data_ptr(), g_u.data_ptr(),
-                                    red.data_ptr(), stream))
+        _lib.check(lib.stl_backward_ex(
+            gy.data_ptr(), N, x.data_ptr(), K, w_planes.data_ptr(), snf.e_x.data_ptr(),
+            snf.d.data_ptr(), u.data_ptr(), y_enc.data_ptr(), cache_fmt, M, K, N, T, R,
+            _lib.STL_BF16, g_ex.data_ptr(), g_d.data_ptr(), g_w.data_ptr(), g_x.data_ptr(), K,
+            g_enc.data_ptr(), g_u.data_ptr(), red.data_ptr(), _lib.STL_PROD_AUTO,
+            gw_ready.cuda_event if allreduce else None, stream))
         if allreduce:
-            dist.all_reduce(grads)
+            # g_w (the bulk of the exchange) is final before the decode kernel: its NCCL
+            # all-reduce runs on a side stream while decode_gu+g_ex computes; the small
+            # encoder / decoder gradients follow on the main stream
+            side.wait_event(gw_ready)
+            with torch.cuda.stream(side):
+                dist.all_reduce(g_w)
+                gw_done.record(side)
+            dist.all_reduce(grads[R * bj * bk:])
+            torch.cuda.current_stream(dev).wait_event(gw_done)
 
     def timed(fn, steps, profile=False):
         if world > 1:
@@ -331,14 +392,21 @@ def main() -> None:
     tp = ROOT / "profiles" / "gemm_traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get("bytes_per_launch")
+    # Denominator: the measured BURST bf16 peak when the timed region saw no power cap (short
+    # regions run at full clock), the sustained peak when sw_power_cap was active.
+    capped = "sw_power_cap" in (clocks.get("reasons") or [])
+    peak = peaks["bf16_sustained"] if capped else peaks["bf16_burst"]
     roofline = {"kernel": "slice_gemm_tc2_kernel (CTA-pair tcgen05 slice GEMM; the step's 3 "
                           "slice-GEMMs over its launches, FLOP-weighted)", "bound": "tensor",
-                "achieved": gemm_tflops, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
-                "frac": gemm_tflops / peaks["bf16_sustained"], "traffic": traffic,
+                "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
+                "frac": gemm_tflops / peak, "traffic": traffic,
                 "traffic_of": "one forward slice-GEMM launch (ncu dram bytes)",
                 "flops_per_step": gemm_flops_step, "ms_per_step": gemm_ms_step,
                 "launches_per_step": gem["calls"] / args.steps,
-                "peak_source": peaks["source"] + ", sustained bf16"}
+                "frac_of_sustained": gemm_tflops / peaks["bf16_sustained"],
+                "peak_source": peaks["source"] + (", sustained bf16 (sw_power_cap seen)" if capped
+                                                  else ", burst bf16 (no power cap in the timed "
+                                                       "region's clock samples)")}
     breakdown = {}
     step_kernel_ms = sum(v["ms"] for v in kern.values()) / args.steps
     hbm_bytes = {"encode_x": cost.encode_bytes(), "decode_y": cost.decode_bytes(),
@@ -419,19 +487,44 @@ def main() -> None:
         timed(fwd8192, steps_f, profile=True)  # attribution pass (events between launches)
         recs_f = _lib.profile_records()
         gemm_f = [ms for name, ms, _ in recs_f
-                  if name in ("slice_gemm_tcgen05", "slice_gemm_decode_fused")]
+                  if name == "slice_gemm_tcgen05"]
         cub_f = timed(lambda: torch.matmul(xf, wdf, out=ydf), steps_f) / steps_f
-        cost_f = stl.LayerCost(m_loc, n3, n3, T, R, 2)
+        cost_f = stl.LayerCost(m_loc, n3, n3, T, R, 2, 2)
         gf_ms = sum(gemm_f) / max(len(gemm_f), 1)
+        xf_ms = {n: sum(ms for nm, ms, _ in recs_f if nm == n) / steps_f
+                 for n in ("encode_x", "decode_y")}
+        gemm_tf = cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12
         line["north_star_fwd_8192"] = {
             "stl_ms": stl_f, "cublas_ms": cub_f, "speedup": cub_f / stl_f, "target": 1.8,
             "dense_equiv_tflops": 2 * n3 ** 3 / (stl_f * 1e-3) / 1e12,
             "m_sharded_over": world, "rows_per_rank": m_loc,
-            "gemm_ms": gf_ms, "gemm_tflops": cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12,
-            "gemm_frac_of_burst": cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12 / peaks["bf16_burst"],
+            "gemm_ms": gf_ms, "gemm_tflops": gemm_tf,
+            "gemm_frac_of_burst": gemm_tf / peaks["bf16_burst"],
+            "roofline": {
+                "gemm": {"bound": "tensor", "achieved": gemm_tf, "peak": peaks["bf16_burst"],
+                         "unit": "TFLOP/s", "frac": gemm_tf / peaks["bf16_burst"],
+                         "flops_per_launch": cost_f.gemm_flops()},
+                "encode_x": {"bound": "hbm", "bytes": cost_f.encode_bytes(),
+                             "achieved": cost_f.encode_bytes() / (xf_ms["encode_x"] * 1e-3) / 1e9,
+                             "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                             "frac": cost_f.encode_bytes() / (xf_ms["encode_x"] * 1e-3) / 1e9
+                             / peaks["hbm_gbs"], "ms": xf_ms["encode_x"]},
+                "decode_y": {"bound": "hbm", "bytes": cost_f.decode_bytes(),
+                             "achieved": cost_f.decode_bytes() / (xf_ms["decode_y"] * 1e-3) / 1e9,
+                             "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                             "frac": cost_f.decode_bytes() / (xf_ms["decode_y"] * 1e-3) / 1e9
+                             / peaks["hbm_gbs"], "ms": xf_ms["decode_y"]},
+                "how": "CUDA events around each launch (library profiler), attribution pass "
+                       "after the timed region; peaks from MEASURED_PEAKS.json (burst bf16, "
+                       "copy bandwidth)"},
         }
         del wf, xf, uf, sf, yf, wdf, ydf
         torch.cuda.empty_cache()
+
+        # ---- configs[2]: rank / tile sweep of the forward at 8192^3 (rank 0; t = 2 slice
+        # GEMMs are FLOP-losing by construction: the points report the fraction of roofline).
+        if world == 1 and not args.no_sweep:
+            line["rank_sweep"] = rank_sweep(stl, lib, _lib, dev, stream, peaks, timed)
 
         # ---- e2e: public API (StlLinear autograd) with pinned host inputs, copies timed: a
         # training step's input is the batch X (the output gradient comes from the loss, here
@@ -529,14 +622,18 @@ def main() -> None:
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rows = args.cpu_rows
         step = cpu_reference_step(rows)
-        t0 = time.perf_counter()
-        step()
-        sec = time.perf_counter() - t0
+        runs = []
+        for _ in range(3):  # best of 3
+            t0 = time.perf_counter()
+            step()
+            runs.append(time.perf_counter() - t0)
+        sec = min(runs)
         line["cpu_baseline"] = {
             "value": dense_equiv_flops(m=rows) / sec / 1e12, "unit": UNIT, "cores": cpu_cores(),
             "kind": "port",
             "sample": f"{rows} tokens x K=N=4096 fwd+bwd, f64, oracle port of stl_batched + "
-                      f"_layer_backward (np.einsum as the reference), one run, {sec:.1f} s"}
+                      f"_layer_backward (np.einsum as the reference), best of 3 runs "
+                      f"({', '.join(f'{r:.1f}' for r in runs)} s)"}
 
     if rank == 0:
         print(json.dumps(line), flush=True)

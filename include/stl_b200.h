@@ -154,15 +154,18 @@ STL_API int stl_forward(const void* x, int64_t M, int64_t K, int64_t ld_x, const
  * gu_prod: STL_PROD_AUTO (the cache's format family: F24 cache -> F24 g_u where the shape
  * allows, else the AUTO rule) or a forced format. red_ws: stl_reduce_workspace_floats floats.
  * Any of g_ex, g_d, g_w, g_x may be NULL to skip that gradient, except that g_ex is fused with
- * g_x (g_ex without g_x -> STL_ERR_VALUE). stl_backward = stl_backward_ex with the AUTO cache
- * format and gu_prod = STL_PROD_AUTO.
+ * g_x (g_ex without g_x -> STL_ERR_VALUE). gw_ready: a cudaEvent_t or NULL; when given it is
+ * recorded on `stream` as soon as g_w is final (before the g_x / g_ex decode), so a
+ * data-parallel caller can all-reduce g_w on another stream while the decode runs.
+ * stl_backward = stl_backward_ex with the AUTO cache format, gu_prod = STL_PROD_AUTO and no
+ * event.
  */
 STL_API int stl_backward_ex(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x,
                             const void* w_enc, const float* e_x, const float* d,
                             const void* x_enc, const void* y_enc, int y_enc_format, int64_t M,
                             int64_t K, int64_t N, int t, int r, int dtype, float* g_ex, float* g_d,
                             float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws, float* g_u_ws,
-                            float* red_ws, int gu_prod, void* stream);
+                            float* red_ws, int gu_prod, void* gw_ready, void* stream);
 STL_API int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, const void* w_enc,
                  const float* e_x, const float* d, const void* x_enc, const void* y_enc,
                  int64_t M, int64_t K, int64_t N, int t, int r, int dtype, float* g_ex,

@@ -47,7 +47,7 @@ SIGNATURES = {
     "stl_backward_ex": ([c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                          c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int, c_int,
                          c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
-                         c_void_p, c_void_p, c_int, c_void_p], c_int),
+                         c_void_p, c_void_p, c_int, c_void_p, c_void_p], c_int),
     "stl_forward": ([c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                      c_int, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                      c_int64, c_void_p], c_int),

@@ -315,7 +315,7 @@ int stl_backward_ex(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, 
                     const float* e_x, const float* d, const void* x_enc, const void* y_enc,
                     int y_enc_format, int64_t M, int64_t K, int64_t N, int t, int r, int dtype,
                     float* g_ex, float* g_d, float* g_w, void* g_x, int64_t ld_gx, void* g_enc_ws,
-                    float* g_u_ws, float* red_ws, int gu_prod, void* stream) {
+                    float* g_u_ws, float* red_ws, int gu_prod, void* gw_ready, void* stream) {
   if (int st = check_tr(t, r)) return st;
   if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype");
   if (M < 0 || K < 0 || N < 0 || M % t || K % t || N % t)
@@ -388,6 +388,12 @@ int stl_backward_ex(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, 
     }
     if (st) return st;
   }
+  // g_w is final here (the g_x / g_ex decode does not touch it): let the caller start its
+  // data-parallel all-reduce on another stream while the decode runs.
+  if (g_w && gw_ready) {
+    st = check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(gw_ready), s), "g_w event");
+    if (st) return st;
+  }
   if (g_x) {
     if (!gu_done) {
       st = run_gemm(g_enc_ws, STL_K_MAJOR, w_enc, STL_MN_MAJOR, g_u_ws, gu_dt, dtype, r, bi, bk,
@@ -413,7 +419,7 @@ int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t ld_x, con
   const int fmt = t > 0 ? cache_format(M / t, N / t, K / t, t, r, dtype, STL_PROD_AUTO) : dtype;
   return stl_backward_ex(gy, ld_gy, x, ld_x, w_enc, e_x, d, x_enc, y_enc, fmt, M, K, N, t, r, dtype,
                          g_ex, g_d, g_w, g_x, ld_gx, g_enc_ws, g_u_ws, red_ws, STL_PROD_AUTO,
-                         stream);
+                         nullptr, stream);
 }
 
 namespace {

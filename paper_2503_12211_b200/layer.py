@@ -98,8 +98,10 @@ def _layer_forward_cached(layer: StlLayer, x, *, products=None):
 
 
 def backward_raw(snf: SnfTriple, w_planes: torch.Tensor, cache: LayerCache, gy: torch.Tensor,
-                 need_gx: bool = True, need_gw: bool = True, need_enc: bool = True):
-    """Launch stl_backward; returns (g_ex, g_d, g_w planes (r, bj, bk) fp32, g_x)."""
+                 need_gx: bool = True, need_gw: bool = True, need_enc: bool = True,
+                 gw_ready: torch.cuda.Event | None = None):
+    """Launch stl_backward_ex; returns (g_ex, g_d, g_w planes (r, bj, bk) fp32, g_x).
+    gw_ready: an event recorded once g_w is final (before the g_x / g_ex decode)."""
     x, u, y_enc = cache
     t, r = snf.t, snf.r
     M, K = x.shape
@@ -119,12 +121,15 @@ def backward_raw(snf: SnfTriple, w_planes: torch.Tensor, cache: LayerCache, gy: 
     def ptr(tns):
         return tns.data_ptr() if tns is not None else None
 
+    if gw_ready is not None and not gw_ready.cuda_event:
+        gw_ready.record()  # torch creates events lazily: materialise the handle
     # the cache carries its format (its dtype); the backward is told, never guesses
     _lib.check(lib.stl_backward_ex(
         gy.data_ptr(), gy.stride(0), x.data_ptr(), x.stride(0), w_planes.data_ptr(),
         snf.e_x.data_ptr(), snf.d.data_ptr(), u.data_ptr(), y_enc.data_ptr(),
         cache_dtype_format(y_enc), M, K, N, t, r, _dt(x.dtype), ptr(g_ex), ptr(g_d), ptr(g_w),
-        ptr(g_x), K, g_enc.data_ptr(), ptr(g_u), ptr(red), _lib.STL_PROD_AUTO, _stream(dev)))
+        ptr(g_x), K, g_enc.data_ptr(), ptr(g_u), ptr(red), _lib.STL_PROD_AUTO,
+        gw_ready.cuda_event if gw_ready is not None else None, _stream(dev)))
     return g_ex, g_d, g_w, g_x
 
 

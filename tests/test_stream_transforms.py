@@ -106,7 +106,7 @@ def test_cache_format_is_explicit():
             x_dev.data_ptr(), K, x_dev.data_ptr(), K, layer.w_planes.data_ptr(),
             snf.e_x.data_ptr(), snf.d.data_ptr(), cache.u.data_ptr(), cache.y_enc.data_ptr(), bad,
             M, K, N, t, r, _lib.STL_BF16, None, None, None, g_x.data_ptr(), K, g_enc.data_ptr(),
-            g_u.data_ptr(), None, _lib.STL_PROD_AUTO, torch.cuda.current_stream().cuda_stream)
+            g_u.data_ptr(), None, _lib.STL_PROD_AUTO, None, torch.cuda.current_stream().cuda_stream)
         assert st == 2, bad  # STL_ERR_VALUE
     torch.cuda.synchronize()
 
