@@ -283,11 +283,11 @@ struct OutStage {
       kSecOff + (OUT == kOutF32Bf16 ? 128 * 64 : (OUT == kOutF24 ? 128 * 32 : 0));
 };
 
-template <int BN, int OUT0, int OUT1>
+template <int BN, int OUT0, int OUT1, int ST = 0>
 struct Smem2 {
-  // ring depth chosen so ring + epilogue staging fits the 227 KB opt-in limit
+  // ring depth chosen so ring + epilogue staging fits the 227 KB opt-in limit (ST > 0: forced)
   static constexpr bool kDual = OUT0 == kOutF32Bf16 || OUT1 == kOutF32Bf16;
-  static constexpr int kStages = BN == 256 ? (kDual ? 5 : 6) : (kDual ? 7 : 8);
+  static constexpr int kStages = ST > 0 ? ST : (BN == 256 ? (kDual ? 5 : 6) : (kDual ? 7 : 8));
   static constexpr uint32_t kABytes = 128 * kBK * 2;
   static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
   static constexpr uint32_t kRing = kStages * (kABytes + kBBytes);
@@ -494,7 +494,7 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
   }
 }
 
-template <int BN, class K0, class K1>
+template <int BN, class K0, class K1, int ST = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     slice_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA0,
                           const __grid_constant__ CUtensorMap tmB0,
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const __grid_constant__ CUtensorMap tmB1,
                           const __grid_constant__ CUtensorMap tmC1,
                           const __grid_constant__ CUtensorMap tmC21, GroupArgs args) {
-  using S = Smem2<BN, K0::OUT, K1::OUT>;
+  using S = Smem2<BN, K0::OUT, K1::OUT, ST>;
   constexpr int kSt = S::kStages;
   constexpr uint32_t kTmemCols = (2 * BN <= 256) ? 256 : 512;
 
@@ -746,17 +746,19 @@ struct PairLaunch {
 };
 
 // One persistent launch over np (1 or 2) problems of kinds K0, K1.
-template <int BN, class K0, class K1>
+template <int BN, class K0, class K1, int ST = 0>
 cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s) {
   Tc2Maps m0, m1;
   bool ok = make_tc2_maps<BN, K0>(pbs[0], &m0);
   if (np > 1) ok = ok && make_tc2_maps<BN, K1>(pbs[1], &m1);
   else m1 = m0;
   if (!ok) return cudaErrorInvalidValue;
-  auto kern = slice_gemm_tc2_kernel<BN, K0, K1>;
-  const int smem = Smem2<BN, K0::OUT, K1::OUT>::kTotal;
+  auto kern = slice_gemm_tc2_kernel<BN, K0, K1, ST>;
+  const int smem = Smem2<BN, K0::OUT, K1::OUT, ST>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
+  if (probe_env("STL_SMEM_MAX_CARVEOUT", 0))  // probe: let a transform CTA share the SM
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   const int64_t t0 = tc2_tiles(pbs[0], BN);
   const int64_t tiles = t0 + (np > 1 ? tc2_tiles(pbs[1], BN) : 0);
   if (tiles <= 0) return cudaSuccess;
@@ -786,6 +788,11 @@ template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch_tc2_any(const SliceGemmProblem& pb, cudaStream_t s) {
   if (pb.c_dtype == kBF16) {
     using Kd = GemmKind<A_MN, B_MN, kOutBf16>;
+#ifdef STL_PROBES
+    // probe: a 4-stage ring (161.5 KB) leaves room for a co-resident transform CTA
+    if (BN == 256 && !A_MN && !B_MN && probe_env("STL_GEMM_STAGES", 0) == 4)
+      return launch_tc2_group<BN, Kd, Kd, 4>(&pb, 1, s);
+#endif
     return launch_tc2_group<BN, Kd, Kd>(&pb, 1, s);
   }
   if (pb.c_dtype == kF24) {

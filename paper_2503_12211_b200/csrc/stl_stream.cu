@@ -824,6 +824,8 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(L.total));
   if (e != cudaSuccess) return e;
+  if (probe_env("STL_SMEM_MAX_CARVEOUT", 0))
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   a.stg = stg;
   static const int noc = probe_env("STL_STREAM_NOCOMPUTE", 0);
   a.nocompute = noc;
@@ -868,6 +870,12 @@ cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, floa
   const bool use512 = force_t ? force_t == 512
                               : (L512.nstages >= (MODE == kDecRed ? 3u : 2u * groups_of<MODE, 16>()) &&
                                  L512.total <= 227 * 1024 && a.bc >= 512);
+#ifdef STL_PROBES
+  // probe: an 8-consumer-warp CTA (288 threads) that fits beside a slice-GEMM CTA
+  if constexpr (!has_red<MODE>() && std::is_same<ZT, __nv_bfloat16>::value)
+    if (probe_env("STL_STREAM_CW", 16) == 8)
+      return launch_mt<MODE, ZT, MT, 256, 8>(a, planes_in, planes_out, red_out, s, budget);
+#endif
   if (use512) return launch_mt<MODE, ZT, MT, 512, 16>(a, planes_in, planes_out, red_out, s, budget);
   return launch_mt<MODE, ZT, MT, 256, 16>(a, planes_in, planes_out, red_out, s, budget);
 }
