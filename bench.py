@@ -219,7 +219,7 @@ def rank_sweep(stl, lib, _lib, dev, stream, peaks, timed, n=8192, iters=5):
             recs = _lib.profile_records()
             g_ms = sum(m for nm, m, _ in recs if nm.startswith("slice_gemm")) / iters
             x_ms = sum(m for nm, m, _ in recs if nm in ("encode_x", "decode_y")) / iters
-            p_bytes = 2 if (t == 4 and r <= 32) else (3 if t == 4 else 4)  # bf16 / F24 / fp32
+            p_bytes = 2 if r <= 32 else (3 if t == 4 else 4)  # bf16 / F24 / fp32 products
             cost = stl.LayerCost(n, n, n, t, r, 2, p_bytes)
             g_tf = cost.gemm_flops() / (g_ms * 1e-3) / 1e12
             xf_gbs = (cost.encode_bytes() + cost.decode_bytes()) / (x_ms * 1e-3) / 1e9

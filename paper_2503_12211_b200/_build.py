@@ -21,7 +21,8 @@ LIB_PATH = PKG / LIB_NAME
 # (scripts/) select A/B variants and timers. The product library never reads the environment.
 PROBE_LIB_PATH = PKG / "libstl_b200_probe.so"
 
-SOURCES = ["stl_capi.cu", "stl_slice_gemm.cu", "stl_transform.cu", "stl_transform4.cu",
+SOURCES = ["stl_capi.cu", "stl_slice_gemm.cu", "stl_transform.cu", "stl_transform2.cu",
+           "stl_transform4.cu",
            "stl_transform_mma.cu", "stl_stream.cu", "stl_tokens.cu"]
 HEADERS = ["sm100_ptx.cuh", "sm100_pair_pipeline.cuh", "stl_internal.h"]
 

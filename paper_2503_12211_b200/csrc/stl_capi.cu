@@ -167,14 +167,19 @@ bool bf16_tc_path(int64_t rows, int64_t kt, int t, int dtype) {
 int product_format(int64_t rows, int64_t cols, int64_t kt, int t, int r, int dtype, int prod,
                    bool inference) {
   const bool tc = bf16_tc_path(rows, kt, t, dtype);
+  // t = 2 (configs[2]; FLOP-losing by construction, so a cache-less forward only): bf16
+  // products halve the r/4 x |Y| plane traffic the decode streams
+  const bool tc2 = dtype == STL_BF16 && t == 2 && rows > 128 && kt % 8 == 0 && cols % 4 == 0;
   switch (prod) {
     case STL_PROD_AUTO:
+      if (tc2 && inference && r <= 32) return STL_BF16;
       if (!tc) return kFp32Products;
       if (r > 32) return inference && r <= 64 && cols % 128 == 0 ? stl::kF24 : kFp32Products;
       return cols % 64 == 0 ? STL_BF16 : kFp32Products;
     case STL_F32:
       return kFp32Products;
     case STL_BF16:
+      if (tc2 && inference) return STL_BF16;
       return tc && cols % 64 == 0 && (inference || r <= 32) ? STL_BF16 : kBadFormat;
     case STL_F24:
       return tc && cols % 128 == 0 && r <= (inference ? 64 : 32) ? stl::kF24 : kBadFormat;

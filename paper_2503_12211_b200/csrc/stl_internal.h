@@ -141,6 +141,12 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
                                    const float* coef, void* out, int odt, int64_t ldo,
                                    const void* rm, int rdt, int64_t ldr, float* ro, float* rw,
                                    cudaStream_t s, int64_t plane_rows = 0);
+// Register-streaming t = 2 transforms (stl_transform2.cu), tried first for t = 2 without a
+// fused reduction: bf16 matrix, bf16 (encode) / bf16 or fp32 (decode) planes, bc % 4 == 0.
+cudaError_t tiles_to_planes2(const void* m, int mdt, int64_t ldm, int64_t br, int64_t bc,
+                             const float* coef, int P, void* out, int odt, cudaStream_t s);
+cudaError_t planes_to_tiles2(const void* in, int idt, int Q, int64_t br, int64_t bc,
+                             const float* coef, void* out, int odt, int64_t ldo, cudaStream_t s);
 // out[o] = sum_b partial[b * n + o], deterministic fixed-order tree.
 cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t s);
 cudaError_t compose_coefs(const float* a, const float* b, int r, int tt, float* out,

@@ -58,6 +58,7 @@ struct Layout {
   uint32_t row_stride, rows_bytes;  // padded matrix rows of a stage
   uint32_t stage_bytes;
   uint32_t out_stride, out_bytes;   // one output staging buffer
+  uint32_t nbuf;                    // output staging buffers per consumer group (2..4)
   uint32_t red_bytes;
   uint32_t nstages;
   uint32_t total;                   // dynamic smem incl. barriers and alignment slack
@@ -85,7 +86,19 @@ inline Layout make_layout(int P, int Pb, uint32_t budget) {
   }
   L.red_bytes = 0;  // the final per-warp reduction partials reuse the (drained) stage ring
   static const uint32_t max_st = probe_env("STL_STREAM_STAGES", 8);
-  const uint32_t fixed = 2 * groups_of<MODE, CW>() * L.out_bytes + L.red_bytes;
+  // Output staging buffers per consumer group: 3 for the plain encode / decode when that still
+  // leaves two input stages per group (the store of unit i-1 may still be draining while unit i
+  // is staged: 8192^3 encode 63 -> 58 us, decode 60 -> 56 us), else 2. The fused reductions
+  // keep 2 (a third buffer costs them input stages: decode_gu+g_ex 49 -> 65 us).
+  static const int nbuf_env = probe_env("STL_STREAM_NBUF", 0);
+  L.nbuf = 2;
+  if (nbuf_env >= 2 && nbuf_env <= 4) {
+    L.nbuf = nbuf_env;
+  } else if (!has_red<MODE>()) {
+    const uint32_t f3 = 3 * groups_of<MODE, CW>() * L.out_bytes;
+    if (budget > f3 && (budget - f3) / L.stage_bytes >= 2u * groups_of<MODE, CW>()) L.nbuf = 3;
+  }
+  const uint32_t fixed = L.nbuf * groups_of<MODE, CW>() * L.out_bytes + L.red_bytes;
   uint32_t ns = (budget - fixed) / L.stage_bytes;
   if (ns > max_st) ns = max_st;
   L.nstages = ns > kMaxStages ? kMaxStages : (ns < 2 ? 2 : ns);
@@ -238,7 +251,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   const uint32_t s_out = s_stages + L.nstages * L.stage_bytes;
   float* s_red = reinterpret_cast<float*>(smem);  // after the unit loop only
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.nstages * L.stage_bytes +
-                                               2 * groups_of<MODE, CW>() * L.out_bytes + L.red_bytes);
+                                               L.nbuf * groups_of<MODE, CW>() * L.out_bytes + L.red_bytes);
   constexpr int kCWarps = CW;
   constexpr int kCThreads = 32 * CW;
   constexpr int kGroups = groups_of<MODE, CW>();
@@ -432,7 +445,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     const uint32_t J0 = urows > 1 ? 0u : (u - I * upr) * kT;
     const uint32_t nrows = urows > 1 ? min(static_cast<uint32_t>(urows), br - I) : 1u;
     const int Tw = static_cast<int>(urows > 1 ? nrows * bc : min(bc - J0, static_cast<uint32_t>(kT)));
-    const uint32_t buf = s_out + (grp * 2 + ((it / kGroups) & 1)) * L.out_bytes;
+    const uint32_t buf = s_out + (grp * L.nbuf + (it / kGroups) % L.nbuf) * L.out_bytes;
     const uint32_t planes = s_stages + stage * L.stage_bytes;
     const uint32_t rows = planes + L.pl_bytes;
     const uint64_t t_w0 = args.dbg ? ptx::globaltimer_ns() : 0;
@@ -702,7 +715,13 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     ptx::fence_proxy_async_smem();
     // The stores of the previous unit (other buffer) must have finished reading it before the
     // barrier: the next unit writes that buffer. One barrier per unit.
-    if (wl == 0) ptx::bulk_wait_read<0>();
+    // With nbuf buffers the one written next was last stored nbuf - 1 units ago: allow the
+    // nbuf - 2 younger stores to stay in flight.
+    if (wl == 0) {
+      if (L.nbuf == 2) ptx::bulk_wait_read<0>();
+      else if (L.nbuf == 3) ptx::bulk_wait_read<1>();
+      else ptx::bulk_wait_read<2>();
+    }
     gbar<kGThreads>(grp);
     // the group's warp 0 issues the unit's stores: the plane box (one 4-D TMA op, clipped at
     // the matrix edge) or the 4 output rows (1-D bulk copies).

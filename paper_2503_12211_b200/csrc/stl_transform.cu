@@ -394,6 +394,10 @@ cudaError_t tiles_to_planes(const void* m, int m_dtype, int64_t ldm, int64_t br,
                                            red_planes, red_dtype, red_out, red_ws, s);
     if (e != cudaErrorNotSupported) return e;
   }
+  if (t == 2 && !red_planes) {
+    cudaError_t e = tiles_to_planes2(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (red_planes && red_dtype == kF24) return cudaErrorNotSupported;
   if (t == 4) {
     cudaError_t e = tiles_to_planes_mma(m, m_dtype, ldm, br, bc, coef, P, out, out_dtype,
@@ -423,6 +427,10 @@ cudaError_t planes_to_tiles(const void* in, int in_dtype, int Q, int64_t br, int
     if (e != cudaErrorNotSupported) return e;
   }
   if (in_dtype == kF24) return cudaErrorNotSupported;
+  if (t == 2 && !red_m) {
+    cudaError_t e = planes_to_tiles2(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (t == 4) {
     cudaError_t e = planes_to_tiles4(in, in_dtype, Q, br, bc, coef, out, out_dtype, ldo, red_m,
                                      red_dtype, ldr, red_out, red_ws, s);

@@ -155,3 +155,41 @@ def test_stage_protocol_bitwise_repeat_with_compute():
             for a, b in zip(out, first):
                 assert torch.equal(a, b)
     torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- t = 2 (stl_transform2.cu)
+@pytest.mark.parametrize("rows,cols", [(64, 2048), (130, 72), (6, 520), (256, 36)])
+@pytest.mark.parametrize("r", [3, 16, 24, 32, 49])
+def test_encode_decode_t2_bf16(rows, cols, r):
+    """t = 2 register-streaming encode / decode (4 tiles per thread; tile columns % 4 == 0) and
+    the generic fallback (cols / 2 = 36 / 18: not a multiple of 4), bf16 and fp32 planes."""
+    rng = O.make_rng(rows * 7 + cols + r)
+    e_x, _, d = O.random_gaussian_init(2, r, rng, scale=0.5)
+    m_dev, m64 = bf(rng.standard_normal((rows, cols)))
+    enc = stl.encode_tiles(m_dev, e_x, 2)
+    ref_enc = O.encode_tiles(m64, e_x, 2)
+    assert rel(enc, ref_enc) <= 5e-3
+    enc_dev, enc64 = bf(ref_enc)
+    dec = stl.decode_tiles(enc_dev.permute(2, 0, 1).contiguous().permute(1, 2, 0), d, 2)
+    assert dec.dtype == torch.bfloat16
+    assert rel(dec, O.decode_tiles(enc64, d, 2)) <= 5e-3
+    enc32 = torch.tensor(ref_enc, dtype=torch.float32, device="cuda")
+    dec32 = stl.decode_tiles(enc32.permute(2, 0, 1).contiguous().permute(1, 2, 0), d, 2)
+    assert rel(dec32, O.decode_tiles(ref_enc, d, 2)) <= 1e-5
+
+
+@pytest.mark.parametrize("M,K,N,r", [(1024, 512, 768, 16), (1024, 256, 1024, 24),
+                                     (520, 256, 264, 32)])
+def test_forward_t2_bf16_products(M, K, N, r):
+    """Cache-less bf16 forward at t = 2: bf16 slice products (STL_PROD_AUTO) decoded by the
+    t = 2 streaming kernel; within the bf16 bar of the oracle."""
+    t = 2
+    rng = O.make_rng(M + 3 * K + N + r)
+    e_x, e_w, d = O.random_gaussian_init(t, r, rng, scale=0.5)
+    x_dev, x64 = bf(rng.standard_normal((M, K)))
+    w_dev, w64 = bf(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
+    fmt = stl.cache_format(M, K, N, t, r, torch.bfloat16, None)
+    y = stl.stl_batched(x_dev, w_dev, stl.SnfTriple(t, r, e_x, e_w, d))
+    torch.cuda.synchronize()
+    assert rel(y, O.stl_batched(x64, w64, e_x, d, t)) <= 1e-2
+    assert fmt in (_lib.STL_BF16, _lib.STL_F32)  # the training cache keeps fp32 products at t = 2
