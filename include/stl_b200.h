@@ -181,6 +181,16 @@ STL_API int stl_backward(const void* gy, int64_t ld_gy, const void* x, int64_t l
 STL_API int stl_fused_step(const float* x_prev, int64_t block_rows, int64_t block_k, const void* w_enc,
                    int64_t block_n, const float* e_x, const float* d, int t, int r, int dtype,
                    float* out, void* mixed_ws, float* comp_ws, void* stream);
+/*
+ * stl_fused_step_ex: the same step with the encoded activations' formats explicit, so a bf16
+ * chain stays in 2-byte planes end to end: x_prev_dtype / out_dtype = STL_F32 or STL_BF16
+ * (STL_BF16 requires dtype == STL_BF16). The bf16 path remixes with the streaming tensor-core
+ * kernel (r <= 32, BK % 64 == 0): one HBM pass over the r planes in and out.
+ */
+STL_API int stl_fused_step_ex(const void* x_prev, int x_prev_dtype, int64_t block_rows,
+                              int64_t block_k, const void* w_enc, int64_t block_n,
+                              const float* e_x, const float* d, int t, int r, int dtype, void* out,
+                              int out_dtype, void* mixed_ws, float* comp_ws, void* stream);
 
 /*
  * Token-row plumbing for STL layers over (B, T, features) activations with T % t == 1 (the

@@ -58,6 +58,9 @@ SIGNATURES = {
                       c_void_p, c_void_p], c_int),
     "stl_fused_step": ([c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int,
                         c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p], c_int),
+    "stl_fused_step_ex": ([c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                           c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p,
+                           c_void_p], c_int),
     "stl_token_pad": ([c_void_p, c_int, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64,
                        c_void_p], c_int),
     "stl_token_unpad": ([c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int, c_int64, c_int64,

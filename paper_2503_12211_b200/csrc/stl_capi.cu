@@ -488,26 +488,53 @@ int stl_token_fold_backward(const void* g_out, const void* y, int64_t B, int64_t
                     "token fold backward");
 }
 
-int stl_fused_step(const float* x_prev, int64_t block_rows, int64_t block_k, const void* w_enc,
-                   int64_t block_n, const float* e_x, const float* d, int t, int r, int dtype,
-                   float* out, void* mixed_ws, float* comp_ws, void* stream) {
+int stl_fused_step_ex(const void* x_prev, int x_prev_dtype, int64_t block_rows, int64_t block_k,
+                      const void* w_enc, int64_t block_n, const float* e_x, const float* d, int t,
+                      int r, int dtype, void* out, int out_dtype, void* mixed_ws, float* comp_ws,
+                      void* stream) {
   if (int st = check_tr(t, r)) return st;
-  if (!valid_dtype(dtype)) return fail(STL_ERR_VALUE, "invalid dtype");
+  if (!valid_dtype(dtype) || !valid_dtype(x_prev_dtype) || !valid_dtype(out_dtype))
+    return fail(STL_ERR_VALUE, "invalid dtype");
+  if ((x_prev_dtype == STL_BF16 || out_dtype == STL_BF16) && dtype != STL_BF16)
+    return fail(STL_ERR_VALUE, "bf16 encoded activations need bf16 weights");
   if (block_rows < 0 || block_k < 0 || block_n < 0) return fail(STL_ERR_SHAPE, "negative extent");
   cudaStream_t s = as_stream(stream);
   int st;
+  // bf16 chain: the streaming tensor-core remix (planes in, planes out, one HBM pass; it reads
+  // C^T, so the composite is built transposed); else the generic kernel
+  const bool streamed = dtype == STL_BF16 && r <= 32 && block_k % 64 == 0;
   {
     Prof prof("compose", s);
-    st = check_cuda(stl::compose_coefs(e_x, d, r, t * t, comp_ws, s), "compose");
+    st = check_cuda(streamed ? stl::compose_coefs(d, e_x, r, t * t, comp_ws, s)
+                             : stl::compose_coefs(e_x, d, r, t * t, comp_ws, s),
+                    "compose");
   }
   if (st) return st;
-  Prof prof("remix", s);
-  st = check_cuda(stl::planes_to_planes(x_prev, STL_F32, r, block_rows * block_k, comp_ws, r,
-                                        mixed_ws, dtype, s),
-                  "fused-step remix");
+  {
+    Prof prof("remix", s);
+    cudaError_t e = cudaErrorNotSupported;
+    if (streamed)
+      e = stl::planes_to_planes_stream(x_prev, x_prev_dtype, r, block_rows, block_k, comp_ws,
+                                       mixed_ws, s);
+    if (e == cudaErrorNotSupported) {
+      if (streamed)  // declined (alignment): the generic kernel wants C, not C^T
+        st = check_cuda(stl::compose_coefs(e_x, d, r, t * t, comp_ws, s), "compose");
+      if (st) return st;
+      e = stl::planes_to_planes(x_prev, x_prev_dtype, r, block_rows * block_k, comp_ws, r,
+                                mixed_ws, dtype, s);
+    }
+    st = check_cuda(e, "fused-step remix");
+  }
   if (st) return st;
-  return run_gemm(mixed_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, out, STL_F32, dtype, r, block_rows,
+  return run_gemm(mixed_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, out, out_dtype, dtype, r, block_rows,
                   block_n, block_k, s);
+}
+
+int stl_fused_step(const float* x_prev, int64_t block_rows, int64_t block_k, const void* w_enc,
+                   int64_t block_n, const float* e_x, const float* d, int t, int r, int dtype,
+                   float* out, void* mixed_ws, float* comp_ws, void* stream) {
+  return stl_fused_step_ex(x_prev, STL_F32, block_rows, block_k, w_enc, block_n, e_x, d, t, r,
+                           dtype, out, STL_F32, mixed_ws, comp_ws, stream);
 }
 
 int stl_profile_enable(int on) {

@@ -6,6 +6,8 @@
 //                                                                     (toy_network.py:100-101)
 //   kDec    : tile(I, J)[c] = sum_p Z[p][I][J] D[p][c]                decode_tiles (snf_operator.py:88-96)
 //   kDecRed : kDec, plus  R[p][c] += sum_tiles Z[p][tile] X[tile][c]  g_x and g_ex (toy_network.py:104-105)
+//   kRemix  : out[p][I][J] = sum_q C[p][q] Z[q][I][J], C = e_x d^T       the fused-chain step's
+//             composite (snf_operator.py:175-188, Algorithm 2): planes in, planes out
 // Tiles follow the reference layout contract (dense_core.py:98-108): element c = 4a + b of
 // tile (I, J) is m[4I + a, 4J + b].
 //
@@ -29,7 +31,7 @@
 namespace stl {
 namespace {
 
-enum Mode { kEnc = 0, kEncRed = 1, kDec = 2, kDecRed = 3 };
+enum Mode { kEnc = 0, kEncRed = 1, kDec = 2, kDecRed = 3, kRemix = 4 };
 
 // CW = consumer warps per CTA (template; 16). A measured negative result: an 8-warp, 56 KB
 // "lite" configuration meant to share each SM with a slice-GEMM CTA (overlapping the g_x/g_ex
@@ -40,10 +42,12 @@ enum Mode { kEnc = 0, kEncRed = 1, kDec = 2, kDecRed = 3 };
 constexpr int kMaxStages = 16;
 constexpr uint32_t kRowPad = 64;            // matrix rows: 16-word bank shift per row
 
-template <int MODE> constexpr bool has_rows() { return MODE != kDec; }
+template <int MODE> constexpr bool has_rows() { return MODE != kDec && MODE != kRemix; }
 template <int MODE> constexpr bool has_planes_in() { return MODE != kEnc; }
 template <int MODE> constexpr bool is_enc() { return MODE == kEnc || MODE == kEncRed; }
 template <int MODE> constexpr bool has_red() { return MODE == kEncRed || MODE == kDecRed; }
+// the unit's output is a plane box (TMA store) rather than 4 matrix rows
+template <int MODE> constexpr bool out_planes() { return is_enc<MODE>() || MODE == kRemix; }
 template <int MODE, int CW> constexpr int groups_of() { return CW < 16 ? 1 : 2; }
 
 // Plane element types: float, __nv_bfloat16, or F24 (kF24 of stl_internal.h: a 16-bit high
@@ -77,7 +81,7 @@ inline Layout make_layout(int P, int Pb, uint32_t budget) {
   L.row_stride = kT * 4 * 2 + kRowPad;
   L.rows_bytes = has_rows<MODE>() ? 4 * L.row_stride : 0;
   L.stage_bytes = rup(L.pl_bytes + L.rows_bytes, 1024);
-  if (is_enc<MODE>()) {
+  if (out_planes<MODE>()) {
     L.out_stride = 0;  // swizzled plane box
     L.out_bytes = rup(P * kT * 2, 1024);
   } else {
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   if (warp == kCWarps && lane == 0) {
     if constexpr (has_planes_in<MODE>()) ptx::prefetch_tmap(&tm_in);
     if constexpr (kZ24) ptx::prefetch_tmap(&tm_in2);
-    if constexpr (is_enc<MODE>()) ptx::prefetch_tmap(&tm_out);
+    if constexpr (out_planes<MODE>()) ptx::prefetch_tmap(&tm_out);
   }
   __syncthreads();
   griddep_wait();  // inputs of this launch are complete (PDL)
@@ -350,7 +354,11 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   // Coefficient fragments, split hi + lo.
   //  ENC (A = E, M = p, K = c): a0 = E[16m+g][2q, 2q+1], a1 = E[16m+g+8][..], a2/a3: c + 8.
   //  DEC (B = D, K = p, N = c): b0 = (D[16ks+2q][c], D[16ks+2q+1][c]), b1: planes + 8.
-  uint32_t fh[MT][4], fl[MT][4];
+  //  REMIX: the same with B = C^T (coef = C^T, row stride P; N = output plane, kNT n-tiles).
+  constexpr int kNT = MODE == kRemix ? 2 * MT : 2;  // DEC n-tiles (16 tile values / P planes)
+  const int CS = MODE == kRemix ? P : 16;            // coefficient row stride
+  const int NC = MODE == kRemix ? P : 16;            // valid output columns
+  uint32_t fh[MT][is_enc<MODE>() ? 4 : 2 * kNT], fl[MT][is_enc<MODE>() ? 4 : 2 * kNT];
   if constexpr (is_enc<MODE>()) {
 #pragma unroll
     for (int m = 0; m < MT; ++m)
@@ -365,11 +373,11 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 #pragma unroll
     for (int ks = 0; ks < MT; ++ks)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {  // i = nt * 2 + h
+      for (int i = 0; i < 2 * kNT; ++i) {  // i = nt * 2 + h
         const int nt = i >> 1, h = i & 1, c = 8 * nt + g;
         const int pa = 16 * ks + 2 * q + 8 * h, pb = pa + 1;
-        const float d0 = pa < P ? args.coef[pa * 16 + c] : 0.f;
-        const float d1 = pb < P ? args.coef[pb * 16 + c] : 0.f;
+        const float d0 = pa < P && c < NC ? args.coef[pa * CS + c] : 0.f;
+        const float d1 = pb < P && c < NC ? args.coef[pb * CS + c] : 0.f;
         split2(d0, d1, fh[ks][i], fl[ks][i]);
       }
   }
@@ -417,16 +425,23 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   // thread loads, see below): bt[s][nt][0] = D[8s+2q][8nt+g], bt[s][nt][1] = D[8s+2q+1][8nt+g].
   constexpr bool kTf32 = ZSZ == 4 || kZ24;
   constexpr int KS8 = 2 * MT;
-  uint32_t bt[KS8][2][2];
+  uint32_t bt[KS8][kNT][2];
 #pragma unroll
   for (int s8 = 0; s8 < KS8; ++s8)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < kNT; ++nt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int pl = 8 * s8 + 2 * q + h, c = 8 * nt + g;
-        bt[s8][nt][h] = (!is_enc<MODE>() && kTf32 && pl < P) ? tf32_rna(args.coef[pl * 16 + c]) : 0u;
+        bt[s8][nt][h] = (!is_enc<MODE>() && kTf32 && pl < P && c < NC) ? tf32_rna(args.coef[pl * CS + c]) : 0u;
       }
+  // REMIX: C stores at buf + ro[k][h] + 1024 nt (output plane 8nt + 2q + h, tiles t0, t0 + 1)
+  uint32_t ro[kMK][2];
+#pragma unroll
+  for (int k = 0; k < kMK; ++k)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      ro[k][h] = MODE == kRemix ? pl_off<2>(P, 2 * q + h, 16 * (wl + kGWarps * k) + 2 * g) : 0u;
 
   float R[2][2][4];
 #pragma unroll
@@ -488,7 +503,9 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   #pragma unroll
         for (int k = 0; k < kMK; ++k) {
           if (kFull || wl + kGWarps * k < nmt) {
-            float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            float acc[kNT][4];
+  #pragma unroll
+            for (int nt = 0; nt < kNT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
             if constexpr (kTf32) {
               // m16n8k8 tf32 per 8 planes: rows g / g+8 = tiles t0 / t0+1, k = q / q+4 = planes
               // 8s+2q / 8s+2q+1: a0 a1 = Z[8s+2q][t0, t0+1] (one 8-byte or F24 load), a2 a3 =
@@ -506,7 +523,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                 const uint32_t a0 = tf32_rna(v[0].x), a1 = tf32_rna(v[0].y);
                 const uint32_t a2 = tf32_rna(v[1].x), a3 = tf32_rna(v[1].y);
   #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
+                for (int nt = 0; nt < kNT; ++nt)
+                  if (8 * nt < NC) mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
               }
             } else {
   #pragma unroll
@@ -523,7 +541,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                 const uint32_t a0 = __byte_perm(w[0], w[1], 0x5410), a1 = __byte_perm(w[0], w[1], 0x7632);
                 const uint32_t a2 = __byte_perm(w[2], w[3], 0x5410), a3 = __byte_perm(w[2], w[3], 0x7632);
   #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
+                for (int nt = 0; nt < kNT; ++nt) {
+                  if (8 * nt >= NC) break;  // warp-uniform: REMIX n-tiles past the P planes
                   mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
                   mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
                 }
@@ -560,7 +579,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                 split2(v[2][0], v[3][0], h2, l2);
                 split2(v[2][1], v[3][1], h3, l3);
   #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
+                for (int nt = 0; nt < kNT; ++nt) {
                   const uint32_t bh0 = fh[ks][2 * nt], bh1 = fh[ks][2 * nt + 1];
                   mma(acc[nt], h0, h1, h2, h3, bh0, bh1);
                   mma(acc[nt], l0, l1, l2, l3, bh0, bh1);
@@ -570,19 +589,29 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                 const uint32_t a0 = pack2(v[0][0], v[1][0]), a1 = pack2(v[0][1], v[1][1]);
                 const uint32_t a2 = pack2(v[2][0], v[3][0]), a3 = pack2(v[2][1], v[3][1]);
   #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
+                for (int nt = 0; nt < kNT; ++nt) {
                   mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
                   mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
                 }
               }
             }
             }  // bf16 planes
+            if constexpr (MODE == kRemix) {
+              // acc[nt][0] / [2] -> output plane 8nt + 2q at tiles t0 / t0 + 1, [1] / [3] -> plane
+              // 8nt + 2q + 1: one 4-byte store per plane into the swizzled plane box
+  #pragma unroll
+              for (int nt = 0; nt < kNT; ++nt) {
+                if (8 * nt + 2 * q < P) sts32(buf + ro[k][0] + 1024 * nt, pack2(acc[nt][0], acc[nt][2]));
+                if (8 * nt + 2 * q + 1 < P) sts32(buf + ro[k][1] + 1024 * nt, pack2(acc[nt][1], acc[nt][3]));
+              }
+            } else {
             // acc[nt][0,1] -> tile t0, c = 8nt + 2q (+1): row a = 2nt + (q>>1), col b = 2(q&1).
   #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
               const uint32_t o = buf + ooff + 128 * kGWarps * k + 2 * nt * RS;
               sts32(o, pack2(acc[nt][0], acc[nt][1]));
               sts32(o + 8, pack2(acc[nt][2], acc[nt][3]));
+            }
             }
           }
         }
@@ -691,7 +720,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     if (args.stg) {
       // Consumers copy the staged unit to global memory with 16-byte stores (coalesced rows).
       gbar<kGThreads>(grp);
-      if constexpr (is_enc<MODE>()) {
+      if constexpr (out_planes<MODE>()) {
         __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(I) * bc + J0;
         const int64_t ntiles = args.br * args.bc;
         const int pieces = P * (Tw >> 3);  // 16-byte pieces: (p, chunk k, c16)
@@ -726,7 +755,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     // the group's warp 0 issues the unit's stores: the plane box (one 4-D TMA op, clipped at
     // the matrix edge) or the 4 output rows (1-D bulk copies).
     if (wl == 0) {
-      if constexpr (is_enc<MODE>()) {
+      if constexpr (out_planes<MODE>()) {
         if (lane == 0) tma_store_4d(&tm_out, sbase + buf, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
       } else {
         __nv_bfloat16* o =
@@ -837,7 +866,7 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
       !plane_tmap(&tin2, static_cast<const uint8_t*>(planes_in) + 2 * a.P * a.prow * a.bc, 1, a.P,
                   a.Pb, a.br, a.bc, kT, R, a.prow))
     return cudaErrorNotSupported;
-  if (is_enc<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.P, a.br, a.bc, kT, R, a.prow))
+  if (out_planes<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.P, a.br, a.bc, kT, R, a.prow))
     return cudaErrorNotSupported;
   auto k = k_stream<MODE, ZT, MT, kT, CW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -905,9 +934,9 @@ cudaError_t launch(StreamArgs a, const void* planes_in, void* planes_out, float*
   switch ((a.P + 15) / 16) {
     case 1: return launch_t<MODE, ZT, 1>(a, planes_in, planes_out, red_out, s);
     case 2: return launch_t<MODE, ZT, 2>(a, planes_in, planes_out, red_out, s);
-    case 3: if constexpr (!has_red<MODE>()) return launch_t<MODE, ZT, 3>(a, planes_in, planes_out, red_out, s);
+    case 3: if constexpr (!has_red<MODE>() && MODE != kRemix) return launch_t<MODE, ZT, 3>(a, planes_in, planes_out, red_out, s);
             return cudaErrorNotSupported;
-    case 4: if constexpr (!has_red<MODE>()) return launch_t<MODE, ZT, 4>(a, planes_in, planes_out, red_out, s);
+    case 4: if constexpr (!has_red<MODE>() && MODE != kRemix) return launch_t<MODE, ZT, 4>(a, planes_in, planes_out, red_out, s);
             return cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
   }
@@ -973,6 +1002,23 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
   if (idt == kF32) return launch<kDec, float>(a, in, nullptr, nullptr, s);
   if (idt == kF24) return launch<kDec, F24>(a, in, nullptr, nullptr, s);
   return launch<kDec, __nv_bfloat16>(a, in, nullptr, nullptr, s);
+}
+
+// the fused-chain remix: r bf16 or fp32 planes -> r bf16 planes, out[p] = sum_q coef_t[q][p] in[q]
+// (coef_t = C^T, r x r row-major). r <= 32.
+cudaError_t planes_to_planes_stream(const void* in, int idt, int P, int64_t br, int64_t bc,
+                                    const float* coef_t, void* out, cudaStream_t s) {
+  if ((idt != kBF16 && idt != kF32) || bc % 64 || P < 1 || P > 32 || !al16(in) || !al16(out))
+    return cudaErrorNotSupported;
+  StreamArgs a{};
+  a.out = out;
+  a.coef = coef_t;
+  a.P = P;
+  a.br = br;
+  a.bc = bc;
+  a.prow = br;
+  if (idt == kF32) return launch<kRemix, float>(a, in, out, nullptr, s);
+  return launch<kRemix, __nv_bfloat16>(a, in, out, nullptr, s);
 }
 
 }  // namespace stl

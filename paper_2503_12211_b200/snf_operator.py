@@ -343,11 +343,20 @@ def stl_reference(x, w, snf) -> torch.Tensor:
 
 
 def stl_fused_step(x_encoded_prev, w_encoded, snf) -> torch.Tensor:
-    """One fused layer step in encoded space (snf_operator.py:175-188, Algorithm 2)."""
+    """One fused layer step in encoded space (snf_operator.py:175-188, Algorithm 2).
+
+    fp32 (or f64 / numpy) x_encoded_prev -> fp32 slice products (the reference contract). A
+    bf16 x_encoded_prev with bf16 weights keeps a bf16 chain in 2-byte planes end to end: the
+    remix is the streaming tensor-core kernel and the products come back bf16
+    (stl_fused_step_ex)."""
     snf = as_triple(snf)
-    x_prev = _check_encoded(x_encoded_prev, "x_encoded_prev", dtype=torch.float32)
+    bf16_chain = isinstance(x_encoded_prev, torch.Tensor) and x_encoded_prev.dtype == torch.bfloat16
+    x_prev = _check_encoded(x_encoded_prev, "x_encoded_prev",
+                            dtype=None if bf16_chain else torch.float32)
     dtype = torch.bfloat16 if (isinstance(w_encoded, torch.Tensor)
                                and w_encoded.dtype == torch.bfloat16) else torch.float32
+    if bf16_chain and dtype != torch.bfloat16:
+        raise ValueError("a bf16 encoded activation needs bf16 encoded weights")
     w = _check_encoded(w_encoded, "w_encoded", device=x_prev.device, dtype=dtype)
     if x_prev.shape[2] != snf.r or w.shape[2] != snf.r:
         raise ShapeError("encoded ranks must equal the triple rank")
@@ -363,10 +372,12 @@ def stl_fused_step(x_encoded_prev, w_encoded, snf) -> torch.Tensor:
     wp = w.permute(2, 1, 0)
     if not wp.is_contiguous():
         wp = wp.contiguous()
-    out = torch.empty((r, br, bj), dtype=torch.float32, device=dev)
+    out_dtype = torch.bfloat16 if bf16_chain else torch.float32
+    out = torch.empty((r, br, bj), dtype=out_dtype, device=dev)
     mixed = torch.empty((r, br, bk), dtype=dtype, device=dev)
     comp = torch.empty((r, r), dtype=torch.float32, device=dev)
-    _lib.check(_lib.load().stl_fused_step(
-        xp.data_ptr(), br, bk, wp.data_ptr(), bj, snf.e_x.data_ptr(), snf.d.data_ptr(), snf.t, r,
-        _dt(dtype), out.data_ptr(), mixed.data_ptr(), comp.data_ptr(), _stream(dev)))
+    _lib.check(_lib.load().stl_fused_step_ex(
+        xp.data_ptr(), _dt(xp.dtype), br, bk, wp.data_ptr(), bj, snf.e_x.data_ptr(),
+        snf.d.data_ptr(), snf.t, r, _dt(dtype), out.data_ptr(), _dt(out_dtype), mixed.data_ptr(),
+        comp.data_ptr(), _stream(dev)))
     return out.permute(1, 2, 0)

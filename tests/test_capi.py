@@ -62,3 +62,17 @@ def test_status_mapping_without_gpu():
         _lib.check(st)
     # zero-sized problems are no-ops
     assert lib.stl_slice_gemm(None, 0, None, 0, None, 0, 0, 4, 0, 8, 8, None) == 0
+
+
+def test_fused_step_ex_formats_without_gpu():
+    """stl_fused_step_ex: bf16 encoded activations require bf16 weights (ValueError before any
+    launch); invalid dtypes are ValueErrors too."""
+    lib = _lib.load()
+    st = lib.stl_fused_step_ex(None, _lib.STL_BF16, 4, 64, None, 4, None, None, 4, 24,
+                               _lib.STL_F32, None, _lib.STL_F32, None, None, None)
+    with pytest.raises(ValueError, match="bf16"):
+        _lib.check(st)
+    st = lib.stl_fused_step_ex(None, 9, 4, 64, None, 4, None, None, 4, 24, _lib.STL_BF16, None,
+                               _lib.STL_BF16, None, None, None)
+    with pytest.raises(ValueError):
+        _lib.check(st)

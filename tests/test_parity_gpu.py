@@ -536,3 +536,48 @@ def test_inference_forward_product_formats(bits):
     y = _forward(x, w, snf, products="f24" if bits else None)
     err = float((y.double() - yref).norm() / yref.norm())
     assert err < 1e-2 and err < (4e-3 if bits == 0 else 3.5e-3), err
+
+
+# ----------------------------------------------------------------- fused chain (f1)
+def test_three_layer_chain_strassen49_fp32():
+    """Mirror of the reference's test_three_layer_chain_with_strassen
+    (test_snf_operator.py:185-195): Strassen-49 is exact, so encode -> products -> 2 fused steps
+    -> decode equals x W0 W1 W2 (fp32 path, generic remix since r > 32)."""
+    e_x, e_w, d = O.strassen_rank49()
+    s49 = stl.SnfTriple(4, 49, e_x, e_w, d)
+    rng = O.make_rng(18)
+    n = 256
+    x = rng.standard_normal((n, n))
+    ws = [rng.standard_normal((n, n)) / np.sqrt(n) for _ in range(3)]
+    expected = x @ ws[0] @ ws[1] @ ws[2]
+    encs = [torch.tensor(O.encode_tiles(w, e_w, 4), dtype=torch.float32) for w in ws]
+    h = stl._slice_products(stl.encode_tiles(torch.tensor(x, dtype=torch.float32, device="cuda"),
+                                             s49.e_x, 4), encs[0])
+    for enc in encs[1:]:
+        h = stl.stl_fused_step(h, enc, s49)
+    got = stl.decode_tiles(h, s49.d, 4)
+    assert rel(got, expected) <= FP32_TOL
+
+
+@pytest.mark.parametrize("r,n", [(24, 512), (13, 256), (32, 768)])
+def test_chain_bf16_streamed_remix(r, n):
+    """A bf16 chain kept in 2-byte planes: bf16 products -> stl_fused_step (streaming remix,
+    bf16 out) x 2 -> decode, against the oracle chain on the same bf16 weights (bar 1e-2)."""
+    t = 4
+    rng = O.make_rng(100 + r)
+    e_x, e_w, d = O.random_gaussian_init(t, r, rng, scale=0.5)
+    snf = stl.SnfTriple(t, r, e_x, e_w, d)
+    x_dev, x64 = bf16_round(rng.standard_normal((n, n)))
+    w_dev, w64 = [], []
+    for _ in range(3):
+        a, b = bf16_round(O.encode_tiles(rng.standard_normal((n, n)) / np.sqrt(n), e_w, t))
+        w_dev.append(a.cuda())
+        w64.append(b)
+    h = stl._slice_products(stl.encode_tiles(x_dev.cuda(), snf.e_x, t), w_dev[0]).to(torch.bfloat16)
+    h64 = O.slice_products(O.encode_tiles(x64, e_x, t), w64[0])
+    for wd, w6 in zip(w_dev[1:], w64[1:]):
+        h = stl.stl_fused_step(h, wd, snf)
+        assert h.dtype == torch.bfloat16
+        h64 = O.stl_fused_step(h64, w6, e_x, d)
+    got = stl.decode_tiles(h, snf.d, t)
+    assert rel(got, O.decode_tiles(h64, d, t)) <= BF16_TOL
