@@ -290,7 +290,7 @@ def main() -> None:
     bi, bk, bj = M // T, K // T, N // T
     u = torch.empty((R, bi, bk), dtype=torch.bfloat16, device=dev)
     y_enc = torch.empty((int(lib.stl_cache_bytes(M, K, N, T, R, _lib.STL_BF16)),),
-                        dtype=torch.uint8, device=dev)  # forward cache (F24 slice products)
+                        dtype=torch.uint8, device=dev)  # forward cache (slice products, AUTO format)
     fwd_scratch = torch.empty((int(lib.stl_forward_scratch_bytes(M, K, N, T, R, _lib.STL_BF16)),),
                               dtype=torch.uint8, device=dev)
     y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
@@ -450,10 +450,18 @@ def main() -> None:
 
         for _ in range(args.warmup):
             dense_step()
-        dense_ms = timed(dense_step, args.steps) / args.steps
-        stl_ms = ms_step if world == 1 else timed(lambda: stl_step(False), args.steps) / args.steps
+        # STL and cuBLAS timed in alternating blocks (same thermal / power state for both),
+        # median block of each
+        blk = max(args.steps // 4, 10)
+        d_blocks, s_blocks = [], []
+        for _ in range(5):
+            s_blocks.append(timed(lambda: stl_step(False), blk) / blk)
+            d_blocks.append(timed(dense_step, blk) / blk)
+        dense_ms = statistics.median(d_blocks)
+        stl_ms = statistics.median(s_blocks)
         line["vs_cublas"] = {"cublas_ms_per_step": dense_ms, "stl_ms_per_step": stl_ms,
-                             "speedup": dense_ms / stl_ms,
+                             "speedup": dense_ms / stl_ms, "timing": "5 alternating blocks of "
+                             f"{blk} steps each (STL, cuBLAS), medians",
                              "cublas_tflops": dense_equiv_flops() / (dense_ms * 1e-3) / 1e12}
         del wd, yd, gxd, gwd
 
@@ -483,12 +491,17 @@ def main() -> None:
         for _ in range(args.warmup):
             fwd8192()
             torch.matmul(xf, wdf, out=ydf)
-        stl_f = timed(fwd8192, steps_f) / steps_f
+        # alternating blocks, medians (see vs_cublas)
+        sf_blocks, cf_blocks = [], []
+        for _ in range(5):
+            sf_blocks.append(timed(fwd8192, steps_f) / steps_f)
+            cf_blocks.append(timed(lambda: torch.matmul(xf, wdf, out=ydf), steps_f) / steps_f)
+        stl_f = statistics.median(sf_blocks)
         timed(fwd8192, steps_f, profile=True)  # attribution pass (events between launches)
         recs_f = _lib.profile_records()
         gemm_f = [ms for name, ms, _ in recs_f
                   if name == "slice_gemm_tcgen05"]
-        cub_f = timed(lambda: torch.matmul(xf, wdf, out=ydf), steps_f) / steps_f
+        cub_f = statistics.median(cf_blocks)
         cost_f = stl.LayerCost(m_loc, n3, n3, T, R, 2, 2)
         gf_ms = sum(gemm_f) / max(len(gemm_f), 1)
         xf_ms = {n: sum(ms for nm, ms, _ in recs_f if nm == n) / steps_f
@@ -496,6 +509,8 @@ def main() -> None:
         gemm_tf = cost_f.gemm_flops() / (gf_ms * 1e-3) / 1e12
         line["north_star_fwd_8192"] = {
             "stl_ms": stl_f, "cublas_ms": cub_f, "speedup": cub_f / stl_f, "target": 1.8,
+            "timing": f"5 alternating blocks of {steps_f} launches (STL forward, cuBLAS), medians",
+            "blocks_ms": {"stl": sf_blocks, "cublas": cf_blocks},
             "dense_equiv_tflops": 2 * n3 ** 3 / (stl_f * 1e-3) / 1e12,
             "m_sharded_over": world, "rows_per_rank": m_loc,
             "gemm_ms": gf_ms, "gemm_tflops": gemm_tf,
@@ -525,6 +540,14 @@ def main() -> None:
         # GEMMs are FLOP-losing by construction: the points report the fraction of roofline).
         if world == 1 and not args.no_sweep:
             line["rank_sweep"] = rank_sweep(stl, lib, _lib, dev, stream, peaks, timed)
+
+        # ---- f1: a 3-layer bf16 chain at 8192^3 kept in encoded space (Algorithm 2) vs the
+        # same layers as separate forwards (scripts/bench_chain.py; rank 0)
+        if world == 1 and not args.no_sweep:
+            sys.path.insert(0, str(Path(__file__).resolve().parent / "scripts"))
+            from bench_chain import chain_bench
+            line["fused_chain_8192"] = chain_bench()
+            torch.cuda.empty_cache()
 
         # ---- e2e: public API (StlLinear autograd) with pinned host inputs, copies timed: a
         # training step's input is the batch X (the output gradient comes from the loss, here

@@ -355,13 +355,24 @@ def test_fused_step_bf16():
 
 
 # ----------------------------------------------------------------- full-size properties
-def test_full_size_row_slab_and_linearity_bf16():
-    """BASELINE configs[1] shape (M=8192, K=N=4096, t=4, r=24): rows of Y depend only on the
-    same rows of X, so a 64-row slab is checked exactly against the oracle; linearity in x is
-    checked over the whole output."""
-    t, r, M, K, N = 4, 24, 8192, 4096, 4096
+def _triple(init, t, r, rng):
+    """Random N(0, 0.25) encoders, or the paper's training init: a Strassen-49 row subset."""
+    if init == "subset":
+        sub = stl.pruned_subset_init(stl.strassen_rank49(), r, rng)
+        return tuple(np.asarray(getattr(sub, f).cpu() if hasattr(getattr(sub, f), "cpu")
+                                else getattr(sub, f), dtype=np.float64) for f in ("e_x", "e_w", "d"))
+    return O.random_gaussian_init(t, r, rng, scale=0.5)
+
+
+@pytest.mark.parametrize("init", ["gaussian", "subset"])
+@pytest.mark.parametrize("M,K,N", [(8192, 4096, 4096), (8192, 8192, 8192)])
+def test_full_size_row_slab_and_linearity_bf16(init, M, K, N):
+    """BASELINE configs[1] (M=8192, K=N=4096) and north-star (8192^3) shapes, t=4, r=24, through
+    the default bf16-product path: rows of Y depend only on the same rows of X, so 64-row slabs
+    are checked against the oracle; linearity in x is checked over the whole output."""
+    t, r = 4, 24
     rng = O.make_rng(0)
-    e_x, e_w, d = O.random_gaussian_init(t, r, rng, scale=0.5)
+    e_x, e_w, d = _triple(init, t, r, rng)
     w_dev, w64 = bf16_round(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
     snf = stl.SnfTriple(t, r, e_x, e_w, d)
     g = torch.Generator(device=DEV).manual_seed(1)
@@ -389,13 +400,14 @@ def test_full_size_strassen49_equals_matmul_bf16():
     assert rel(got.float(), ref) <= BF16_TOL
 
 
-def test_full_size_backward_properties_bf16():
+@pytest.mark.parametrize("init", ["gaussian", "subset"])
+def test_full_size_backward_properties_bf16(init):
     """BASELINE configs[1] shape, forward + backward: g_x rows depend only on the same rows of
     gY (64-row slabs against the oracle), and g_w, g_d, g_ex are sums over token rows, so the
     backward of the two halves of the batch must add up to the backward of the whole."""
     t, r, M, K, N = 4, 24, 8192, 4096, 4096
     rng = O.make_rng(5)
-    e_x, e_w, d = O.random_gaussian_init(t, r, rng, scale=0.5)
+    e_x, e_w, d = _triple(init, t, r, rng)
     w_dev, w64 = bf16_round(O.encode_tiles(rng.standard_normal((K, N)) / np.sqrt(K), e_w, t))
     layer = stl.StlLayer(stl.SnfTriple(t, r, e_x, e_w, d), w_dev)
     g = torch.Generator(device=DEV).manual_seed(6)
