@@ -312,7 +312,6 @@ struct GroupArgs {
   int r;
   int total0, total;
   int nostore;
-  int c_evict_first;  // C stored with an L2 evict_first policy (written back during this launch)
 };
 
 // Tile `tile` of a group: problem, slice, 256-row block, BN-column block.
@@ -407,7 +406,7 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
                                              uint8_t* stage_base, uint32_t tmem_acc,
                                              int& chunk_no, int p, int col_base,
                                              int row_base, int M, int N, bool nostore, int q,
-                                             int lane, bool issuer, bool evict_first) {
+                                             int lane, bool issuer) {
   constexpr int OUT = Kd::OUT;
   constexpr uint32_t kSec = OutStage<OUT>::kSecOff;
   const int r = q * 32 + lane;  // staging row = TMEM lane
@@ -487,10 +486,7 @@ __device__ __forceinline__ void tc2_epilogue(const CUtensorMap* tmC, const CUten
     if (issuer) ptx::bulk_wait_read<0>();
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (issuer && active) {
-      if (evict_first)
-        ptx::tma_store_3d_hint(tmC, sf, col_base + c, row_base, p, ptx::policy_evict_first());
-      else
-        ptx::tma_store_3d(tmC, sf, col_base + c, row_base, p);
+      ptx::tma_store_3d(tmC, sf, col_base + c, row_base, p);
       if constexpr (OUT == kOutF32Bf16 || OUT == kOutF24)
         ptx::tma_store_3d(tmC2, sf + kSec, col_base + c, row_base, p);
       ptx::bulk_commit();
@@ -607,12 +603,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tmem_acc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       if (tc.prob == 0)
         tc2_epilogue<BN, K0, S>(&tmC0, &tmC20, stage_base, tmem_acc, chunk_no, tc.p, tc.nb * BN, row_base,
-                                args.M[0], args.N[0], args.nostore, q, lane, issuer,
-                                args.c_evict_first != 0);
+                                args.M[0], args.N[0], args.nostore, q, lane, issuer);
       else
         tc2_epilogue<BN, K1, S>(&tmC1, &tmC21, stage_base, tmem_acc, chunk_no, tc.p, tc.nb * BN, row_base,
-                                args.M[1], args.N[1], args.nostore, q, lane, issuer,
-                                args.c_evict_first != 0);
+                                args.M[1], args.N[1], args.nostore, q, lane, issuer);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0)
@@ -784,7 +778,6 @@ cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s
   ga.total0 = static_cast<int>(t0);
   ga.total = static_cast<int>(tiles);
   ga.nostore = probe_env("STL_GEMM_NOSTORE", 0);
-  ga.c_evict_first = probe_env("STL_GEMM_EVICT_FIRST", 0);
   if (probe_env("STL_GEMM_VERBOSE", 0))
     fprintf(stderr, "[tc2] max_clusters=%d clusters=%d tiles=%d BN=%d smem=%d\n", max_clusters,
             clusters, ga.total, BN, smem);

@@ -126,7 +126,6 @@ struct StreamArgs {
   int64_t prow;              // tile rows between planes (>= br: a row band of taller planes)
   int stg;                   // 1: consumers write outputs with st.global (else TMA/bulk stores)
   int nocompute;             // probe: skip the math (pure data movement)
-  int out_evict_first;       // DEC*: output rows stored with an L2 evict_first policy
   unsigned long long* dbg;   // probe: per-CTA phase timers [grid][4] (ns), or null
 };
 
@@ -138,12 +137,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
           "r"(dst),
       "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(ptx::smem_u32(bar))
       : "memory");
-}
-__device__ __forceinline__ void bulk_s2g_hint(void* dst, uint32_t src, uint32_t bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
-                   reinterpret_cast<uint64_t>(dst)),
-               "r"(src), "r"(bytes), "l"(pol)
-               : "memory");
 }
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
@@ -772,11 +765,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
           if (r < nrows)
             bulk_s2g(o + (4 * r + a) * args.ldo, sbase + buf + a * L.out_stride + r * bc * 8, bc * 8);
         } else if (lane < 4) {
-          if (args.out_evict_first)
-            bulk_s2g_hint(o + lane * args.ldo, sbase + buf + lane * L.out_stride, Tw * 8,
-                          ptx::policy_evict_first());
-          else
-            bulk_s2g(o + lane * args.ldo, sbase + buf + lane * L.out_stride, Tw * 8);
+          bulk_s2g(o + lane * args.ldo, sbase + buf + lane * L.out_stride, Tw * 8);
         }
       }
       ptx::bulk_commit();
@@ -888,8 +877,6 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   a.stg = stg;
   static const int noc = probe_env("STL_STREAM_NOCOMPUTE", 0);
   a.nocompute = noc;
-  static const int dec_ef = probe_env("STL_DEC_EVICT_FIRST", 0);
-  a.out_evict_first = dec_ef;
   static const int dbg_on = probe_env("STL_STREAM_DEBUG", 0);
   static unsigned long long* dbg = nullptr;
   if (dbg_on && !dbg) cudaMalloc(&dbg, 4 * 1024 * sizeof(unsigned long long));
