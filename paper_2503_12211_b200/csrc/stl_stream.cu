@@ -71,6 +71,25 @@ struct Layout {
 __host__ __device__ inline uint32_t rup(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 
+// bf16 plane segments moved as one 1-D bulk copy per plane into / out of plain shared-memory
+// rows padded by 16 bytes (bank-conflict-free fragment accesses, see the offsets below) instead
+// of one 4-D TMA box with 128-byte box rows. Measured per mode (profiles/r02_bulk_planes_ab.log):
+// the fused-chain remix's output 105 -> 96 us at 8192^2; but the encode's output 58 -> 72 us,
+// the decode's input 55 -> 85 us and the backward's fused reductions ~2x slower — so only the
+// remix output uses it (the others keep the TMA boxes; STL_BULK_IN / STL_BULK_OUT: probes).
+template <int MODE> inline bool bulk_planes_out() {
+  static const bool on = probe_env("STL_BULK_OUT", MODE == kRemix ? 1 : 0) != 0;
+  return on;
+}
+template <int MODE> inline bool bulk_planes_in() {
+  static const bool on = probe_env("STL_BULK_IN", 0) != 0;
+  return on;
+}
+template <int kT> constexpr uint32_t bulk_plane_stride() { return kT * 2 + 16; }
+template <int MODE, typename ZT> constexpr bool bulk_in_capable() {
+  return has_planes_in<MODE>() && std::is_same<ZT, __nv_bfloat16>::value;
+}
+
 template <int MODE, typename ZT, int kT, int CW>
 inline Layout make_layout(int P, int Pb, uint32_t budget) {
   // Pb >= P: planes of the input box (the TMA zero-fills planes P..Pb-1, so the consumers'
@@ -78,12 +97,16 @@ inline Layout make_layout(int P, int Pb, uint32_t budget) {
   Layout L{};
   L.pl_lo = is_f24<ZT>() ? rup(Pb * kT * 2, 1024) : 0;
   L.pl_bytes = has_planes_in<MODE>() ? rup(Pb * kT * zhi<ZT>(), 1024) + (is_f24<ZT>() ? rup(Pb * kT, 1024) : 0) : 0;
+  if (bulk_in_capable<MODE, ZT>() && bulk_planes_in<MODE>())
+    L.pl_bytes = rup(Pb * bulk_plane_stride<kT>(), 1024);
   L.row_stride = kT * 4 * 2 + kRowPad;
   L.rows_bytes = has_rows<MODE>() ? 4 * L.row_stride : 0;
   L.stage_bytes = rup(L.pl_bytes + L.rows_bytes, 1024);
   if (out_planes<MODE>()) {
     L.out_stride = 0;  // swizzled plane box
-    L.out_bytes = rup(P * kT * 2, 1024);
+    L.out_bytes = rup((MODE == kRemix ? Pb : P) * kT * 2, 1024);
+    if (bulk_planes_out<MODE>())  // plain planes, 16-byte padded (1-D bulk stores)
+      L.out_bytes = rup(Pb * bulk_plane_stride<kT>(), 1024);
   } else {
     L.out_stride = kT * 4 * 2 + kRowPad;
     L.out_bytes = rup(4 * L.out_stride, 1024);
@@ -126,6 +149,10 @@ struct StreamArgs {
   int64_t prow;              // tile rows between planes (>= br: a row band of taller planes)
   int stg;                   // 1: consumers write outputs with st.global (else TMA/bulk stores)
   int nocompute;             // probe: skip the math (pure data movement)
+  int hilo;                  // REMIX: coefficients as bf16 hi + lo (1) or hi only (0)
+  int bulk_in;               // bf16 input planes: 1-D bulk copies into plain padded rows
+  const uint8_t* planes_in;  // the input planes (bulk path)
+  int bulk_out;              // plane outputs: plain padded staging rows, 1-D bulk stores
   unsigned long long* dbg;   // probe: per-CTA phase timers [grid][4] (ns), or null
 };
 
@@ -189,6 +216,13 @@ __device__ __forceinline__ void mma(float (&c)[4], uint32_t a0, uint32_t a1, uin
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+// m16n8k8 bf16 (half a k16 step): a0 = (row g, k 2q..2q+1), a1 = row g+8; b0 = (k 2q..2q+1, col g)
+__device__ __forceinline__ void mma_k8(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
 // fp32 -> tf32 operand, rounded to nearest (ties away) by adding half an ulp of the 10-bit
 // mantissa; the tensor core ignores the low 13 bits. (Finite inputs.)
 __device__ __forceinline__ uint32_t tf32_rna(float x) { return __float_as_uint(x) + 0x1000u; }
@@ -237,7 +271,9 @@ __device__ __forceinline__ uint32_t pl_off(int P, int p, int t) {
 
 // ------------------------------------------------------------------ the kernel
 // MT = number of 16-plane groups (ceil(P / 16)), a template so every plane loop unrolls.
-template <int MODE, typename ZT, int MT, int kT, int CW>
+// NTR (kRemix only): output n-tiles = ceil(P / 8); the output staging holds Pb = 8 NTR planes
+// per chunk (the TMA store clips planes >= P), so every fragment store is unconditional.
+template <int MODE, typename ZT, int MT, int kT, int CW, int NTR = 0>
 __global__ void __launch_bounds__(32 * CW + 32, 1)
     k_stream(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_in2,
              const __grid_constant__ CUtensorMap tm_out,
@@ -315,15 +351,29 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
       if (lane == 0) stage_tag[stage] = it;  // before the expect_tx arrive (release) below
       const uint32_t rows_b = has_rows<MODE>() ? Tw * 8 : 0;
       const uint32_t st = s_stages + stage * L.stage_bytes;
+      const bool bin = bulk_in_capable<MODE, ZT>() && args.bulk_in;
       if (lane == 0) {
         ptx::mbar_arrive_expect_tx(&full[stage],
-                                   4 * rows_b + (has_planes_in<MODE>() ? Pb * kT * (ZSZ + (kZ24 ? 1 : 0)) : 0));
+                                   4 * rows_b + (!has_planes_in<MODE>() ? 0u
+                                                 : bin ? P * Tw * 2
+                                                       : Pb * kT * (ZSZ + (kZ24 ? 1 : 0))));
         if constexpr (has_planes_in<MODE>())
-          tma_load_4d(&tm_in, &full[stage], sbase + st, 0, 0, static_cast<int>(J0 / (128 / ZSZ)),
-                      static_cast<int>(I));
+          if (!bin)
+            tma_load_4d(&tm_in, &full[stage], sbase + st, 0, 0, static_cast<int>(J0 / (128 / ZSZ)),
+                        static_cast<int>(I));
         if constexpr (kZ24)
           tma_load_4d(&tm_in2, &full[stage], sbase + st + L.pl_lo, 0, 0, static_cast<int>(J0 / 128),
                       static_cast<int>(I));
+      }
+      if constexpr (bulk_in_capable<MODE, ZT>()) {
+        if (bin) {
+          // one bulk copy per plane: the unit's Tw tiles (contiguous also for R > 1)
+          __syncwarp();  // the expect_tx above precedes the copies' complete_tx
+          for (int p = lane; p < P; p += 32)
+            bulk_g2s(sbase + st + p * bulk_plane_stride<kT>(),
+                     args.planes_in + 2 * ((static_cast<int64_t>(p) * args.prow + I) * bc + J0),
+                     Tw * 2, &full[stage]);
+        }
       }
       if constexpr (has_rows<MODE>()) {
         if (urows > 1) {
@@ -355,9 +405,10 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   //  ENC (A = E, M = p, K = c): a0 = E[16m+g][2q, 2q+1], a1 = E[16m+g+8][..], a2/a3: c + 8.
   //  DEC (B = D, K = p, N = c): b0 = (D[16ks+2q][c], D[16ks+2q+1][c]), b1: planes + 8.
   //  REMIX: the same with B = C^T (coef = C^T, row stride P; N = output plane, kNT n-tiles).
-  constexpr int kNT = MODE == kRemix ? 2 * MT : 2;  // DEC n-tiles (16 tile values / P planes)
+  constexpr int kNT = MODE == kRemix ? NTR : 2;     // DEC n-tiles (16 tile values / P planes)
+  static_assert(MODE != kRemix || (NTR >= 1 && NTR <= 2 * MT), "remix n-tiles");
   const int CS = MODE == kRemix ? P : 16;            // coefficient row stride
-  const int NC = MODE == kRemix ? P : 16;            // valid output columns
+  const int NC = MODE == kRemix ? P : 16;            // valid output columns (zero past them)
   uint32_t fh[MT][is_enc<MODE>() ? 4 : 2 * kNT], fl[MT][is_enc<MODE>() ? 4 : 2 * kNT];
   if constexpr (is_enc<MODE>()) {
 #pragma unroll
@@ -386,7 +437,16 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   const uint32_t xoff = (q >> 1) * RS + 64 * wl + 8 * g + 4 * (q & 1);
   uint32_t soff[kNK];
 #pragma unroll
-  for (int k = 0; k < kNK; ++k) soff[k] = is_enc<MODE>() ? pl_off<2>(P, g, 8 * (wl + kGWarps * k) + 2 * q) : 0u;
+  // plane steps of the input / output plane regions: 128-byte swizzled box rows, or plain rows
+  // of bulk_plane_stride bytes (16-byte pad: word offset 4 per plane -> the fragment accesses
+  // below hit 32 distinct banks)
+  const bool bin = bulk_in_capable<MODE, ZT>() && args.bulk_in, bout = args.bulk_out != 0;
+  constexpr uint32_t PS = bulk_plane_stride<kT>();
+  const uint32_t PSi = bin ? PS : 128u, PSo = bout ? PS : 128u;
+  for (int k = 0; k < kNK; ++k)
+    soff[k] = !is_enc<MODE>() ? 0u
+              : bout ? g * PS + (8 * (wl + kGWarps * k) + 2 * q) * 2
+                     : pl_off<2>(P, g, 8 * (wl + kGWarps * k) + 2 * q);
   // Stores/loads of planes >= P exist only in the last 16-plane group.
   const bool lastp0 = 16 * (MT - 1) + g < P, lastp1 = 16 * (MT - 1) + g + 8 < P;
   const bool okb1 = 16 * (MT - 1) + g + 8 < Pb;  // row inside the (8-padded) input box
@@ -400,8 +460,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 #pragma unroll
   for (int k = 0; k < kMK; ++k) {
     const int t = 16 * (wl + kGWarps * k) + 2 * q;
-    ra0[k] = has_red<MODE>() ? pl_off<ZSZ>(Pb, g, t) : 0u;
-    ra2[k] = has_red<MODE>() ? pl_off<ZSZ>(Pb, g, t + 8) : 0u;
+    ra0[k] = !has_red<MODE>() ? 0u : bin ? g * PS + t * 2 : pl_off<ZSZ>(Pb, g, t);
+    ra2[k] = !has_red<MODE>() ? 0u : bin ? g * PS + (t + 8) * 2 : pl_off<ZSZ>(Pb, g, t + 8);
     ra0l[k] = kZ24 ? L.pl_lo + pl_off<1>(Pb, g, t) : 0u;   // F24 low bytes: same rule, W = 128
     ra2l[k] = kZ24 ? L.pl_lo + pl_off<1>(Pb, g, t + 8) : 0u;
   }
@@ -412,7 +472,9 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   for (int k = 0; k < kMK; ++k)
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      da[k][j] = is_enc<MODE>() ? 0u : pl_off<ZSZ>(Pb, 2 * q + j, 16 * (wl + kGWarps * k) + 2 * g);
+      da[k][j] = is_enc<MODE>() ? 0u
+                 : bin ? (2 * q + j) * PS + (16 * (wl + kGWarps * k) + 2 * g) * 2
+                       : pl_off<ZSZ>(Pb, 2 * q + j, 16 * (wl + kGWarps * k) + 2 * g);
       dal[k][j] = kZ24 ? L.pl_lo + pl_off<1>(Pb, 2 * q + j, 16 * (wl + kGWarps * k) + 2 * g) : 0u;
     }
   const uint32_t ooff = (q >> 1) * RS + 128 * wl + 16 * g + 4 * (q & 1);
@@ -441,7 +503,10 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   for (int k = 0; k < kMK; ++k)
 #pragma unroll
     for (int h = 0; h < 2; ++h)
-      ro[k][h] = MODE == kRemix ? pl_off<2>(P, 2 * q + h, 16 * (wl + kGWarps * k) + 2 * g) : 0u;
+      ro[k][h] = MODE != kRemix ? 0u
+                 : bout ? (2 * q + h) * PS + (16 * (wl + kGWarps * k) + 2 * g) * 2
+                        : pl_off<2>(Pb, 2 * q + h, 16 * (wl + kGWarps * k) + 2 * g);
+  const uint32_t ro_nt = 8 * PSo;
 
   float R[2][2][4];
 #pragma unroll
@@ -489,9 +554,9 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
               float c[4] = {0.f, 0.f, 0.f, 0.f};
               mma(c, fh[m][0], fh[m][1], fh[m][2], fh[m][3], b0, b1);
               mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0, b1);
-              const uint32_t o = buf + soff[k] + 16 * m * 128;
+              const uint32_t o = buf + soff[k] + 16 * m * PSo;
               if (m < MT - 1 || lastp0) sts32(o, pack2(c[0], c[1]));
-              if (m < MT - 1 || lastp1) sts32(o + 8 * 128, pack2(c[2], c[3]));
+              if (m < MT - 1 || lastp1) sts32(o + 8 * PSo, pack2(c[2], c[3]));
             }
           }
         }
@@ -524,7 +589,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                 const uint32_t a2 = tf32_rna(v[1].x), a3 = tf32_rna(v[1].y);
   #pragma unroll
                 for (int nt = 0; nt < kNT; ++nt)
-                  if (8 * nt < NC) mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
+                  mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
               }
             } else {
   #pragma unroll
@@ -536,15 +601,25 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   #pragma unroll
                 for (int j = 0; j < 4; ++j)
                   w[j] = (ks < MT - 1 || dok[j])
-                             ? lds32(planes + da[k][j & 1] + (16 * ks + 8 * (j >> 1)) * 128)
+                             ? lds32(planes + da[k][j & 1] + (16 * ks + 8 * (j >> 1)) * PSi)
                              : 0u;
                 const uint32_t a0 = __byte_perm(w[0], w[1], 0x5410), a1 = __byte_perm(w[0], w[1], 0x7632);
                 const uint32_t a2 = __byte_perm(w[2], w[3], 0x5410), a3 = __byte_perm(w[2], w[3], 0x7632);
+                if (MODE == kRemix && ks == MT - 1 && P <= 16 * (MT - 1) + 8) {
+                  // REMIX: the last plane group holds <= 8 planes: a k8 step (the mma.sync pipe
+                  // bounds the remix: r = 24 needs 1.5 k16-steps, not 2)
+  #pragma unroll
+                  for (int nt = 0; nt < kNT; ++nt) {
+                    mma_k8(acc[nt], a0, a1, fh[ks][2 * nt]);
+                    if (args.hilo) mma_k8(acc[nt], a0, a1, fl[ks][2 * nt]);
+                  }
+                  continue;
+                }
   #pragma unroll
                 for (int nt = 0; nt < kNT; ++nt) {
-                  if (8 * nt >= NC) break;  // warp-uniform: REMIX n-tiles past the P planes
                   mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
-                  mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
+                  if (MODE != kRemix || args.hilo)
+                    mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
                 }
                 continue;
               }
@@ -601,8 +676,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
               // 8nt + 2q + 1: one 4-byte store per plane into the swizzled plane box
   #pragma unroll
               for (int nt = 0; nt < kNT; ++nt) {
-                if (8 * nt + 2 * q < P) sts32(buf + ro[k][0] + 1024 * nt, pack2(acc[nt][0], acc[nt][2]));
-                if (8 * nt + 2 * q + 1 < P) sts32(buf + ro[k][1] + 1024 * nt, pack2(acc[nt][1], acc[nt][3]));
+                sts32(buf + ro[k][0] + ro_nt * nt, pack2(acc[nt][0], acc[nt][2]));
+                sts32(buf + ro[k][1] + ro_nt * nt, pack2(acc[nt][1], acc[nt][3]));
               }
             } else {
             // acc[nt][0,1] -> tile t0, c = 8nt + 2q (+1): row a = 2nt + (q>>1), col b = 2(q&1).
@@ -640,7 +715,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
               const bool ok0 = mt < MT - 1 || lastp0, ok1 = mt < MT - 1 || lastp1;
-              const uint32_t z0 = planes + ra0[k] + 16 * mt * 128, z2 = planes + ra2[k] + 16 * mt * 128;
+              const uint32_t z0 = planes + ra0[k] + 16 * mt * PSi, z2 = planes + ra2[k] + 16 * mt * PSi;
               if constexpr (kTf32) {
                 // two m16n8k8 tf32 steps (tiles t0..t0+7, t0+8..t0+15): rows g / g+8 = planes,
                 // k = q / q+4 = tiles 2q / 2q+1 of the step; B = X as fp32 (bf16 << 16, exact).
@@ -669,7 +744,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                 }
               } else if constexpr (ZSZ == 2 && !kZ24) {
                 const uint32_t a0 = ok0 ? lds32(z0) : 0u, a2 = ok0 ? lds32(z2) : 0u;
-                const uint32_t a1 = ok1 ? lds32(z0 + 1024) : 0u, a3 = ok1 ? lds32(z2 + 1024) : 0u;
+                const uint32_t a1 = ok1 ? lds32(z0 + 8 * PSi) : 0u, a3 = ok1 ? lds32(z2 + 8 * PSi) : 0u;
   #pragma unroll
                 for (int nt = 0; nt < 2; ++nt) mma(R[mt][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
               } else {
@@ -756,7 +831,16 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     // the matrix edge) or the 4 output rows (1-D bulk copies).
     if (wl == 0) {
       if constexpr (out_planes<MODE>()) {
-        if (lane == 0) tma_store_4d(&tm_out, sbase + buf, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
+        if (bout) {
+          // one bulk store per plane: the unit's Tw tiles of tile row I (contiguous also for
+          // R > 1: whole tile rows)
+          for (int p = lane; p < P; p += 32)
+            bulk_s2g(static_cast<__nv_bfloat16*>(args.out) +
+                         (static_cast<int64_t>(p) * args.prow + I) * bc + J0,
+                     sbase + buf + p * PS, static_cast<uint32_t>(Tw) * 2);
+        } else if (lane == 0) {
+          tma_store_4d(&tm_out, sbase + buf, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
+        }
       } else {
         __nv_bfloat16* o =
             static_cast<__nv_bfloat16*>(args.out) + (4 * static_cast<int64_t>(I)) * args.ldo + 4 * J0;
@@ -842,7 +926,7 @@ bool plane_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_
   return r == CUDA_SUCCESS;
 }
 
-template <int MODE, typename ZT, int MT, int kT, int CW>
+template <int MODE, typename ZT, int MT, int kT, int CW, int NTR = 0>
 cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                       cudaStream_t s, uint32_t budget) {
   a.Pb = ((a.P + 7) / 8) * 8;
@@ -866,9 +950,10 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
       !plane_tmap(&tin2, static_cast<const uint8_t*>(planes_in) + 2 * a.P * a.prow * a.bc, 1, a.P,
                   a.Pb, a.br, a.bc, kT, R, a.prow))
     return cudaErrorNotSupported;
-  if (out_planes<MODE>() && !plane_tmap(&tout, planes_out, 2, a.P, a.P, a.br, a.bc, kT, R, a.prow))
+  if (out_planes<MODE>() &&
+      !plane_tmap(&tout, planes_out, 2, a.P, MODE == kRemix ? a.Pb : a.P, a.br, a.bc, kT, R, a.prow))
     return cudaErrorNotSupported;
-  auto k = k_stream<MODE, ZT, MT, kT, CW>;
+  auto k = k_stream<MODE, ZT, MT, kT, CW, NTR>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(L.total));
   if (e != cudaSuccess) return e;
@@ -877,6 +962,11 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   a.stg = stg;
   static const int noc = probe_env("STL_STREAM_NOCOMPUTE", 0);
   a.nocompute = noc;
+  static const int hilo = probe_env("STL_REMIX_HILO", 1);
+  a.hilo = hilo;
+  a.bulk_in = bulk_in_capable<MODE, ZT>() && bulk_planes_in<MODE>();
+  a.planes_in = static_cast<const uint8_t*>(planes_in);
+  a.bulk_out = out_planes<MODE>() && bulk_planes_out<MODE>() && !stg;
   static const int dbg_on = probe_env("STL_STREAM_DEBUG", 0);
   static unsigned long long* dbg = nullptr;
   if (dbg_on && !dbg) cudaMalloc(&dbg, 4 * 1024 * sizeof(unsigned long long));
@@ -908,7 +998,7 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
 // 512-tile units whenever two pipeline stages per consumer group fit (measured: longer bulk
 // segments beat deeper pipelines; the g_x / g_ex decode-reduction even with 3 stages: 47.7 vs
 // 55.9 us at config 2, while the g_enc / g_d encode-reduction is faster with 256), else 256.
-template <int MODE, typename ZT, int MT>
+template <int MODE, typename ZT, int MT, int NTR = 0>
 cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                      cudaStream_t s) {
   static const int force_t = probe_env("STL_STREAM_T", 0);
@@ -920,17 +1010,26 @@ cudaError_t launch_t(StreamArgs a, const void* planes_in, void* planes_out, floa
                                  L512.total <= 227 * 1024 && a.bc >= 512);
 #ifdef STL_PROBES
   // probe: an 8-consumer-warp CTA (288 threads) that fits beside a slice-GEMM CTA
-  if constexpr (!has_red<MODE>() && std::is_same<ZT, __nv_bfloat16>::value)
+  if constexpr (!has_red<MODE>() && MODE != kRemix && std::is_same<ZT, __nv_bfloat16>::value)
     if (probe_env("STL_STREAM_CW", 16) == 8)
       return launch_mt<MODE, ZT, MT, 256, 8>(a, planes_in, planes_out, red_out, s, budget);
 #endif
-  if (use512) return launch_mt<MODE, ZT, MT, 512, 16>(a, planes_in, planes_out, red_out, s, budget);
-  return launch_mt<MODE, ZT, MT, 256, 16>(a, planes_in, planes_out, red_out, s, budget);
+  if (use512) return launch_mt<MODE, ZT, MT, 512, 16, NTR>(a, planes_in, planes_out, red_out, s, budget);
+  return launch_mt<MODE, ZT, MT, 256, 16, NTR>(a, planes_in, planes_out, red_out, s, budget);
 }
 
 template <int MODE, typename ZT>
 cudaError_t launch(StreamArgs a, const void* planes_in, void* planes_out, float* red_out,
                    cudaStream_t s) {
+  if constexpr (MODE == kRemix) {
+    switch ((a.P + 7) / 8) {  // n-tiles of the output planes
+      case 1: return launch_t<MODE, ZT, 1, 1>(a, planes_in, planes_out, red_out, s);
+      case 2: return launch_t<MODE, ZT, 1, 2>(a, planes_in, planes_out, red_out, s);
+      case 3: return launch_t<MODE, ZT, 2, 3>(a, planes_in, planes_out, red_out, s);
+      case 4: return launch_t<MODE, ZT, 2, 4>(a, planes_in, planes_out, red_out, s);
+      default: return cudaErrorNotSupported;
+    }
+  } else {
   switch ((a.P + 15) / 16) {
     case 1: return launch_t<MODE, ZT, 1>(a, planes_in, planes_out, red_out, s);
     case 2: return launch_t<MODE, ZT, 2>(a, planes_in, planes_out, red_out, s);
@@ -939,6 +1038,7 @@ cudaError_t launch(StreamArgs a, const void* planes_in, void* planes_out, float*
     case 4: if constexpr (!has_red<MODE>() && MODE != kRemix) return launch_t<MODE, ZT, 4>(a, planes_in, planes_out, red_out, s);
             return cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
+  }
   }
 }
 

@@ -43,6 +43,20 @@ def run(name, src, dst, pin, pout, nunits, grid, nst, total_bytes):
                       "GBs": round(total_bytes / ms / 1e6, 1)}), flush=True)
 
 
+# planes -> planes (the fused-chain remix): 24 segments in, 24 out per unit
+if os.environ.get("PP_REMIX"):  # only these cases
+    P2 = torch.empty_like(P)
+    for U in (512, 1024):
+        planes = (1, r, U * 2, 0, 0, b * b * 2)
+        nunits = b * (b // U)
+        for grid_mult, nst in ((1, 4), (2, 2), (2, 3), (1, 8)):
+            try:
+                run(f"remix U={U}", P, P2, planes, planes, nunits, sms * grid_mult, nst, 2 * r * b * b * 2)
+            except AssertionError:
+                pass
+    sys.exit(0)
+
+
 tot = n * n * 2 + r * b * b * 2
 for U in (128, 256, 512, 1024, 2048):
     upr = b // U
