@@ -20,6 +20,37 @@ __device__ __forceinline__ void griddep_wait() {
 __device__ __forceinline__ void griddep_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Probe build only (-DSTL_PROBES, STL_TRACE=1): every hot-path launch takes a trace slot and its
+// CTAs record [first entry, last exit] globaltimer spans there (scripts/trace_fwd.py reads them
+// back with stl_trace_read): where a pipeline's time goes between and inside kernels.
+struct Trace {
+  unsigned long long* buf;  // 2 per slot, or null
+  int slot;
+  unsigned long long* cta;  // per-CTA event stamps [kTraceCtaSlots][gridDim][4], or null
+};
+constexpr int kTraceCtaSlots = 64;
+#ifdef STL_PROBES
+Trace trace_next();
+__device__ __forceinline__ void trace_mark(const Trace& t, bool end) {
+  if (!t.buf) return;
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+  if (end) atomicMax(t.buf + 2 * t.slot + 1, now);
+  else atomicMin(t.buf + 2 * t.slot, now);
+}
+// per-CTA stamp e (0 entry, 1 after griddep_wait, 2 first unit's data, 3 loop end)
+__device__ __forceinline__ void trace_cta(const Trace& t, int e) {
+  if (!t.cta || t.slot >= kTraceCtaSlots) return;
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+  t.cta[(static_cast<size_t>(t.slot) * gridDim.x + blockIdx.x) * 4 + e] = now;
+}
+#else
+inline Trace trace_next() { return Trace{nullptr, 0, nullptr}; }
+__device__ __forceinline__ void trace_mark(const Trace&, bool) {}
+__device__ __forceinline__ void trace_cta(const Trace&, int) {}
+#endif
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t s, Args... args) {

@@ -312,6 +312,7 @@ struct GroupArgs {
   int r;
   int total0, total;
   int nostore;
+  Trace trace;  // probe: launch span
 };
 
 // Tile `tile` of a group: problem, slice, 256-row block, BN-column block.
@@ -535,6 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   if (warp == 1 && lane == 0) {
+    trace_mark(args.trace, false);
     for (int s = 0; s < kSt; ++s) {
       ptx::mbar_init(&full[s], 2);
       ptx::mbar_init(&empty[s], 1);
@@ -619,6 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, kTmemCols);
+  if (threadIdx.x == 0) trace_mark(args.trace, true);
 }
 
 // ------------------------------------------------------------------ host side
@@ -778,6 +781,7 @@ cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s
   ga.total0 = static_cast<int>(t0);
   ga.total = static_cast<int>(tiles);
   ga.nostore = probe_env("STL_GEMM_NOSTORE", 0);
+  ga.trace = trace_next();
   if (probe_env("STL_GEMM_VERBOSE", 0))
     fprintf(stderr, "[tc2] max_clusters=%d clusters=%d tiles=%d BN=%d smem=%d\n", max_clusters,
             clusters, ga.total, BN, smem);
@@ -1053,3 +1057,52 @@ cudaError_t slice_gemm_simt(const SliceGemmProblem& pb, cudaStream_t s) {
 }
 
 }  // namespace stl
+
+#ifdef STL_PROBES
+namespace stl {
+namespace {
+unsigned long long* g_trace = nullptr;
+unsigned long long* g_trace_cta = nullptr;
+int g_trace_n = 0;
+constexpr int kTraceSlots = 4096;
+}  // namespace
+Trace trace_next() {
+  static const int on = probe_env("STL_TRACE", 0);
+  if (!on) return Trace{nullptr, 0, nullptr};
+  if (!g_trace) {
+    cudaMalloc(&g_trace, 2 * kTraceSlots * sizeof(unsigned long long));
+    g_trace_n = kTraceSlots;  // forces a reset before first use
+  }
+  if (g_trace_n >= kTraceSlots) return Trace{nullptr, 0, nullptr};
+  if (!g_trace_cta) cudaMalloc(&g_trace_cta, kTraceCtaSlots * 2048 * 4 * sizeof(unsigned long long));
+  return Trace{g_trace, g_trace_n++, g_trace_cta};
+}
+}  // namespace stl
+
+// probe-only exports (not in include/stl_b200.h): reset the trace slots, read them back
+extern "C" __attribute__((visibility("default"))) int stl_trace_reset(void) {
+  using namespace stl;
+  if (!g_trace) cudaMalloc(&g_trace, 2 * kTraceSlots * sizeof(unsigned long long));
+  static unsigned long long h[2 * kTraceSlots];
+  for (int i = 0; i < kTraceSlots; ++i) { h[2 * i] = ~0ull; h[2 * i + 1] = 0; }
+  g_trace_n = 0;
+  return static_cast<int>(cudaMemcpy(g_trace, h, sizeof(h), cudaMemcpyHostToDevice));
+}
+extern "C" __attribute__((visibility("default"))) int stl_trace_read_cta(unsigned long long* out,
+                                                                         int slot, int grid) {
+  using namespace stl;
+  if (!g_trace_cta || slot >= kTraceCtaSlots) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, g_trace_cta + static_cast<size_t>(slot) * grid * 4, grid * 4 * sizeof(unsigned long long),
+             cudaMemcpyDeviceToHost);
+  return grid;
+}
+extern "C" __attribute__((visibility("default"))) int stl_trace_read(unsigned long long* out, int n) {
+  using namespace stl;
+  if (!g_trace) return 0;
+  const int k = n < g_trace_n ? n : g_trace_n;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, g_trace, 2 * k * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return k;
+}
+#endif

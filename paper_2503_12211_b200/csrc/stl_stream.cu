@@ -152,6 +152,7 @@ struct StreamArgs {
   int hilo;                  // REMIX: coefficients as bf16 hi + lo (1) or hi only (0)
   int bulk_in;               // bf16 input planes: 1-D bulk copies into plain padded rows
   const uint8_t* planes_in;  // the input planes (bulk path)
+  Trace trace;               // probe: launch span
   int bulk_out;              // plane outputs: plain padded staging rows, 1-D bulk stores
   unsigned long long* dbg;   // probe: per-CTA phase timers [grid][4] (ns), or null
 };
@@ -317,6 +318,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   const uint32_t bc = static_cast<uint32_t>(args.bc);
 
   if (threadIdx.x == 0) {
+    trace_mark(args.trace, false);
+    trace_cta(args.trace, 0);
     for (uint32_t s = 0; s < L.nstages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], kGWarps);
@@ -332,6 +335,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   }
   __syncthreads();
   griddep_wait();  // inputs of this launch are complete (PDL)
+  if (threadIdx.x == 0) trace_cta(args.trace, 1);
 
   if (warp == kCWarps) {
     // ---------------------------------------------------------------- producer
@@ -516,6 +520,11 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 #pragma unroll
       for (int k = 0; k < 4; ++k) R[a][b][k] = 0.f;
 
+  uint64_t dbg_c0 = 0, dbg_t0 = 0;
+  if (args.dbg && ctid == 0) {
+    dbg_c0 = clock64();
+    dbg_t0 = ptx::globaltimer_ns();
+  }
   // group grp takes this CTA's units it = grp, grp + 2, ... (stage it % nstages)
   for (uint32_t u = blockIdx.x + grp * gridDim.x, it = grp; u < nunits;
        u += kGroups * gridDim.x, it += kGroups) {
@@ -532,6 +541,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     while (stage_tag[stage] != it) {
     }
     ptx::mbar_wait(&full[stage], phase);
+    if (it == 0 && ctid == 0) trace_cta(args.trace, 2);
     const uint64_t t_w1 = args.dbg ? ptx::globaltimer_ns() : 0;
 
     // The unit's math. Full units (Tw == kT) take a copy with compile-time bounds so the
@@ -856,6 +866,12 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     }
   }
   if (wl == 0) ptx::bulk_wait_all();
+  if (wl == 0 && lane == 0) trace_mark(args.trace, true);
+  if (ctid == 0) trace_cta(args.trace, 3);
+  if (args.dbg && ctid == 0) {  // probe: SM clock over the unit loop (cycles / ns)
+    args.dbg[4 * blockIdx.x + 2] = clock64() - dbg_c0;
+    args.dbg[4 * blockIdx.x + 3] = ptx::globaltimer_ns() - dbg_t0;
+  }
 
   if constexpr (has_red<MODE>()) {
     // per-warp fragments -> smem (the stage ring, once every warp is done with it) ->
@@ -964,6 +980,7 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   a.nocompute = noc;
   static const int hilo = probe_env("STL_REMIX_HILO", 1);
   a.hilo = hilo;
+  a.trace = trace_next();
   a.bulk_in = bulk_in_capable<MODE, ZT>() && bulk_planes_in<MODE>();
   a.planes_in = static_cast<const uint8_t*>(planes_in);
   a.bulk_out = out_planes<MODE>() && bulk_planes_out<MODE>() && !stg;
@@ -986,10 +1003,12 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
     unsigned long long h[4 * 1024];
     cudaMemcpyAsync(h, a.dbg, sizeof(unsigned long long) * 4 * grid, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    double w = 0, c = 0;
-    for (int i = 0; i < grid; ++i) { w += h[4 * i]; c += h[4 * i + 1]; }
-    fprintf(stderr, "[stream dbg] mode=%d T=%d units/cta=%.1f stages=%u  avg us: wait=%.1f math=%.1f\n",
-            MODE, kT, double(a.nunits) / grid, L.nstages, w / grid / 1e3, c / grid / 1e3);
+    double w = 0, c = 0, cyc = 0, ns = 0;
+    for (int i = 0; i < grid; ++i) { w += h[4 * i]; c += h[4 * i + 1]; cyc += h[4 * i + 2]; ns += h[4 * i + 3]; }
+    fprintf(stderr, "[stream dbg] mode=%d T=%d units/cta=%.1f stages=%u  avg us: wait=%.1f math=%.1f "
+            "loop=%.1f  sm_mhz=%.0f\n",
+            MODE, kT, double(a.nunits) / grid, L.nstages, w / grid / 1e3, c / grid / 1e3,
+            ns / grid / 1e3, ns > 0 ? 1e3 * cyc / ns : 0.0);
   }
   if constexpr (has_red<MODE>()) return sum_partials(a.red_partial, static_cast<int>(grid), a.P * 16, red_out, s);
   return cudaSuccess;
