@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <mutex>
+#include <vector>
 #include "sm100_ptx.cuh"
 #include "stl_internal.h"
 
@@ -313,7 +314,22 @@ struct GroupArgs {
   int total0, total;
   int nostore;
   Trace trace;  // probe: launch span
+  // Tile order: rounds of nclusters tiles; -1 = every round left to right (round robin:
+  // tile = cluster + k * nclusters); 0 / 1 = alternating directions (snake; round 0 left to
+  // right when 0); 2 = left to right except the last round. For groups whose tiles have
+  // different K (the backward's g_w and g_u) the host picks the order whose busiest cluster
+  // has the fewest K-blocks (config 2: 352 -> 336 K-blocks against a mean of 332).
+  int order;
 };
+
+// k-th tile of cluster c in the group's order (>= total: done).
+__device__ __forceinline__ int group_tile(const GroupArgs& g, int c, int nc, int k) {
+  bool rev;
+  if (g.order < 0) rev = false;
+  else if (g.order == 2) rev = k == (g.total + nc - 1) / nc - 1;
+  else rev = ((k + g.order) & 1) != 0;
+  return k * nc + (rev ? nc - 1 - c : c);
+}
 
 // Tile `tile` of a group: problem, slice, 256-row block, BN-column block.
 template <int BN>
@@ -560,7 +576,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------------------ TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < total; tile += nclusters) {
+      for (int kk = 0, tile = group_tile(args, cluster, nclusters, 0); tile < total;
+           tile = group_tile(args, cluster, nclusters, ++kk)) {
         const TileCoord<BN> tc(args, tile);
         if (tc.prob == 0)
           tc2_produce<BN, K0, S>(&tmA0, &tmB0, sA, sB, full, empty, stage, phase, tc, prank);
@@ -574,7 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = cluster; tile < total; tile += nclusters, ++it) {
+      for (int kk = 0, tile = group_tile(args, cluster, nclusters, 0); tile < total;
+           tile = group_tile(args, cluster, nclusters, ++kk), ++it) {
         const TileCoord<BN> tc(args, tile);
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
@@ -595,7 +613,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int chunk_no = 0;
     int it = 0;
     uint8_t* stage_base = smem + S::kRing;
-    for (int tile = cluster; tile < total; tile += nclusters, ++it) {
+    for (int kk = 0, tile = group_tile(args, cluster, nclusters, 0); tile < total;
+         tile = group_tile(args, cluster, nclusters, ++kk), ++it) {
       const TileCoord<BN> tc(args, tile);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
@@ -780,6 +799,27 @@ cudaError_t launch_tc2_group(const SliceGemmProblem* pbs, int np, cudaStream_t s
   ga.r = pbs[0].r;
   ga.total0 = static_cast<int>(t0);
   ga.total = static_cast<int>(tiles);
+  ga.order = -1;
+  if (np > 1 && pbs[0].K != pbs[1].K && probe_env("STL_GEMM_ORDER", 1)) {
+    // per-cluster K-block load of each order; keep the best (ties: round robin)
+    const int64_t kb0 = (pbs[0].K + kBK - 1) / kBK, kb1 = (pbs[1].K + kBK - 1) / kBK;
+    const int64_t rounds = (tiles + clusters - 1) / clusters;
+    int64_t best = -1;
+    for (int order = -1; order <= 2; ++order) {
+      std::vector<int64_t> load(clusters, 0);
+      for (int c = 0; c < clusters; ++c)
+        for (int64_t k = 0; k < rounds; ++k) {
+          const bool rev = order < 0 ? false : order == 2 ? k == rounds - 1 : ((k + order) & 1) != 0;
+          const int64_t t = k * clusters + (rev ? clusters - 1 - c : c);
+          if (t < tiles) load[c] += t < t0 ? kb0 : kb1;
+        }
+      const int64_t mx = *std::max_element(load.begin(), load.end());
+      if (best < 0 || mx < best) {
+        best = mx;
+        ga.order = order;
+      }
+    }
+  }
   ga.nostore = probe_env("STL_GEMM_NOSTORE", 0);
   ga.trace = trace_next();
   if (probe_env("STL_GEMM_VERBOSE", 0))
