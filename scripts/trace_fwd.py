@@ -85,3 +85,16 @@ for slot in (3 * 2, 3 * 2 + 2, 3 * 3, 3 * 3 + 2):  # encode / decode of forwards
         out[nm] = [round(v[0], 1), round(v[len(v) // 2], 1), round(v[-1], 1)]
     print(json.dumps({"slot": slot, "kernel": "encode" if slot % 3 == 0 else "decode",
                       "us_after_predecessor_end_min_med_max": out}), flush=True)
+
+# which CTAs straggle? (encode of forward 3: blockIdx -> loop end after the predecessor's end)
+if os.environ.get("TRACE_CTA_DUMP"):
+    lib.stl_trace_read_cta(cta, 9, grid)
+    pred_end = buf[2 * 8 + 1]
+    ends = sorted(((cta[4 * c + 3] - pred_end) / 1e3, c) for c in range(grid))
+    print(json.dumps({"encode_loop_end_latest": [(round(t, 1), c) for t, c in ends[-12:]],
+                      "earliest": [(round(t, 1), c) for t, c in ends[:6]]}), flush=True)
+    lib.stl_trace_read_cta(cta, 11, grid)
+    pred_end = buf[2 * 10 + 1]
+    ends = sorted(((cta[4 * c + 3] - pred_end) / 1e3, c) for c in range(grid))
+    print(json.dumps({"decode_loop_end_latest": [(round(t, 1), c) for t, c in ends[-12:]],
+                      "earliest": [(round(t, 1), c) for t, c in ends[:6]]}), flush=True)
