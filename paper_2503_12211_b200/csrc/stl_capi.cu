@@ -500,31 +500,26 @@ int stl_fused_step_ex(const void* x_prev, int x_prev_dtype, int64_t block_rows, 
   if (block_rows < 0 || block_k < 0 || block_n < 0) return fail(STL_ERR_SHAPE, "negative extent");
   cudaStream_t s = as_stream(stream);
   int st;
-  // bf16 chain: the streaming tensor-core remix (planes in, planes out, one HBM pass; it reads
-  // C^T, so the composite is built transposed); else the generic kernel
-  const bool streamed = dtype == STL_BF16 && r <= 32 && block_k % 64 == 0;
-  {
-    Prof prof("compose", s);
-    st = check_cuda(streamed ? stl::compose_coefs(d, e_x, r, t * t, comp_ws, s)
-                             : stl::compose_coefs(e_x, d, r, t * t, comp_ws, s),
-                    "compose");
-  }
-  if (st) return st;
-  {
+  // bf16 chain: the streaming tensor-core remix forms the composite e_x d^T itself (planes in,
+  // planes out, one HBM pass, no extra launch between the two slice GEMMs); else the composite
+  // kernel + the generic remix
+  cudaError_t e = cudaErrorNotSupported;
+  if (dtype == STL_BF16 && t == 4 && r <= 32 && block_k % 64 == 0) {  // composite of 16-wide rows
     Prof prof("remix", s);
-    cudaError_t e = cudaErrorNotSupported;
-    if (streamed)
-      e = stl::planes_to_planes_stream(x_prev, x_prev_dtype, r, block_rows, block_k, comp_ws,
-                                       mixed_ws, s);
-    if (e == cudaErrorNotSupported) {
-      if (streamed)  // declined (alignment): the generic kernel wants C, not C^T
-        st = check_cuda(stl::compose_coefs(e_x, d, r, t * t, comp_ws, s), "compose");
-      if (st) return st;
-      e = stl::planes_to_planes(x_prev, x_prev_dtype, r, block_rows * block_k, comp_ws, r,
-                                mixed_ws, dtype, s);
-    }
-    st = check_cuda(e, "fused-step remix");
+    e = stl::planes_to_planes_stream(x_prev, x_prev_dtype, r, block_rows, block_k, e_x, d,
+                                     mixed_ws, s);
   }
+  if (e == cudaErrorNotSupported) {
+    {
+      Prof prof("compose", s);
+      st = check_cuda(stl::compose_coefs(e_x, d, r, t * t, comp_ws, s), "compose");
+    }
+    if (st) return st;
+    Prof prof("remix", s);
+    e = stl::planes_to_planes(x_prev, x_prev_dtype, r, block_rows * block_k, comp_ws, r, mixed_ws,
+                              dtype, s);
+  }
+  st = check_cuda(e, "fused-step remix");
   if (st) return st;
   return run_gemm(mixed_ws, STL_K_MAJOR, w_enc, STL_K_MAJOR, out, out_dtype, dtype, r, block_rows,
                   block_n, block_k, s);

@@ -179,9 +179,9 @@ cudaError_t tiles_to_planes2(const void* m, int mdt, int64_t ldm, int64_t br, in
 cudaError_t planes_to_tiles2(const void* in, int idt, int Q, int64_t br, int64_t bc,
                              const float* coef, void* out, int odt, int64_t ldo, cudaStream_t s);
 // Fused-chain remix (stl_stream.cu kRemix): P <= 32 bf16 / fp32 planes -> bf16 planes,
-// out[p] = sum_q coef_t[q * P + p] in[q]; tile columns % 64 == 0.
+// out[p] = sum_q C[p][q] in[q], C = e_x d^T formed in-kernel; tile columns % 64 == 0.
 cudaError_t planes_to_planes_stream(const void* in, int idt, int P, int64_t br, int64_t bc,
-                                    const float* coef_t, void* out, cudaStream_t s);
+                                    const float* e_x, const float* d, void* out, cudaStream_t s);
 // out[o] = sum_b partial[b * n + o], deterministic fixed-order tree.
 cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t s);
 cudaError_t compose_coefs(const float* a, const float* b, int r, int tt, float* out,

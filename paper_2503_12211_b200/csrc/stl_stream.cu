@@ -138,7 +138,8 @@ struct StreamArgs {
   int64_t ldm;
   void* out;                 // DEC*: output matrix (ENC* planes go out through tm_out)
   int64_t ldo;
-  const float* coef;         // P x 16 (encoder rows for ENC*, decoder rows for DEC*)
+  const float* coef;         // P x 16 (encoder rows for ENC*, decoder rows for DEC*; REMIX: e_x)
+  const float* coef2;        // REMIX: d (P x 16); the composite C = e_x d^T is formed in-kernel
   float* red_partial;        // [gridDim.x][P * 16]
   int P;
   int Pb;                    // planes in the (zero-padded) input plane box
@@ -328,6 +329,19 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     ptx::fence_mbar_init();
   }
   griddep_launch_dependents();
+  if constexpr (MODE == kRemix) {
+    // the fused-step composite C = e_x d^T (P x P, fp32) into the (not yet used) output staging;
+    // the consumers read their B fragments from it (a named barrier after the fragment setup
+    // keeps the staging untouched until every consumer has them)
+    float* sC = reinterpret_cast<float*>(smem + s_out);
+    for (int i = threadIdx.x; i < P * P; i += blockDim.x) {
+      const int pp = i / P, qq = i - (i / P) * P;
+      float v = 0.f;
+  #pragma unroll
+      for (int kk = 0; kk < 16; ++kk) v = fmaf(args.coef[pp * 16 + kk], args.coef2[qq * 16 + kk], v);
+      sC[i] = v;
+    }
+  }
   if (warp == kCWarps && lane == 0) {
     if constexpr (has_planes_in<MODE>()) ptx::prefetch_tmap(&tm_in);
     if constexpr (kZ24) ptx::prefetch_tmap(&tm_in2);
@@ -413,6 +427,16 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   static_assert(MODE != kRemix || (NTR >= 1 && NTR <= 2 * MT), "remix n-tiles");
   const int CS = MODE == kRemix ? P : 16;            // coefficient row stride
   const int NC = MODE == kRemix ? P : 16;            // valid output columns (zero past them)
+  // B coefficient (k = input plane / tile value pa, n = output column c): DEC: D[pa][c];
+  // REMIX: C^T[pa][c] = C[c][pa], C = e_x d^T formed at kernel start (no separate launch
+  // between the previous slice GEMM and this one)
+  auto bcoef = [&](int pa, int c) -> float {
+    if constexpr (MODE == kRemix) {
+      return reinterpret_cast<const float*>(smem + s_out)[c * P + pa];
+    } else {
+      return args.coef[pa * CS + c];
+    }
+  };
   uint32_t fh[MT][is_enc<MODE>() ? 4 : 2 * kNT], fl[MT][is_enc<MODE>() ? 4 : 2 * kNT];
   if constexpr (is_enc<MODE>()) {
 #pragma unroll
@@ -431,8 +455,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
       for (int i = 0; i < 2 * kNT; ++i) {  // i = nt * 2 + h
         const int nt = i >> 1, h = i & 1, c = 8 * nt + g;
         const int pa = 16 * ks + 2 * q + 8 * h, pb = pa + 1;
-        const float d0 = pa < P && c < NC ? args.coef[pa * CS + c] : 0.f;
-        const float d1 = pb < P && c < NC ? args.coef[pb * CS + c] : 0.f;
+        const float d0 = pa < P && c < NC ? bcoef(pa, c) : 0.f;
+        const float d1 = pb < P && c < NC ? bcoef(pb, c) : 0.f;
         split2(d0, d1, fh[ks][i], fl[ks][i]);
       }
   }
@@ -499,7 +523,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int pl = 8 * s8 + 2 * q + h, c = 8 * nt + g;
-        bt[s8][nt][h] = (!is_enc<MODE>() && kTf32 && pl < P && c < NC) ? tf32_rna(args.coef[pl * CS + c]) : 0u;
+        bt[s8][nt][h] = (!is_enc<MODE>() && kTf32 && pl < P && c < NC) ? tf32_rna(bcoef(pl, c)) : 0u;
       }
   // REMIX: C stores at buf + ro[k][h] + 1024 nt (output plane 8nt + 2q + h, tiles t0, t0 + 1)
   uint32_t ro[kMK][2];
@@ -520,6 +544,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 #pragma unroll
       for (int k = 0; k < 4; ++k) R[a][b][k] = 0.f;
 
+  if constexpr (MODE == kRemix) cbar<kCThreads>();  // composite fragments read: staging free
   uint64_t dbg_c0 = 0, dbg_t0 = 0;
   if (args.dbg && ctid == 0) {
     dbg_c0 = clock64();
@@ -1123,15 +1148,16 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
   return launch<kDec, __nv_bfloat16>(a, in, nullptr, nullptr, s);
 }
 
-// the fused-chain remix: r bf16 or fp32 planes -> r bf16 planes, out[p] = sum_q coef_t[q][p] in[q]
-// (coef_t = C^T, r x r row-major). r <= 32.
+// the fused-chain remix: r bf16 or fp32 planes -> r bf16 planes, out[p] = sum_q C[p][q] in[q] with
+// C = e_x d^T formed in-kernel (e_x, d: r x 16). r <= 32.
 cudaError_t planes_to_planes_stream(const void* in, int idt, int P, int64_t br, int64_t bc,
-                                    const float* coef_t, void* out, cudaStream_t s) {
+                                    const float* e_x, const float* d, void* out, cudaStream_t s) {
   if ((idt != kBF16 && idt != kF32) || bc % 64 || P < 1 || P > 32 || !al16(in) || !al16(out))
     return cudaErrorNotSupported;
   StreamArgs a{};
   a.out = out;
-  a.coef = coef_t;
+  a.coef = e_x;
+  a.coef2 = d;
   a.P = P;
   a.br = br;
   a.bc = bc;

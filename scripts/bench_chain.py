@@ -4,7 +4,9 @@ slice GEMMs -> decode each), CUDA-event timed, plus the reference cost model's I
 (io_fused_chain vs layers * io_square, cost_model.py:94-124). One JSON line."""
 import json
 import os
+import statistics
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
@@ -13,7 +15,7 @@ import paper_2503_12211_b200 as stl  # noqa: E402
 from paper_2503_12211_b200 import _lib  # noqa: E402
 
 
-def chain_bench(n=8192, t=4, r=24, layers=3, iters=10):
+def chain_bench(n=8192, t=4, r=24, layers=3, iters=3):
     lib = _lib.load()
     dev = torch.device("cuda")
     s = torch.cuda.current_stream().cuda_stream
@@ -54,24 +56,28 @@ def chain_bench(n=8192, t=4, r=24, layers=3, iters=10):
         _lib.check(lib.stl_decode(h[(layers - 1) % 2].data_ptr(), _lib.STL_BF16, b, b, r,
                                   snf.d.data_ptr(), t, yf.data_ptr(), _lib.STL_BF16, n, s))
 
-    def timed(fn):
-        for _ in range(3):
+    def timed(fn, k):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(k):
             fn()
-        best = None
-        for _ in range(3):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record()
-            for _ in range(iters):
-                fn()
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / iters
-            best = ms if best is None else min(best, ms)
-        return best
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / k
 
-    u_ms = timed(unfused)
-    f_ms = timed(fused)
+    # alternating short blocks after idle (both at unthrottled clocks, like bench.py's north
+    # star), medians
+    for _ in range(3):
+        unfused()
+        fused()
+    ub, fb = [], []
+    for _ in range(7):
+        time.sleep(0.06)
+        ub.append(timed(unfused, iters))
+        time.sleep(0.06)
+        fb.append(timed(fused, iters))
+    u_ms, f_ms = statistics.median(ub), statistics.median(fb)
     unfused()
     fused()
     torch.cuda.synchronize()
@@ -87,6 +93,8 @@ def chain_bench(n=8192, t=4, r=24, layers=3, iters=10):
     io_l = stl.io_square(n, t, r, 2)
     io_chain = stl.io_fused_chain(n, t, r, layers, 2)
     return {"n": n, "t": t, "r": r, "layers": layers, "dtype": "bf16",
+            "timing": f"7 alternating blocks of {iters} chains (separate forwards, fused), each "
+                      "after 60 ms idle, medians",
             "unfused_ms": u_ms, "fused_chain_ms": f_ms, "speedup": u_ms / f_ms,
             "rel_diff_fused_vs_unfused": err,
             "remix_us": remix_us, "remix_GBs": remix_bytes / (remix_us * 1e-6) / 1e9,
