@@ -150,6 +150,8 @@ struct StreamArgs {
   int64_t prow;              // tile rows between planes (>= br: a row band of taller planes)
   int stg;                   // 1: consumers write outputs with st.global (else TMA/bulk stores)
   int nocompute;             // probe: skip the math (pure data movement)
+  int contig;                // probe (with nocompute): each unit's planes as ONE contiguous
+                             // block (a unit-blocked plane layout), one bulk copy
   int hilo;                  // REMIX: coefficients as bf16 hi + lo (1) or hi only (0)
   int bulk_in;               // bf16 input planes: 1-D bulk copies into plain padded rows
   const uint8_t* planes_in;  // the input planes (bulk path)
@@ -387,10 +389,16 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
         if (bin) {
           // one bulk copy per plane: the unit's Tw tiles (contiguous also for R > 1)
           __syncwarp();  // the expect_tx above precedes the copies' complete_tx
-          for (int p = lane; p < P; p += 32)
-            bulk_g2s(sbase + st + p * bulk_plane_stride<kT>(),
-                     args.planes_in + 2 * ((static_cast<int64_t>(p) * args.prow + I) * bc + J0),
-                     Tw * 2, &full[stage]);
+          if (args.contig) {
+            if (lane == 0)
+              bulk_g2s(sbase + st, args.planes_in + 2 * static_cast<int64_t>(u) * P * kT, P * Tw * 2,
+                       &full[stage]);
+          } else {
+            for (int p = lane; p < P; p += 32)
+              bulk_g2s(sbase + st + p * bulk_plane_stride<kT>(),
+                       args.planes_in + 2 * ((static_cast<int64_t>(p) * args.prow + I) * bc + J0),
+                       Tw * 2, &full[stage]);
+          }
         }
       }
       if constexpr (has_rows<MODE>()) {
@@ -588,7 +596,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
             for (int m = 0; m < MT; ++m) {
               float c[4] = {0.f, 0.f, 0.f, 0.f};
               mma(c, fh[m][0], fh[m][1], fh[m][2], fh[m][3], b0, b1);
-              mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0, b1);
+              if (args.hilo) mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0, b1);
               const uint32_t o = buf + soff[k] + 16 * m * PSo;
               if (m < MT - 1 || lastp0) sts32(o, pack2(c[0], c[1]));
               if (m < MT - 1 || lastp1) sts32(o + 8 * PSo, pack2(c[2], c[3]));
@@ -653,7 +661,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   #pragma unroll
                 for (int nt = 0; nt < kNT; ++nt) {
                   mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
-                  if (MODE != kRemix || args.hilo)
+                  if (args.hilo)
                     mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
                 }
                 continue;
@@ -869,10 +877,16 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
         if (bout) {
           // one bulk store per plane: the unit's Tw tiles of tile row I (contiguous also for
           // R > 1: whole tile rows)
-          for (int p = lane; p < P; p += 32)
-            bulk_s2g(static_cast<__nv_bfloat16*>(args.out) +
-                         (static_cast<int64_t>(p) * args.prow + I) * bc + J0,
-                     sbase + buf + p * PS, static_cast<uint32_t>(Tw) * 2);
+          if (args.contig) {
+            if (lane == 0)
+              bulk_s2g(static_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(u) * P * kT,
+                       sbase + buf, static_cast<uint32_t>(P * Tw * 2));
+          } else {
+            for (int p = lane; p < P; p += 32)
+              bulk_s2g(static_cast<__nv_bfloat16*>(args.out) +
+                           (static_cast<int64_t>(p) * args.prow + I) * bc + J0,
+                       sbase + buf + p * PS, static_cast<uint32_t>(Tw) * 2);
+          }
         } else if (lane == 0) {
           tma_store_4d(&tm_out, sbase + buf, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
         }
@@ -1003,7 +1017,9 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   a.stg = stg;
   static const int noc = probe_env("STL_STREAM_NOCOMPUTE", 0);
   a.nocompute = noc;
-  static const int hilo = probe_env("STL_REMIX_HILO", 1);
+  static const int contig = probe_env("STL_PROBE_CONTIG", 0);
+  a.contig = contig && noc;
+  static const int hilo = probe_env("STL_HILO", 1);  // probe 0: bf16 hi coefficients only
   a.hilo = hilo;
   a.trace = trace_next();
   a.bulk_in = bulk_in_capable<MODE, ZT>() && bulk_planes_in<MODE>();
