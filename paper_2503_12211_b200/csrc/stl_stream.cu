@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 
   // ------------------------------------------------------------------ consumers
   const int ctid = threadIdx.x;
-  const uint32_t RS = L.row_stride;
+  constexpr uint32_t RS = kT * 4 * 2 + kRowPad;  // == L.row_stride (compile-time: folds into offsets)
   constexpr int kNK = kT / (8 * kGWarps);    // ENC n-tile rounds per warp
   constexpr int kMK = kT / (16 * kGWarps);   // DEC m-tile / RED k-step rounds per warp
   const int grp = warp / kGWarps, wl = warp % kGWarps;  // group, warp within the group
