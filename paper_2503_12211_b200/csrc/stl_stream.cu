@@ -1015,7 +1015,9 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   if (probe_env("STL_SMEM_MAX_CARVEOUT", 0))
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   a.stg = stg;
-  static const int noc = probe_env("STL_STREAM_NOCOMPUTE", 0);
+  // probe: 1 = every mode skips its math; a bit mask 2 / 4 / 8 / 16 selects the modes (<< MODE)
+  static const int noc_env = probe_env("STL_STREAM_NOCOMPUTE", 0);
+  const int noc = noc_env == 1 ? 1 : ((noc_env >> (MODE + 1)) & 1);
   a.nocompute = noc;
   static const int contig = probe_env("STL_PROBE_CONTIG", 0);
   a.contig = contig && noc;
