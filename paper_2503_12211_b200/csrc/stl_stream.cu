@@ -153,6 +153,8 @@ struct StreamArgs {
   int contig;                // probe (with nocompute): each unit's planes as ONE contiguous
                              // block (a unit-blocked plane layout), one bulk copy
   int hilo;                  // REMIX: coefficients as bf16 hi + lo (1) or hi only (0)
+  int dec_tf32;              // DEC / DEC_RED / REMIX, bf16 planes: single-pass TF32 MMAs (k8 steps
+                             // over exactly the Pb planes, no PRMT regrouping), not bf16 hi + lo
   int bulk_in;               // bf16 input planes: 1-D bulk copies into plain padded rows
   const uint8_t* planes_in;  // the input planes (bulk path)
   Trace trace;               // probe: launch span
@@ -531,7 +533,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int pl = 8 * s8 + 2 * q + h, c = 8 * nt + g;
-        bt[s8][nt][h] = (!is_enc<MODE>() && kTf32 && pl < P && c < NC) ? tf32_rna(bcoef(pl, c)) : 0u;
+        bt[s8][nt][h] = (!is_enc<MODE>() && (kTf32 || args.dec_tf32) && pl < P && c < NC)
+                            ? tf32_rna(bcoef(pl, c)) : 0u;
       }
   // REMIX: C stores at buf + ro[k][h] + 1024 nt (output plane 8nt + 2q + h, tiles t0, t0 + 1)
   uint32_t ro[kMK][2];
@@ -635,6 +638,26 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                   mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
               }
             } else {
+            bool tf32_done = false;
+            if constexpr (!is_enc<MODE>() && ZSZ == 2 && !kZ24) {
+              if (args.dec_tf32) {
+                // bf16 planes through m16n8k8 TF32 (as the fp32-plane path): one 4-byte load
+                // holds plane 8s + 2q (+1) at tiles t0, t0 + 1; bf16 -> tf32 is exact (<< 16)
+  #pragma unroll
+                for (int s8 = 0; s8 < KS8; ++s8) {
+                  if (8 * s8 >= Pb) break;  // warp-uniform; planes P..Pb-1 are zero in the box
+                  const uint32_t w0 = lds32(planes + da[k][0] + 8 * s8 * PSi);
+                  const uint32_t w1 = lds32(planes + da[k][1] + 8 * s8 * PSi);
+                  const uint32_t a0 = w0 << 16, a1 = w0 & 0xFFFF0000u;
+                  const uint32_t a2 = w1 << 16, a3 = w1 & 0xFFFF0000u;
+  #pragma unroll
+                  for (int nt = 0; nt < kNT; ++nt)
+                    mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
+                }
+                tf32_done = true;
+              }
+            }
+            if (!tf32_done) {
   #pragma unroll
             for (int ks = 0; ks < MT; ++ks) {
               if constexpr (ZSZ == 2 && !kZ24) {
@@ -713,6 +736,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                 }
               }
             }
+            }  // !tf32_done
             }  // bf16 planes
             if constexpr (MODE == kRemix) {
               // acc[nt][0] / [2] -> output plane 8nt + 2q at tiles t0 / t0 + 1, [1] / [3] -> plane
@@ -1023,6 +1047,12 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   a.contig = contig && noc;
   static const int hilo = probe_env("STL_HILO", 1);  // probe 0: bf16 hi coefficients only
   a.hilo = hilo;
+  // bf16-plane decodes (decode, g_x decode-reduction, remix) on single-pass TF32 MMAs: 8192^3
+  // decode 62.4 -> 59.1 us, forward -2..4 us, config-2 step -0.5% (profiles/r02_dec_tf32_ab.log);
+  // coefficient rounding 2^-11 (the bf16 output rounding is 2^-9)
+  static const int dec_tf32_env = probe_env("STL_DEC_TF32", -1);
+  a.dec_tf32 = !is_enc<MODE>() && std::is_same<ZT, __nv_bfloat16>::value &&
+               (dec_tf32_env < 0 ? (MODE == kDec || MODE == kDecRed || MODE == kRemix) : dec_tf32_env != 0);
   a.trace = trace_next();
   a.bulk_in = bulk_in_capable<MODE, ZT>() && bulk_planes_in<MODE>();
   a.planes_in = static_cast<const uint8_t*>(planes_in);
