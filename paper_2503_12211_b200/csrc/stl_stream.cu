@@ -194,6 +194,18 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, uint32_t src,
       "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// The stage tags are a flag protocol (one writer, spinning readers) done with shared-memory
+// atomics — formally race-free, and racecheck-clean — by one lane per warp (the warp then
+// reconverges), so a unit costs each consumer warp one atomic when the tag is already set.
+__device__ __forceinline__ void tag_store(volatile uint32_t* p, uint32_t v) {
+  atomicExch(const_cast<uint32_t*>(p), v);
+}
+__device__ __forceinline__ void tag_wait(volatile uint32_t* p, uint32_t v, int lane) {
+  if (lane == 0)
+    while (atomicAdd(const_cast<uint32_t*>(p), 0u) != v) {
+    }
+  __syncwarp();
+}
 template <int NT>
 __device__ __forceinline__ void cbar() {
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
@@ -328,7 +340,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     for (uint32_t s = 0; s < L.nstages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], kGWarps);
-      stage_tag[s] = 0xFFFFFFFFu;
+      tag_store(stage_tag + s, 0xFFFFFFFFu);
     }
     ptx::fence_mbar_init();
   }
@@ -370,7 +382,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
       const uint32_t nrows = urows > 1 ? min(static_cast<uint32_t>(urows), br - I) : 1u;
       const uint32_t Tw = urows > 1 ? nrows * bc : min(bc - J0, static_cast<uint32_t>(kT));
       ptx::mbar_wait(&empty[stage], phase ^ 1);
-      if (lane == 0) stage_tag[stage] = it;  // before the expect_tx arrive (release) below
+      if (lane == 0) tag_store(stage_tag + stage, it);  // before the expect_tx arrive (release) below
       const uint32_t rows_b = has_rows<MODE>() ? Tw * 8 : 0;
       const uint32_t st = s_stages + stage * L.stage_bytes;
       const bool bin = bulk_in_capable<MODE, ZT>() && args.bulk_in;
@@ -574,8 +586,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     const uint32_t planes = s_stages + stage * L.stage_bytes;
     const uint32_t rows = planes + L.pl_bytes;
     const uint64_t t_w0 = args.dbg ? ptx::globaltimer_ns() : 0;
-    while (stage_tag[stage] != it) {
-    }
+    tag_wait(stage_tag + stage, it, lane);
     ptx::mbar_wait(&full[stage], phase);
     if (it == 0 && ctid == 0) trace_cta(args.trace, 2);
     const uint64_t t_w1 = args.dbg ? ptx::globaltimer_ns() : 0;
