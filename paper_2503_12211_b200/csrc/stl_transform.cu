@@ -246,16 +246,16 @@ __global__ void __launch_bounds__(kTB)
   extern __shared__ float sm[];
   for (int i = threadIdx.x; i < P * Q; i += kTB) sm[i] = coef[i];
   __syncthreads();
+  // (the generic fallback of the fused-step remix: fp32 chains, r > 32, odd tile columns)
+  // No per-thread array indexed by a runtime rank (it would live in local memory): each output
+  // re-reads the thread's Q inputs, which stay in L1 after the first output.
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * kTB + threadIdx.x; idx < ntiles;
        idx += static_cast<int64_t>(gridDim.x) * kTB) {
-    float v[kMaxRank];
-#pragma unroll 4
-    for (int q = 0; q < Q; ++q) v[q] = to_f(in[q * ntiles + idx]);
     for (int p = 0; p < P; ++p) {
       float acc = 0.f;
       const float* cp = sm + p * Q;
 #pragma unroll 4
-      for (int q = 0; q < Q; ++q) acc = fmaf(cp[q], v[q], acc);
+      for (int q = 0; q < Q; ++q) acc = fmaf(cp[q], to_f(in[q * ntiles + idx]), acc);
       out[p * ntiles + idx] = from_f<Tout>(acc);
     }
   }
