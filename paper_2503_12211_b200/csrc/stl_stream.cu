@@ -153,8 +153,7 @@ struct StreamArgs {
   int contig;                // probe (with nocompute): each unit's planes as ONE contiguous
                              // block (a unit-blocked plane layout), one bulk copy
   int hilo;                  // REMIX: coefficients as bf16 hi + lo (1) or hi only (0)
-  int dec_tf32;              // DEC / DEC_RED / REMIX, bf16 planes: single-pass TF32 MMAs (k8 steps
-                             // over exactly the Pb planes, no PRMT regrouping), not bf16 hi + lo
+
   int bulk_in;               // bf16 input planes: 1-D bulk copies into plain padded rows
   const uint8_t* planes_in;  // the input planes (bulk path)
   Trace trace;               // probe: launch span
@@ -325,6 +324,11 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
+#ifdef STL_PROBES
+  const bool hilo = args.hilo != 0;  // probe: bf16 hi coefficients only
+#else
+  constexpr bool hilo = true;  // the product build never drops the lo coefficient halves
+#endif
   const int P = args.P, Pb = args.Pb;
   constexpr int ZSZ = zhi<ZT>();         // bytes of the (high) plane element
   constexpr bool kZ24 = is_f24<ZT>();
@@ -536,6 +540,11 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   // DEC B = D with k = q <-> plane 8s + 2q, k = q + 4 <-> plane 8s + 2q + 1 (the planes a
   // thread loads, see below): bt[s][nt][0] = D[8s+2q][8nt+g], bt[s][nt][1] = D[8s+2q+1][8nt+g].
   constexpr bool kTf32 = ZSZ == 4 || kZ24;
+  // bf16-plane decode and remix on single-pass TF32 m16n8k8 MMAs over exactly the Pb planes (no
+  // PRMT regrouping; coefficients rounded to tf32, 2^-11): 8192^3 decode 62.5 -> 59.1 us, the
+  // remix -5 us (profiles/r02_dec_tf32_ab.log). Compile-time per mode: the g_x decode-reduction
+  // keeps bf16 hi + lo (no gain there, and both fragment sets live at once spilled registers).
+  constexpr bool kTf32Dec = (MODE == kDec || MODE == kRemix) && ZSZ == 2 && !kZ24;
   constexpr int KS8 = 2 * MT;
   uint32_t bt[KS8][kNT][2];
 #pragma unroll
@@ -545,7 +554,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int pl = 8 * s8 + 2 * q + h, c = 8 * nt + g;
-        bt[s8][nt][h] = (!is_enc<MODE>() && (kTf32 || args.dec_tf32) && pl < P && c < NC)
+        bt[s8][nt][h] = (!is_enc<MODE>() && (kTf32 || kTf32Dec) && pl < P && c < NC)
                             ? tf32_rna(bcoef(pl, c)) : 0u;
       }
   // REMIX: C stores at buf + ro[k][h] + 1024 nt (output plane 8nt + 2q + h, tiles t0, t0 + 1)
@@ -610,7 +619,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
             for (int m = 0; m < MT; ++m) {
               float c[4] = {0.f, 0.f, 0.f, 0.f};
               mma(c, fh[m][0], fh[m][1], fh[m][2], fh[m][3], b0, b1);
-              if (args.hilo) mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0, b1);
+              if (hilo) mma(c, fl[m][0], fl[m][1], fl[m][2], fl[m][3], b0, b1);
               const uint32_t o = buf + soff[k] + 16 * m * PSo;
               if (m < MT - 1 || lastp0) sts32(o, pack2(c[0], c[1]));
               if (m < MT - 1 || lastp1) sts32(o + 8 * PSo, pack2(c[2], c[3]));
@@ -649,9 +658,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                   mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
               }
             } else {
-            bool tf32_done = false;
-            if constexpr (!is_enc<MODE>() && ZSZ == 2 && !kZ24) {
-              if (args.dec_tf32) {
+            if constexpr (kTf32Dec) {
+              {
                 // bf16 planes through m16n8k8 TF32 (as the fp32-plane path): one 4-byte load
                 // holds plane 8s + 2q (+1) at tiles t0, t0 + 1; bf16 -> tf32 is exact (<< 16)
   #pragma unroll
@@ -665,10 +673,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                   for (int nt = 0; nt < kNT; ++nt)
                     mma_tf32(acc[nt], a0, a1, a2, a3, bt[s8][nt][0], bt[s8][nt][1]);
                 }
-                tf32_done = true;
               }
-            }
-            if (!tf32_done) {
+            } else {
   #pragma unroll
             for (int ks = 0; ks < MT; ++ks) {
               if constexpr (ZSZ == 2 && !kZ24) {
@@ -688,14 +694,14 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   #pragma unroll
                   for (int nt = 0; nt < kNT; ++nt) {
                     mma_k8(acc[nt], a0, a1, fh[ks][2 * nt]);
-                    if (args.hilo) mma_k8(acc[nt], a0, a1, fl[ks][2 * nt]);
+                    if (hilo) mma_k8(acc[nt], a0, a1, fl[ks][2 * nt]);
                   }
                   continue;
                 }
   #pragma unroll
                 for (int nt = 0; nt < kNT; ++nt) {
                   mma(acc[nt], a0, a1, a2, a3, fh[ks][2 * nt], fh[ks][2 * nt + 1]);
-                  if (args.hilo)
+                  if (hilo)
                     mma(acc[nt], a0, a1, a2, a3, fl[ks][2 * nt], fl[ks][2 * nt + 1]);
                 }
                 continue;
@@ -747,7 +753,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
                 }
               }
             }
-            }  // !tf32_done
+            }  // !kTf32Dec
             }  // bf16 planes
             if constexpr (MODE == kRemix) {
               // acc[nt][0] / [2] -> output plane 8nt + 2q at tiles t0 / t0 + 1, [1] / [3] -> plane
@@ -1058,12 +1064,6 @@ cudaError_t launch_mt(StreamArgs a, const void* planes_in, void* planes_out, flo
   a.contig = contig && noc;
   static const int hilo = probe_env("STL_HILO", 1);  // probe 0: bf16 hi coefficients only
   a.hilo = hilo;
-  // bf16-plane decodes (decode, g_x decode-reduction, remix) on single-pass TF32 MMAs: 8192^3
-  // decode 62.4 -> 59.1 us, forward -2..4 us, config-2 step -0.5% (profiles/r02_dec_tf32_ab.log);
-  // coefficient rounding 2^-11 (the bf16 output rounding is 2^-9)
-  static const int dec_tf32_env = probe_env("STL_DEC_TF32", -1);
-  a.dec_tf32 = !is_enc<MODE>() && std::is_same<ZT, __nv_bfloat16>::value &&
-               (dec_tf32_env < 0 ? (MODE == kDec || MODE == kDecRed || MODE == kRemix) : dec_tf32_env != 0);
   a.trace = trace_next();
   a.bulk_in = bulk_in_capable<MODE, ZT>() && bulk_planes_in<MODE>();
   a.planes_in = static_cast<const uint8_t*>(planes_in);
