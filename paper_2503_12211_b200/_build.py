@@ -23,7 +23,7 @@ PROBE_LIB_PATH = PKG / "libstl_b200_probe.so"
 
 SOURCES = ["stl_capi.cu", "stl_slice_gemm.cu", "stl_transform.cu", "stl_transform2.cu",
            "stl_transform4.cu",
-           "stl_transform_mma.cu", "stl_stream.cu", "stl_tokens.cu"]
+           "stl_transform_mma.cu", "stl_stream.cu", "stl_stream_tc.cu", "stl_tokens.cu"]
 HEADERS = ["sm100_ptx.cuh", "sm100_pair_pipeline.cuh", "stl_internal.h"]
 
 NVCC_FLAGS = [

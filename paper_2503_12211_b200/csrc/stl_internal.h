@@ -178,6 +178,19 @@ cudaError_t tiles_to_planes2(const void* m, int mdt, int64_t ldm, int64_t br, in
                              const float* coef, int P, void* out, int odt, cudaStream_t s);
 cudaError_t planes_to_tiles2(const void* in, int idt, int Q, int64_t br, int64_t bc,
                              const float* coef, void* out, int odt, int64_t ldo, cudaStream_t s);
+// 4-D plane-box tensor map of the streaming transforms (stl_stream.cu): box {128 / zsz tiles,
+// Pb planes, kT * zsz / 128 chunks, 1 tile row}, 128-byte swizzle; prow >= br tile rows per plane.
+bool plane_box_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_t br,
+                    int64_t bc, int kT, int64_t prow);
+// t = 4 decode on tcgen05 (stl_stream_tc.cu): P <= 32 bf16 planes -> bf16 matrix;
+// cudaErrorNotSupported -> the mma.sync streaming decode.
+cudaError_t planes_to_tiles_tc(const void* in, int P, int64_t br, int64_t bc, const float* coef,
+                               void* out, int64_t ldo, cudaStream_t s, int64_t plane_rows);
+// t = 4 encode on tcgen05 (stl_stream_tc.cu): bf16 matrix -> P <= 32 bf16 planes;
+// cudaErrorNotSupported -> the mma.sync streaming encode.
+cudaError_t tiles_to_planes_tc(const void* m, int64_t ldm, int64_t br, int64_t bc,
+                               const float* coef, int P, void* out, cudaStream_t s,
+                               int64_t plane_rows);
 // Fused-chain remix (stl_stream.cu kRemix): P <= 32 bf16 / fp32 planes -> bf16 planes,
 // out[p] = sum_q C[p][q] in[q], C = e_x d^T formed in-kernel; tile columns % 64 == 0.
 cudaError_t planes_to_planes_stream(const void* in, int idt, int P, int64_t br, int64_t bc,

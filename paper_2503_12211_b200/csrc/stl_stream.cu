@@ -490,13 +490,13 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
   // ENC: B loads at rows + xoff + 512k (+2 RS); C stores at buf + soff[k] + (16m + 8h) * 128.
   const uint32_t xoff = (q >> 1) * RS + 64 * wl + 8 * g + 4 * (q & 1);
   uint32_t soff[kNK];
-#pragma unroll
   // plane steps of the input / output plane regions: 128-byte swizzled box rows, or plain rows
   // of bulk_plane_stride bytes (16-byte pad: word offset 4 per plane -> the fragment accesses
   // below hit 32 distinct banks)
   const bool bin = bulk_in_capable<MODE, ZT>() && args.bulk_in, bout = args.bulk_out != 0;
   constexpr uint32_t PS = bulk_plane_stride<kT>();
   const uint32_t PSi = bin ? PS : 128u, PSo = bout ? PS : 128u;
+#pragma unroll
   for (int k = 0; k < kNK; ++k)
     soff[k] = !is_enc<MODE>() ? 0u
               : bout ? g * PS + (8 * (wl + kGWarps * k) + 2 * q) * 2
@@ -1159,6 +1159,10 @@ cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t 
     return cudaErrorNotSupported;
   if (rp && (P > 32 || !al16(rp) || !ro || !rw || (rdt == kF24 && bc % 128)))
     return cudaErrorNotSupported;
+  if (!rp) {  // the tensor-core (tcgen05) encode, when it takes the shape
+    const cudaError_t e = tiles_to_planes_tc(m, ldm, br, bc, coef, P, out, s, plane_rows);
+    if (e != cudaErrorNotSupported) return e;
+  }
   StreamArgs a{};
   a.mat = static_cast<const __nv_bfloat16*>(m);
   a.ldm = ldm;
@@ -1175,6 +1179,11 @@ cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t 
   return launch<kEncRed, float>(a, rp, out, ro, s);
 }
 
+bool plane_box_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_t br,
+                    int64_t bc, int kT, int64_t prow) {
+  return plane_tmap(m, base, zsz, P, Pb, br, bc, kT, 1, prow);
+}
+
 // decode (+ g_ex-style reduction): fp32 or bf16 planes -> bf16 matrix; red matrix bf16.
 cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, int64_t bc,
                                    const float* coef, void* out, int odt, int64_t ldo,
@@ -1186,6 +1195,10 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
   if (rm && (rdt != kBF16 || Q > 32 || ldr % 8 || !al16(rm) || !ro || !rw))
     return cudaErrorNotSupported;
   if (idt == kF24 && bc % 128) return cudaErrorNotSupported;
+  if (!rm && idt == kBF16) {  // the tensor-core (tcgen05) decode, when it takes the shape
+    const cudaError_t e = planes_to_tiles_tc(in, Q, br, bc, coef, out, ldo, s, plane_rows);
+    if (e != cudaErrorNotSupported) return e;
+  }
   StreamArgs a{};
   a.mat = static_cast<const __nv_bfloat16*>(rm);
   a.ldm = ldr;
