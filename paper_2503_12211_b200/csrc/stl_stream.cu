@@ -1162,6 +1162,10 @@ cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t 
   if (!rp) {  // the tensor-core (tcgen05) encode, when it takes the shape
     const cudaError_t e = tiles_to_planes_tc(m, ldm, br, bc, coef, P, out, s, plane_rows);
     if (e != cudaErrorNotSupported) return e;
+  } else if (rdt == kBF16) {  // tcgen05 encode + mma.sync reduction
+    const cudaError_t e =
+        red_transform_tc(true, m, ldm, rp, P, br, bc, coef, out, 0, ro, rw, s, plane_rows);
+    if (e != cudaErrorNotSupported) return e;
   }
   StreamArgs a{};
   a.mat = static_cast<const __nv_bfloat16*>(m);
@@ -1197,6 +1201,10 @@ cudaError_t planes_to_tiles_stream(const void* in, int idt, int Q, int64_t br, i
   if (idt == kF24 && bc % 128) return cudaErrorNotSupported;
   if (!rm && idt == kBF16) {  // the tensor-core (tcgen05) decode, when it takes the shape
     const cudaError_t e = planes_to_tiles_tc(in, Q, br, bc, coef, out, ldo, s, plane_rows);
+    if (e != cudaErrorNotSupported) return e;
+  } else if (rm && idt == kBF16) {  // tcgen05 decode + mma.sync reduction
+    const cudaError_t e =
+        red_transform_tc(false, rm, ldr, in, Q, br, bc, coef, out, ldo, ro, rw, s, plane_rows);
     if (e != cudaErrorNotSupported) return e;
   }
   StreamArgs a{};

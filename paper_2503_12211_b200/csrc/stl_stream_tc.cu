@@ -35,6 +35,30 @@ constexpr int kMaxSt = 8;
 // encode: two accumulator sets of 2 M-blocks x N = 32 G columns, rounded up to a power of 2
 template <int G> constexpr uint32_t kTmemColsEnc() { return 4 * 32 * G <= 256 ? 256u : 512u; }
 
+// Unit schedule: each CTA takes its first S units round robin (u = blockIdx.x + it * grid, the
+// SMs stream adjacent DRAM pages in lock step), the rest from an atomic counter, so SMs that the
+// memory system serves faster take more of the tail (dyn0 = S * grid; dyn0 >= nunits: static).
+// The producer publishes each unit index in a 16-entry ring (one mbarrier per entry) that the
+// MMA issuer and the epilogue read; kNoUnit ends the loop (written twice, once per epilogue
+// group's parity). Readers trail the producer by at most nstages + 3 < 16 units.
+constexpr uint32_t kNoUnit = 0xFFFFFFFFu;
+constexpr int kRing = 16;
+constexpr uint32_t kBarBytes = (2 * kMaxSt + 4 + kRing) * 8 + 16 + kRing * 4;
+
+__device__ __forceinline__ uint32_t next_unit(uint32_t it, uint32_t nunits, uint32_t dyn0,
+                                              unsigned* cnt) {
+  uint32_t u = blockIdx.x + it * gridDim.x;
+  if (u >= dyn0) u = dyn0 < nunits ? dyn0 + atomicAdd(cnt, 1u) : kNoUnit;
+  return u < nunits ? u : kNoUnit;
+}
+__device__ __forceinline__ void sched_done(unsigned* cnt, uint32_t dyn0, uint32_t nunits) {
+  // the last CTA out resets the counter pair for the slot's next launch
+  if (dyn0 < nunits && atomicAdd(cnt + 1, 1u) == gridDim.x - 1) {
+    atomicExch(cnt, 0u);
+    atomicExch(cnt + 1, 0u);
+  }
+}
+
 struct TcArgs {
   __nv_bfloat16* out;
   int64_t ldo;
@@ -42,6 +66,8 @@ struct TcArgs {
   int P, Pb;
   int64_t bc, upr, nunits;
   uint32_t nstages, nbuf;
+  unsigned* sched;  // counter pair of this launch's slot
+  uint32_t dyn0;
 };
 
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
@@ -97,7 +123,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kMaxSt;
   uint64_t* tfull = empty + kMaxSt;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + kRing);
+  volatile uint32_t* ring = tslot + 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t nunits = static_cast<uint32_t>(a.nunits), upr = static_cast<uint32_t>(a.upr);
   constexpr int kGW = kEpi / EG;  // warps per epilogue group
@@ -111,6 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], kGW);
     }
+    for (int i = 0; i < kRing; ++i) ptx::mbar_init(&rbar[i], 1);
     ptx::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tm_in);
@@ -138,8 +167,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
     if (lane == 0) {
-      uint32_t it = 0;
-      for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t u = next_unit(it, nunits, a.dyn0, a.sched);
+        ring[it % kRing] = u;
+        ptx::mbar_arrive(&rbar[it % kRing]);
+        if (u == kNoUnit) {
+          ring[(it + 1) % kRing] = u;
+          ptx::mbar_arrive(&rbar[(it + 1) % kRing]);
+          break;
+        }
         const uint32_t st = it % nst, ph = (it / nst) & 1;
         const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
         ptx::mbar_wait(&empty[st], ph ^ 1);
@@ -152,8 +188,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, 32, true, false);
-      uint32_t it = 0;
-      for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+      for (uint32_t it = 0;; ++it) {
+        ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
+        if (ring[it % kRing] == kNoUnit) break;
         const uint32_t st = it % nst, ph = (it / nst) & 1;
         const uint32_t buf = it & 1, bph = (it >> 1) & 1;
         ptx::mbar_wait(&tempty[buf], bph ^ 1);
@@ -183,8 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kMBW = kMB * 4 / kGW;  // M-blocks per warp
     const int mb0 = (gw >> 2) * kMBW;
     const bool issuer = gw == 0 && lane == 0;
-    uint32_t it = grp, k = 0;
-    for (uint32_t u = blockIdx.x + grp * gridDim.x; u < nunits; u += EG * gridDim.x, it += EG, ++k) {
+    for (uint32_t it = grp, k = 0;; it += EG, ++k) {
+      ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
+      const uint32_t u = ring[it % kRing];
+      if (u == kNoUnit) break;
       const uint32_t buf = it & 1, bph = (it >> 1) & 1;
       const uint32_t ob0 = s_out + (grp * nbuf + k % nbuf) * kOutBytes;
       const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
@@ -234,16 +273,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncwarp();
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) sched_done(a.sched, a.dyn0, nunits);
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, kTmemCols);
   }
 }
 
+// Counter pairs for the dynamic tail (one pool per device, slots round robin over launches: a
+// slot comes back after 256 launches, long after its launch finished and reset it).
+constexpr int kSchedSlots = 256;
+template <typename A>
+bool set_schedule(A& a, uint32_t grid) {
+  static unsigned* pools[64] = {};
+  static int next[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  if (!pools[dev]) {
+    unsigned* p = nullptr;
+    if (cudaMalloc(&p, 2 * kSchedSlots * sizeof(unsigned)) != cudaSuccess) return false;
+    if (cudaMemset(p, 0, 2 * kSchedSlots * sizeof(unsigned)) != cudaSuccess) return false;
+    pools[dev] = p;
+  }
+  a.sched = pools[dev] + 2 * (next[dev]++ % kSchedSlots);
+  // trailing rounds taken dynamically: a third of them (measured: 8192^3 with 55 rounds per CTA
+  // best at 12-24 dynamic rounds, config 2 with 28 at 8-12; all-dynamic loses the lock-step
+  // DRAM locality: profiles/r02_tc_dyn_ab.log). Probe STL_TC_DYN: 0 = static, -1 = all dynamic.
+  const uint32_t rounds = static_cast<uint32_t>((a.nunits + grid - 1) / grid);
+  static const int dyn_env = probe_env("STL_TC_DYN", -2);
+  const int dyn = dyn_env != -2 ? dyn_env : static_cast<int>(rounds / 3 > 2 ? rounds / 3 : 2);
+  const uint32_t srounds = dyn < 0 ? 1u : (static_cast<uint32_t>(dyn) >= rounds ? 1u : rounds - dyn);
+  a.dyn0 = dyn == 0 ? static_cast<uint32_t>(a.nunits) : srounds * grid;
+  return true;
+}
+
 template <int KS, int EG>
 cudaError_t launch_tc(const CUtensorMap& tm, TcArgs a, cudaStream_t s) {
   const uint32_t kStage = static_cast<uint32_t>(a.Pb) * kT * 2;
-  const uint32_t budget = 227 * 1024 - 1024 - kBBytes - 2 * (kMaxSt + 4) * 8 - 16;
+  const uint32_t budget = 227 * 1024 - 1024 - kBBytes - kBarBytes;
   static const int nb_env = probe_env("STL_DEC_TC_NBUF", 0);
   static const int st_env = probe_env("STL_DEC_TC_STAGES", 0);
   a.nbuf = nb_env >= 2 && nb_env <= 6 ? nb_env : (EG == 2 ? 3 : 4);
@@ -251,8 +318,7 @@ cudaError_t launch_tc(const CUtensorMap& tm, TcArgs a, cudaStream_t s) {
   uint32_t ns = (budget - EG * a.nbuf * kOutBytes) / kStage;
   a.nstages = ns > kMaxSt ? kMaxSt : ns;
   if (st_env >= 2 && static_cast<uint32_t>(st_env) < a.nstages) a.nstages = st_env;
-  const uint32_t smem = a.nstages * kStage + EG * a.nbuf * kOutBytes + kBBytes +
-                        2 * (kMaxSt + 4) * 8 + 16 + 1024;
+  const uint32_t smem = a.nstages * kStage + EG * a.nbuf * kOutBytes + kBBytes + kBarBytes + 1024;
   auto k = k_decode_tc<KS, EG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -260,6 +326,7 @@ cudaError_t launch_tc(const CUtensorMap& tm, TcArgs a, cudaStream_t s) {
   int64_t grid = sm_count();
   if (grid > a.nunits) grid = a.nunits;
   if (grid < 1) return cudaSuccess;
+  if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
   return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, tm, a);
 }
 
@@ -308,6 +375,8 @@ struct TcEncArgs {
   int P;
   int64_t bc, upr, nunits;
   uint32_t nstages, nbuf, out_bytes;
+  unsigned* sched;
+  uint32_t dyn0;
 };
 
 // G = 8-plane groups (N = 32 G); EG epilogue groups as in the decode.
@@ -329,7 +398,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kMaxSt;
   uint64_t* tfull = empty + kMaxSt;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + kRing);
+  volatile uint32_t* ring = tslot + 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = a.P;
   const uint32_t nunits = static_cast<uint32_t>(a.nunits), upr = static_cast<uint32_t>(a.upr);
@@ -344,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], kGW);
     }
+    for (int i = 0; i < kRing; ++i) ptx::mbar_init(&rbar[i], 1);
     ptx::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tm_out);
@@ -373,8 +445,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer: 4 matrix rows
-    uint32_t it = 0;
-    for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+    for (uint32_t it = 0;; ++it) {
+      uint32_t u = 0;
+      if (lane == 0) {
+        u = next_unit(it, nunits, a.dyn0, a.sched);
+        ring[it % kRing] = u;
+        ptx::mbar_arrive(&rbar[it % kRing]);
+        if (u == kNoUnit) {
+          ring[(it + 1) % kRing] = u;
+          ptx::mbar_arrive(&rbar[(it + 1) % kRing]);
+        }
+      }
+      u = __shfl_sync(0xFFFFFFFFu, u, 0);
+      if (u == kNoUnit) break;
       const uint32_t st = it % nst, ph = (it / nst) & 1;
       const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
       const uint32_t Tw = min(bc - J0, static_cast<uint32_t>(kT));
@@ -390,8 +473,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N, false, false);
-      uint32_t it = 0;
-      for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+      for (uint32_t it = 0;; ++it) {
+        ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
+        if (ring[it % kRing] == kNoUnit) break;
         const uint32_t st = it % nst, ph = (it / nst) & 1;
         const uint32_t buf = it & 1, bph = (it >> 1) & 1;
         ptx::mbar_wait(&tempty[buf], bph ^ 1);
@@ -419,8 +503,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kMBW = kEMB * 4 / kGW;  // M-blocks per warp
     const int mb0 = (gw >> 2) * kMBW;
     const bool issuer = gw == 0 && lane == 0;
-    uint32_t it = grp, k = 0;
-    for (uint32_t u = blockIdx.x + grp * gridDim.x; u < nunits; u += EG * gridDim.x, it += EG, ++k) {
+    for (uint32_t it = grp, k = 0;; it += EG, ++k) {
+      ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
+      const uint32_t u = ring[it % kRing];
+      if (u == kNoUnit) break;
       const uint32_t buf = it & 1, bph = (it >> 1) & 1;
       const uint32_t ob0 = s_out + (grp * nbuf + k % nbuf) * ob_bytes;
       const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
@@ -474,6 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncwarp();
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) sched_done(a.sched, a.dyn0, nunits);
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, kTmemColsEnc<G>());
@@ -485,7 +572,7 @@ cudaError_t launch_enc_tc(const CUtensorMap& tm, TcEncArgs a, cudaStream_t s) {
   constexpr uint32_t kStage = 4 * kERow;
   constexpr uint32_t kB = 32 * G * 128;
   a.out_bytes = (static_cast<uint32_t>(a.P) * kT * 2 + 1023) / 1024 * 1024;
-  const uint32_t budget = 227 * 1024 - 1024 - kB - 2 * (kMaxSt + 4) * 8 - 16;
+  const uint32_t budget = 227 * 1024 - 1024 - kB - kBarBytes;
   static const int nb_env = probe_env("STL_ENC_TC_NBUF", 0);
   static const int st_env = probe_env("STL_ENC_TC_STAGES", 0);
   a.nbuf = nb_env >= 2 && nb_env <= 6 ? nb_env : 2;
@@ -493,8 +580,7 @@ cudaError_t launch_enc_tc(const CUtensorMap& tm, TcEncArgs a, cudaStream_t s) {
   const uint32_t ns = (budget - EG * a.nbuf * a.out_bytes) / kStage;
   a.nstages = ns > kMaxSt ? kMaxSt : ns;
   if (st_env >= 2 && static_cast<uint32_t>(st_env) < a.nstages) a.nstages = st_env;
-  const uint32_t smem = a.nstages * kStage + EG * a.nbuf * a.out_bytes + kB +
-                        2 * (kMaxSt + 4) * 8 + 16 + 1024;
+  const uint32_t smem = a.nstages * kStage + EG * a.nbuf * a.out_bytes + kB + kBarBytes + 1024;
   auto k = k_encode_tc<G, EG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -502,7 +588,414 @@ cudaError_t launch_enc_tc(const CUtensorMap& tm, TcEncArgs a, cudaStream_t s) {
   int64_t grid = sm_count();
   if (grid > a.nunits) grid = a.nunits;
   if (grid < 1) return cudaSuccess;
+  if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
   return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, tm, a);
+}
+
+// ------------------------------------------------------------------ fused reductions
+// The backward's two transforms with a reduction riding on the same stream:
+//   ENC (encode_gy + g_d, toy_network.py:100-101): planes = encode(rows), E = coef
+//   DEC (decode_gu + g_ex, toy_network.py:104-105): rows = decode(Z), D = coef
+//   both: R[p][c] += sum over tiles j of Z[p][j] rows[j][c]   (Z: P bf16 planes, rows: bf16)
+// The change of basis runs on tcgen05 exactly as in k_encode_tc / k_decode_tc; the reduction
+// needs Z and the rows transposed against each other (the tile values interleave along the
+// matrix rows), so eight more warps run it on mma.sync m16n8k16 from the same landed stage —
+// the fragment scheme of k_stream's reductions (stl_stream.cu) — and each stage is released by
+// the UMMA commit plus those eight warps. The unit schedule stays static (round robin) so the
+// per-warp fragments, their fixed-order sum and the per-CTA partials (summed by sum_partials in
+// a fixed order) are bit-reproducible.
+// Warps: 0 producer, 1 MMA, 2..9 epilogue (two groups), 10..17 reduction.
+constexpr int kRedW = 8;
+constexpr int kThreadsRed = 32 * (2 + kEpi + kRedW);
+constexpr uint32_t kRowPadR = 64;
+
+struct TcRedArgs {
+  const __nv_bfloat16* rows;   // ENC: the matrix encoded; DEC: the reduction's matrix
+  int64_t ldr;
+  __nv_bfloat16* out;          // DEC: output matrix (ENC planes leave through tm_out)
+  int64_t ldo;
+  const float* coef;           // ENC: E, DEC: D (P x 16)
+  float* red_partial;          // [grid][P * 16]
+  int P, Pb;                   // Pb: planes per chunk of the Z box
+  int64_t bc, upr, nunits;
+  uint32_t nstages, nbuf, out_bytes, stage_bytes, rows_off;
+};
+
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// byte offset of (plane p, tile t) in a 128B-swizzled bf16 plane box with Pb planes per chunk
+__device__ __forceinline__ uint32_t zbox_off(int Pb, int p, int t) {
+  const uint32_t row = static_cast<uint32_t>((t >> 6) * Pb + p);
+  const uint32_t byte = static_cast<uint32_t>((t & 63) * 2);
+  return row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15));
+}
+
+// TU = tiles per unit (256 / 512); NK = ENC: 8-plane output groups G, DEC: K-steps KS;
+// MT = 16-plane groups of the reduction (ceil(P / 16)).
+template <bool ENC, int TU, int NK, int MT>
+__global__ void __launch_bounds__(kThreadsRed, 1)
+    k_red_tc(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_out,
+             TcRedArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = ptx::smem_u32(smem);
+  constexpr uint32_t RS = TU * 8 + kRowPadR;                // padded matrix row
+  constexpr int N = ENC ? 32 * NK : 32;                     // UMMA N
+  constexpr int kUMB = ENC ? TU / 256 : TU / 128;           // UMMA M-blocks per unit
+  constexpr uint32_t kB = ENC ? N * 128 : kBBytes;
+  constexpr uint32_t kTcols = (2 * kUMB * N <= 256) ? 256u : 512u;
+  constexpr int kGW = kEpi / 2;
+  const int Pb = a.Pb, P = a.P;
+  const uint32_t nst = a.nstages, nbuf = a.nbuf, ob_bytes = a.out_bytes, SB = a.stage_bytes;
+  const uint32_t s_out = nst * SB;
+  const uint32_t s_b = s_out + 2 * nbuf * ob_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + s_b + kB);
+  uint64_t* empty = full + kMaxSt;
+  uint64_t* tfull = empty + kMaxSt;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + kRing);
+  volatile uint32_t* ring = tslot + 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t nunits = static_cast<uint32_t>(a.nunits), upr = static_cast<uint32_t>(a.upr);
+  const uint32_t bc = static_cast<uint32_t>(a.bc);
+
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < nst; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1 + kRedW);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], kGW);
+    }
+    for (int i = 0; i < kRing; ++i) ptx::mbar_init(&rbar[i], 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm_z);
+    if constexpr (ENC) ptx::prefetch_tmap(&tm_out);
+  }
+  if (warp == 1) ptx::tmem_alloc(tslot, kTcols);
+  // the UMMA B operand (as in k_encode_tc / k_decode_tc)
+  if constexpr (ENC) {
+    for (int i = threadIdx.x; i < N * 64; i += kThreadsRed) {
+      const int n = i >> 6, k = i & 63;
+      const int g = n >> 5, par = (n >> 4) & 1, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
+      const int ka = k >> 3, kpar = (k >> 2) & 1, kb = k & 3;
+      const float e = k < 32 && kpar == par && p < P ? a.coef[p * 16 + 4 * ka + kb] : 0.f;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(e);
+      const __nv_bfloat16 v = hl == 0 ? hi : __float2bfloat16_rn(e - __bfloat162float(hi));
+      const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
+      *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
+    }
+  } else {
+    for (int i = threadIdx.x; i < 32 * 64; i += kThreadsRed) {
+      const int n = i >> 6, k = i & 63, c = n & 15, st = k >> 4;
+      const int pl = (st == 0 ? 0 : Pb - 16) + (k & 15);
+      const float d = st < NK && pl < P && pl >= 16 * st ? a.coef[pl * 16 + c] : 0.f;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(d);
+      const __nv_bfloat16 v = n < 16 ? hi : __float2bfloat16_rn(d - __bfloat162float(hi));
+      const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
+      *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
+    }
+  }
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  griddep_launch_dependents();
+  griddep_wait();
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer
+    for (uint32_t it = 0;; ++it) {
+      uint32_t u = blockIdx.x + it * gridDim.x;
+      if (u >= nunits) u = kNoUnit;
+      if (lane == 0) {
+        ring[it % kRing] = u;
+        ptx::mbar_arrive(&rbar[it % kRing]);
+        if (u == kNoUnit) {
+          ring[(it + 1) % kRing] = u;
+          ptx::mbar_arrive(&rbar[(it + 1) % kRing]);
+        }
+      }
+      if (u == kNoUnit) break;
+      const uint32_t st = it % nst, ph = (it / nst) & 1;
+      const uint32_t I = u / upr, J0 = (u - I * upr) * TU;
+      const uint32_t Tw = min(bc - J0, static_cast<uint32_t>(TU));
+      ptx::mbar_wait(&empty[st], ph ^ 1);
+      const uint32_t sz = sbase + st * SB;
+      if (lane == 0) {
+        ptx::mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(Pb) * TU * 2 + 4 * Tw * 8);
+        tma_load_4d(&tm_z, &full[st], sz, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
+      }
+      __syncwarp();
+      if (lane < 4)
+        bulk_g2s(sz + a.rows_off + lane * RS,
+                 a.rows + (4 * static_cast<int64_t>(I) + lane) * a.ldr + 4 * static_cast<int64_t>(J0),
+                 Tw * 8, &full[st]);
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N, !ENC, false);
+      for (uint32_t it = 0;; ++it) {
+        ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
+        if (ring[it % kRing] == kNoUnit) break;
+        const uint32_t st = it % nst, ph = (it / nst) & 1;
+        const uint32_t buf = it & 1, bph = (it >> 1) & 1;
+        ptx::mbar_wait(&tempty[buf], bph ^ 1);
+        ptx::mbar_wait(&full[st], ph);
+        ptx::tc_fence_after();
+        const uint32_t s0 = sbase + st * SB;
+#pragma unroll
+        for (int mb = 0; mb < kUMB; ++mb)
+#pragma unroll
+          for (int ks = 0; ks < (ENC ? 2 : NK); ++ks) {
+            uint64_t ad;
+            if constexpr (ENC) {
+              ad = smem_desc_plain(s0 + a.rows_off + 2 * ks * RS + mb * 2048, RS, 128);
+            } else {
+              const uint32_t off = ks == 0 ? 0u : static_cast<uint32_t>(Pb - 16);
+              ad = ptx::smem_desc_sw128(s0 + (2 * mb * Pb + off) * 128, Pb * 128, 1024);
+            }
+            const uint64_t bd = ptx::smem_desc_sw128(sbase + s_b + ks * 32, 16, 1024);
+            ptx::mma_bf16_ss(tmem + buf * (kUMB * N) + mb * N, ad, bd, idesc, ks > 0 ? 1u : 0u);
+          }
+        ptx::mma_commit(&empty[st]);
+        ptx::mma_commit(&tfull[buf]);
+      }
+    }
+  } else if (warp < 2 + kEpi) {
+    // ---------------------------------------------------------------- epilogue
+    const int ew = warp - 2;
+    const int grp = ew / kGW, gw = ew % kGW;
+    const uint32_t quarter = warp & 3;
+    const bool issuer = gw == 0 && lane == 0;
+    for (uint32_t it = grp, k = 0;; it += 2, ++k) {
+      ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
+      const uint32_t u = ring[it % kRing];
+      if (u == kNoUnit) break;
+      const uint32_t buf = it & 1, bph = (it >> 1) & 1;
+      const uint32_t ob0 = s_out + (grp * nbuf + k % nbuf) * ob_bytes;
+      const uint32_t I = u / upr, J0 = (u - I * upr) * TU;
+      ptx::mbar_wait(&tfull[buf], bph);
+      ptx::tc_fence_after();
+      if constexpr (ENC) {
+#pragma unroll 1
+        for (int mb = 0; mb < kUMB; ++mb) {
+          const uint32_t chunk = 4 * mb + quarter;
+#pragma unroll
+          for (int g0 = 0; g0 < NK; g0 += 2) {
+            float v[2][32];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (g0 + h < NK)
+                tmem_ld_x32(tmem + ((quarter * 32) << 16) + buf * (kUMB * N) + mb * N + 32 * (g0 + h), v[h]);
+            ptx::tmem_ld_wait();
+            if (mb == kUMB - 1 && g0 + 2 >= NK) {
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int pp = 0; pp < 8; ++pp) {
+                const int p = 8 * (g0 + h) + pp;
+                if (g0 + h < NK && p < P) {
+                  const uint32_t row = chunk * P + p;
+                  const uint32_t byte = 4 * lane;
+                  const uint32_t off = row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15));
+                  *reinterpret_cast<uint32_t*>(smem + ob0 + off) =
+                      pack_bf16(v[h][pp] + v[h][8 + pp], v[h][16 + pp] + v[h][24 + pp]);
+                }
+              }
+          }
+        }
+      } else {
+        constexpr int kMBW = kUMB * 4 / kGW;  // M-blocks per warp (all of the unit's)
+        static_assert(kMBW % 2 == 0, "M-blocks per warp");
+        constexpr uint32_t OS = TU * 8;
+#pragma unroll
+        for (int j = 0; j < kMBW; j += 2) {
+          float v[2][32];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            tmem_ld_x32(tmem + ((quarter * 32) << 16) + buf * (kUMB * 32) + (j + h) * 32, v[h]);
+          ptx::tmem_ld_wait();
+          if (j == kMBW - 2) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t m = (j + h) * 128 + quarter * 32 + lane;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const uint32_t w0 = pack_bf16(v[h][4 * r] + v[h][16 + 4 * r], v[h][4 * r + 1] + v[h][17 + 4 * r]);
+              const uint32_t w1 = pack_bf16(v[h][4 * r + 2] + v[h][18 + 4 * r], v[h][4 * r + 3] + v[h][19 + 4 * r]);
+              *reinterpret_cast<uint2*>(smem + ob0 + r * OS + m * 8) = make_uint2(w0, w1);
+            }
+          }
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      if (issuer) bulk_wait_read_n(nbuf - 2);
+      epi_bar(grp, 32 * kGW);
+      if (issuer) {
+        if constexpr (ENC) {
+          tma_store_4d(&tm_out, sbase + ob0, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
+        } else {
+          const uint32_t Tw = min(bc - J0, static_cast<uint32_t>(TU));
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            bulk_s2g(a.out + (4 * static_cast<int64_t>(I) + r) * a.ldo + 4 * static_cast<int64_t>(J0),
+                     sbase + ob0 + r * (TU * 8), Tw * 8);
+        }
+        ptx::bulk_commit();
+      }
+    }
+    if (issuer) ptx::bulk_wait_all();
+  } else {
+    // ---------------------------------------------------------------- reduction (mma.sync)
+    // warp wr takes the unit's 16-tile k-steps wr, wr + 8, ...: A = Z (rows = planes g / g + 8
+    // of each 16-plane group, k = tiles 2q, 2q + 1 | + 8), B = rows (n = c = 8 nt + g: matrix row
+    // c >> 2, element c & 3 of tiles 2q, 2q + 1 | + 8; 16-bit loads, distinct words)
+    const int wr = warp - 2 - kEpi;
+    const int g = lane >> 2, q = lane & 3;
+    constexpr int kKS = TU / (16 * kRedW);
+    float R[MT][2][4];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) R[m][n][k] = 0.f;
+    uint32_t rb[2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int c = 8 * nt + g;
+      rb[nt] = (c >> 2) * RS + 16 * q + 2 * (c & 3);
+    }
+    bool ok[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      ok[mt][0] = 16 * mt + g < P;
+      ok[mt][1] = 16 * mt + g + 8 < P;
+    }
+    for (uint32_t it = 0;; ++it) {
+      ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
+      const uint32_t u = ring[it % kRing];
+      if (u == kNoUnit) break;
+      const uint32_t st = it % nst, ph = (it / nst) & 1;
+      const uint32_t J0 = (u - (u / upr) * upr) * TU;
+      const int Tw = static_cast<int>(min(bc - J0, static_cast<uint32_t>(TU)));
+      ptx::mbar_wait(&full[st], ph);
+      const uint32_t so = st * SB;
+#pragma unroll
+      for (int k = 0; k < kKS; ++k) {
+        const int t0 = 16 * (wr + kRedW * k);
+        if (t0 < Tw) {
+          uint32_t b[2][2];
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const uint8_t* base = smem + so + a.rows_off + rb[nt] + t0 * 8;
+            const uint32_t x0 = *reinterpret_cast<const uint16_t*>(base);
+            const uint32_t x1 = *reinterpret_cast<const uint16_t*>(base + 8);
+            const uint32_t x8 = *reinterpret_cast<const uint16_t*>(base + 64);
+            const uint32_t x9 = *reinterpret_cast<const uint16_t*>(base + 72);
+            b[nt][0] = x0 | (x1 << 16);
+            b[nt][1] = x8 | (x9 << 16);
+          }
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const int p0 = 16 * mt + g;
+            const uint32_t z0 = so + zbox_off(Pb, p0, t0 + 2 * q);
+            const uint32_t z2 = so + zbox_off(Pb, p0, t0 + 2 * q + 8);
+            const uint32_t a0 = ok[mt][0] ? *reinterpret_cast<const uint32_t*>(smem + z0) : 0u;
+            const uint32_t a2 = ok[mt][0] ? *reinterpret_cast<const uint32_t*>(smem + z2) : 0u;
+            const uint32_t a1 = ok[mt][1] ? *reinterpret_cast<const uint32_t*>(smem + z0 + 1024) : 0u;
+            const uint32_t a3 = ok[mt][1] ? *reinterpret_cast<const uint32_t*>(smem + z2 + 1024) : 0u;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) mma16816(R[mt][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[st]);
+    }
+    // per-warp fragments -> a dedicated smem region -> fixed-order sum -> this CTA's partial
+    const int n = P * 16;
+    float* s_red = reinterpret_cast<float*>(smem + s_b + kB + kBarBytes);
+    float* mine = s_red + wr * n;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int c = 8 * nt + 2 * q, p0 = 16 * mt + g, p1 = p0 + 8;
+        if (p0 < P) {
+          mine[p0 * 16 + c] = R[mt][nt][0];
+          mine[p0 * 16 + c + 1] = R[mt][nt][1];
+        }
+        if (p1 < P) {
+          mine[p1 * 16 + c] = R[mt][nt][2];
+          mine[p1 * 16 + c + 1] = R[mt][nt][3];
+        }
+      }
+    asm volatile("bar.sync 3, %0;" ::"n"(32 * kRedW) : "memory");
+    for (int o = (warp - 2 - kEpi) * 32 + lane; o < n; o += 32 * kRedW) {
+      float sum = s_red[o];
+#pragma unroll
+      for (int w = 1; w < kRedW; ++w) sum += s_red[w * n + o];
+      a.red_partial[static_cast<int64_t>(blockIdx.x) * n + o] = sum;
+    }
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, kTcols);
+  }
+}
+
+template <bool ENC, int TU, int NK, int MT>
+cudaError_t launch_red_tc(const CUtensorMap& tz, const CUtensorMap& to, TcRedArgs a, float* red_out,
+                          cudaStream_t s) {
+  constexpr int N = ENC ? 32 * NK : 32;
+  constexpr uint32_t kB = ENC ? N * 128 : kBBytes;
+  const uint32_t zbytes = (static_cast<uint32_t>(a.Pb) * TU * 2 + 1023) / 1024 * 1024;
+  a.rows_off = zbytes;
+  a.stage_bytes = (zbytes + 4 * (TU * 8 + kRowPadR) + 1023) / 1024 * 1024;
+  a.out_bytes = ENC ? (static_cast<uint32_t>(a.P) * TU * 2 + 1023) / 1024 * 1024 : 4 * TU * 8;
+  const uint32_t red_bytes = kRedW * a.P * 16 * 4;  // the per-warp partials
+  const uint32_t budget = 227 * 1024 - 1024 - kB - kBarBytes - red_bytes;
+  static const int nb_env = probe_env("STL_RED_TC_NBUF", 0);
+  a.nbuf = nb_env >= 2 && nb_env <= 4 ? nb_env : 2;
+  if (2 * a.nbuf * a.out_bytes + 2 * a.stage_bytes > budget) return cudaErrorNotSupported;
+  const uint32_t ns = (budget - 2 * a.nbuf * a.out_bytes) / a.stage_bytes;
+  a.nstages = ns > kMaxSt ? kMaxSt : ns;
+  const uint32_t smem =
+      a.nstages * a.stage_bytes + 2 * a.nbuf * a.out_bytes + kB + kBarBytes + red_bytes + 1024;
+  auto k = k_red_tc<ENC, TU, NK, MT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int64_t grid = sm_count();
+  if (grid > a.nunits) grid = a.nunits;
+  if (grid < 1) return cudaSuccess;
+  e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreadsRed), smem, s, tz, to, a);
+  if (e != cudaSuccess) return e;
+  return sum_partials(a.red_partial, static_cast<int>(grid), a.P * 16, red_out, s);
 }
 
 }  // namespace
@@ -557,6 +1050,63 @@ cudaError_t tiles_to_planes_tc(const void* m, int64_t ldm, int64_t br, int64_t b
     case 3: return eg == 1 ? launch_enc_tc<3, 1>(tm, a, s) : launch_enc_tc<3, 2>(tm, a, s);
     default: return eg == 1 ? launch_enc_tc<4, 1>(tm, a, s) : launch_enc_tc<4, 2>(tm, a, s);
   }
+}
+
+// The backward's fused transforms on tcgen05 + mma.sync (k_red_tc): bf16 rows, bf16 Z planes,
+// P <= 32. enc: planes_out = encode(rows) (tiles_to_planes_stream with reduction planes);
+// dec: rows_out = decode(Z) (planes_to_tiles_stream with a reduction matrix).
+cudaError_t red_transform_tc(bool enc, const void* rows, int64_t ldr, const void* z, int P,
+                             int64_t br, int64_t bc, const float* coef, void* out, int64_t ldo,
+                             float* red_out, float* red_ws, cudaStream_t s, int64_t plane_rows) {
+  // default: the decode-reduction only (g_x + g_ex 52 -> 49 us at config 2); the encode-
+  // reduction on tcgen05 measured even with the mma.sync one (profiles/r02_red_tc_ab.log), so it
+  // stays there (probe STL_RED_TC=1: both, 0: neither)
+  static const int on = probe_env("STL_RED_TC", 2);
+  static const int tu_env = probe_env("STL_RED_TC_T", 0);
+  const int TU = tu_env ? tu_env : (enc ? 256 : 512);
+  if (on == 2 && enc) return cudaErrorNotSupported;  // probe: decode-reduction only
+  if (!on || P < 1 || P > 32 || bc < TU || bc % 64 || ldr % 8 || (!enc && ldo % 8) ||
+      (reinterpret_cast<uintptr_t>(rows) & 15) || (reinterpret_cast<uintptr_t>(z) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15) || !red_out || !red_ws || (TU != 256 && TU != 512))
+    return cudaErrorNotSupported;
+  if (plane_rows < br) plane_rows = br;
+  const int Pb = enc ? (P + 7) / 8 * 8 : (P <= 16 ? 16 : (P + 7) / 8 * 8);
+  CUtensorMap tz{}, to{};
+  if (!plane_box_tmap(&tz, z, 2, P, Pb, br, bc, TU, plane_rows)) return cudaErrorNotSupported;
+  if (enc && !plane_box_tmap(&to, out, 2, P, P, br, bc, TU, plane_rows)) return cudaErrorNotSupported;
+  TcRedArgs a{};
+  a.rows = static_cast<const __nv_bfloat16*>(rows);
+  a.ldr = ldr;
+  a.out = static_cast<__nv_bfloat16*>(out);
+  a.ldo = ldo;
+  a.coef = coef;
+  a.red_partial = red_ws;
+  a.P = P;
+  a.Pb = Pb;
+  a.bc = bc;
+  a.upr = (bc + TU - 1) / TU;
+  a.nunits = br * a.upr;
+  const int MT = (P + 15) / 16;
+  if (enc) {
+    const int G = (P + 7) / 8;
+#define STL_RED_ENC(TUV)                                                                          \
+  switch (G) {                                                                                    \
+    case 1: return launch_red_tc<true, TUV, 1, 1>(tz, to, a, red_out, s);                         \
+    case 2: return launch_red_tc<true, TUV, 2, 1>(tz, to, a, red_out, s);                         \
+    case 3: return launch_red_tc<true, TUV, 3, 2>(tz, to, a, red_out, s);                         \
+    default: return launch_red_tc<true, TUV, 4, 2>(tz, to, a, red_out, s);                        \
+  }
+    if (TU == 256) { STL_RED_ENC(256) }
+    STL_RED_ENC(512)
+#undef STL_RED_ENC
+  }
+  const int KS = Pb <= 16 ? 1 : 2;
+  if (TU == 256)
+    return KS == 1 ? launch_red_tc<false, 256, 1, 1>(tz, to, a, red_out, s)
+                   : launch_red_tc<false, 256, 2, 2>(tz, to, a, red_out, s);
+  return KS == 1 ? launch_red_tc<false, 512, 1, 1>(tz, to, a, red_out, s)
+                 : (MT == 1 ? launch_red_tc<false, 512, 2, 1>(tz, to, a, red_out, s)
+                            : launch_red_tc<false, 512, 2, 2>(tz, to, a, red_out, s));
 }
 
 }  // namespace stl
