@@ -198,6 +198,10 @@ cudaError_t tiles_to_planes_tc(const void* m, int64_t ldm, int64_t br, int64_t b
 cudaError_t red_transform_tc(bool enc, const void* rows, int64_t ldr, const void* z, int P,
                              int64_t br, int64_t bc, const float* coef, void* out, int64_t ldo,
                              float* red_out, float* red_ws, cudaStream_t s, int64_t plane_rows);
+// The fused-chain remix on tcgen05 (stl_stream_tc.cu): P <= 32 bf16 planes -> bf16 planes;
+// cudaErrorNotSupported -> the mma.sync streaming remix.
+cudaError_t planes_to_planes_tc(const void* in, int P, int64_t br, int64_t bc, const float* e_x,
+                                const float* d, void* out, cudaStream_t s);
 // Fused-chain remix (stl_stream.cu kRemix): P <= 32 bf16 / fp32 planes -> bf16 planes,
 // out[p] = sum_q C[p][q] in[q], C = e_x d^T formed in-kernel; tile columns % 64 == 0.
 cudaError_t planes_to_planes_stream(const void* in, int idt, int P, int64_t br, int64_t bc,

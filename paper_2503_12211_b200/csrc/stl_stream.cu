@@ -1234,6 +1234,10 @@ cudaError_t planes_to_planes_stream(const void* in, int idt, int P, int64_t br, 
                                     const float* e_x, const float* d, void* out, cudaStream_t s) {
   if ((idt != kBF16 && idt != kF32) || bc % 64 || P < 1 || P > 32 || !al16(in) || !al16(out))
     return cudaErrorNotSupported;
+  if (idt == kBF16) {  // the tcgen05 remix, when it takes the shape
+    const cudaError_t e = planes_to_planes_tc(in, P, br, bc, e_x, d, out, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   StreamArgs a{};
   a.out = out;
   a.coef = e_x;

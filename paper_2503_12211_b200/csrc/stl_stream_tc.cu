@@ -998,6 +998,214 @@ cudaError_t launch_red_tc(const CUtensorMap& tz, const CUtensorMap& to, TcRedArg
   return sum_partials(a.red_partial, static_cast<int>(grid), a.P * 16, red_out, s);
 }
 
+// ------------------------------------------------------------------ remix (fused chain)
+//   out[p][I][J] = sum_q C[p][q] Z[q][I][J],  C = e_x d^T     (snf_operator.py:175-188)
+// K11's operand scheme with the plane box on both sides: A = the landed input box (MN-major),
+// B[q][n] = C split into bf16 hi + lo, n = 16 g + 8 hl + pp (output plane p = 8 g + pp), so a
+// 32x32b.x16 read-back holds a group's hi and lo columns; the epilogue writes the output planes
+// into a swizzled box for one TMA store. C is formed in the kernel prologue.
+template <int KS, int G>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_remix_tc(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+               TcEncArgs a, const float* __restrict__ e_x, const float* __restrict__ dcoef) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = ptx::smem_u32(smem);
+  constexpr int N = 16 * G;
+  constexpr uint32_t kB = N * 128 < 1024 ? 1024 : N * 128;
+  constexpr uint32_t kTc = 2 * kMB * N <= 256 ? 256u : 512u;
+  constexpr int kGW = kEpi / 2;
+  const int P = a.P;
+  const int Pb = P <= 16 ? 16 : (P + 7) / 8 * 8;
+  const uint32_t kStage = static_cast<uint32_t>(Pb) * kT * 2;
+  const uint32_t nst = a.nstages, nbuf = a.nbuf, ob_bytes = a.out_bytes;
+  const uint32_t s_out = nst * kStage;
+  const uint32_t s_b = s_out + 2 * nbuf * ob_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + s_b + kB);
+  uint64_t* empty = full + kMaxSt;
+  uint64_t* tfull = empty + kMaxSt;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + kRing);
+  volatile uint32_t* ring = tslot + 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t nunits = static_cast<uint32_t>(a.nunits), upr = static_cast<uint32_t>(a.upr);
+
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < nst; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], kGW);
+    }
+    for (int i = 0; i < kRing; ++i) ptx::mbar_init(&rbar[i], 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm_in);
+    ptx::prefetch_tmap(&tm_out);
+  }
+  if (warp == 1) ptx::tmem_alloc(tslot, kTc);
+  for (int i = threadIdx.x; i < N * 64; i += kThreads) {
+    const int n = i >> 6, k = i & 63, st = k >> 4;
+    const int g = n >> 4, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
+    const int q = (st == 0 ? 0 : Pb - 16) + (k & 15);
+    float c = 0.f;
+    if (st < KS && p < P && q < P && q >= 16 * st) {
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) c = fmaf(e_x[p * 16 + kk], dcoef[q * 16 + kk], c);
+    }
+    const __nv_bfloat16 hi = __float2bfloat16_rn(c);
+    const __nv_bfloat16 v = hl == 0 ? hi : __float2bfloat16_rn(c - __bfloat162float(hi));
+    const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
+    *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
+  }
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  griddep_launch_dependents();
+  griddep_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t u = next_unit(it, nunits, a.dyn0, a.sched);
+        ring[it % kRing] = u;
+        ptx::mbar_arrive(&rbar[it % kRing]);
+        if (u == kNoUnit) {
+          ring[(it + 1) % kRing] = u;
+          ptx::mbar_arrive(&rbar[(it + 1) % kRing]);
+          break;
+        }
+        const uint32_t st = it % nst, ph = (it / nst) & 1;
+        const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
+        ptx::mbar_wait(&empty[st], ph ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[st], kStage);
+        tma_load_4d(&tm_in, &full[st], sbase + st * kStage, 0, 0, static_cast<int>(J0 / 64),
+                    static_cast<int>(I));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N, true, false);
+      for (uint32_t it = 0;; ++it) {
+        ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
+        if (ring[it % kRing] == kNoUnit) break;
+        const uint32_t st = it % nst, ph = (it / nst) & 1;
+        const uint32_t buf = it & 1, bph = (it >> 1) & 1;
+        ptx::mbar_wait(&tempty[buf], bph ^ 1);
+        ptx::mbar_wait(&full[st], ph);
+        ptx::tc_fence_after();
+        const uint32_t a0 = sbase + st * kStage;
+#pragma unroll
+        for (int mb = 0; mb < kMB; ++mb)
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            const uint32_t off = ks == 0 ? 0u : static_cast<uint32_t>(Pb - 16);
+            const uint64_t ad = ptx::smem_desc_sw128(a0 + (2 * mb * Pb + off) * 128, Pb * 128, 1024);
+            const uint64_t bd = ptx::smem_desc_sw128(sbase + s_b + ks * 32, 16, 1024);
+            ptx::mma_bf16_ss(tmem + buf * (kMB * N) + mb * N, ad, bd, idesc, ks > 0 ? 1u : 0u);
+          }
+        ptx::mma_commit(&empty[st]);
+        ptx::mma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    const int ew = warp - 2;
+    const int grp = ew / kGW, gw = ew % kGW;
+    const uint32_t quarter = warp & 3;
+    const bool issuer = gw == 0 && lane == 0;
+    for (uint32_t it = grp, k = 0;; it += 2, ++k) {
+      ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
+      const uint32_t u = ring[it % kRing];
+      if (u == kNoUnit) break;
+      const uint32_t buf = it & 1, bph = (it >> 1) & 1;
+      const uint32_t ob0 = s_out + (grp * nbuf + k % nbuf) * ob_bytes;
+      const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
+      ptx::mbar_wait(&tfull[buf], bph);
+      ptx::tc_fence_after();
+#pragma unroll 1
+      for (int mb = 0; mb < kMB; ++mb) {
+        const uint32_t m = mb * 128 + quarter * 32 + lane;  // tile of the unit
+        const uint32_t chunk = m >> 6, byte = (m & 63) * 2;
+#pragma unroll
+        for (int g0 = 0; g0 < G; g0 += 2) {
+          float v[2][16];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (g0 + h < G) {
+              uint32_t (&uu)[16] = reinterpret_cast<uint32_t(&)[16]>(v[h]);
+              ptx::tmem_ld_32x32b_x16(tmem + ((quarter * 32) << 16) + buf * (kMB * N) + mb * N + 16 * (g0 + h), uu);
+            }
+          ptx::tmem_ld_wait();
+          if (mb == kMB - 1 && g0 + 2 >= G) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int pp = 0; pp < 8; ++pp) {
+              const int p = 8 * (g0 + h) + pp;
+              if (g0 + h < G && p < P) {
+                const uint32_t row = chunk * P + p;
+                const uint32_t off = row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15));
+                *reinterpret_cast<__nv_bfloat16*>(smem + ob0 + off) = __float2bfloat16_rn(v[h][pp] + v[h][8 + pp]);
+              }
+            }
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      if (issuer) bulk_wait_read_n(nbuf - 2);
+      epi_bar(grp, 32 * kGW);
+      if (issuer) {
+        tma_store_4d(&tm_out, sbase + ob0, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
+        ptx::bulk_commit();
+      }
+    }
+    if (issuer) ptx::bulk_wait_all();
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) sched_done(a.sched, a.dyn0, nunits);
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, kTc);
+  }
+}
+
+template <int KS, int G>
+cudaError_t launch_remix_tc(const CUtensorMap& ti, const CUtensorMap& to, TcEncArgs a,
+                            const float* e_x, const float* d, cudaStream_t s) {
+  constexpr int N = 16 * G;
+  constexpr uint32_t kB = N * 128 < 1024 ? 1024 : N * 128;
+  const int Pb = a.P <= 16 ? 16 : (a.P + 7) / 8 * 8;
+  const uint32_t kStage = static_cast<uint32_t>(Pb) * kT * 2;
+  a.out_bytes = (static_cast<uint32_t>(a.P) * kT * 2 + 1023) / 1024 * 1024;
+  const uint32_t budget = 227 * 1024 - 1024 - kB - kBarBytes;
+  static const int nb_env = probe_env("STL_REMIX_TC_NBUF", 0);
+  a.nbuf = nb_env >= 2 && nb_env <= 4 ? nb_env : 2;
+  if (2 * a.nbuf * a.out_bytes + 2 * kStage > budget) return cudaErrorNotSupported;
+  const uint32_t ns = (budget - 2 * a.nbuf * a.out_bytes) / kStage;
+  a.nstages = ns > kMaxSt ? kMaxSt : ns;
+  const uint32_t smem = a.nstages * kStage + 2 * a.nbuf * a.out_bytes + kB + kBarBytes + 1024;
+  auto k = k_remix_tc<KS, G>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int64_t grid = sm_count();
+  if (grid > a.nunits) grid = a.nunits;
+  if (grid < 1) return cudaSuccess;
+  if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
+  return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, ti, to, a, e_x, d);
+}
+
 }  // namespace
 
 cudaError_t planes_to_tiles_tc(const void* in, int P, int64_t br, int64_t bc, const float* coef,
@@ -1107,6 +1315,32 @@ cudaError_t red_transform_tc(bool enc, const void* rows, int64_t ldr, const void
   return KS == 1 ? launch_red_tc<false, 512, 1, 1>(tz, to, a, red_out, s)
                  : (MT == 1 ? launch_red_tc<false, 512, 2, 1>(tz, to, a, red_out, s)
                             : launch_red_tc<false, 512, 2, 2>(tz, to, a, red_out, s));
+}
+
+// The fused-chain remix on tcgen05 (k_remix_tc): P <= 32 bf16 planes -> P bf16 planes,
+// out[p] = sum_q (e_x d^T)[p][q] in[q]; cudaErrorNotSupported -> the mma.sync streaming remix.
+cudaError_t planes_to_planes_tc(const void* in, int P, int64_t br, int64_t bc, const float* e_x,
+                                const float* d, void* out, cudaStream_t s) {
+  static const int on = probe_env("STL_REMIX_TC", 1);
+  if (!on || P < 1 || P > 32 || bc < kT || bc % 64 || (reinterpret_cast<uintptr_t>(in) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15))
+    return cudaErrorNotSupported;
+  const int Pb = P <= 16 ? 16 : (P + 7) / 8 * 8;
+  CUtensorMap ti{}, to{};
+  if (!plane_box_tmap(&ti, in, 2, P, Pb, br, bc, kT, br)) return cudaErrorNotSupported;
+  if (!plane_box_tmap(&to, out, 2, P, P, br, bc, kT, br)) return cudaErrorNotSupported;
+  TcEncArgs a{};
+  a.P = P;
+  a.bc = bc;
+  a.upr = (bc + kT - 1) / kT;
+  a.nunits = br * a.upr;
+  const int KS = Pb <= 16 ? 1 : 2;
+  switch ((P + 7) / 8) {
+    case 1: return launch_remix_tc<1, 1>(ti, to, a, e_x, d, s);
+    case 2: return launch_remix_tc<1, 2>(ti, to, a, e_x, d, s);
+    case 3: return launch_remix_tc<2, 3>(ti, to, a, e_x, d, s);
+    default: return KS == 1 ? cudaErrorNotSupported : launch_remix_tc<2, 4>(ti, to, a, e_x, d, s);
+  }
 }
 
 }  // namespace stl
