@@ -68,6 +68,7 @@ struct TcArgs {
   uint32_t nstages, nbuf;
   unsigned* sched;  // counter pair of this launch's slot
   uint32_t dyn0;
+  Trace trace;      // probe build: launch span
 };
 
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
@@ -131,6 +132,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kGW = kEpi / EG;  // warps per epilogue group
 
   if (threadIdx.x == 0) {
+    trace_mark(a.trace, false);
+    trace_cta(a.trace, 0);
     for (uint32_t i = 0; i < nst; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
@@ -162,7 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tslot;
   griddep_launch_dependents();
-  griddep_wait();  // the planes of this launch are complete (PDL)
+  griddep_wait();
+  if (threadIdx.x == 0) trace_cta(a.trace, 1);  // the planes of this launch are complete (PDL)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
       ptx::mbar_wait(&tfull[buf], bph);
       ptx::tc_fence_after();
+      if (it == 0 && issuer) trace_cta(a.trace, 2);
 #pragma unroll
       // two M-blocks' accumulators per tcgen05.wait::ld (the loads' latencies overlap)
       static_assert(kMBW % 2 == 0, "M-blocks per warp");
@@ -274,6 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) sched_done(a.sched, a.dyn0, nunits);
+  if (threadIdx.x == 0) {
+    trace_cta(a.trace, 3);
+    trace_mark(a.trace, true);
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, kTmemCols);
@@ -327,6 +336,7 @@ cudaError_t launch_tc(const CUtensorMap& tm, TcArgs a, cudaStream_t s) {
   if (grid > a.nunits) grid = a.nunits;
   if (grid < 1) return cudaSuccess;
   if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
+  a.trace = trace_next();
   return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, tm, a);
 }
 
@@ -377,6 +387,7 @@ struct TcEncArgs {
   uint32_t nstages, nbuf, out_bytes;
   unsigned* sched;
   uint32_t dyn0;
+  Trace trace;
 };
 
 // G = 8-plane groups (N = 32 G); EG epilogue groups as in the decode.
@@ -407,6 +418,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bc = static_cast<uint32_t>(a.bc);
 
   if (threadIdx.x == 0) {
+    trace_mark(a.trace, false);
+    trace_cta(a.trace, 0);
     for (uint32_t i = 0; i < nst; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
@@ -442,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tslot;
   griddep_launch_dependents();
   griddep_wait();
+  if (threadIdx.x == 0) trace_cta(a.trace, 1);
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer: 4 matrix rows
@@ -512,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
       ptx::mbar_wait(&tfull[buf], bph);
       ptx::tc_fence_after();
+      if (it == 0 && issuer) trace_cta(a.trace, 2);
 #pragma unroll 1
       for (int j = 0; j < kMBW; ++j) {
         const int mb = mb0 + j;
@@ -561,6 +576,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) sched_done(a.sched, a.dyn0, nunits);
+  if (threadIdx.x == 0) {
+    trace_cta(a.trace, 3);
+    trace_mark(a.trace, true);
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, kTmemColsEnc<G>());
@@ -589,6 +608,7 @@ cudaError_t launch_enc_tc(const CUtensorMap& tm, TcEncArgs a, cudaStream_t s) {
   if (grid > a.nunits) grid = a.nunits;
   if (grid < 1) return cudaSuccess;
   if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
+  a.trace = trace_next();
   return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, tm, a);
 }
 
@@ -619,6 +639,7 @@ struct TcRedArgs {
   int P, Pb;                   // Pb: planes per chunk of the Z box
   int64_t bc, upr, nunits;
   uint32_t nstages, nbuf, out_bytes, stage_bytes, rows_off;
+  Trace trace;
 };
 
 __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
@@ -666,6 +687,8 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
   const uint32_t bc = static_cast<uint32_t>(a.bc);
 
   if (threadIdx.x == 0) {
+    trace_mark(a.trace, false);
+    trace_cta(a.trace, 0);
     for (uint32_t i = 0; i < nst; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1 + kRedW);
@@ -712,6 +735,7 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
   const uint32_t tmem = *tslot;
   griddep_launch_dependents();
   griddep_wait();
+  if (threadIdx.x == 0) trace_cta(a.trace, 1);
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
@@ -788,6 +812,7 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
       const uint32_t I = u / upr, J0 = (u - I * upr) * TU;
       ptx::mbar_wait(&tfull[buf], bph);
       ptx::tc_fence_after();
+      if (it == 0 && issuer) trace_cta(a.trace, 2);
       if constexpr (ENC) {
 #pragma unroll 1
         for (int mb = 0; mb < kUMB; ++mb) {
@@ -962,6 +987,10 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
   __syncwarp();
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) {
+    trace_cta(a.trace, 3);
+    trace_mark(a.trace, true);
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, kTcols);
@@ -993,6 +1022,7 @@ cudaError_t launch_red_tc(const CUtensorMap& tz, const CUtensorMap& to, TcRedArg
   int64_t grid = sm_count();
   if (grid > a.nunits) grid = a.nunits;
   if (grid < 1) return cudaSuccess;
+  a.trace = trace_next();
   e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreadsRed), smem, s, tz, to, a);
   if (e != cudaSuccess) return e;
   return sum_partials(a.red_partial, static_cast<int>(grid), a.P * 16, red_out, s);
@@ -1032,6 +1062,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t nunits = static_cast<uint32_t>(a.nunits), upr = static_cast<uint32_t>(a.upr);
 
   if (threadIdx.x == 0) {
+    trace_mark(a.trace, false);
+    trace_cta(a.trace, 0);
     for (uint32_t i = 0; i < nst; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
@@ -1069,6 +1101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tslot;
   griddep_launch_dependents();
   griddep_wait();
+  if (threadIdx.x == 0) trace_cta(a.trace, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1128,6 +1161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
       ptx::mbar_wait(&tfull[buf], bph);
       ptx::tc_fence_after();
+      if (it == 0 && issuer) trace_cta(a.trace, 2);
 #pragma unroll 1
       for (int mb = 0; mb < kMB; ++mb) {
         const uint32_t m = mb * 128 + quarter * 32 + lane;  // tile of the unit
@@ -1174,6 +1208,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) sched_done(a.sched, a.dyn0, nunits);
+  if (threadIdx.x == 0) {
+    trace_cta(a.trace, 3);
+    trace_mark(a.trace, true);
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, kTc);
@@ -1203,6 +1241,7 @@ cudaError_t launch_remix_tc(const CUtensorMap& ti, const CUtensorMap& to, TcEncA
   if (grid > a.nunits) grid = a.nunits;
   if (grid < 1) return cudaSuccess;
   if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
+  a.trace = trace_next();
   return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, ti, to, a, e_x, d);
 }
 
