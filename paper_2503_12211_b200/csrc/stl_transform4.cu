@@ -539,8 +539,40 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 }  // namespace
 
+// out[o] = sum_b partial[b][o], 32 outputs per block: warp w sums partials b = w, w + 16, ...
+// of its lane's output (each warp load one 128-byte row segment, all of a thread's loads
+// independent), then lane l of warp 0 adds the 16 warp sums in order — a fixed order
+// (deterministic); 12 blocks for the r = 24 reductions instead of 384 one-output trees.
+__global__ void __launch_bounds__(512) k_sum_partials_cols(const float* __restrict__ partial,
+                                                           int nblocks, int n,
+                                                           float* __restrict__ out) {
+  __shared__ float s[16][33];
+  griddep_launch_dependents();
+  griddep_wait();  // the partials of the preceding launch are complete (PDL)
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int o = blockIdx.x * 32 + l;
+  float v0 = 0.f, v1 = 0.f;
+  if (o < n) {
+    int b = w;
+    for (; b + 16 < nblocks; b += 32) {
+      v0 += partial[static_cast<int64_t>(b) * n + o];
+      v1 += partial[static_cast<int64_t>(b + 16) * n + o];
+    }
+    if (b < nblocks) v0 += partial[static_cast<int64_t>(b) * n + o];
+  }
+  s[w][l] = v0 + v1;
+  __syncthreads();
+  if (w == 0 && o < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t += s[k][l];
+    out[o] = t;
+  }
+}
+
 cudaError_t sum_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t s) {
-  return launch_pdl(k_sum_partials_tree, dim3(n), dim3(256), 0, s, partial, nblocks, n, out);
+  return launch_pdl(k_sum_partials_cols, dim3((n + 31) / 32), dim3(512), 0, s, partial, nblocks,
+                    n, out);
 }
 
 // Fast-path dispatch; returns cudaErrorNotSupported when the generic kernels must be used.
