@@ -640,7 +640,13 @@ struct TcRedArgs {
   int64_t bc, upr, nunits;
   uint32_t nstages, nbuf, out_bytes, stage_bytes, rows_off;
   Trace trace;
+  unsigned* sched;   // dynamic tail: item counter (pair) of this launch's slot
+  uint32_t dyn0;     // first dynamically scheduled unit (>= nunits: all static)
+  uint32_t kitem;    // units per dynamic work item
+  uint32_t nitems;   // dynamic work items
 };
+constexpr uint32_t kNoItem = 0x7FFFFFFFu;
+constexpr uint32_t kBarBytesR = kBarBytes + kRing * 4;  // + the ring's work-item entries
 
 __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -682,6 +688,7 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
   uint64_t* rbar = tempty + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + kRing);
   volatile uint32_t* ring = tslot + 4;
+  volatile uint32_t* ritem = ring + kRing;  // work item | last-unit flag, or kNoItem
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t nunits = static_cast<uint32_t>(a.nunits), upr = static_cast<uint32_t>(a.upr);
   const uint32_t bc = static_cast<uint32_t>(a.bc);
@@ -739,17 +746,41 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
+    // static rounds, then work items of kitem consecutive units from the counter
+    uint32_t sk = 0, item = 0, jj = a.kitem;
+    bool dyn = false;
     for (uint32_t it = 0;; ++it) {
-      uint32_t u = blockIdx.x + it * gridDim.x;
-      if (u >= nunits) u = kNoUnit;
+      uint32_t u = kNoUnit;
       if (lane == 0) {
+        uint32_t info = kNoItem;
+        if (!dyn) {
+          u = blockIdx.x + sk * gridDim.x;
+          if (u < a.dyn0 && u < nunits) ++sk;
+          else dyn = true;
+        }
+        if (dyn) {
+          if (jj == a.kitem) {
+            item = a.nitems ? atomicAdd(a.sched, 1u) : kNoItem;
+            jj = 0;
+          }
+          u = item < a.nitems ? a.dyn0 + item * a.kitem + jj : kNoUnit;
+          if (u >= nunits) u = kNoUnit;
+          if (u != kNoUnit) {
+            const bool last = jj + 1 == a.kitem || u + 1 == nunits;
+            info = item | (last ? 0x80000000u : 0u);
+            ++jj;
+          }
+        }
         ring[it % kRing] = u;
+        ritem[it % kRing] = info;
         ptx::mbar_arrive(&rbar[it % kRing]);
         if (u == kNoUnit) {
           ring[(it + 1) % kRing] = u;
+          ritem[(it + 1) % kRing] = kNoItem;
           ptx::mbar_arrive(&rbar[(it + 1) % kRing]);
         }
       }
+      u = __shfl_sync(0xFFFFFFFFu, u, 0);
       if (u == kNoUnit) break;
       const uint32_t st = it % nst, ph = (it / nst) & 1;
       const uint32_t I = u / upr, J0 = (u - I * upr) * TU;
@@ -917,10 +948,48 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
       ok[mt][0] = 16 * mt + g < P;
       ok[mt][1] = 16 * mt + g + 8 < P;
     }
+    // per-warp fragments -> a dedicated smem region -> fixed-order sum over the warps -> one
+    // partial: this CTA's static units (slot blockIdx.x), then one per dynamic work item (slot
+    // grid + item), so every partial covers a fixed set of units whichever CTA ran it
+    const int n = P * 16;
+    float* s_red = reinterpret_cast<float*>(smem + s_b + kB + kBarBytesR);
+    auto flush = [&](uint32_t slot) {
+      float* mine = s_red + wr * n;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const int c = 8 * nt + 2 * q, p0 = 16 * mt + g, p1 = p0 + 8;
+          if (p0 < P) {
+            mine[p0 * 16 + c] = R[mt][nt][0];
+            mine[p0 * 16 + c + 1] = R[mt][nt][1];
+          }
+          if (p1 < P) {
+            mine[p1 * 16 + c] = R[mt][nt][2];
+            mine[p1 * 16 + c + 1] = R[mt][nt][3];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) R[mt][nt][k] = 0.f;
+        }
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * kRedW) : "memory");
+      for (int o = wr * 32 + lane; o < n; o += 32 * kRedW) {
+        float sum = s_red[o];
+#pragma unroll
+        for (int w = 1; w < kRedW; ++w) sum += s_red[w * n + o];
+        a.red_partial[static_cast<int64_t>(slot) * n + o] = sum;
+      }
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * kRedW) : "memory");
+    };
+    bool static_done = false;
     for (uint32_t it = 0;; ++it) {
       ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
       const uint32_t u = ring[it % kRing];
+      const uint32_t info = ritem[it % kRing];
       if (u == kNoUnit) break;
+      if (info != kNoItem && !static_done) {
+        flush(blockIdx.x);
+        static_done = true;
+      }
       const uint32_t st = it % nst, ph = (it / nst) & 1;
       const uint32_t J0 = (u - (u / upr) * upr) * TU;
       const int Tw = static_cast<int>(min(bc - J0, static_cast<uint32_t>(TU)));
@@ -957,36 +1026,14 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[st]);
+      if (info != kNoItem && (info >> 31)) flush(gridDim.x + (info & 0x7FFFFFFFu));
     }
-    // per-warp fragments -> a dedicated smem region -> fixed-order sum -> this CTA's partial
-    const int n = P * 16;
-    float* s_red = reinterpret_cast<float*>(smem + s_b + kB + kBarBytes);
-    float* mine = s_red + wr * n;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int c = 8 * nt + 2 * q, p0 = 16 * mt + g, p1 = p0 + 8;
-        if (p0 < P) {
-          mine[p0 * 16 + c] = R[mt][nt][0];
-          mine[p0 * 16 + c + 1] = R[mt][nt][1];
-        }
-        if (p1 < P) {
-          mine[p1 * 16 + c] = R[mt][nt][2];
-          mine[p1 * 16 + c + 1] = R[mt][nt][3];
-        }
-      }
-    asm volatile("bar.sync 3, %0;" ::"n"(32 * kRedW) : "memory");
-    for (int o = (warp - 2 - kEpi) * 32 + lane; o < n; o += 32 * kRedW) {
-      float sum = s_red[o];
-#pragma unroll
-      for (int w = 1; w < kRedW; ++w) sum += s_red[w * n + o];
-      a.red_partial[static_cast<int64_t>(blockIdx.x) * n + o] = sum;
-    }
+    if (!static_done) flush(blockIdx.x);
   }
   __syncwarp();
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) sched_done(a.sched, a.dyn0, nunits);
   if (threadIdx.x == 0) {
     trace_cta(a.trace, 3);
     trace_mark(a.trace, true);
@@ -1007,14 +1054,14 @@ cudaError_t launch_red_tc(const CUtensorMap& tz, const CUtensorMap& to, TcRedArg
   a.stage_bytes = (zbytes + 4 * (TU * 8 + kRowPadR) + 1023) / 1024 * 1024;
   a.out_bytes = ENC ? (static_cast<uint32_t>(a.P) * TU * 2 + 1023) / 1024 * 1024 : 4 * TU * 8;
   const uint32_t red_bytes = kRedW * a.P * 16 * 4;  // the per-warp partials
-  const uint32_t budget = 227 * 1024 - 1024 - kB - kBarBytes - red_bytes;
+  const uint32_t budget = 227 * 1024 - 1024 - kB - kBarBytesR - red_bytes;
   static const int nb_env = probe_env("STL_RED_TC_NBUF", 0);
   a.nbuf = nb_env >= 2 && nb_env <= 4 ? nb_env : 2;
   if (2 * a.nbuf * a.out_bytes + 2 * a.stage_bytes > budget) return cudaErrorNotSupported;
   const uint32_t ns = (budget - 2 * a.nbuf * a.out_bytes) / a.stage_bytes;
   a.nstages = ns > kMaxSt ? kMaxSt : ns;
   const uint32_t smem =
-      a.nstages * a.stage_bytes + 2 * a.nbuf * a.out_bytes + kB + kBarBytes + red_bytes + 1024;
+      a.nstages * a.stage_bytes + 2 * a.nbuf * a.out_bytes + kB + kBarBytesR + red_bytes + 1024;
   auto k = k_red_tc<ENC, TU, NK, MT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -1022,10 +1069,26 @@ cudaError_t launch_red_tc(const CUtensorMap& tz, const CUtensorMap& to, TcRedArg
   int64_t grid = sm_count();
   if (grid > a.nunits) grid = a.nunits;
   if (grid < 1) return cudaSuccess;
+  // Probe STL_RED_DYN=1: a dynamic tail (the last third of the rounds as work items of >= 4
+  // units, at most kRedBlocks - grid of them, each with its own partial so the sum stays
+  // bit-reproducible). Measured slower at config 2 (decode_gu + g_ex 53.8 -> 59.7 us: the
+  // per-item partial flushes; profiles/r02_red_dyn_ab.log), so the product runs static.
+  if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
+  static const int red_dyn = probe_env("STL_RED_DYN", 0);
+  a.kitem = 4;
+  a.nitems = 0;
+  if (!red_dyn || a.dyn0 >= a.nunits) {
+    a.dyn0 = static_cast<uint32_t>(a.nunits);
+  } else {
+    const uint32_t ndyn = static_cast<uint32_t>(a.nunits) - a.dyn0;
+    const uint32_t cap = static_cast<uint32_t>(kRedBlocks - grid);
+    if (ndyn > a.kitem * cap) a.kitem = (ndyn + cap - 1) / cap;
+    a.nitems = (ndyn + a.kitem - 1) / a.kitem;
+  }
   a.trace = trace_next();
   e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreadsRed), smem, s, tz, to, a);
   if (e != cudaSuccess) return e;
-  return sum_partials(a.red_partial, static_cast<int>(grid), a.P * 16, red_out, s);
+  return sum_partials(a.red_partial, static_cast<int>(grid + a.nitems), a.P * 16, red_out, s);
 }
 
 // ------------------------------------------------------------------ remix (fused chain)
