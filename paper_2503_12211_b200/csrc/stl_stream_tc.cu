@@ -17,6 +17,7 @@
 // the SMs clock lower and the mma.sync decode's consumers set its pace.
 // Warp roles: 0 = TMA producer, 1 = MMA issuer (and TMEM owner), 2..9 = epilogue.
 #include <cstdio>
+#include <mutex>
 #include "sm100_ptx.cuh"
 #include "stl_internal.h"
 
@@ -292,19 +293,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Counter pairs for the dynamic tail (one pool per device, slots round robin over launches: a
 // slot comes back after 256 launches, long after its launch finished and reset it).
 constexpr int kSchedSlots = 256;
+// Host threads may launch concurrently (one mutex around the pool and the slot counter); a
+// first call inside a stream capture cannot allocate and falls back to the mma.sync kernels.
+std::mutex g_sched_mu;
 template <typename A>
 bool set_schedule(A& a, uint32_t grid) {
   static unsigned* pools[64] = {};
-  static int next[64] = {};
+  static uint32_t next[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
-  if (!pools[dev]) {
-    unsigned* p = nullptr;
-    if (cudaMalloc(&p, 2 * kSchedSlots * sizeof(unsigned)) != cudaSuccess) return false;
-    if (cudaMemset(p, 0, 2 * kSchedSlots * sizeof(unsigned)) != cudaSuccess) return false;
-    pools[dev] = p;
+  {
+    std::lock_guard<std::mutex> lock(g_sched_mu);
+    if (!pools[dev]) {
+      unsigned* p = nullptr;
+      if (cudaMalloc(&p, 2 * kSchedSlots * sizeof(unsigned)) != cudaSuccess) return false;
+      if (cudaMemset(p, 0, 2 * kSchedSlots * sizeof(unsigned)) != cudaSuccess) {
+        cudaFree(p);
+        return false;
+      }
+      pools[dev] = p;
+    }
+    a.sched = pools[dev] + 2 * (next[dev]++ % kSchedSlots);
   }
-  a.sched = pools[dev] + 2 * (next[dev]++ % kSchedSlots);
   // trailing rounds taken dynamically: a third of them (measured: 8192^3 with 55 rounds per CTA
   // best at 12-24 dynamic rounds, config 2 with 28 at 8-12; all-dynamic loses the lock-step
   // DRAM locality: profiles/r02_tc_dyn_ab.log). Probe STL_TC_DYN: 0 = static, -1 = all dynamic.
