@@ -148,19 +148,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tm_in);
   if (warp == 1) ptx::tmem_alloc(tslot, kTmemCols);
-  // B = [D_hi | D_lo]: row n < 16 holds the hi halves of decoder column n, row 16 + n the lo
-  // halves; K runs along the 128-byte row (16 elements per step), 16-byte chunks XOR-swizzled
-  // by (n & 7).
-  for (int i = threadIdx.x; i < 32 * 64; i += kThreads) {
-    const int n = i >> 6, k = i & 63, c = n & 15, st = k >> 4;
-    const int pl = (st == 0 ? 0 : Pb - 16) + (k & 15);
-    const float d = st < KS && pl < a.P && pl >= 16 * st ? a.coef[pl * 16 + c] : 0.f;
-    const __nv_bfloat16 hi = __float2bfloat16_rn(d);
-    const __nv_bfloat16 v = n < 16 ? hi : __float2bfloat16_rn(d - __bfloat162float(hi));
-    const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
-    *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
-  }
-  ptx::fence_proxy_async_smem();  // the generic-proxy B writes, before the UMMAs read them
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -168,6 +155,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   griddep_launch_dependents();
   griddep_wait();
   if (threadIdx.x == 0) trace_cta(a.trace, 1);  // the planes of this launch are complete (PDL)
+  // The UMMA B operand, after griddep_wait (the coefficients may come from the previous
+  // launch) and off the producer's path: the first loads are in flight while it is built;
+  // the MMA issuer meets the other non-producer warps at a named barrier before its first MMA.
+  if (warp != 0) {
+    // B = [D_hi | D_lo]: row n < 16 holds the hi halves of decoder column n, row 16 + n the lo
+    // halves; K runs along the 128-byte row (16 elements per step), 16-byte chunks XOR-swizzled
+    // by (n & 7).
+    for (int i = threadIdx.x - 32; i < 32 * 64; i += kThreads - 32) {
+      const int n = i >> 6, k = i & 63, c = n & 15, st = k >> 4;
+      const int pl = (st == 0 ? 0 : Pb - 16) + (k & 15);
+      const float d = st < KS && pl < a.P && pl >= 16 * st ? a.coef[pl * 16 + c] : 0.f;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(d);
+      const __nv_bfloat16 v = n < 16 ? hi : __float2bfloat16_rn(d - __bfloat162float(hi));
+      const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
+      *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
+    }
+    ptx::fence_proxy_async_smem();  // generic-proxy B writes -> the UMMAs (async proxy)
+    asm volatile("bar.sync 5, %0;" ::"n"(kThreads - 32) : "memory");
+  }
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
@@ -443,22 +449,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tm_out);
   if (warp == 1) ptx::tmem_alloc(tslot, kTmemColsEnc<G>());
-  for (int i = threadIdx.x; i < N * 32; i += kThreads) {
-    const int n = i >> 5, k = i & 31;
-    const int g = n >> 5, par = (n >> 4) & 1, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
-    const int ka = k >> 3, kpar = (k >> 2) & 1, kb = k & 3;
-    const float e = kpar == par && p < P ? a.coef[p * 16 + 4 * ka + kb] : 0.f;
-    const __nv_bfloat16 hi = __float2bfloat16_rn(e);
-    const __nv_bfloat16 v = hl == 0 ? hi : __float2bfloat16_rn(e - __bfloat162float(hi));
-    const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
-    *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
-  }
-  for (int i = threadIdx.x; i < N * 32; i += kThreads) {  // K 32..63 of each B row: zero
-    const int n = i >> 5, k = 32 + (i & 31);
-    const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
-    *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = __float2bfloat16_rn(0.f);
-  }
-  ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -466,6 +456,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   griddep_launch_dependents();
   griddep_wait();
   if (threadIdx.x == 0) trace_cta(a.trace, 1);
+  // The UMMA B operand, after griddep_wait (the coefficients may come from the previous
+  // launch) and off the producer's path: the first loads are in flight while it is built;
+  // the MMA issuer meets the other non-producer warps at a named barrier before its first MMA.
+  if (warp != 0) {
+    for (int i = threadIdx.x - 32; i < N * 32; i += kThreads - 32) {
+      const int n = i >> 5, k = i & 31;
+      const int g = n >> 5, par = (n >> 4) & 1, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
+      const int ka = k >> 3, kpar = (k >> 2) & 1, kb = k & 3;
+      const float e = kpar == par && p < P ? a.coef[p * 16 + 4 * ka + kb] : 0.f;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(e);
+      const __nv_bfloat16 v = hl == 0 ? hi : __float2bfloat16_rn(e - __bfloat162float(hi));
+      const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
+      *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
+    }
+    for (int i = threadIdx.x - 32; i < N * 32; i += kThreads - 32) {  // K 32..63 of each B row: zero
+      const int n = i >> 5, k = 32 + (i & 31);
+      const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
+      *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = __float2bfloat16_rn(0.f);
+    }
+    ptx::fence_proxy_async_smem();  // generic-proxy B writes -> the UMMAs (async proxy)
+    asm volatile("bar.sync 5, %0;" ::"n"(kThreads - 32) : "memory");
+  }
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer: 4 matrix rows
@@ -722,30 +734,6 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
     if constexpr (ENC) ptx::prefetch_tmap(&tm_out);
   }
   if (warp == 1) ptx::tmem_alloc(tslot, kTcols);
-  // the UMMA B operand (as in k_encode_tc / k_decode_tc)
-  if constexpr (ENC) {
-    for (int i = threadIdx.x; i < N * 64; i += kThreadsRed) {
-      const int n = i >> 6, k = i & 63;
-      const int g = n >> 5, par = (n >> 4) & 1, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
-      const int ka = k >> 3, kpar = (k >> 2) & 1, kb = k & 3;
-      const float e = k < 32 && kpar == par && p < P ? a.coef[p * 16 + 4 * ka + kb] : 0.f;
-      const __nv_bfloat16 hi = __float2bfloat16_rn(e);
-      const __nv_bfloat16 v = hl == 0 ? hi : __float2bfloat16_rn(e - __bfloat162float(hi));
-      const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
-      *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
-    }
-  } else {
-    for (int i = threadIdx.x; i < 32 * 64; i += kThreadsRed) {
-      const int n = i >> 6, k = i & 63, c = n & 15, st = k >> 4;
-      const int pl = (st == 0 ? 0 : Pb - 16) + (k & 15);
-      const float d = st < NK && pl < P && pl >= 16 * st ? a.coef[pl * 16 + c] : 0.f;
-      const __nv_bfloat16 hi = __float2bfloat16_rn(d);
-      const __nv_bfloat16 v = n < 16 ? hi : __float2bfloat16_rn(d - __bfloat162float(hi));
-      const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
-      *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
-    }
-  }
-  ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -753,6 +741,36 @@ __global__ void __launch_bounds__(kThreadsRed, 1)
   griddep_launch_dependents();
   griddep_wait();
   if (threadIdx.x == 0) trace_cta(a.trace, 1);
+  // The UMMA B operand, after griddep_wait (the coefficients may come from the previous
+  // launch) and off the producer's path: the first loads are in flight while it is built;
+  // the MMA issuer meets the other non-producer warps at a named barrier before its first MMA.
+  if (warp != 0) {
+    // the UMMA B operand (as in k_encode_tc / k_decode_tc)
+    if constexpr (ENC) {
+      for (int i = threadIdx.x - 32; i < N * 64; i += kThreadsRed - 32) {
+        const int n = i >> 6, k = i & 63;
+        const int g = n >> 5, par = (n >> 4) & 1, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
+        const int ka = k >> 3, kpar = (k >> 2) & 1, kb = k & 3;
+        const float e = k < 32 && kpar == par && p < P ? a.coef[p * 16 + 4 * ka + kb] : 0.f;
+        const __nv_bfloat16 hi = __float2bfloat16_rn(e);
+        const __nv_bfloat16 v = hl == 0 ? hi : __float2bfloat16_rn(e - __bfloat162float(hi));
+        const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
+        *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
+      }
+    } else {
+      for (int i = threadIdx.x - 32; i < 32 * 64; i += kThreadsRed - 32) {
+        const int n = i >> 6, k = i & 63, c = n & 15, st = k >> 4;
+        const int pl = (st == 0 ? 0 : Pb - 16) + (k & 15);
+        const float d = st < NK && pl < P && pl >= 16 * st ? a.coef[pl * 16 + c] : 0.f;
+        const __nv_bfloat16 hi = __float2bfloat16_rn(d);
+        const __nv_bfloat16 v = n < 16 ? hi : __float2bfloat16_rn(d - __bfloat162float(hi));
+        const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
+        *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
+      }
+    }
+    ptx::fence_proxy_async_smem();  // generic-proxy B writes -> the UMMAs (async proxy)
+    asm volatile("bar.sync 5, %0;" ::"n"(kThreadsRed - 32) : "memory");
+  }
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
@@ -1153,21 +1171,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tm_out);
   }
   if (warp == 1) ptx::tmem_alloc(tslot, kTc);
-  for (int i = threadIdx.x; i < N * 64; i += kThreads) {
-    const int n = i >> 6, k = i & 63, st = k >> 4;
-    const int g = n >> 4, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
-    const int q = (st == 0 ? 0 : Pb - 16) + (k & 15);
-    float c = 0.f;
-    if (st < KS && p < P && q < P && q >= 16 * st) {
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) c = fmaf(e_x[p * 16 + kk], dcoef[q * 16 + kk], c);
-    }
-    const __nv_bfloat16 hi = __float2bfloat16_rn(c);
-    const __nv_bfloat16 v = hl == 0 ? hi : __float2bfloat16_rn(c - __bfloat162float(hi));
-    const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
-    *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
-  }
-  ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -1175,6 +1178,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   griddep_launch_dependents();
   griddep_wait();
   if (threadIdx.x == 0) trace_cta(a.trace, 1);
+  // The UMMA B operand, after griddep_wait (the coefficients may come from the previous
+  // launch) and off the producer's path: the first loads are in flight while it is built;
+  // the MMA issuer meets the other non-producer warps at a named barrier before its first MMA.
+  if (warp != 0) {
+    for (int i = threadIdx.x - 32; i < N * 64; i += kThreads - 32) {
+      const int n = i >> 6, k = i & 63, st = k >> 4;
+      const int g = n >> 4, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
+      const int q = (st == 0 ? 0 : Pb - 16) + (k & 15);
+      float c = 0.f;
+      if (st < KS && p < P && q < P && q >= 16 * st) {
+  #pragma unroll
+        for (int kk = 0; kk < 16; ++kk) c = fmaf(e_x[p * 16 + kk], dcoef[q * 16 + kk], c);
+      }
+      const __nv_bfloat16 hi = __float2bfloat16_rn(c);
+      const __nv_bfloat16 v = hl == 0 ? hi : __float2bfloat16_rn(c - __bfloat162float(hi));
+      const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
+      *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
+    }
+    ptx::fence_proxy_async_smem();  // generic-proxy B writes -> the UMMAs (async proxy)
+    asm volatile("bar.sync 5, %0;" ::"n"(kThreads - 32) : "memory");
+  }
 
   if (warp == 0) {
     if (lane == 0) {
