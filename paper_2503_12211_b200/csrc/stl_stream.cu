@@ -349,6 +349,8 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     ptx::fence_mbar_init();
   }
   griddep_launch_dependents();
+  // e_x / d (remix) and every input may be the previous launch's output (PDL)
+  if constexpr (MODE == kRemix) griddep_wait();
   if constexpr (MODE == kRemix) {
     // the fused-step composite C = e_x d^T (P x P, fp32) into the (not yet used) output staging;
     // the consumers read their B fragments from it (a named barrier after the fragment setup
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(32 * CW + 32, 1)
     if constexpr (out_planes<MODE>()) ptx::prefetch_tmap(&tm_out);
   }
   __syncthreads();
-  griddep_wait();  // inputs of this launch are complete (PDL)
+  if constexpr (MODE != kRemix) griddep_wait();  // inputs of this launch are complete (PDL)
   if (threadIdx.x == 0) trace_cta(args.trace, 1);
 
   if (warp == kCWarps) {
