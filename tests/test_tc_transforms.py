@@ -99,3 +99,49 @@ def test_tc_remix_chain(r):
         h64 = O.stl_fused_step(h64, w6, e_x, d)
     got = stl.decode_tiles(h, snf.d, t)
     assert rel(got, O.decode_tiles(h64, d, t)) <= 1e-2
+
+
+def test_tc_strided_and_concurrent():
+    """Through the C ABI: a matrix with a padded leading dimension (ld = cols + 64) into and out of
+    the tcgen05 encode / decode, and the same encode launched on two streams at once many times
+    (the dynamic tail's counter slots must not collide): every result bit-identical."""
+    from paper_2503_12211_b200 import _lib
+
+    lib = _lib.load()
+    dev = torch.device("cuda")
+    rows, cols, ld, r = 64, 4096, 4096 + 64, 24
+    rng = O.make_rng(41)
+    e_x, _, d = O.random_gaussian_init(4, r, rng, scale=0.5)
+    ex = torch.tensor(e_x, dtype=torch.float32, device=dev)
+    dd = torch.tensor(d, dtype=torch.float32, device=dev)
+    m_dev, m64 = bf(rng.standard_normal((rows, cols)))
+    wide = torch.zeros((rows, ld), dtype=torch.bfloat16, device=dev)
+    wide[:, :cols] = m_dev
+    planes = torch.empty((r, rows // 4, cols // 4), dtype=torch.bfloat16, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.stl_encode(wide.data_ptr(), _lib.STL_BF16, rows, cols, ld, ex.data_ptr(), 4, r,
+                              planes.data_ptr(), _lib.STL_BF16, s))
+    ref_enc = O.encode_tiles(m64, e_x, 4)
+    assert rel(planes.permute(1, 2, 0), ref_enc) <= 5e-3
+    out = torch.full((rows, ld), 7.0, dtype=torch.bfloat16, device=dev)
+    _lib.check(lib.stl_decode(planes.data_ptr(), _lib.STL_BF16, rows // 4, cols // 4, r,
+                              dd.data_ptr(), 4, out.data_ptr(), _lib.STL_BF16, ld, s))
+    torch.cuda.synchronize()
+    enc64 = planes.permute(1, 2, 0).double().cpu().numpy()
+    assert rel(out[:, :cols], O.decode_tiles(enc64, d, 4)) <= 5e-3
+    assert torch.all(out[:, cols:] == 7.0)  # the padding columns are never written
+
+    big = torch.randn((4096, 4096), device=dev).to(torch.bfloat16)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = [torch.empty((r, 1024, 1024), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    torch.cuda.synchronize()
+    _lib.check(lib.stl_encode(big.data_ptr(), _lib.STL_BF16, 4096, 4096, 4096, ex.data_ptr(), 4, r,
+                              outs[0].data_ptr(), _lib.STL_BF16, s))
+    torch.cuda.synchronize()
+    ref = outs[0].clone()
+    for _ in range(50):
+        for st, o in zip((s1, s2), outs):
+            _lib.check(lib.stl_encode(big.data_ptr(), _lib.STL_BF16, 4096, 4096, 4096, ex.data_ptr(),
+                                      4, r, o.data_ptr(), _lib.STL_BF16, st.cuda_stream))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], ref) and torch.equal(outs[1], ref)
