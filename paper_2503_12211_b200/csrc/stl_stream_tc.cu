@@ -110,8 +110,8 @@ __device__ __forceinline__ void epi_bar(int grp, int nthreads) {
 // the previous step's planes, whose B rows it then carries as zeros).
 // EG = epilogue groups: 1 (all 8 warps per unit, each a half of the M-blocks) or 2 (4 warps per
 // unit, alternate units: two units' read-back, staging and stores in flight).
-template <int KS, int EG>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int KS, int EG, int EPW = kEpi>
+__global__ void __launch_bounds__(32 * (2 + EPW), 1)
     k_decode_tc(const __grid_constant__ CUtensorMap tm_in, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   volatile uint32_t* ring = tslot + 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t nunits = static_cast<uint32_t>(a.nunits), upr = static_cast<uint32_t>(a.upr);
-  constexpr int kGW = kEpi / EG;  // warps per epilogue group
+  constexpr int kGW = EPW / EG;  // warps per epilogue group
 
   if (threadIdx.x == 0) {
     trace_mark(a.trace, false);
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // B = [D_hi | D_lo]: row n < 16 holds the hi halves of decoder column n, row 16 + n the lo
     // halves; K runs along the 128-byte row (16 elements per step), 16-byte chunks XOR-swizzled
     // by (n & 7).
-    for (int i = threadIdx.x - 32; i < 32 * 64; i += kThreads - 32) {
+    for (int i = threadIdx.x - 32; i < 32 * 64; i += 32 * (2 + EPW) - 32) {
       const int n = i >> 6, k = i & 63, c = n & 15, st = k >> 4;
       const int pl = (st == 0 ? 0 : Pb - 16) + (k & 15);
       const float d = st < KS && pl < a.P && pl >= 16 * st ? a.coef[pl * 16 + c] : 0.f;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
     }
     ptx::fence_proxy_async_smem();  // generic-proxy B writes -> the UMMAs (async proxy)
-    asm volatile("bar.sync 5, %0;" ::"n"(kThreads - 32) : "memory");
+    asm volatile("bar.sync 5, %0;" ::"n"(32 * (2 + EPW) - 32) : "memory");
   }
 
   if (warp == 0) {
@@ -332,7 +332,7 @@ bool set_schedule(A& a, uint32_t grid) {
   return true;
 }
 
-template <int KS, int EG>
+template <int KS, int EG, int EPW = kEpi>
 cudaError_t launch_tc(const CUtensorMap& tm, TcArgs a, cudaStream_t s) {
   const uint32_t kStage = static_cast<uint32_t>(a.Pb) * kT * 2;
   const uint32_t budget = 227 * 1024 - 1024 - kBBytes - kBarBytes;
@@ -344,7 +344,7 @@ cudaError_t launch_tc(const CUtensorMap& tm, TcArgs a, cudaStream_t s) {
   a.nstages = ns > kMaxSt ? kMaxSt : ns;
   if (st_env >= 2 && static_cast<uint32_t>(st_env) < a.nstages) a.nstages = st_env;
   const uint32_t smem = a.nstages * kStage + EG * a.nbuf * kOutBytes + kBBytes + kBarBytes + 1024;
-  auto k = k_decode_tc<KS, EG>;
+  auto k = k_decode_tc<KS, EG, EPW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -353,7 +353,7 @@ cudaError_t launch_tc(const CUtensorMap& tm, TcArgs a, cudaStream_t s) {
   if (grid < 1) return cudaSuccess;
   if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
   a.trace = trace_next();
-  return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, tm, a);
+  return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(32 * (2 + EPW)), smem, s, tm, a);
 }
 
 // ------------------------------------------------------------------ encode
@@ -407,8 +407,8 @@ struct TcEncArgs {
 };
 
 // G = 8-plane groups (N = 32 G); EG epilogue groups as in the decode.
-template <int G, int EG>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int G, int EG, int EPW = kEpi>
+__global__ void __launch_bounds__(32 * (2 + EPW), 1)
     k_encode_tc(const __grid_constant__ CUtensorMap tm_out, TcEncArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int N = 32 * G;
   constexpr uint32_t kStage = 4 * kERow;
   constexpr uint32_t kB = N * 128;
-  constexpr int kGW = kEpi / EG;
+  constexpr int kGW = EPW / EG;
   constexpr int kEMB = 2;  // M-blocks (128 tile pairs) per unit
   const uint32_t nst = a.nstages, nbuf = a.nbuf, ob_bytes = a.out_bytes;
   const uint32_t s_out = nst * kStage;
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // launch) and off the producer's path: the first loads are in flight while it is built;
   // the MMA issuer meets the other non-producer warps at a named barrier before its first MMA.
   if (warp != 0) {
-    for (int i = threadIdx.x - 32; i < N * 32; i += kThreads - 32) {
+    for (int i = threadIdx.x - 32; i < N * 32; i += 32 * (2 + EPW) - 32) {
       const int n = i >> 5, k = i & 31;
       const int g = n >> 5, par = (n >> 4) & 1, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
       const int ka = k >> 3, kpar = (k >> 2) & 1, kb = k & 3;
@@ -470,13 +470,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
       *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
     }
-    for (int i = threadIdx.x - 32; i < N * 32; i += kThreads - 32) {  // K 32..63 of each B row: zero
+    for (int i = threadIdx.x - 32; i < N * 32; i += 32 * (2 + EPW) - 32) {  // K 32..63 of each B row: zero
       const int n = i >> 5, k = 32 + (i & 31);
       const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
       *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = __float2bfloat16_rn(0.f);
     }
     ptx::fence_proxy_async_smem();  // generic-proxy B writes -> the UMMAs (async proxy)
-    asm volatile("bar.sync 5, %0;" ::"n"(kThreads - 32) : "memory");
+    asm volatile("bar.sync 5, %0;" ::"n"(32 * (2 + EPW) - 32) : "memory");
   }
 
   if (warp == 0) {
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int G, int EG>
+template <int G, int EG, int EPW = kEpi>
 cudaError_t launch_enc_tc(const CUtensorMap& tm, TcEncArgs a, cudaStream_t s) {
   constexpr uint32_t kStage = 4 * kERow;
   constexpr uint32_t kB = 32 * G * 128;
@@ -622,7 +622,7 @@ cudaError_t launch_enc_tc(const CUtensorMap& tm, TcEncArgs a, cudaStream_t s) {
   a.nstages = ns > kMaxSt ? kMaxSt : ns;
   if (st_env >= 2 && static_cast<uint32_t>(st_env) < a.nstages) a.nstages = st_env;
   const uint32_t smem = a.nstages * kStage + EG * a.nbuf * a.out_bytes + kB + kBarBytes + 1024;
-  auto k = k_encode_tc<G, EG>;
+  auto k = k_encode_tc<G, EG, EPW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -631,7 +631,7 @@ cudaError_t launch_enc_tc(const CUtensorMap& tm, TcEncArgs a, cudaStream_t s) {
   if (grid < 1) return cudaSuccess;
   if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
   a.trace = trace_next();
-  return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, tm, a);
+  return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(32 * (2 + EPW)), smem, s, tm, a);
 }
 
 // ------------------------------------------------------------------ fused reductions
@@ -1125,8 +1125,10 @@ cudaError_t launch_red_tc(const CUtensorMap& tz, const CUtensorMap& to, TcRedArg
 // B[q][n] = C split into bf16 hi + lo, n = 16 g + 8 hl + pp (output plane p = 8 g + pp), so a
 // 32x32b.x16 read-back holds a group's hi and lo columns; the epilogue writes the output planes
 // into a swizzled box for one TMA store. C is formed in the kernel prologue.
-template <int KS, int G>
-__global__ void __launch_bounds__(kThreads, 1)
+// GW = epilogue warps per group: 4 (each warp all 4 M-blocks of its TMEM lane quarter) or 8
+// (two warps per quarter, 2 M-blocks each).
+template <int KS, int G, int GW>
+__global__ void __launch_bounds__(32 * (2 + 2 * GW), 1)
     k_remix_tc(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                TcEncArgs a, const float* __restrict__ e_x, const float* __restrict__ dcoef) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1135,7 +1137,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int N = 16 * G;
   constexpr uint32_t kB = N * 128 < 1024 ? 1024 : N * 128;
   constexpr uint32_t kTc = 2 * kMB * N <= 256 ? 256u : 512u;
-  constexpr int kGW = kEpi / 2;
+  constexpr int kGW = GW;
+  constexpr int kThr = 32 * (2 + 2 * GW);
   const int P = a.P;
   const int Pb = P <= 16 ? 16 : (P + 7) / 8 * 8;
   const uint32_t kStage = static_cast<uint32_t>(Pb) * kT * 2;
@@ -1182,7 +1185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // launch) and off the producer's path: the first loads are in flight while it is built;
   // the MMA issuer meets the other non-producer warps at a named barrier before its first MMA.
   if (warp != 0) {
-    for (int i = threadIdx.x - 32; i < N * 64; i += kThreads - 32) {
+    for (int i = threadIdx.x - 32; i < N * 64; i += kThr - 32) {
       const int n = i >> 6, k = i & 63, st = k >> 4;
       const int g = n >> 4, hl = (n >> 3) & 1, p = 8 * g + (n & 7);
       const int q = (st == 0 ? 0 : Pb - 16) + (k & 15);
@@ -1197,7 +1200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
     }
     ptx::fence_proxy_async_smem();  // generic-proxy B writes -> the UMMAs (async proxy)
-    asm volatile("bar.sync 5, %0;" ::"n"(kThreads - 32) : "memory");
+    asm volatile("bar.sync 5, %0;" ::"n"(kThr - 32) : "memory");
   }
 
   if (warp == 0) {
@@ -1259,8 +1262,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(&tfull[buf], bph);
       ptx::tc_fence_after();
       if (it == 0 && issuer) trace_cta(a.trace, 2);
+      constexpr int kMBW = kMB * 4 / kGW;  // M-blocks per warp
+      const int mb0 = (gw >> 2) * kMBW;
 #pragma unroll 1
-      for (int mb = 0; mb < kMB; ++mb) {
+      for (int mb = mb0; mb < mb0 + kMBW; ++mb) {
         const uint32_t m = mb * 128 + quarter * 32 + lane;  // tile of the unit
         const uint32_t chunk = m >> 6, byte = (m & 63) * 2;
 #pragma unroll
@@ -1273,7 +1278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::tmem_ld_32x32b_x16(tmem + ((quarter * 32) << 16) + buf * (kMB * N) + mb * N + 16 * (g0 + h), uu);
             }
           ptx::tmem_ld_wait();
-          if (mb == kMB - 1 && g0 + 2 >= G) {
+          if (mb == mb0 + kMBW - 1 && g0 + 2 >= G) {
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
@@ -1315,9 +1320,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int KS, int G>
+// 8 epilogue warps per group (8192^2 remix 95.6 -> 93.5 us, profiles/r02_remix_gw_ab.log);
+// probe STL_REMIX_TC_GW=4: 4
+template <int KS, int G, int GW = 8>
 cudaError_t launch_remix_tc(const CUtensorMap& ti, const CUtensorMap& to, TcEncArgs a,
                             const float* e_x, const float* d, cudaStream_t s) {
+  static const int gw4 = probe_env("STL_REMIX_TC_GW", 8) == 4;
+  if constexpr (GW == 8)
+    if (gw4) return launch_remix_tc<KS, G, 4>(ti, to, a, e_x, d, s);
   constexpr int N = 16 * G;
   constexpr uint32_t kB = N * 128 < 1024 ? 1024 : N * 128;
   const int Pb = a.P <= 16 ? 16 : (a.P + 7) / 8 * 8;
@@ -1330,7 +1340,7 @@ cudaError_t launch_remix_tc(const CUtensorMap& ti, const CUtensorMap& to, TcEncA
   const uint32_t ns = (budget - 2 * a.nbuf * a.out_bytes) / kStage;
   a.nstages = ns > kMaxSt ? kMaxSt : ns;
   const uint32_t smem = a.nstages * kStage + 2 * a.nbuf * a.out_bytes + kB + kBarBytes + 1024;
-  auto k = k_remix_tc<KS, G>;
+  auto k = k_remix_tc<KS, G, GW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -1339,7 +1349,8 @@ cudaError_t launch_remix_tc(const CUtensorMap& ti, const CUtensorMap& to, TcEncA
   if (grid < 1) return cudaSuccess;
   if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
   a.trace = trace_next();
-  return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, ti, to, a, e_x, d);
+  return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(32 * (2 + 2 * GW)), smem, s, ti, to, a,
+                    e_x, d);
 }
 
 }  // namespace
