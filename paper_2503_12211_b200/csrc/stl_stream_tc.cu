@@ -1,21 +1,27 @@
-// stl_stream_tc.cu — the t = 4 decode on the 5th-generation tensor cores (tcgen05 + TMEM).
+// stl_stream_tc.cu — the t = 4 tile transforms on the 5th-generation tensor cores (tcgen05 +
+// TMEM): the default bf16 path for r <= 32 and tile columns >= 512 (K10-K13).
 //
-//   tile(I, J)[c] = sum_p Z[p][I][J] D[p][c]          decode_tiles (snf_operator.py:88-96)
+//   k_decode_tc  tile(I, J)[c] = sum_p Z[p][I][J] D[p][c]        decode_tiles (snf_operator.py:88-96)
+//   k_encode_tc  planes[p][I][J] = sum_c E[p][c] tile(I, J)[c]   encode_tiles (snf_operator.py:80-85)
+//   k_red_tc     the decode plus g_ex = sum Z (x) X on mma.sync warps (toy_network.py:104-105)
+//   k_remix_tc   out[p] = sum_q (e_x d^T)[p][q] Z[q]             stl_fused_step (snf_operator.py:175-188)
 //
-// The same HBM stream as k_stream<kDec> (stl_stream.cu): a unit is a 512-tile segment of one
-// tile row, its P bf16 planes land in shared memory as one 4-D TMA box (64 tiles x Pb planes x 8
-// chunks, 128-byte swizzle) and its 4 output matrix rows leave as 1-D bulk stores. What changes
-// is who does the change of basis: instead of 16 consumer warps running mma.sync fragments, one
-// thread issues UMMAs straight on the landed box —
+// The same HBM streams as stl_stream.cu's k_stream: a unit is a 512-tile segment of one tile
+// row, its bf16 planes land in shared memory as one 4-D TMA box (64 tiles x Pb planes x 8
+// chunks, 128-byte swizzle), its 4 matrix rows as 1-D bulk copies, outputs leave by TMA / bulk
+// stores. What changes is who does the change of basis: instead of 16 consumer warps running
+// mma.sync fragments, one thread issues UMMAs straight on the landed data. Decode:
 //   D[tile m][n] = sum_p A[m][p] B[p][n],  A = the plane box read as an MN-major (tile-major)
 //   SW128 operand (64-tile atoms Pb * 128 bytes apart, 8-plane groups 1024 bytes apart),
 //   B = [D_hi | D_lo] (K-major, 32 columns: the decoder rows split into bf16 hi + lo),
-// M = 128 tiles per MMA, N = 32, K = 16 planes per step, fp32 accumulation in TMEM — and eight
+// M = 128 tiles per MMA, N = 32, K = 16 planes per step, fp32 accumulation in TMEM — and the
 // epilogue warps read the accumulators back (tcgen05.ld), add the hi and lo columns, round to
-// bf16 and stage the output rows for the bulk stores. The tensor pipe does the arithmetic the
-// SM's issue slots did before, which matters inside the forward pipeline: after the slice GEMM
-// the SMs clock lower and the mma.sync decode's consumers set its pace.
-// Warp roles: 0 = TMA producer, 1 = MMA issuer (and TMEM owner), 2..9 = epilogue.
+// bf16 and stage the output rows for the bulk stores (the encode's operand scheme is described
+// at k_encode_tc). The tensor pipe does the arithmetic the SM's issue slots did before, which
+// matters inside the forward pipeline: after the slice GEMM the SMs clock lower and the
+// mma.sync decode's consumers set its pace.
+// Warp roles: 0 = TMA producer, 1 = MMA issuer (and TMEM owner), 2..9 = two epilogue groups on
+// alternate units (k_red_tc: + 10..17 reduction warps; k_remix_tc: 2..17, 8 per group).
 #include <cstdio>
 #include <mutex>
 #include "sm100_ptx.cuh"
