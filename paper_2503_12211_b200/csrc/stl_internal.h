@@ -180,8 +180,9 @@ cudaError_t planes_to_tiles2(const void* in, int idt, int Q, int64_t br, int64_t
                              const float* coef, void* out, int odt, int64_t ldo, cudaStream_t s);
 // 4-D plane-box tensor map of the streaming transforms (stl_stream.cu): box {128 / zsz tiles,
 // Pb planes, kT * zsz / 128 chunks, 1 tile row}, 128-byte swizzle; prow >= br tile rows per plane.
+// R > 1 (narrow matrices, R * bc = kT): a box of R whole tile rows {W, Pb, bc / W, R}.
 bool plane_box_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_t br,
-                    int64_t bc, int kT, int64_t prow);
+                    int64_t bc, int kT, int64_t prow, int R = 1);
 // t = 4 decode on tcgen05 (stl_stream_tc.cu): P <= 32 bf16 planes -> bf16 matrix;
 // cudaErrorNotSupported -> the mma.sync streaming decode.
 cudaError_t planes_to_tiles_tc(const void* in, int P, int64_t br, int64_t bc, const float* coef,

@@ -1186,8 +1186,8 @@ cudaError_t tiles_to_planes_stream(const void* m, int mdt, int64_t ldm, int64_t 
 }
 
 bool plane_box_tmap(CUtensorMap* m, const void* base, int zsz, int P, int Pb, int64_t br,
-                    int64_t bc, int kT, int64_t prow) {
-  return plane_tmap(m, base, zsz, P, Pb, br, bc, kT, 1, prow);
+                    int64_t bc, int kT, int64_t prow, int R) {
+  return plane_tmap(m, base, zsz, P, Pb, br, bc, kT, R, prow);
 }
 
 // decode (+ g_ex-style reduction): fp32 or bf16 planes -> bf16 matrix; red matrix bf16.

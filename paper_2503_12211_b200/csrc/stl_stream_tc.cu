@@ -66,6 +66,18 @@ __device__ __forceinline__ void sched_done(unsigned* cnt, uint32_t dyn0, uint32_
   }
 }
 
+// first tile row and column of unit u: a 512-tile segment of one row, or (R > 1) R whole rows
+__device__ __forceinline__ void unit_coord(uint32_t u, uint32_t upr, uint32_t R, uint32_t& I,
+                                           uint32_t& J0) {
+  if (R > 1) {
+    I = u * R;
+    J0 = 0;
+  } else {
+    I = u / upr;
+    J0 = (u - I * upr) * 512u;
+  }
+}
+
 struct TcArgs {
   __nv_bfloat16* out;
   int64_t ldo;
@@ -73,6 +85,7 @@ struct TcArgs {
   int P, Pb;
   int64_t bc, upr, nunits;
   uint32_t nstages, nbuf;
+  uint32_t br, R;   // tile rows; R > 1: a unit is R whole tile rows (narrow matrices)
   unsigned* sched;  // counter pair of this launch's slot
   uint32_t dyn0;
   Trace trace;      // probe build: launch span
@@ -194,7 +207,8 @@ __global__ void __launch_bounds__(32 * (2 + EPW), 1)
           break;
         }
         const uint32_t st = it % nst, ph = (it / nst) & 1;
-        const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
+        uint32_t I, J0;
+        unit_coord(u, upr, a.R, I, J0);
         ptx::mbar_wait(&empty[st], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&full[st], kStage);
         tma_load_4d(&tm_in, &full[st], sbase + st * kStage, 0, 0, static_cast<int>(J0 / 64),
@@ -243,7 +257,8 @@ __global__ void __launch_bounds__(32 * (2 + EPW), 1)
       if (u == kNoUnit) break;
       const uint32_t buf = it & 1, bph = (it >> 1) & 1;
       const uint32_t ob0 = s_out + (grp * nbuf + k % nbuf) * kOutBytes;
-      const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
+      uint32_t I, J0;
+        unit_coord(u, upr, a.R, I, J0);
       ptx::mbar_wait(&tfull[buf], bph);
       ptx::tc_fence_after();
       if (it == 0 && issuer) trace_cta(a.trace, 2);
@@ -278,11 +293,20 @@ __global__ void __launch_bounds__(32 * (2 + EPW), 1)
       if (issuer) bulk_wait_read_n(nbuf - 2);
       epi_bar(grp, 32 * kGW);
       if (issuer) {
-        const uint32_t Tw = min(static_cast<uint32_t>(a.bc) - J0, static_cast<uint32_t>(kT));
+        if (a.R > 1) {  // R whole tile rows: row r of the unit at staging offset r * bc * 8
+          const uint32_t nrows = min(a.R, a.br - I), rb = static_cast<uint32_t>(a.bc) * 8;
+          for (uint32_t rr = 0; rr < nrows; ++rr)
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          bulk_s2g(a.out + (4 * static_cast<int64_t>(I) + r) * a.ldo + 4 * static_cast<int64_t>(J0),
-                   sbase + ob0 + r * kOS, Tw * 8);
+            for (int r = 0; r < 4; ++r)
+              bulk_s2g(a.out + (4 * static_cast<int64_t>(I + rr) + r) * a.ldo,
+                       sbase + ob0 + r * kOS + rr * rb, rb);
+        } else {
+          const uint32_t Tw = min(static_cast<uint32_t>(a.bc) - J0, static_cast<uint32_t>(kT));
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            bulk_s2g(a.out + (4 * static_cast<int64_t>(I) + r) * a.ldo + 4 * static_cast<int64_t>(J0),
+                     sbase + ob0 + r * kOS, Tw * 8);
+        }
         ptx::bulk_commit();
       }
     }
@@ -407,6 +431,7 @@ struct TcEncArgs {
   int P;
   int64_t bc, upr, nunits;
   uint32_t nstages, nbuf, out_bytes;
+  uint32_t br, R;   // tile rows; R > 1: a unit is R whole tile rows (narrow matrices)
   unsigned* sched;
   uint32_t dyn0;
   Trace trace;
@@ -501,15 +526,27 @@ __global__ void __launch_bounds__(32 * (2 + EPW), 1)
       u = __shfl_sync(0xFFFFFFFFu, u, 0);
       if (u == kNoUnit) break;
       const uint32_t st = it % nst, ph = (it / nst) & 1;
-      const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
-      const uint32_t Tw = min(bc - J0, static_cast<uint32_t>(kT));
+      uint32_t I, J0;
+      unit_coord(u, upr, a.R, I, J0);
       ptx::mbar_wait(&empty[st], ph ^ 1);
-      if (lane == 0) ptx::mbar_arrive_expect_tx(&full[st], 4 * Tw * 8);
-      __syncwarp();
-      if (lane < 4)
-        bulk_g2s(sbase + st * kStage + lane * kERow,
-                 a.mat + (4 * static_cast<int64_t>(I) + lane) * a.ldm + 4 * static_cast<int64_t>(J0),
-                 Tw * 8, &full[st]);
+      if (a.R > 1) {
+        // R whole tile rows: lane 4 rr + r copies matrix row 4 (I + rr) + r after row rr - 1's
+        const uint32_t nrows = min(a.R, a.br - I);
+        if (lane == 0) ptx::mbar_arrive_expect_tx(&full[st], nrows * 4 * bc * 8);
+        __syncwarp();
+        const uint32_t rr = lane >> 2, r = lane & 3;
+        if (rr < nrows)
+          bulk_g2s(sbase + st * kStage + r * kERow + rr * bc * 8,
+                   a.mat + (4 * static_cast<int64_t>(I + rr) + r) * a.ldm, bc * 8, &full[st]);
+      } else {
+        const uint32_t Tw = min(bc - J0, static_cast<uint32_t>(kT));
+        if (lane == 0) ptx::mbar_arrive_expect_tx(&full[st], 4 * Tw * 8);
+        __syncwarp();
+        if (lane < 4)
+          bulk_g2s(sbase + st * kStage + lane * kERow,
+                   a.mat + (4 * static_cast<int64_t>(I) + lane) * a.ldm + 4 * static_cast<int64_t>(J0),
+                   Tw * 8, &full[st]);
+      }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
@@ -551,7 +588,8 @@ __global__ void __launch_bounds__(32 * (2 + EPW), 1)
       if (u == kNoUnit) break;
       const uint32_t buf = it & 1, bph = (it >> 1) & 1;
       const uint32_t ob0 = s_out + (grp * nbuf + k % nbuf) * ob_bytes;
-      const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
+      uint32_t I, J0;
+      unit_coord(u, upr, a.R, I, J0);
       ptx::mbar_wait(&tfull[buf], bph);
       ptx::tc_fence_after();
       if (it == 0 && issuer) trace_cta(a.trace, 2);
@@ -1364,22 +1402,27 @@ cudaError_t launch_remix_tc(const CUtensorMap& ti, const CUtensorMap& to, TcEncA
 cudaError_t planes_to_tiles_tc(const void* in, int P, int64_t br, int64_t bc, const float* coef,
                                void* out, int64_t ldo, cudaStream_t s, int64_t plane_rows) {
   static const int on = probe_env("STL_DEC_TC", 1);
-  if (!on || P < 1 || P > 32 || bc < kT || bc % 64 || ldo % 8 ||
+  // narrow matrices (bc < 512, bc | 512): units of R = 512 / bc whole tile rows
+  const int R = bc < kT && bc >= 64 && kT % bc == 0 ? static_cast<int>(kT / bc) : 1;
+  if (!on || P < 1 || P > 32 || (bc < kT && R == 1) || bc % 64 || ldo % 8 ||
       (reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
     return cudaErrorNotSupported;
   const int Pb = P <= 16 ? 16 : (P + 7) / 8 * 8;
   CUtensorMap tm{};
   if (plane_rows < br) plane_rows = br;
-  if (!plane_box_tmap(&tm, in, 2, P, Pb, br, bc, kT, plane_rows)) return cudaErrorNotSupported;
+  if (R > 1 && plane_rows != br) return cudaErrorNotSupported;
+  if (!plane_box_tmap(&tm, in, 2, P, Pb, br, bc, kT, plane_rows, R)) return cudaErrorNotSupported;
   TcArgs a{};
+  a.br = static_cast<uint32_t>(br);
+  a.R = static_cast<uint32_t>(R);
   a.out = static_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
   a.coef = coef;
   a.P = P;
   a.Pb = Pb;
   a.bc = bc;
-  a.upr = (bc + kT - 1) / kT;
-  a.nunits = br * a.upr;
+  a.upr = R > 1 ? 1 : (bc + kT - 1) / kT;
+  a.nunits = R > 1 ? (br + R - 1) / R : br * a.upr;
   static const int eg = probe_env("STL_DEC_TC_EG", 2);
   if (Pb <= 16) return eg == 1 ? launch_tc<1, 1>(tm, a, s) : launch_tc<1, 2>(tm, a, s);
   return eg == 1 ? launch_tc<2, 1>(tm, a, s) : launch_tc<2, 2>(tm, a, s);
@@ -1390,20 +1433,24 @@ cudaError_t tiles_to_planes_tc(const void* m, int64_t ldm, int64_t br, int64_t b
                                const float* coef, int P, void* out, cudaStream_t s,
                                int64_t plane_rows) {
   static const int on = probe_env("STL_ENC_TC", 1);
-  if (!on || P < 1 || P > 32 || bc < kT || bc % 64 || ldm % 8 ||
+  const int R = bc < kT && bc >= 64 && kT % bc == 0 ? static_cast<int>(kT / bc) : 1;
+  if (!on || P < 1 || P > 32 || (bc < kT && R == 1) || bc % 64 || ldm % 8 ||
       (reinterpret_cast<uintptr_t>(m) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
     return cudaErrorNotSupported;
   CUtensorMap tm{};
   if (plane_rows < br) plane_rows = br;
-  if (!plane_box_tmap(&tm, out, 2, P, P, br, bc, kT, plane_rows)) return cudaErrorNotSupported;
+  if (R > 1 && plane_rows != br) return cudaErrorNotSupported;
+  if (!plane_box_tmap(&tm, out, 2, P, P, br, bc, kT, plane_rows, R)) return cudaErrorNotSupported;
   TcEncArgs a{};
+  a.br = static_cast<uint32_t>(br);
+  a.R = static_cast<uint32_t>(R);
   a.mat = static_cast<const __nv_bfloat16*>(m);
   a.ldm = ldm;
   a.coef = coef;
   a.P = P;
   a.bc = bc;
-  a.upr = (bc + kT - 1) / kT;
-  a.nunits = br * a.upr;
+  a.upr = R > 1 ? 1 : (bc + kT - 1) / kT;
+  a.nunits = R > 1 ? (br + R - 1) / R : br * a.upr;
   static const int eg = probe_env("STL_ENC_TC_EG", 2);
   switch ((P + 7) / 8) {
     case 1: return eg == 1 ? launch_enc_tc<1, 1>(tm, a, s) : launch_enc_tc<1, 2>(tm, a, s);
