@@ -225,6 +225,10 @@ cudaError_t tiles_to_planes2(const void* m, int mdt, int64_t ldm, int64_t br, in
   if (mdt != kBF16 || odt != kBF16 || bc % 4 || ldm % 8 || !al16(m) || !al16(out) || P < 1 ||
       P > kMaxRank)
     return cudaErrorNotSupported;
+  {  // the tcgen05 t = 2 encode (stl_stream_tc.cu), when it takes the shape
+    const cudaError_t e = tiles_to_planes2_tc(m, ldm, br, bc, coef, P, out, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const auto* x = static_cast<const __nv_bfloat16*>(m);
   auto* o = static_cast<__nv_bfloat16*>(out);
   return bc % 8 == 0 ? encode2_launch<8>(x, ldm, br, bc, coef, P, o, s)
@@ -238,6 +242,8 @@ cudaError_t planes_to_tiles2(const void* in, int idt, int Q, int64_t br, int64_t
     return cudaErrorNotSupported;
   auto* o = static_cast<__nv_bfloat16*>(out);
   if (idt == kBF16) {
+    const cudaError_t e = planes_to_tiles2_tc(in, Q, br, bc, coef, out, ldo, s);
+    if (e != cudaErrorNotSupported) return e;
     const auto* z = static_cast<const __nv_bfloat16*>(in);
     return bc % 8 == 0 ? decode2_launch<8>(z, Q, br, bc, coef, o, ldo, s)
                        : decode2_launch<4>(z, Q, br, bc, coef, o, ldo, s);

@@ -145,3 +145,19 @@ def test_tc_strided_and_concurrent():
                                       4, r, o.data_ptr(), _lib.STL_BF16, st.cuda_stream))
     torch.cuda.synchronize()
     assert torch.equal(outs[0], ref) and torch.equal(outs[1], ref)
+
+
+@pytest.mark.parametrize("rows,cols", [(8, 2304), (4, 4096)])
+@pytest.mark.parametrize("r", [1, 4, 5, 8, 9, 17, 24, 32])
+def test_tc_t2_encode_decode(rows, cols, r):
+    """t = 2 on tcgen05 (k_encode2_tc / k_decode2_tc): 1152 tile columns = two full units and a
+    partial one, every 4-plane output-group count and both K-step regimes of the decode."""
+    rng = O.make_rng(rows * 13 + cols + r)
+    e_x, _, d = O.random_gaussian_init(2, r, rng, scale=0.5)
+    m_dev, m64 = bf(rng.standard_normal((rows, cols)))
+    enc = stl.encode_tiles(m_dev, e_x, 2)
+    ref_enc = O.encode_tiles(m64, e_x, 2)
+    assert rel(enc, ref_enc) <= 5e-3
+    enc_dev, enc64 = bf(ref_enc)
+    dec = stl.decode_tiles(enc_dev.permute(2, 0, 1).contiguous().permute(1, 2, 0), d, 2)
+    assert rel(dec, O.decode_tiles(enc64, d, 2)) <= 5e-3
