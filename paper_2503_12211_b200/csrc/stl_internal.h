@@ -203,10 +203,8 @@ cudaError_t red_transform_tc(bool enc, const void* rows, int64_t ldr, const void
 // cudaErrorNotSupported -> the mma.sync streaming remix.
 cudaError_t planes_to_planes_tc(const void* in, int P, int64_t br, int64_t bc, const float* e_x,
                                 const float* d, void* out, cudaStream_t s);
-// t = 2 on tcgen05 (stl_stream_tc.cu): bf16 matrix <-> P <= 32 bf16 planes, tile columns >= 512;
-// cudaErrorNotSupported -> the register-streaming t = 2 kernels (stl_transform2.cu).
-cudaError_t tiles_to_planes2_tc(const void* m, int64_t ldm, int64_t br, int64_t bc,
-                                const float* coef, int P, void* out, cudaStream_t s);
+// t = 2 decode on tcgen05 (stl_stream_tc.cu): P <= 32 bf16 planes -> bf16 matrix, tile columns
+// >= 512; cudaErrorNotSupported -> the register-streaming t = 2 decode (stl_transform2.cu).
 cudaError_t planes_to_tiles2_tc(const void* in, int P, int64_t br, int64_t bc, const float* coef,
                                 void* out, int64_t ldo, cudaStream_t s);
 // Fused-chain remix (stl_stream.cu kRemix): P <= 32 bf16 / fp32 planes -> bf16 planes,

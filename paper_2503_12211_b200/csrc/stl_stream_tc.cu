@@ -1398,15 +1398,12 @@ cudaError_t launch_remix_tc(const CUtensorMap& ti, const CUtensorMap& to, TcEncA
 }
 
 // ------------------------------------------------------------------ t = 2 (configs[2])
-// The same two kernels for 2x2 tiles (c = 2a + b: matrix row 2I + a, column 2J + b).
+// The decode for 2x2 tiles (c = 2a + b: matrix row 2I + a, column 2J + b).
 // Decode (k_decode2_tc): A = the plane box exactly as in k_decode_tc, B = [D_hi | D_lo | 0]
 // (N = 16: 4 + 4 columns and 8 zero ones, the smallest N an M = 128 UMMA takes); the epilogue
 // packs a tile's two values of each of its 2 matrix rows into one bf16x2 word.
-// Encode (k_encode2_tc): row a read as quads of tiles (16 bytes: element b of tiles 4i..4i+3) is
-// the K-major no-swizzle operand (SBO = 128, LBO = the row stride, the K-step's two core matrices
-// being rows 0 and 1), so ONE K = 16 step covers all 4 tile values of 4 tiles; B pairs each
-// quad position with its own columns: n = 32 g4 + 8 q4 + 4 hl + pp (plane p = 4 g4 + pp);
-// M = 128 quads = the whole 512-tile unit; the epilogue writes 4 tiles (8 bytes) per plane.
+// (An encode twin — tile quads as the K-major operand, one K-step per unit — measured even to
+// slower than the register-streaming t = 2 encode and was removed: profiles/r02_t2_tc_ab.log.)
 constexpr uint32_t kOS2 = kT * 4;         // t = 2 output staging row: 512 tiles x 2 bf16
 constexpr uint32_t kBBytes2 = 16 * 128;   // decode B: 16 rows
 
@@ -1569,178 +1566,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int G4>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_encode2_tc(const __grid_constant__ CUtensorMap tm_out, TcEncArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  const uint32_t sbase = ptx::smem_u32(smem);
-  constexpr int N = 32 * G4;
-  constexpr uint32_t kRow = kT * 4;            // one matrix row of a unit
-  constexpr uint32_t kStage = 2 * kRow;
-  constexpr uint32_t kB = N * 128;
-  constexpr uint32_t kTc = 2 * N <= 256 ? 256u : 512u;
-  constexpr int kGW = kEpi / 2;
-  const uint32_t nst = a.nstages, nbuf = a.nbuf, ob_bytes = a.out_bytes;
-  const uint32_t s_out = nst * kStage;
-  const uint32_t s_b = (s_out + 2 * nbuf * ob_bytes + 1023) / 1024 * 1024;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + s_b + kB);
-  uint64_t* empty = full + kMaxSt;
-  uint64_t* tfull = empty + kMaxSt;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + kRing);
-  volatile uint32_t* ring = tslot + 4;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int P = a.P;
-  const uint32_t nunits = static_cast<uint32_t>(a.nunits), upr = static_cast<uint32_t>(a.upr);
-  const uint32_t bc = static_cast<uint32_t>(a.bc);
-
-  if (threadIdx.x == 0) {
-    trace_mark(a.trace, false);
-    for (uint32_t i = 0; i < nst; ++i) {
-      ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], kGW);
-    }
-    for (int i = 0; i < kRing; ++i) ptx::mbar_init(&rbar[i], 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tm_out);
-  if (warp == 1) ptx::tmem_alloc(tslot, kTc);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tslot;
-  griddep_launch_dependents();
-  griddep_wait();
-  if (warp != 0) {
-    // B[n][k]: k = 8 a + 2 q4 + b (row a, quad position q4, element b); n = 32 g4 + 8 q4' + 4 hl
-    // + pp -> E_hl[4 g4 + pp][2 a + b] where q4 == q4'; K 16..63 of each 128-byte row zero
-    for (int i = threadIdx.x - 32; i < N * 64; i += kThreads - 32) {
-      const int n = i >> 6, k = i & 63;
-      const int g4 = n >> 5, q4n = (n >> 3) & 3, hl = (n >> 2) & 1, p = 4 * g4 + (n & 3);
-      const int ka = (k >> 3) & 1, q4k = (k >> 1) & 3, kb = k & 1;
-      const float e = k < 16 && q4k == q4n && p < P ? a.coef[p * 4 + 2 * ka + kb] : 0.f;
-      const __nv_bfloat16 hi = __float2bfloat16_rn(e);
-      const __nv_bfloat16 v = hl == 0 ? hi : __float2bfloat16_rn(e - __bfloat162float(hi));
-      const uint32_t off = n * 128 + ((((k * 2) >> 4) ^ (n & 7)) << 4) + ((k * 2) & 15);
-      *reinterpret_cast<__nv_bfloat16*>(smem + s_b + off) = v;
-    }
-    ptx::fence_proxy_async_smem();
-    asm volatile("bar.sync 5, %0;" ::"n"(kThreads - 32) : "memory");
-  }
-
-  if (warp == 0) {
-    for (uint32_t it = 0;; ++it) {
-      uint32_t u = 0;
-      if (lane == 0) {
-        u = next_unit(it, nunits, a.dyn0, a.sched);
-        ring[it % kRing] = u;
-        ptx::mbar_arrive(&rbar[it % kRing]);
-        if (u == kNoUnit) {
-          ring[(it + 1) % kRing] = u;
-          ptx::mbar_arrive(&rbar[(it + 1) % kRing]);
-        }
-      }
-      u = __shfl_sync(0xFFFFFFFFu, u, 0);
-      if (u == kNoUnit) break;
-      const uint32_t st = it % nst, ph = (it / nst) & 1;
-      const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
-      const uint32_t Tw = min(bc - J0, static_cast<uint32_t>(kT));
-      ptx::mbar_wait(&empty[st], ph ^ 1);
-      if (lane == 0) ptx::mbar_arrive_expect_tx(&full[st], 2 * Tw * 4);
-      __syncwarp();
-      if (lane < 2)
-        bulk_g2s(sbase + st * kStage + lane * kRow,
-                 a.mat + (2 * static_cast<int64_t>(I) + lane) * a.ldm + 2 * static_cast<int64_t>(J0),
-                 Tw * 4, &full[st]);
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N, false, false);
-      for (uint32_t it = 0;; ++it) {
-        ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
-        if (ring[it % kRing] == kNoUnit) break;
-        const uint32_t st = it % nst, ph = (it / nst) & 1;
-        const uint32_t buf = it & 1, bph = (it >> 1) & 1;
-        ptx::mbar_wait(&tempty[buf], bph ^ 1);
-        ptx::mbar_wait(&full[st], ph);
-        ptx::tc_fence_after();
-        const uint64_t ad = smem_desc_plain(sbase + st * kStage, kRow, 128);
-        const uint64_t bd = ptx::smem_desc_sw128(sbase + s_b, 16, 1024);
-        ptx::mma_bf16_ss(tmem + buf * N, ad, bd, idesc, 0u);
-        ptx::mma_commit(&empty[st]);
-        ptx::mma_commit(&tfull[buf]);
-      }
-    }
-  } else {
-    const int ew = warp - 2;
-    const int grp = ew / kGW, gw = ew % kGW;
-    const uint32_t quarter = warp & 3;
-    const bool issuer = gw == 0 && lane == 0;
-    // quad i = 32 quarter + lane: tiles 4 i .. 4 i + 3 = chunk 2 quarter + lane / 16, bytes
-    // 8 (lane % 16) of the chunk's plane rows
-    const uint32_t chunk = 2 * quarter + (lane >> 4), byte = 8 * (lane & 15);
-    for (uint32_t it = grp, k = 0;; it += 2, ++k) {
-      ptx::mbar_wait(&rbar[it % kRing], (it / kRing) & 1);
-      const uint32_t u = ring[it % kRing];
-      if (u == kNoUnit) break;
-      const uint32_t buf = it & 1, bph = (it >> 1) & 1;
-      const uint32_t ob0 = s_out + (grp * nbuf + k % nbuf) * ob_bytes;
-      const uint32_t I = u / upr, J0 = (u - I * upr) * kT;
-      ptx::mbar_wait(&tfull[buf], bph);
-      ptx::tc_fence_after();
-#pragma unroll
-      for (int g0 = 0; g0 < G4; g0 += 2) {
-        float v[2][32];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (g0 + h < G4) tmem_ld_x32(tmem + ((quarter * 32) << 16) + buf * N + 32 * (g0 + h), v[h]);
-        ptx::tmem_ld_wait();
-        if (g0 + 2 >= G4) {
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int pp = 0; pp < 4; ++pp) {
-            const int p = 4 * (g0 + h) + pp;
-            if (g0 + h < G4 && p < P) {
-              const uint32_t row = chunk * P + p;
-              const uint32_t off = row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15));
-              const uint32_t w0 = pack_bf16(v[h][pp] + v[h][4 + pp], v[h][8 + pp] + v[h][12 + pp]);
-              const uint32_t w1 = pack_bf16(v[h][16 + pp] + v[h][20 + pp], v[h][24 + pp] + v[h][28 + pp]);
-              *reinterpret_cast<uint2*>(smem + ob0 + off) = make_uint2(w0, w1);
-            }
-          }
-      }
-      ptx::fence_proxy_async_smem();
-      if (issuer) bulk_wait_read_n(nbuf - 2 > 1 ? 1 : nbuf - 2);
-      epi_bar(grp, 32 * kGW);
-      if (issuer) {
-        tma_store_4d(&tm_out, sbase + ob0, 0, 0, static_cast<int>(J0 / 64), static_cast<int>(I));
-        ptx::bulk_commit();
-      }
-    }
-    if (issuer) ptx::bulk_wait_all();
-  }
-  __syncwarp();
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (threadIdx.x == 0) sched_done(a.sched, a.dyn0, nunits);
-  if (threadIdx.x == 0) trace_mark(a.trace, true);
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, kTc);
-  }
-}
-
 template <int KS>
 cudaError_t launch_dec2_tc(const CUtensorMap& tm, TcArgs a, cudaStream_t s) {
   const uint32_t kStage = static_cast<uint32_t>(a.Pb) * kT * 2;
@@ -1752,30 +1577,6 @@ cudaError_t launch_dec2_tc(const CUtensorMap& tm, TcArgs a, cudaStream_t s) {
   a.nstages = ns > kMaxSt ? kMaxSt : ns;
   const uint32_t smem = a.nstages * kStage + 2 * a.nbuf * kOut2 + kBBytes2 + kBarBytes + 1024;
   auto k = k_decode2_tc<KS>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  int64_t grid = sm_count();
-  if (grid > a.nunits) grid = a.nunits;
-  if (grid < 1) return cudaSuccess;
-  if (!set_schedule(a, static_cast<uint32_t>(grid))) return cudaErrorNotSupported;
-  a.trace = trace_next();
-  return launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, tm, a);
-}
-
-template <int G4>
-cudaError_t launch_enc2_tc(const CUtensorMap& tm, TcEncArgs a, cudaStream_t s) {
-  constexpr uint32_t kStage = 2 * kT * 4;
-  constexpr uint32_t kB = 32 * G4 * 128;
-  a.out_bytes = (static_cast<uint32_t>(a.P) * kT * 2 + 1023) / 1024 * 1024;
-  const uint32_t budget = 227 * 1024 - 2048 - kB - kBarBytes;
-  a.nbuf = 2;
-  if (2 * a.nbuf * a.out_bytes + 2 * kStage > budget) return cudaErrorNotSupported;
-  const uint32_t ns = (budget - 2 * a.nbuf * a.out_bytes) / kStage;
-  a.nstages = ns > kMaxSt ? kMaxSt : ns;
-  const uint32_t smem =
-      (a.nstages * kStage + 2 * a.nbuf * a.out_bytes + 1023) / 1024 * 1024 + kB + kBarBytes + 1024;
-  auto k = k_encode2_tc<G4>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -1933,40 +1734,8 @@ cudaError_t planes_to_planes_tc(const void* in, int P, int64_t br, int64_t bc, c
   }
 }
 
-// t = 2 on tcgen05 (k_encode2_tc / k_decode2_tc): bf16 matrix <-> P <= 32 bf16 planes, tile
-// columns >= 512 and % 64; cudaErrorNotSupported -> the register-streaming t = 2 kernels.
-cudaError_t tiles_to_planes2_tc(const void* m, int64_t ldm, int64_t br, int64_t bc,
-                                const float* coef, int P, void* out, cudaStream_t s) {
-  // measured against the register-streaming t = 2 encode at 8192^2 (profiles/r02_t2_tc_ab.log):
-  // r = 16 slower (132 vs 115 us), r = 24 / 32 even -> kept as a probe (STL_T2_TC_ENC=1); the
-  // tcgen05 t = 2 decode wins (r = 16: 121 vs 146 us, r = 32: 202-271 vs 275-284 us) and is the
-  // default
-  static const int on = probe_env("STL_T2_TC_ENC", 0);
-  if (!on || P < 1 || P > 32 || bc < kT || bc % 64 || ldm % 8 ||
-      (reinterpret_cast<uintptr_t>(m) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
-    return cudaErrorNotSupported;
-  CUtensorMap tm{};
-  if (!plane_box_tmap(&tm, out, 2, P, P, br, bc, kT, br)) return cudaErrorNotSupported;
-  TcEncArgs a{};
-  a.mat = static_cast<const __nv_bfloat16*>(m);
-  a.ldm = ldm;
-  a.coef = coef;
-  a.P = P;
-  a.bc = bc;
-  a.upr = (bc + kT - 1) / kT;
-  a.nunits = br * a.upr;
-  switch ((P + 3) / 4) {
-    case 1: return launch_enc2_tc<1>(tm, a, s);
-    case 2: return launch_enc2_tc<2>(tm, a, s);
-    case 3: return launch_enc2_tc<3>(tm, a, s);
-    case 4: return launch_enc2_tc<4>(tm, a, s);
-    case 5: return launch_enc2_tc<5>(tm, a, s);
-    case 6: return launch_enc2_tc<6>(tm, a, s);
-    case 7: return launch_enc2_tc<7>(tm, a, s);
-    default: return launch_enc2_tc<8>(tm, a, s);
-  }
-}
-
+// t = 2 decode on tcgen05 (k_decode2_tc): P <= 32 bf16 planes -> bf16 matrix, tile columns
+// >= 512 and % 64; cudaErrorNotSupported -> the register-streaming t = 2 decode.
 cudaError_t planes_to_tiles2_tc(const void* in, int P, int64_t br, int64_t bc, const float* coef,
                                 void* out, int64_t ldo, cudaStream_t s) {
   static const int on = probe_env("STL_T2_TC", 1);

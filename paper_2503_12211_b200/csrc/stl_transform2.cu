@@ -225,10 +225,6 @@ cudaError_t tiles_to_planes2(const void* m, int mdt, int64_t ldm, int64_t br, in
   if (mdt != kBF16 || odt != kBF16 || bc % 4 || ldm % 8 || !al16(m) || !al16(out) || P < 1 ||
       P > kMaxRank)
     return cudaErrorNotSupported;
-  {  // the tcgen05 t = 2 encode (stl_stream_tc.cu), when it takes the shape
-    const cudaError_t e = tiles_to_planes2_tc(m, ldm, br, bc, coef, P, out, s);
-    if (e != cudaErrorNotSupported) return e;
-  }
   const auto* x = static_cast<const __nv_bfloat16*>(m);
   auto* o = static_cast<__nv_bfloat16*>(out);
   return bc % 8 == 0 ? encode2_launch<8>(x, ldm, br, bc, coef, P, o, s)
