@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(32 * (2 + EPW), 1)
         }
         const uint32_t st = it % nst, ph = (it / nst) & 1;
         uint32_t I, J0;
-        unit_coord(u, upr, a.R, I, J0);
+      unit_coord(u, upr, a.R, I, J0);
         ptx::mbar_wait(&empty[st], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&full[st], kStage);
         tma_load_4d(&tm_in, &full[st], sbase + st * kStage, 0, 0, static_cast<int>(J0 / 64),
@@ -258,11 +258,10 @@ __global__ void __launch_bounds__(32 * (2 + EPW), 1)
       const uint32_t buf = it & 1, bph = (it >> 1) & 1;
       const uint32_t ob0 = s_out + (grp * nbuf + k % nbuf) * kOutBytes;
       uint32_t I, J0;
-        unit_coord(u, upr, a.R, I, J0);
+      unit_coord(u, upr, a.R, I, J0);
       ptx::mbar_wait(&tfull[buf], bph);
       ptx::tc_fence_after();
       if (it == 0 && issuer) trace_cta(a.trace, 2);
-#pragma unroll
       // two M-blocks' accumulators per tcgen05.wait::ld (the loads' latencies overlap)
       static_assert(kMBW % 2 == 0, "M-blocks per warp");
 #pragma unroll
@@ -1369,9 +1368,10 @@ __global__ void __launch_bounds__(32 * (2 + 2 * GW), 1)
 template <int KS, int G, int GW = 8>
 cudaError_t launch_remix_tc(const CUtensorMap& ti, const CUtensorMap& to, TcEncArgs a,
                             const float* e_x, const float* d, cudaStream_t s) {
-  static const int gw4 = probe_env("STL_REMIX_TC_GW", 8) == 4;
+#ifdef STL_PROBES
   if constexpr (GW == 8)
-    if (gw4) return launch_remix_tc<KS, G, 4>(ti, to, a, e_x, d, s);
+    if (probe_env("STL_REMIX_TC_GW", 8) == 4) return launch_remix_tc<KS, G, 4>(ti, to, a, e_x, d, s);
+#endif
   constexpr int N = 16 * G;
   constexpr uint32_t kB = N * 128 < 1024 ? 1024 : N * 128;
   const int Pb = a.P <= 16 ? 16 : (a.P + 7) / 8 * 8;
@@ -1614,9 +1614,11 @@ cudaError_t planes_to_tiles_tc(const void* in, int P, int64_t br, int64_t bc, co
   a.bc = bc;
   a.upr = R > 1 ? 1 : (bc + kT - 1) / kT;
   a.nunits = R > 1 ? (br + R - 1) / R : br * a.upr;
-  static const int eg = probe_env("STL_DEC_TC_EG", 2);
-  if (Pb <= 16) return eg == 1 ? launch_tc<1, 1>(tm, a, s) : launch_tc<1, 2>(tm, a, s);
-  return eg == 1 ? launch_tc<2, 1>(tm, a, s) : launch_tc<2, 2>(tm, a, s);
+#ifdef STL_PROBES
+  if (probe_env("STL_DEC_TC_EG", 2) == 1)  // probe: one 8-warp epilogue group
+    return Pb <= 16 ? launch_tc<1, 1>(tm, a, s) : launch_tc<2, 1>(tm, a, s);
+#endif
+  return Pb <= 16 ? launch_tc<1, 2>(tm, a, s) : launch_tc<2, 2>(tm, a, s);
 }
 
 // bf16 matrix (4 br x 4 bc, leading dim ldm) -> P <= 32 bf16 planes (P x plane_rows x bc).
@@ -1642,12 +1644,21 @@ cudaError_t tiles_to_planes_tc(const void* m, int64_t ldm, int64_t br, int64_t b
   a.bc = bc;
   a.upr = R > 1 ? 1 : (bc + kT - 1) / kT;
   a.nunits = R > 1 ? (br + R - 1) / R : br * a.upr;
-  static const int eg = probe_env("STL_ENC_TC_EG", 2);
+#ifdef STL_PROBES
+  if (probe_env("STL_ENC_TC_EG", 2) == 1) {  // probe: one 8-warp epilogue group
+    switch ((P + 7) / 8) {
+      case 1: return launch_enc_tc<1, 1>(tm, a, s);
+      case 2: return launch_enc_tc<2, 1>(tm, a, s);
+      case 3: return launch_enc_tc<3, 1>(tm, a, s);
+      default: return launch_enc_tc<4, 1>(tm, a, s);
+    }
+  }
+#endif
   switch ((P + 7) / 8) {
-    case 1: return eg == 1 ? launch_enc_tc<1, 1>(tm, a, s) : launch_enc_tc<1, 2>(tm, a, s);
-    case 2: return eg == 1 ? launch_enc_tc<2, 1>(tm, a, s) : launch_enc_tc<2, 2>(tm, a, s);
-    case 3: return eg == 1 ? launch_enc_tc<3, 1>(tm, a, s) : launch_enc_tc<3, 2>(tm, a, s);
-    default: return eg == 1 ? launch_enc_tc<4, 1>(tm, a, s) : launch_enc_tc<4, 2>(tm, a, s);
+    case 1: return launch_enc_tc<1, 2>(tm, a, s);
+    case 2: return launch_enc_tc<2, 2>(tm, a, s);
+    case 3: return launch_enc_tc<3, 2>(tm, a, s);
+    default: return launch_enc_tc<4, 2>(tm, a, s);
   }
 }
 
@@ -1686,7 +1697,8 @@ cudaError_t red_transform_tc(bool enc, const void* rows, int64_t ldr, const void
   a.upr = (bc + TU - 1) / TU;
   a.nunits = br * a.upr;
   const int MT = (P + 15) / 16;
-  if (enc) {
+#ifdef STL_PROBES
+  if (enc) {  // probe STL_RED_TC=1: the encode + g_d reduction on this kernel
     const int G = (P + 7) / 8;
 #define STL_RED_ENC(TUV)                                                                          \
   switch (G) {                                                                                    \
@@ -1699,10 +1711,13 @@ cudaError_t red_transform_tc(bool enc, const void* rows, int64_t ldr, const void
     STL_RED_ENC(512)
 #undef STL_RED_ENC
   }
+  if (TU == 256)  // probe STL_RED_TC_T=256
+    return Pb <= 16 ? launch_red_tc<false, 256, 1, 1>(tz, to, a, red_out, s)
+                    : launch_red_tc<false, 256, 2, 2>(tz, to, a, red_out, s);
+#else
+  if (enc || TU != 512) return cudaErrorNotSupported;
+#endif
   const int KS = Pb <= 16 ? 1 : 2;
-  if (TU == 256)
-    return KS == 1 ? launch_red_tc<false, 256, 1, 1>(tz, to, a, red_out, s)
-                   : launch_red_tc<false, 256, 2, 2>(tz, to, a, red_out, s);
   return KS == 1 ? launch_red_tc<false, 512, 1, 1>(tz, to, a, red_out, s)
                  : (MT == 1 ? launch_red_tc<false, 512, 2, 1>(tz, to, a, red_out, s)
                             : launch_red_tc<false, 512, 2, 2>(tz, to, a, red_out, s));
